@@ -1,0 +1,230 @@
+/*
+ * sbr200.h -- C ABI of the B200-native SBR trace-integrate library
+ * (libsbr200.so, built from paper_2604_09243_b200/csrc for sm_100a).
+ *
+ * This is the drop-in boundary for the reference package's hot path.  The
+ * reference (pkg/src/sbr, Python + numba) has no formal FFI; its de-facto
+ * kernel interface is the numba signature of
+ *   _trace_rows(nodes_min, nodes_max, node_first, node_count, tri_order,
+ *               v0, v1, v2, normals, corner, uvec, vvec, kvec, spacing, n_v,
+ *               i_start, i_end, max_bounces, eps, strict, stack_depth, out*6)
+ *   (pkg/src/sbr/transport.py:330-335)
+ * plus the module functions re-exported by pkg/src/sbr/__init__.py:10-46.
+ * Each entry point below names the reference interface it replaces.
+ *
+ * Conventions
+ *  - All pointers are plain host pointers owned by the caller unless the
+ *    parameter name ends in `_dev` (a device pointer on the context's GPU).
+ *    Arrays are C-contiguous; (N,3) arrays are row-major xyz triples.
+ *  - Every function returns an sbr_status; on failure sbr_last_error()
+ *    returns a thread-local message.  Status codes mirror the reference
+ *    exception mapping (pkg/src/sbr/errors.py:8-17, cli.py:196-205):
+ *    SBR_EINVAL -> ValidationError, SBR_ENUMERIC -> NumericalError.
+ *  - Results are a pure function of the inputs: no dependence on launch
+ *    configuration, GPU count or scheduling (reference "workers"
+ *    invariance, pkg/src/sbr/sweep.py:5-8).
+ *  - Handles are not thread-safe across threads without external locking;
+ *    use one context per GPU (one process per GPU in the sweep driver).
+ */
+#ifndef SBR200_H
+#define SBR200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SBR200_ABI_VERSION 1
+
+typedef enum {
+    SBR_OK = 0,
+    SBR_EINVAL = 2,    /* ValidationError (errors.py:12) */
+    SBR_EIO = 3,       /* OSError */
+    SBR_ENUMERIC = 4,  /* NumericalError (errors.py:16) */
+    SBR_ECUDA = 10,    /* CUDA runtime failure */
+    SBR_ENOMEM = 12    /* device or host allocation failure */
+} sbr_status;
+
+/* Triangle storage on device (geometry.py:88-127 Mesh precision). */
+typedef enum {
+    SBR_STORAGE_AUTO = 0,      /* F32_EXACT if every coordinate is float32-representable, else F64 */
+    SBR_STORAGE_F32_EXACT = 1, /* float32 storage, lossless; FP64 edges (== reference precision="double") */
+    SBR_STORAGE_F64 = 2,       /* float64 storage (72 B/triangle) */
+    SBR_STORAGE_SINGLE = 3     /* reference precision="single": float32 vertices AND float32 edge
+                                  subtraction, FP64 ray state */
+} sbr_storage;
+
+typedef struct sbr_ctx sbr_ctx;
+typedef struct sbr_mesh sbr_mesh;
+typedef struct sbr_bvh sbr_bvh;
+
+/* Replaces bvh.py:22-49 BuildParams.  split_rule is accepted for API
+ * parity; the GPU always builds an LBVH (closest-hit results are tree-
+ * independent).  n_leaf bounds the leaf size. */
+typedef struct {
+    int32_t split_rule;   /* 0 median, 1 sah (informational) */
+    int32_t n_leaf;       /* >= 1 */
+    int32_t max_depth;    /* reference default 64; informational */
+    int32_t reserved;
+} sbr_build_params;
+
+/* One incident direction's launch grid (transport.py:84-127 ApertureGrid).
+ * Ray (i,j) starts at corner + ((i+.5)*spacing)*u + ((j+.5)*spacing)*v
+ * and travels along k (transport.py:339-345). */
+typedef struct {
+    double corner[3], u[3], v[3], k[3];
+    double spacing;
+    double cell_area;
+    int64_t n_u, n_v;
+} sbr_grid;
+
+/* transport.py:215-239 TraceParams + the sampling rule of
+ * transport.py:75-81 (checked again on device by the launcher). */
+typedef struct {
+    int32_t max_bounces;      /* >= 1 */
+    int32_t strict;           /* strict_orientation */
+    int32_t allow_aliasing;   /* skip the spacing <= lambda_min / factor rule */
+    int32_t reserved;
+    double eps;               /* resolved epsilon (> 0) */
+    double lambda_min;        /* shortest wavelength of the solve (0: no check) */
+    double sampling_factor;   /* 5.0 by default */
+} sbr_trace_params;
+
+/* Per-solve diagnostics (sweep.py:256-259): arrays of length ngrids,
+ * hist is ngrids*(max_bounces+1).  Any pointer may be NULL. */
+typedef struct {
+    int64_t *valid_rays;
+    int32_t *max_bounce;
+    int64_t *hist;
+    int64_t *queries;         /* closest-hit queries = sum(N_i + 1) */
+} sbr_diag;
+
+const char *sbr_last_error(void);
+int sbr_abi_version(void);
+
+/* ---- context ---------------------------------------------------------- */
+int sbr_ctx_create(int device, sbr_ctx **out);
+int sbr_ctx_destroy(sbr_ctx *ctx);
+int sbr_ctx_synchronize(sbr_ctx *ctx);
+/* Stream the library launches on (cudaStream_t as void*). */
+int sbr_ctx_stream(sbr_ctx *ctx, void **stream_out);
+/* Number of kernels this context has launched (instrumentation). */
+int sbr_ctx_launch_count(sbr_ctx *ctx, int64_t *count_out);
+
+/* ---- mesh: geometry.py:130-180 mesh_from_soup output -> device --------- */
+int sbr_mesh_create(sbr_ctx *ctx, const double *v0, const double *v1,
+                    const double *v2, const double *normals, int64_t ntri,
+                    int32_t storage, sbr_mesh **out);
+int sbr_mesh_destroy(sbr_mesh *mesh);
+/* aabb = {min x,y,z, max x,y,z}; storage = resolved sbr_storage. */
+int sbr_mesh_info(const sbr_mesh *mesh, int64_t *ntri, int32_t *storage,
+                  double aabb[6]);
+
+/* ---- BVH: bvh.py:218-299 build (GPU LBVH) ------------------------------ */
+int sbr_bvh_build(sbr_ctx *ctx, const sbr_mesh *mesh,
+                  const sbr_build_params *params, sbr_bvh **out);
+/* Upload a reference-layout tree (bvh.py:58-88): preorder, left child
+ * = i+1, node_first = right child (internal) or first index (leaf). */
+int sbr_bvh_upload(sbr_ctx *ctx, const sbr_mesh *mesh, const double *nodes_min,
+                   const double *nodes_max, const int32_t *node_first,
+                   const int32_t *node_count, const int32_t *tri_order,
+                   int64_t nnodes, sbr_bvh **out);
+/* Size of the reference-layout export. */
+int sbr_bvh_info(const sbr_bvh *bvh, int64_t *nnodes_export,
+                 int64_t *nnodes_device, int32_t *max_depth);
+/* Export into the reference layout so bvh.py:90-121 Bvh.validate() and
+ * the CPU _traverse can consume it.  Arrays sized by sbr_bvh_info. */
+int sbr_bvh_export(const sbr_bvh *bvh, double *nodes_min, double *nodes_max,
+                   int32_t *node_first, int32_t *node_count, int32_t *tri_order);
+int sbr_bvh_destroy(sbr_bvh *bvh);
+
+/* ---- queries ------------------------------------------------------------ */
+/* bvh.py:407-423 closest_hit_batch: tri (-1 on miss), t, node visits. */
+int sbr_closest_hit(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *bvh,
+                    const double *origins, const double *dirs, int64_t n,
+                    double t_min, double t_max, int64_t *tri, double *t,
+                    int64_t *visits);
+
+/* geometry.py:394-409 ray_triangle_intersect over n independent
+ * (ray, triangle) pairs (pair r uses triangle v0[r],v1[r],v2[r]);
+ * t[r] = hit distance in (t_min, t_max] or -1.  single=1 evaluates the
+ * reference float32 variant (float32 edge subtraction). */
+int sbr_tri_hit_pairs(sbr_ctx *ctx, const double *v0, const double *v1,
+                      const double *v2, const double *origins, const double *dirs,
+                      int64_t n, double t_min, double t_max, int32_t single,
+                      double *t);
+
+/* geometry.py:412-425 ray_aabb_intersect (FP64 slab, geometry.py:358-391)
+ * over n independent (ray, box) pairs; dir_inv holds reciprocals with
+ * +-inf for zero components. */
+int sbr_aabb_hit_pairs(sbr_ctx *ctx, const double *box_min, const double *box_max,
+                       const double *origins, const double *dir_inv, int64_t n,
+                       double t_max, uint8_t *hit, double *entry);
+
+/* transport.py:375-422 trace_grid -> HitRecords (transport.py:251-273).
+ * tri_ids (optional, n*max_bounces, -1 padded) records the hit triangle of
+ * every bounce (the per-ray id parity channel). */
+int sbr_trace_grid(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *bvh,
+                   const sbr_grid *grid, const sbr_trace_params *params,
+                   uint8_t *valid, double *normal0, double *path,
+                   int32_t *bounces, uint8_t *escaped, double *out_dir,
+                   int32_t *tri_ids);
+
+/* transport.py:359-372 trace_ray over an explicit ray list. */
+int sbr_trace_rays(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *bvh,
+                   const double *origins, const double *dirs, int64_t n,
+                   const sbr_trace_params *params, uint8_t *valid,
+                   double *normal0, double *path, int32_t *bounces,
+                   uint8_t *escaped, double *out_dir, int32_t *tri_ids);
+
+/* po.py:83-113 accumulate over host HitRecords (multi-frequency):
+ * amp[f] = complex amplitude for wavenumber k[f], interleaved re,im.
+ * On a non-finite term returns SBR_ENUMERIC with *bad_index = record. */
+int sbr_accumulate(sbr_ctx *ctx, const uint8_t *valid, const double *normal0,
+                   const double *path, const int32_t *bounces,
+                   const uint8_t *escaped, int64_t n, const double k_inc[3],
+                   const double *k, int32_t nk, double cell_area, double gamma,
+                   int32_t count_trapped, double *amp, int64_t *bad_index);
+
+/* ---- fused pipeline: sweep.py:240-263 solve_direction over many grids --
+ * trace -> warp-ballot compaction -> PO integral -> deterministic reduce.
+ * amp is ngrids*nk*2 (re,im) for wavenumbers k[0..nk).  Records never
+ * leave the GPU. */
+int sbr_solve(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *bvh,
+              const sbr_grid *grids, int32_t ngrids,
+              const sbr_trace_params *params, const double *k, int32_t nk,
+              double gamma, int32_t count_trapped, double *amp,
+              sbr_diag *diag);
+
+/* ---- sharded solve (multi-GPU; one process per GPU) ---------------------
+ * Work is cut into fixed units of (grid g, segment s) where a segment is
+ * SBR_SEGMENT_RAYS consecutive ray indices r = i*n_v + j of grid g.
+ * shard_mode 0: unit (g,s) belongs to rank g % nranks (angle sharding);
+ * shard_mode 1: unit index u (row-major over all units) belongs to rank
+ *               u % nranks (ray-tile sharding).
+ * The call writes FP64 segment partial sums into seg_dev (layout from
+ * sbr_segment_layout: nseg_total*nk*2 doubles, zero for foreign units) and
+ * integer diagnostics into diag_dev (ngrids*(3+max_bounces+1) int64:
+ * valid, queries, max_bounce, hist...).  Summing seg_dev and diag_dev
+ * element-wise over ranks (one NCCL reduce; max_bounce via a MAX reduce on
+ * its rows) and calling sbr_finalize yields bit-identical results to
+ * sbr_solve for any nranks. */
+#define SBR_SEGMENT_RAYS (1 << 19)
+int sbr_segment_layout(const sbr_grid *grids, int32_t ngrids,
+                       int64_t *seg_base /* ngrids+1 */);
+int sbr_solve_shard(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *bvh,
+                    const sbr_grid *grids, int32_t ngrids,
+                    const sbr_trace_params *params, const double *k, int32_t nk,
+                    double gamma, int32_t count_trapped, int32_t rank,
+                    int32_t nranks, int32_t shard_mode, double *seg_dev,
+                    int64_t *diag_dev);
+int sbr_finalize(sbr_ctx *ctx, const sbr_grid *grids, int32_t ngrids,
+                 const double *k, int32_t nk, int32_t max_bounces,
+                 const double *seg_dev, const int64_t *diag_dev, double *amp,
+                 sbr_diag *diag);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SBR200_H */

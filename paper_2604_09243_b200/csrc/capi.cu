@@ -1,0 +1,1125 @@
+// capi.cu -- the extern "C" boundary (include/sbr200.h): handles, argument
+// validation, host<->device staging and the batched solve orchestration.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/sbr200.h"
+#include "lbvh.h"
+#include "pipeline.h"
+
+using namespace sbr;
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+static thread_local std::string g_err;
+
+static int fail(int code, const char *fmt, ...)
+{
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CUDA_TRY(x)                                                                     \
+    do {                                                                                \
+        cudaError_t e_ = (x);                                                           \
+        if (e_ != cudaSuccess)                                                          \
+            return fail(e_ == cudaErrorMemoryAllocation ? SBR_ENOMEM : SBR_ECUDA,       \
+                        "%s failed: %s (%s:%d)", #x, cudaGetErrorString(e_), __FILE__,  \
+                        __LINE__);                                                      \
+    } while (0)
+
+#define REQUIRE(cond, ...)                       \
+    do {                                         \
+        if (!(cond)) return fail(SBR_EINVAL, __VA_ARGS__); \
+    } while (0)
+
+extern "C" const char *sbr_last_error(void) { return g_err.c_str(); }
+extern "C" int sbr_abi_version(void) { return SBR200_ABI_VERSION; }
+
+// ---------------------------------------------------------------------------
+// handles
+// ---------------------------------------------------------------------------
+struct sbr_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int num_sms = 148;
+    int64_t launches = 0;
+    std::mutex mu;
+    DevBuf<unsigned long long> counter;
+    DevBuf<unsigned int> err_flag;
+    DevBuf<unsigned long long> bad;
+    // solve scratch (grow-only)
+    DevBuf<SlotRec> slots;
+    DevBuf<UnitDev> units;
+    DevBuf<GridDev> grids;
+    DevBuf<double2> chunk_part;
+    DevBuf<double2> seg_part;
+    DevBuf<int64_t> diag;
+    DevBuf<int64_t> seg_base;
+    DevBuf<double> k2, gpow, scale;
+    DevBuf<double2> amp;
+    LaunchStats stats() { return LaunchStats{&launches, num_sms}; }
+};
+
+struct sbr_mesh {
+    sbr_ctx *ctx = nullptr;
+    int64_t ntri = 0;
+    int storage = kF64;
+    double aabb[6];
+    double cmin[3], cmax[3];
+    DevBuf<double> verts;    // (T,9) original order
+    DevBuf<double> normals;  // (T,3)
+};
+
+struct sbr_bvh {
+    sbr_ctx *ctx = nullptr;
+    const sbr_mesh *mesh = nullptr;
+    LbvhOutput out;
+    double frame[3];
+    float scale = 0.f;
+    BvhView view() const
+    {
+        BvhView v;
+        v.nodes = out.nodes.p;
+        v.tri32 = out.tri32.p;
+        v.tri64 = out.tri64.p;
+        v.normals = mesh->normals.p;
+        v.cx = frame[0]; v.cy = frame[1]; v.cz = frame[2];
+        v.scale = scale;
+        v.root = out.root;
+        return v;
+    }
+};
+
+static int set_device(sbr_ctx *ctx)
+{
+    CUDA_TRY(cudaSetDevice(ctx->device));
+    return SBR_OK;
+}
+
+extern "C" int sbr_ctx_create(int device, sbr_ctx **out)
+{
+    REQUIRE(out, "out is NULL");
+    int ndev = 0;
+    CUDA_TRY(cudaGetDeviceCount(&ndev));
+    REQUIRE(device >= 0 && device < ndev, "device %d out of range (have %d)", device, ndev);
+    sbr_ctx *ctx = new sbr_ctx();
+    ctx->device = device;
+    cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+    if (e == cudaSuccess) e = ctx->counter.alloc(1);
+    if (e == cudaSuccess) e = ctx->err_flag.alloc(1);
+    if (e == cudaSuccess) e = ctx->bad.alloc(1);
+    if (e != cudaSuccess) {
+        delete ctx;
+        return fail(SBR_ECUDA, "context creation failed: %s", cudaGetErrorString(e));
+    }
+    *out = ctx;
+    return SBR_OK;
+}
+
+extern "C" int sbr_ctx_destroy(sbr_ctx *ctx)
+{
+    if (!ctx) return SBR_OK;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return SBR_OK;
+}
+
+extern "C" int sbr_ctx_synchronize(sbr_ctx *ctx)
+{
+    REQUIRE(ctx, "ctx is NULL");
+    if (int rc = set_device(ctx)) return rc;
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    return SBR_OK;
+}
+
+extern "C" int sbr_ctx_stream(sbr_ctx *ctx, void **stream_out)
+{
+    REQUIRE(ctx && stream_out, "NULL argument");
+    *stream_out = (void *)ctx->stream;
+    return SBR_OK;
+}
+
+extern "C" int sbr_ctx_launch_count(sbr_ctx *ctx, int64_t *count_out)
+{
+    REQUIRE(ctx && count_out, "NULL argument");
+    *count_out = ctx->launches;
+    return SBR_OK;
+}
+
+// ---------------------------------------------------------------------------
+// mesh
+// ---------------------------------------------------------------------------
+static bool f32_exact(double x) { return (double)(float)x == x; }
+
+extern "C" int sbr_mesh_create(sbr_ctx *ctx, const double *v0, const double *v1,
+                               const double *v2, const double *normals, int64_t ntri,
+                               int32_t storage, sbr_mesh **out)
+{
+    REQUIRE(ctx && v0 && v1 && v2 && normals && out, "NULL argument");
+    REQUIRE(ntri >= 1, "mesh has no triangles");
+    REQUIRE(ntri < kMaxTriangles, "mesh has %lld triangles; the device layout supports < %lld",
+            (long long)ntri, (long long)kMaxTriangles);
+    REQUIRE(storage >= SBR_STORAGE_AUTO && storage <= SBR_STORAGE_SINGLE, "bad storage %d",
+            storage);
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (int rc = set_device(ctx)) return rc;
+    std::vector<double> verts((size_t)ntri * 9);
+    bool all_f32 = true, finite = true;
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    double clo[3] = {INFINITY, INFINITY, INFINITY}, chi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int64_t t = 0; t < ntri; ++t) {
+        const double *src[3] = {v0 + 3 * t, v1 + 3 * t, v2 + 3 * t};
+        for (int c = 0; c < 3; ++c)
+            for (int a = 0; a < 3; ++a) {
+                double x = src[c][a];
+                verts[9 * t + 3 * c + a] = x;
+                all_f32 &= f32_exact(x);
+                finite &= std::isfinite(x);
+            }
+        for (int a = 0; a < 3; ++a) {
+            double mn = fmin(fmin(src[0][a], src[1][a]), src[2][a]);
+            double mx = fmax(fmax(src[0][a], src[1][a]), src[2][a]);
+            lo[a] = fmin(lo[a], mn);
+            hi[a] = fmax(hi[a], mx);
+            double cc = (mn + mx) * 0.5;
+            clo[a] = fmin(clo[a], cc);
+            chi[a] = fmax(chi[a], cc);
+        }
+    }
+    REQUIRE(finite, "mesh has non-finite vertex coordinates");
+    int st = storage;
+    if (st == SBR_STORAGE_AUTO) st = all_f32 ? SBR_STORAGE_F32_EXACT : SBR_STORAGE_F64;
+    REQUIRE(!(st == SBR_STORAGE_F32_EXACT || st == SBR_STORAGE_SINGLE) || all_f32,
+            "storage requires float32-representable vertices");
+    sbr_mesh *m = new sbr_mesh();
+    m->ctx = ctx;
+    m->ntri = ntri;
+    m->storage = st;
+    for (int a = 0; a < 3; ++a) {
+        m->aabb[a] = lo[a]; m->aabb[3 + a] = hi[a];
+        m->cmin[a] = clo[a]; m->cmax[a] = chi[a];
+    }
+    cudaError_t e = m->verts.alloc((size_t)ntri * 9);
+    if (e == cudaSuccess) e = m->normals.alloc((size_t)ntri * 3);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(m->verts.p, verts.data(), sizeof(double) * 9 * ntri,
+                            cudaMemcpyHostToDevice, ctx->stream);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(m->normals.p, normals, sizeof(double) * 3 * ntri,
+                            cudaMemcpyHostToDevice, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) {
+        delete m;
+        return fail(e == cudaErrorMemoryAllocation ? SBR_ENOMEM : SBR_ECUDA, "mesh upload: %s",
+                    cudaGetErrorString(e));
+    }
+    *out = m;
+    return SBR_OK;
+}
+
+extern "C" int sbr_mesh_destroy(sbr_mesh *mesh)
+{
+    if (!mesh) return SBR_OK;
+    cudaSetDevice(mesh->ctx->device);
+    delete mesh;
+    return SBR_OK;
+}
+
+extern "C" int sbr_mesh_info(const sbr_mesh *mesh, int64_t *ntri, int32_t *storage,
+                             double aabb[6])
+{
+    REQUIRE(mesh, "mesh is NULL");
+    if (ntri) *ntri = mesh->ntri;
+    if (storage) *storage = mesh->storage;
+    if (aabb) memcpy(aabb, mesh->aabb, sizeof(double) * 6);
+    return SBR_OK;
+}
+
+// ---------------------------------------------------------------------------
+// BVH
+// ---------------------------------------------------------------------------
+static void set_frame(sbr_bvh *b, const sbr_mesh *m)
+{
+    double s = 0.0;
+    for (int a = 0; a < 3; ++a) {
+        b->frame[a] = 0.5 * (m->aabb[a] + m->aabb[3 + a]);
+        s = fmax(s, fmax(fabs(m->aabb[a] - b->frame[a]), fabs(m->aabb[3 + a] - b->frame[a])));
+    }
+    b->scale = (float)s * 1.0001f + 1e-30f;
+}
+
+extern "C" int sbr_bvh_build(sbr_ctx *ctx, const sbr_mesh *mesh,
+                             const sbr_build_params *params, sbr_bvh **out)
+{
+    REQUIRE(ctx && mesh && out, "NULL argument");
+    int n_leaf = params ? params->n_leaf : 4;
+    REQUIRE(n_leaf >= 1 && n_leaf <= kMaxLeafCount, "n_leaf must be in [1, %d], got %d",
+            kMaxLeafCount, n_leaf);
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (int rc = set_device(ctx)) return rc;
+    sbr_bvh *b = new sbr_bvh();
+    b->ctx = ctx;
+    b->mesh = mesh;
+    set_frame(b, mesh);
+    LbvhInput in;
+    in.d_verts = mesh->verts.p;
+    in.ntri = mesh->ntri;
+    in.storage = mesh->storage;
+    in.n_leaf = n_leaf;
+    for (int a = 0; a < 3; ++a) {
+        in.cmin[a] = mesh->cmin[a]; in.cmax[a] = mesh->cmax[a];
+        in.frame[a] = b->frame[a];
+    }
+    memcpy(in.aabb, mesh->aabb, sizeof(in.aabb));
+    cudaError_t e = lbvh_build(in, b->out, ctx->stream, &ctx->launches);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) {
+        delete b;
+        return fail(e == cudaErrorMemoryAllocation ? SBR_ENOMEM : SBR_ECUDA, "LBVH build: %s",
+                    cudaGetErrorString(e));
+    }
+    if (b->out.max_depth + 1 >= kStack) {
+        int d = b->out.max_depth;
+        delete b;
+        return fail(SBR_EINVAL, "BVH depth %d exceeds the traversal stack (%d)", d, kStack);
+    }
+    *out = b;
+    return SBR_OK;
+}
+
+// host conversion of a reference preorder tree into child-pair nodes
+struct UploadBuilder {
+    const double *nmin, *nmax;
+    const int32_t *first, *count;
+    int64_t nn;
+    double frame[3];
+    std::vector<Node> nodes;
+    int max_depth = 0;
+    bool ok = true;
+    std::string why;
+
+    void rel(const double *lo, const double *hi, float out[6]) const
+    {
+        for (int a = 0; a < 3; ++a) {
+            float l = (float)(lo[a] - frame[a]), h = (float)(hi[a] - frame[a]);
+            out[a] = nextafterf(l, -INFINITY);
+            out[3 + a] = nextafterf(h, INFINITY);
+        }
+    }
+    // reference for a leaf range; splits ranges > kMaxLeafCount into a
+    // balanced subtree of internal nodes sharing the leaf box
+    int leaf_range(int f, int c, const float box[6], int depth)
+    {
+        if (c <= kMaxLeafCount) return leaf_ref(f, c);
+        int me = (int)nodes.size();
+        nodes.push_back(Node());
+        max_depth = std::max(max_depth, depth);
+        int h = c / 2;
+        int l = leaf_range(f, h, box, depth + 1);
+        int r = leaf_range(f + h, c - h, box, depth + 1);
+        Node nd;
+        nd.a = make_float4(box[0], box[1], box[2], box[3]);
+        nd.b = make_float4(box[4], box[5], box[0], box[1]);
+        nd.c = make_float4(box[2], box[3], box[4], box[5]);
+        nd.d = make_int4(l, r, 0, 0);
+        nodes[me] = nd;
+        return me;
+    }
+    int child_ref(int64_t i, int depth, float box[6])
+    {
+        rel(nmin + 3 * i, nmax + 3 * i, box);
+        if (count[i] > 0) return leaf_range(first[i], count[i], box, depth);
+        return internal(i, depth);
+    }
+    int internal(int64_t i, int depth)
+    {
+        if (!ok) return 0;
+        int64_t l = i + 1, r = first[i];
+        if (!(l > 0 && l < nn && r > 0 && r < nn)) {
+            ok = false;
+            why = "bad child index";
+            return 0;
+        }
+        int me = (int)nodes.size();
+        nodes.push_back(Node());
+        max_depth = std::max(max_depth, depth);
+        float bl[6], br[6];
+        int rl = child_ref(l, depth + 1, bl);
+        int rr = child_ref(r, depth + 1, br);
+        Node nd;
+        nd.a = make_float4(bl[0], bl[1], bl[2], bl[3]);
+        nd.b = make_float4(bl[4], bl[5], br[0], br[1]);
+        nd.c = make_float4(br[2], br[3], br[4], br[5]);
+        nd.d = make_int4(rl, rr, 0, 0);
+        nodes[me] = nd;
+        return me;
+    }
+};
+
+extern "C" int sbr_bvh_upload(sbr_ctx *ctx, const sbr_mesh *mesh, const double *nodes_min,
+                              const double *nodes_max, const int32_t *node_first,
+                              const int32_t *node_count, const int32_t *tri_order,
+                              int64_t nnodes, sbr_bvh **out)
+{
+    REQUIRE(ctx && mesh && nodes_min && nodes_max && node_first && node_count && tri_order && out,
+            "NULL argument");
+    REQUIRE(nnodes >= 1, "empty tree");
+    // permutation check (bvh.py:95-97)
+    std::vector<char> seen((size_t)mesh->ntri, 0);
+    for (int64_t k = 0; k < mesh->ntri; ++k) {
+        int32_t t = tri_order[k];
+        REQUIRE(t >= 0 && t < mesh->ntri && !seen[t], "tri_order is not a permutation");
+        seen[t] = 1;
+    }
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (int rc = set_device(ctx)) return rc;
+    sbr_bvh *b = new sbr_bvh();
+    b->ctx = ctx;
+    b->mesh = mesh;
+    set_frame(b, mesh);
+    UploadBuilder U{nodes_min, nodes_max, node_first, node_count, nnodes,
+                    {b->frame[0], b->frame[1], b->frame[2]}};
+    if (node_count[0] > 0) {
+        // root is a leaf: wrap it in a node carrying the leaf twice
+        float box[6];
+        U.rel(nodes_min, nodes_max, box);
+        U.nodes.push_back(Node());
+        int r = U.leaf_range(node_first[0], node_count[0], box, 1);
+        Node nd;
+        nd.a = make_float4(box[0], box[1], box[2], box[3]);
+        nd.b = make_float4(box[4], box[5], box[0], box[1]);
+        nd.c = make_float4(box[2], box[3], box[4], box[5]);
+        nd.d = make_int4(r, r, 0, 0);
+        U.nodes[0] = nd;
+    } else {
+        U.internal(0, 0);
+    }
+    if (!U.ok) {
+        delete b;
+        return fail(SBR_EINVAL, "invalid BVH: %s", U.why.c_str());
+    }
+    if (U.max_depth + 1 >= kStack) {
+        delete b;
+        return fail(SBR_EINVAL, "BVH depth %d exceeds the traversal stack (%d)", U.max_depth,
+                    kStack);
+    }
+    DevBuf<int> order(mesh->ntri);
+    cudaError_t e = order.status();
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(order.p, tri_order, sizeof(int) * mesh->ntri, cudaMemcpyHostToDevice,
+                            ctx->stream);
+    if (e == cudaSuccess)
+        e = pack_tris(mesh->verts.p, order.p, mesh->ntri, mesh->storage, b->out, ctx->stream,
+                      &ctx->launches);
+    if (e == cudaSuccess) e = b->out.leaf_ids.alloc(mesh->ntri);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(b->out.leaf_ids.p, order.p, sizeof(int) * mesh->ntri,
+                            cudaMemcpyDeviceToDevice, ctx->stream);
+    if (e == cudaSuccess) e = b->out.nodes.alloc(U.nodes.size());
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(b->out.nodes.p, U.nodes.data(), sizeof(Node) * U.nodes.size(),
+                            cudaMemcpyHostToDevice, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) {
+        delete b;
+        return fail(SBR_ECUDA, "BVH upload: %s", cudaGetErrorString(e));
+    }
+    b->out.nnodes = (int64_t)U.nodes.size();
+    b->out.n_leaf_slots = mesh->ntri;
+    b->out.root = 0;
+    b->out.max_depth = U.max_depth;
+    b->out.storage = mesh->storage;
+    *out = b;
+    return SBR_OK;
+}
+
+// ---- export to the reference preorder layout -------------------------------
+struct Exporter {
+    const std::vector<Node> &nodes;
+    const double *frame;
+    std::vector<double> nmin, nmax;
+    std::vector<int32_t> first, count;
+
+    static void box_of(const Node &n, int which, float b[6])
+    {
+        if (which == 0) {
+            b[0] = n.a.x; b[1] = n.a.y; b[2] = n.a.z; b[3] = n.a.w; b[4] = n.b.x; b[5] = n.b.y;
+        } else {
+            b[0] = n.b.z; b[1] = n.b.w; b[2] = n.c.x; b[3] = n.c.y; b[4] = n.c.z; b[5] = n.c.w;
+        }
+    }
+    int64_t emit_box(const float b[6], const float b2[6])
+    {
+        int64_t me = (int64_t)first.size();
+        for (int a = 0; a < 3; ++a) {
+            double lo = (double)b[a], hi = (double)b[3 + a];
+            if (b2) { lo = fmin(lo, (double)b2[a]); hi = fmax(hi, (double)b2[3 + a]); }
+            nmin.push_back(lo + frame[a]);
+            nmax.push_back(hi + frame[a]);
+        }
+        first.push_back(0);
+        count.push_back(0);
+        return me;
+    }
+    // preorder emit of reference `ref` with box b; returns node index
+    int64_t emit(int ref, const float b[6])
+    {
+        int64_t me = emit_box(b, nullptr);
+        if (ref < 0) {
+            first[me] = leaf_first(ref);
+            count[me] = leaf_count(ref);
+            return me;
+        }
+        const Node &n = nodes[ref];
+        float bl[6], br[6];
+        box_of(n, 0, bl);
+        box_of(n, 1, br);
+        emit(n.d.x, bl);
+        int64_t r = emit(n.d.y, br);
+        first[me] = (int32_t)r;
+        count[me] = 0;
+        return me;
+    }
+};
+
+static int export_tree(const sbr_bvh *b, std::vector<Node> &nodes, Exporter **ex)
+{
+    nodes.resize(b->out.nnodes);
+    CUDA_TRY(cudaMemcpy(nodes.data(), b->out.nodes.p, sizeof(Node) * nodes.size(),
+                        cudaMemcpyDeviceToHost));
+    Exporter *E = new Exporter{nodes, b->frame, {}, {}, {}, {}};
+    const Node &r = nodes[0];
+    float bl[6], br[6], root[6];
+    Exporter::box_of(r, 0, bl);
+    Exporter::box_of(r, 1, br);
+    for (int a = 0; a < 3; ++a) {
+        root[a] = fminf(bl[a], br[a]);
+        root[3 + a] = fmaxf(bl[3 + a], br[3 + a]);
+    }
+    if (r.d.x == r.d.y) {
+        E->emit(r.d.x, root);  // single-leaf tree
+    } else {
+        int64_t me = E->emit_box(root, nullptr);
+        E->emit(r.d.x, bl);
+        int64_t right = E->emit(r.d.y, br);
+        E->first[me] = (int32_t)right;
+        E->count[me] = 0;
+    }
+    *ex = E;
+    return SBR_OK;
+}
+
+extern "C" int sbr_bvh_info(const sbr_bvh *bvh, int64_t *nnodes_export, int64_t *nnodes_device,
+                            int32_t *max_depth)
+{
+    REQUIRE(bvh, "bvh is NULL");
+    if (nnodes_device) *nnodes_device = bvh->out.nnodes;
+    if (max_depth) *max_depth = bvh->out.max_depth + 1;
+    if (nnodes_export) {
+        if (int rc = set_device(bvh->ctx)) return rc;
+        std::vector<Node> nodes;
+        Exporter *E = nullptr;
+        if (int rc = export_tree(bvh, nodes, &E)) return rc;
+        *nnodes_export = (int64_t)E->first.size();
+        delete E;
+    }
+    return SBR_OK;
+}
+
+extern "C" int sbr_bvh_export(const sbr_bvh *bvh, double *nodes_min, double *nodes_max,
+                              int32_t *node_first, int32_t *node_count, int32_t *tri_order)
+{
+    REQUIRE(bvh && nodes_min && nodes_max && node_first && node_count && tri_order,
+            "NULL argument");
+    if (int rc = set_device(bvh->ctx)) return rc;
+    std::vector<Node> nodes;
+    Exporter *E = nullptr;
+    if (int rc = export_tree(bvh, nodes, &E)) return rc;
+    memcpy(nodes_min, E->nmin.data(), sizeof(double) * E->nmin.size());
+    memcpy(nodes_max, E->nmax.data(), sizeof(double) * E->nmax.size());
+    memcpy(node_first, E->first.data(), sizeof(int32_t) * E->first.size());
+    memcpy(node_count, E->count.data(), sizeof(int32_t) * E->count.size());
+    delete E;
+    CUDA_TRY(cudaMemcpy(tri_order, bvh->out.leaf_ids.p, sizeof(int32_t) * bvh->mesh->ntri,
+                        cudaMemcpyDeviceToHost));
+    return SBR_OK;
+}
+
+extern "C" int sbr_bvh_destroy(sbr_bvh *bvh)
+{
+    if (!bvh) return SBR_OK;
+    cudaSetDevice(bvh->ctx->device);
+    delete bvh;
+    return SBR_OK;
+}
+
+// ---------------------------------------------------------------------------
+// queries
+// ---------------------------------------------------------------------------
+static int check_pair(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *bvh)
+{
+    REQUIRE(ctx && mesh && bvh, "NULL handle");
+    REQUIRE(bvh->mesh == mesh, "BVH was built for a different mesh");
+    REQUIRE(mesh->ctx == ctx && bvh->ctx == ctx, "handles belong to another context");
+    return SBR_OK;
+}
+
+static TraceCfg make_cfg(const sbr_bvh *bvh, const sbr_trace_params *p, sbr_ctx *ctx)
+{
+    TraceCfg c;
+    c.B = bvh->view();
+    c.storage = bvh->mesh->storage;
+    c.max_bounces = p->max_bounces;
+    c.eps = p->eps;
+    c.strict = p->strict;
+    c.count_trapped = 0;
+    c.allow_aliasing = p->allow_aliasing;
+    c.spacing_limit = (p->lambda_min > 0.0 && p->sampling_factor > 0.0)
+                          ? p->lambda_min / p->sampling_factor
+                          : INFINITY;
+    c.error_flag = ctx->err_flag.p;
+    return c;
+}
+
+static int check_params(const sbr_trace_params *p)
+{
+    REQUIRE(p, "params is NULL");
+    REQUIRE(p->max_bounces >= 1, "max_bounces must be >= 1");
+    REQUIRE(p->max_bounces <= 0xffff, "max_bounces too large");
+    REQUIRE(p->eps > 0.0 && std::isfinite(p->eps), "epsilon must be positive");
+    return SBR_OK;
+}
+
+extern "C" int sbr_closest_hit(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *bvh,
+                               const double *origins, const double *dirs, int64_t n,
+                               double t_min, double t_max, int64_t *tri, double *t,
+                               int64_t *visits)
+{
+    if (int rc = check_pair(ctx, mesh, bvh)) return rc;
+    REQUIRE(n >= 0, "negative ray count");
+    if (n == 0) return SBR_OK;
+    REQUIRE(origins && dirs && tri && t, "NULL argument");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (int rc = set_device(ctx)) return rc;
+    DevBuf<double> o(3 * n), d(3 * n), tt(n);
+    DevBuf<int64_t> ti(n), vi(n);
+    CUDA_TRY(o.status()); CUDA_TRY(d.status()); CUDA_TRY(tt.status());
+    CUDA_TRY(ti.status()); CUDA_TRY(vi.status());
+    cudaStream_t st = ctx->stream;
+    CUDA_TRY(cudaMemcpyAsync(o.p, origins, 24 * n, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(d.p, dirs, 24 * n, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(launch_closest(bvh->view(), mesh->storage, o.p, d.p, n, t_min, t_max, ti.p, tt.p,
+                            vi.p, st, ctx->stats()));
+    CUDA_TRY(cudaMemcpyAsync(tri, ti.p, 8 * n, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(t, tt.p, 8 * n, cudaMemcpyDeviceToHost, st));
+    if (visits) CUDA_TRY(cudaMemcpyAsync(visits, vi.p, 8 * n, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return SBR_OK;
+}
+
+static int trace_full_common(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *bvh,
+                             const sbr_grid *grid, const double *origins, const double *dirs,
+                             int64_t n, const sbr_trace_params *params, uint8_t *valid,
+                             double *normal0, double *path, int32_t *bounces, uint8_t *escaped,
+                             double *out_dir, int32_t *tri_ids)
+{
+    if (int rc = check_pair(ctx, mesh, bvh)) return rc;
+    if (int rc = check_params(params)) return rc;
+    REQUIRE(valid && normal0 && path && bounces && escaped && out_dir, "NULL output");
+    if (n == 0) return SBR_OK;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (int rc = set_device(ctx)) return rc;
+    cudaStream_t st = ctx->stream;
+    const int B = params->max_bounces;
+    DevBuf<uint8_t> dv(n), de(n);
+    DevBuf<double> dn(3 * n), dp(n), dd(3 * n), o, d;
+    DevBuf<int32_t> db(n), di;
+    DevBuf<GridDev> dg;
+    CUDA_TRY(dv.status()); CUDA_TRY(de.status()); CUDA_TRY(dn.status()); CUDA_TRY(dp.status());
+    CUDA_TRY(dd.status()); CUDA_TRY(db.status());
+    if (tri_ids) CUDA_TRY(di.alloc((size_t)n * B));
+    if (grid) {
+        GridDev g;
+        for (int a = 0; a < 3; ++a) {
+            g.corner[a] = grid->corner[a]; g.u[a] = grid->u[a];
+            g.v[a] = grid->v[a]; g.k[a] = grid->k[a];
+        }
+        g.spacing = grid->spacing;
+        g.n_v = grid->n_v;
+        g.n_rays = n;
+        CUDA_TRY(dg.alloc(1));
+        CUDA_TRY(cudaMemcpyAsync(dg.p, &g, sizeof(g), cudaMemcpyHostToDevice, st));
+    } else {
+        CUDA_TRY(o.alloc(3 * n));
+        CUDA_TRY(d.alloc(3 * n));
+        CUDA_TRY(cudaMemcpyAsync(o.p, origins, 24 * n, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaMemcpyAsync(d.p, dirs, 24 * n, cudaMemcpyHostToDevice, st));
+    }
+    TraceCfg cfg = make_cfg(bvh, params, ctx);
+    FullOut fo{dv.p, dn.p, dp.p, db.p, de.p, dd.p, tri_ids ? di.p : nullptr};
+    CUDA_TRY(launch_trace_full(cfg, dg.p, o.p, d.p, n, fo, ctx->counter.p, st, ctx->stats()));
+    CUDA_TRY(cudaMemcpyAsync(valid, dv.p, n, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(escaped, de.p, n, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(normal0, dn.p, 24 * n, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(path, dp.p, 8 * n, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(out_dir, dd.p, 24 * n, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(bounces, db.p, 4 * n, cudaMemcpyDeviceToHost, st));
+    if (tri_ids)
+        CUDA_TRY(cudaMemcpyAsync(tri_ids, di.p, sizeof(int32_t) * n * B, cudaMemcpyDeviceToHost,
+                                 st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return SBR_OK;
+}
+
+extern "C" int sbr_trace_grid(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *bvh,
+                              const sbr_grid *grid, const sbr_trace_params *params,
+                              uint8_t *valid, double *normal0, double *path, int32_t *bounces,
+                              uint8_t *escaped, double *out_dir, int32_t *tri_ids)
+{
+    REQUIRE(grid, "grid is NULL");
+    REQUIRE(grid->n_u >= 1 && grid->n_v >= 1 && grid->spacing > 0.0, "invalid grid");
+    return trace_full_common(ctx, mesh, bvh, grid, nullptr, nullptr, grid->n_u * grid->n_v,
+                             params, valid, normal0, path, bounces, escaped, out_dir, tri_ids);
+}
+
+extern "C" int sbr_trace_rays(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *bvh,
+                              const double *origins, const double *dirs, int64_t n,
+                              const sbr_trace_params *params, uint8_t *valid, double *normal0,
+                              double *path, int32_t *bounces, uint8_t *escaped,
+                              double *out_dir, int32_t *tri_ids)
+{
+    REQUIRE(n >= 0, "negative ray count");
+    REQUIRE(n == 0 || (origins && dirs), "NULL rays");
+    return trace_full_common(ctx, mesh, bvh, nullptr, origins, dirs, n, params, valid, normal0,
+                             path, bounces, escaped, out_dir, tri_ids);
+}
+
+// ---------------------------------------------------------------------------
+// integrate + fused solve
+// ---------------------------------------------------------------------------
+static int64_t seg_count(int64_t n_rays) { return (n_rays + kSegRays - 1) / kSegRays; }
+static int64_t round_chunk(int64_t n) { return (n + kChunk - 1) / kChunk * kChunk; }
+
+extern "C" int sbr_segment_layout(const sbr_grid *grids, int32_t ngrids, int64_t *seg_base)
+{
+    REQUIRE(grids && seg_base && ngrids >= 0, "bad arguments");
+    seg_base[0] = 0;
+    for (int g = 0; g < ngrids; ++g)
+        seg_base[g + 1] = seg_base[g] + seg_count(grids[g].n_u * grids[g].n_v);
+    return SBR_OK;
+}
+
+// slots (16 B each) staged per batch; SBR_SLOT_BUDGET overrides (tests use
+// tiny budgets to prove results do not depend on batching)
+static int64_t slot_budget()
+{
+    const char *s = getenv("SBR_SLOT_BUDGET");
+    int64_t v = s ? atoll(s) : ((int64_t)1 << 25);
+    if (v < kChunk) v = kChunk;
+    return round_chunk(v);
+}
+
+// k (wavenumbers) -> device 2k table, and gamma^N host table (po.py:107
+// evaluates gamma ** N with libm pow: same as the host pow here).
+static int upload_freqs(sbr_ctx *ctx, const double *k, int nk, double gamma, int B)
+{
+    std::vector<double> k2(nk), gp(B + 1);
+    for (int f = 0; f < nk; ++f) k2[f] = 2.0 * k[f];
+    for (int b = 0; b <= B; ++b) gp[b] = pow(gamma, (double)b);
+    CUDA_TRY(ctx->k2.reserve(nk));
+    CUDA_TRY(ctx->gpow.reserve(B + 1));
+    CUDA_TRY(cudaMemcpyAsync(ctx->k2.p, k2.data(), 8 * nk, cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(ctx->gpow.p, gp.data(), 8 * (B + 1), cudaMemcpyHostToDevice,
+                             ctx->stream));
+    return SBR_OK;
+}
+
+// Runs the batched trace -> PO -> segment pipeline over `units` (all on
+// ctx->stream); writes segment partials into seg_dev and diagnostics into
+// diag_dev (both pre-zeroed by the caller).
+static int run_units(sbr_ctx *ctx, const sbr_bvh *bvh, const std::vector<UnitDev> &all_units,
+                     int nk, const TraceCfg &cfg, double2 *seg_dev, int64_t *diag_dev)
+{
+    cudaStream_t st = ctx->stream;
+    const int64_t budget = slot_budget();
+    size_t u0 = 0;
+    std::vector<UnitDev> batch;
+    while (u0 < all_units.size()) {
+        batch.clear();
+        int64_t slots = 0;
+        size_t u1 = u0;
+        while (u1 < all_units.size()) {
+            UnitDev u = all_units[u1];
+            int64_t need = round_chunk(u.ray_end - u.ray_begin);
+            if (!batch.empty() && slots + need > budget) break;
+            u.slot_base = slots;
+            slots += need;
+            batch.push_back(u);
+            ++u1;
+        }
+        CUDA_TRY(ctx->slots.reserve(slots));
+        CUDA_TRY(ctx->units.reserve(batch.size()));
+        CUDA_TRY(ctx->chunk_part.reserve((size_t)(slots / kChunk) * nk));
+        CUDA_TRY(cudaMemcpyAsync(ctx->units.p, batch.data(), sizeof(UnitDev) * batch.size(),
+                                 cudaMemcpyHostToDevice, st));
+        CUDA_TRY(launch_trace_solve(cfg, ctx->grids.p, ctx->units.p, (int)batch.size(), slots,
+                                    ctx->slots.p, ctx->counter.p, st, ctx->stats()));
+        CUDA_TRY(launch_po(ctx->slots.p, ctx->units.p, (int)batch.size(), slots / kChunk,
+                           ctx->k2.p, nk, ctx->gpow.p, cfg.max_bounces, ctx->chunk_part.p,
+                           diag_dev, ctx->bad.p, st, ctx->stats()));
+        CUDA_TRY(launch_seg_reduce(ctx->chunk_part.p, ctx->units.p, (int)batch.size(), nk,
+                                   seg_dev, st, ctx->stats()));
+        // the units buffer is rewritten by the next batch: keep batches ordered
+        CUDA_TRY(cudaStreamSynchronize(st));
+        u0 = u1;
+    }
+    return SBR_OK;
+}
+
+static int upload_grids(sbr_ctx *ctx, const sbr_grid *grids, int ngrids)
+{
+    std::vector<GridDev> g(ngrids);
+    for (int i = 0; i < ngrids; ++i) {
+        for (int a = 0; a < 3; ++a) {
+            g[i].corner[a] = grids[i].corner[a]; g[i].u[a] = grids[i].u[a];
+            g[i].v[a] = grids[i].v[a]; g[i].k[a] = grids[i].k[a];
+        }
+        g[i].spacing = grids[i].spacing;
+        g[i].n_v = grids[i].n_v;
+        g[i].n_rays = grids[i].n_u * grids[i].n_v;
+    }
+    CUDA_TRY(ctx->grids.reserve(ngrids));
+    CUDA_TRY(cudaMemcpyAsync(ctx->grids.p, g.data(), sizeof(GridDev) * ngrids,
+                             cudaMemcpyHostToDevice, ctx->stream));
+    return SBR_OK;
+}
+
+static int check_grids(const sbr_grid *grids, int ngrids)
+{
+    REQUIRE(grids && ngrids >= 1, "no grids");
+    for (int g = 0; g < ngrids; ++g) {
+        REQUIRE(grids[g].n_u >= 1 && grids[g].n_v >= 1, "grid %d: empty", g);
+        REQUIRE(grids[g].spacing > 0.0 && grids[g].cell_area > 0.0, "grid %d: bad spacing", g);
+    }
+    return SBR_OK;
+}
+
+static int check_sampling(const sbr_grid *grids, int ngrids, const sbr_trace_params *p)
+{
+    if (p->allow_aliasing || !(p->lambda_min > 0.0)) return SBR_OK;
+    const double limit = p->lambda_min / p->sampling_factor;
+    for (int g = 0; g < ngrids; ++g)
+        REQUIRE(grids[g].spacing <= limit,
+                "ray spacing %g exceeds wavelength/%g = %g (ratio %.3f); pass allow_aliasing "
+                "to override",
+                grids[g].spacing, p->sampling_factor, limit,
+                grids[g].spacing * p->sampling_factor / p->lambda_min);
+    return SBR_OK;
+}
+
+static int solve_shard_locked(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *bvh,
+                              const sbr_grid *grids, int32_t ngrids,
+                              const sbr_trace_params *params, const double *k, int32_t nk,
+                              double gamma, int32_t count_trapped, int32_t rank, int32_t nranks,
+                              int32_t shard_mode, double2 *seg_dev, int64_t *diag_dev)
+{
+    cudaStream_t st = ctx->stream;
+    std::vector<int64_t> seg_base(ngrids + 1);
+    sbr_segment_layout(grids, ngrids, seg_base.data());
+    const int B = params->max_bounces;
+    const int64_t dstride = 3 + B + 1;
+    CUDA_TRY(cudaMemsetAsync(seg_dev, 0, sizeof(double2) * seg_base[ngrids] * nk, st));
+    CUDA_TRY(cudaMemsetAsync(diag_dev, 0, sizeof(int64_t) * ngrids * dstride, st));
+    CUDA_TRY(cudaMemsetAsync(ctx->err_flag.p, 0, sizeof(unsigned int), st));
+    CUDA_TRY(cudaMemsetAsync(ctx->bad.p, 0xff, sizeof(unsigned long long), st));
+    if (int rc = upload_grids(ctx, grids, ngrids)) return rc;
+    if (int rc = upload_freqs(ctx, k, nk, gamma, B)) return rc;
+    std::vector<UnitDev> units;
+    int64_t uidx = 0;
+    for (int g = 0; g < ngrids; ++g) {
+        const int64_t n = grids[g].n_u * grids[g].n_v;
+        for (int64_t s = 0; s < seg_base[g + 1] - seg_base[g]; ++s, ++uidx) {
+            const int owner = shard_mode == 0 ? (g % nranks) : (int)(uidx % nranks);
+            if (owner != rank) continue;
+            UnitDev u;
+            u.grid = g;
+            u.seg = (int)s;
+            u.ray_begin = s * kSegRays;
+            u.ray_end = std::min(n, (s + 1) * kSegRays);
+            u.slot_base = 0;
+            u.seg_out = seg_base[g] + s;
+            units.push_back(u);
+        }
+    }
+    TraceCfg cfg = make_cfg(bvh, params, ctx);
+    cfg.count_trapped = count_trapped;
+    if (int rc = run_units(ctx, bvh, units, nk, cfg, seg_dev, diag_dev)) return rc;
+    unsigned int flag = 0;
+    unsigned long long bad = 0;
+    CUDA_TRY(cudaMemcpyAsync(&flag, ctx->err_flag.p, sizeof(flag), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(&bad, ctx->bad.p, sizeof(bad), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (flag & 1u) return fail(SBR_EINVAL, "device launcher: ray spacing violates the sampling rule");
+    if (bad != ~0ULL)
+        return fail(SBR_ENUMERIC, "non-finite contribution at record index %llu", bad);
+    return SBR_OK;
+}
+
+static int validate_solve(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *bvh,
+                          const sbr_grid *grids, int32_t ngrids, const sbr_trace_params *params,
+                          const double *k, int32_t nk, double gamma)
+{
+    if (int rc = check_pair(ctx, mesh, bvh)) return rc;
+    if (int rc = check_params(params)) return rc;
+    if (int rc = check_grids(grids, ngrids)) return rc;
+    REQUIRE(k && nk >= 1, "need at least one wavenumber");
+    for (int f = 0; f < nk; ++f) REQUIRE(k[f] > 0.0 && std::isfinite(k[f]), "bad wavenumber");
+    REQUIRE(std::fabs(gamma) <= 1.0, "|gamma| must be <= 1");
+    return check_sampling(grids, ngrids, params);
+}
+
+extern "C" int sbr_solve_shard(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *bvh,
+                               const sbr_grid *grids, int32_t ngrids,
+                               const sbr_trace_params *params, const double *k, int32_t nk,
+                               double gamma, int32_t count_trapped, int32_t rank,
+                               int32_t nranks, int32_t shard_mode, double *seg_dev,
+                               int64_t *diag_dev)
+{
+    if (int rc = validate_solve(ctx, mesh, bvh, grids, ngrids, params, k, nk, gamma)) return rc;
+    REQUIRE(nranks >= 1 && rank >= 0 && rank < nranks, "bad rank %d / %d", rank, nranks);
+    REQUIRE(shard_mode == 0 || shard_mode == 1, "bad shard_mode");
+    REQUIRE(seg_dev && diag_dev, "NULL device buffers");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (int rc = set_device(ctx)) return rc;
+    return solve_shard_locked(ctx, mesh, bvh, grids, ngrids, params, k, nk, gamma, count_trapped,
+                              rank, nranks, shard_mode, (double2 *)seg_dev, diag_dev);
+}
+
+static int finalize_locked(sbr_ctx *ctx, const sbr_grid *grids, int32_t ngrids, const double *k,
+                           int32_t nk, int32_t B, const double2 *seg_dev, const int64_t *diag_dev,
+                           double *amp, sbr_diag *diag)
+{
+    cudaStream_t st = ctx->stream;
+    std::vector<int64_t> seg_base(ngrids + 1);
+    sbr_segment_layout(grids, ngrids, seg_base.data());
+    std::vector<double> scale((size_t)ngrids * nk);
+    for (int g = 0; g < ngrids; ++g)
+        for (int f = 0; f < nk; ++f)
+            scale[(size_t)g * nk + f] = k[f] * grids[g].cell_area / (4.0 * M_PI);
+    CUDA_TRY(ctx->seg_base.reserve(ngrids + 1));
+    CUDA_TRY(ctx->scale.reserve(scale.size()));
+    CUDA_TRY(ctx->amp.reserve(scale.size()));
+    CUDA_TRY(cudaMemcpyAsync(ctx->seg_base.p, seg_base.data(), 8 * (ngrids + 1),
+                             cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(ctx->scale.p, scale.data(), 8 * scale.size(), cudaMemcpyHostToDevice,
+                             st));
+    CUDA_TRY(launch_finalize(seg_dev, ctx->seg_base.p, ngrids, nk, ctx->scale.p, ctx->amp.p, st,
+                             ctx->stats()));
+    CUDA_TRY(cudaMemcpyAsync(amp, ctx->amp.p, sizeof(double2) * scale.size(),
+                             cudaMemcpyDeviceToHost, st));
+    const int64_t dstride = 3 + B + 1;
+    std::vector<int64_t> dg((size_t)ngrids * dstride);
+    CUDA_TRY(cudaMemcpyAsync(dg.data(), diag_dev, 8 * dg.size(), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (diag) {
+        for (int g = 0; g < ngrids; ++g) {
+            const int64_t *row = dg.data() + (size_t)g * dstride;
+            if (diag->valid_rays) diag->valid_rays[g] = row[0];
+            if (diag->queries) diag->queries[g] = row[1];
+            if (diag->max_bounce) diag->max_bounce[g] = (int32_t)row[2];
+            if (diag->hist)
+                for (int b = 0; b <= B; ++b) diag->hist[(size_t)g * (B + 1) + b] = row[3 + b];
+        }
+    }
+    return SBR_OK;
+}
+
+extern "C" int sbr_finalize(sbr_ctx *ctx, const sbr_grid *grids, int32_t ngrids,
+                            const double *k, int32_t nk, int32_t max_bounces,
+                            const double *seg_dev, const int64_t *diag_dev, double *amp,
+                            sbr_diag *diag)
+{
+    REQUIRE(ctx && amp && seg_dev && diag_dev, "NULL argument");
+    if (int rc = check_grids(grids, ngrids)) return rc;
+    REQUIRE(k && nk >= 1, "need at least one wavenumber");
+    REQUIRE(max_bounces >= 1, "max_bounces must be >= 1");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (int rc = set_device(ctx)) return rc;
+    return finalize_locked(ctx, grids, ngrids, k, nk, max_bounces, (const double2 *)seg_dev,
+                           diag_dev, amp, diag);
+}
+
+extern "C" int sbr_solve(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *bvh,
+                         const sbr_grid *grids, int32_t ngrids, const sbr_trace_params *params,
+                         const double *k, int32_t nk, double gamma, int32_t count_trapped,
+                         double *amp, sbr_diag *diag)
+{
+    if (int rc = validate_solve(ctx, mesh, bvh, grids, ngrids, params, k, nk, gamma)) return rc;
+    REQUIRE(amp, "amp is NULL");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (int rc = set_device(ctx)) return rc;
+    std::vector<int64_t> seg_base(ngrids + 1);
+    sbr_segment_layout(grids, ngrids, seg_base.data());
+    const int B = params->max_bounces;
+    CUDA_TRY(ctx->seg_part.reserve((size_t)seg_base[ngrids] * nk));
+    CUDA_TRY(ctx->diag.reserve((size_t)ngrids * (3 + B + 1)));
+    if (int rc = solve_shard_locked(ctx, mesh, bvh, grids, ngrids, params, k, nk, gamma,
+                                    count_trapped, 0, 1, 0, ctx->seg_part.p, ctx->diag.p))
+        return rc;
+    return finalize_locked(ctx, grids, ngrids, k, nk, B, ctx->seg_part.p, ctx->diag.p, amp, diag);
+}
+
+extern "C" int sbr_accumulate(sbr_ctx *ctx, const uint8_t *valid, const double *normal0,
+                              const double *path, const int32_t *bounces, const uint8_t *escaped,
+                              int64_t n, const double k_inc[3], const double *k, int32_t nk,
+                              double cell_area, double gamma, int32_t count_trapped, double *amp,
+                              int64_t *bad_index)
+{
+    REQUIRE(ctx && amp && k_inc && k && nk >= 1, "NULL argument");
+    REQUIRE(n >= 0, "negative record count");
+    REQUIRE(cell_area > 0.0, "cell_area must be positive");
+    REQUIRE(std::fabs(gamma) <= 1.0, "|gamma| must be <= 1");
+    if (bad_index) *bad_index = -1;
+    if (n == 0) {
+        for (int f = 0; f < 2 * nk; ++f) amp[f] = 0.0;
+        return SBR_OK;
+    }
+    REQUIRE(valid && normal0 && path && bounces && escaped, "NULL records");
+    int maxb = 0;
+    for (int64_t r = 0; r < n; ++r) {
+        REQUIRE(bounces[r] >= 0 && bounces[r] <= 0xffff, "bounce count out of range at %lld",
+                (long long)r);
+        maxb = std::max(maxb, (int)bounces[r]);
+    }
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (int rc = set_device(ctx)) return rc;
+    cudaStream_t st = ctx->stream;
+    const int64_t nseg = seg_count(n);
+    const int64_t n_slots = nseg * kSegRays;  // one unit per segment
+    std::vector<UnitDev> units(nseg);
+    int64_t slots_used = 0;
+    for (int64_t s = 0; s < nseg; ++s) {
+        units[s].grid = 0;
+        units[s].seg = (int)s;
+        units[s].ray_begin = s * kSegRays;
+        units[s].ray_end = std::min(n, (s + 1) * kSegRays);
+        units[s].slot_base = s * kSegRays;
+        units[s].seg_out = s;
+        slots_used = units[s].slot_base + round_chunk(units[s].ray_end - units[s].ray_begin);
+    }
+    (void)n_slots;
+    DevBuf<uint8_t> dv(n), de(n);
+    DevBuf<double> dn(3 * n), dp(n);
+    DevBuf<int32_t> db(n);
+    CUDA_TRY(dv.status()); CUDA_TRY(de.status()); CUDA_TRY(dn.status()); CUDA_TRY(dp.status());
+    CUDA_TRY(db.status());
+    CUDA_TRY(cudaMemcpyAsync(dv.p, valid, n, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(de.p, escaped, n, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(dn.p, normal0, 24 * n, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(dp.p, path, 8 * n, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(db.p, bounces, 4 * n, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(ctx->slots.reserve(slots_used));
+    CUDA_TRY(ctx->units.reserve(nseg));
+    CUDA_TRY(ctx->chunk_part.reserve((size_t)(slots_used / kChunk) * nk));
+    CUDA_TRY(ctx->seg_part.reserve((size_t)nseg * nk));
+    CUDA_TRY(ctx->diag.reserve(3 + maxb + 1));
+    CUDA_TRY(cudaMemsetAsync(ctx->diag.p, 0, 8 * (3 + maxb + 1), st));
+    CUDA_TRY(cudaMemsetAsync(ctx->bad.p, 0xff, sizeof(unsigned long long), st));
+    CUDA_TRY(cudaMemcpyAsync(ctx->units.p, units.data(), sizeof(UnitDev) * nseg,
+                             cudaMemcpyHostToDevice, st));
+    if (int rc = upload_freqs(ctx, k, nk, gamma, maxb)) return rc;
+    CUDA_TRY(launch_records_to_slots(dv.p, dn.p, dp.p, db.p, de.p, n, k_inc[0], k_inc[1],
+                                     k_inc[2], count_trapped, slots_used, ctx->slots.p, st,
+                                     ctx->stats()));
+    CUDA_TRY(launch_po(ctx->slots.p, ctx->units.p, (int)nseg, slots_used / kChunk, ctx->k2.p, nk,
+                       ctx->gpow.p, maxb, ctx->chunk_part.p, ctx->diag.p, ctx->bad.p, st,
+                       ctx->stats()));
+    CUDA_TRY(launch_seg_reduce(ctx->chunk_part.p, ctx->units.p, (int)nseg, nk, ctx->seg_part.p, st,
+                               ctx->stats()));
+    sbr_grid g;
+    memset(&g, 0, sizeof(g));
+    g.n_u = n;
+    g.n_v = 1;
+    g.spacing = 1.0;
+    g.cell_area = cell_area;
+    unsigned long long bad = 0;
+    CUDA_TRY(cudaMemcpyAsync(&bad, ctx->bad.p, sizeof(bad), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (bad != ~0ULL) {
+        if (bad_index) *bad_index = (int64_t)bad;
+        return fail(SBR_ENUMERIC, "non-finite contribution at record index %llu", bad);
+    }
+    return finalize_locked(ctx, &g, 1, k, nk, maxb, ctx->seg_part.p, ctx->diag.p, amp, nullptr);
+}
+
+// ---------------------------------------------------------------------------
+// scalar predicates
+// ---------------------------------------------------------------------------
+extern "C" int sbr_tri_hit_pairs(sbr_ctx *ctx, const double *v0, const double *v1,
+                                 const double *v2, const double *origins, const double *dirs,
+                                 int64_t n, double t_min, double t_max, int32_t single,
+                                 double *t)
+{
+    REQUIRE(ctx, "ctx is NULL");
+    REQUIRE(n >= 0, "negative count");
+    if (n == 0) return SBR_OK;
+    REQUIRE(v0 && v1 && v2 && origins && dirs && t, "NULL argument");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (int rc = set_device(ctx)) return rc;
+    cudaStream_t st = ctx->stream;
+    DevBuf<double> a(3 * n), b(3 * n), c(3 * n), o(3 * n), d(3 * n), tt(n);
+    CUDA_TRY(a.status()); CUDA_TRY(b.status()); CUDA_TRY(c.status());
+    CUDA_TRY(o.status()); CUDA_TRY(d.status()); CUDA_TRY(tt.status());
+    CUDA_TRY(cudaMemcpyAsync(a.p, v0, 24 * n, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(b.p, v1, 24 * n, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(c.p, v2, 24 * n, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(o.p, origins, 24 * n, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(d.p, dirs, 24 * n, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(launch_tri_pairs(a.p, b.p, c.p, o.p, d.p, n, t_min, t_max, single, tt.p, st,
+                              ctx->stats()));
+    CUDA_TRY(cudaMemcpyAsync(t, tt.p, 8 * n, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return SBR_OK;
+}
+
+extern "C" int sbr_aabb_hit_pairs(sbr_ctx *ctx, const double *box_min, const double *box_max,
+                                  const double *origins, const double *dir_inv, int64_t n,
+                                  double t_max, uint8_t *hit, double *entry)
+{
+    REQUIRE(ctx, "ctx is NULL");
+    REQUIRE(n >= 0, "negative count");
+    if (n == 0) return SBR_OK;
+    REQUIRE(box_min && box_max && origins && dir_inv && hit && entry, "NULL argument");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (int rc = set_device(ctx)) return rc;
+    cudaStream_t st = ctx->stream;
+    DevBuf<double> lo(3 * n), hi(3 * n), o(3 * n), iv(3 * n), en(n);
+    DevBuf<uint8_t> h(n);
+    CUDA_TRY(lo.status()); CUDA_TRY(hi.status()); CUDA_TRY(o.status());
+    CUDA_TRY(iv.status()); CUDA_TRY(en.status()); CUDA_TRY(h.status());
+    CUDA_TRY(cudaMemcpyAsync(lo.p, box_min, 24 * n, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(hi.p, box_max, 24 * n, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(o.p, origins, 24 * n, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(iv.p, dir_inv, 24 * n, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(launch_box_pairs(lo.p, hi.p, o.p, iv.p, n, t_max, h.p, en.p, st, ctx->stats()));
+    CUDA_TRY(cudaMemcpyAsync(hit, h.p, n, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(entry, en.p, 8 * n, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return SBR_OK;
+}

@@ -1,0 +1,689 @@
+// pipeline.cu -- the hot path: ray launch + multi-bounce traversal,
+// warp-ballot compaction + physical-optics integral, deterministic reduce.
+//
+//   k_trace_solve  persistent warps fetch 32-ray work items with one atomic
+//                  per warp; each lane computes its ray origin on the fly
+//                  from the grid scalars (transport.py:339-345, no record of
+//                  the launch is materialised), walks up to B bounces
+//                  (transport.py:276-327) and stores a 16-byte SlotRec.
+//   k_po           one block per 2048-slot chunk: coalesced SlotRec loads,
+//                  warp __ballot_sync + popc + block scan compact the
+//                  selected records (po.py:96-101) into shared memory in
+//                  slot order, then evaluates (po.py:105-108)
+//                    term_f = j k_f dA/4pi * 2 cos Gamma^N exp(-2j k_f R)
+//                  for nk wavenumbers: phase reduced mod 2pi in FP64,
+//                  FP32 __sincosf on the SFU, FP64 accumulation, warp
+//                  shuffle tree then a fixed cross-warp order.
+//   k_seg_reduce / k_finalize  fixed pairwise trees (po.py:59-80 shape)
+//                  over chunk -> segment -> grid partials: results are
+//                  bit-stable and independent of GPU count.
+#include "pipeline.h"
+#include "traverse.cuh"
+
+namespace sbr {
+
+// ---------------------------------------------------------------------------
+// helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int find_unit(const UnitDev *u, int n, int64_t slot)
+{
+    int lo = 0, hi = n - 1;
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (__ldg(&u[mid].slot_base) <= slot) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ void grid_origin(const GridDev &g, int64_t r, double &ox,
+                                            double &oy, double &oz)
+{
+    int64_t i = r / g.n_v, j = r - i * g.n_v;
+    double si = DM(DA((double)i, 0.5), g.spacing);
+    double sj = DM(DA((double)j, 0.5), g.spacing);
+    double bx = DA(g.corner[0], DM(si, g.u[0]));
+    double by = DA(g.corner[1], DM(si, g.u[1]));
+    double bz = DA(g.corner[2], DM(si, g.u[2]));
+    ox = DA(bx, DM(sj, g.v[0]));
+    oy = DA(by, DM(sj, g.v[1]));
+    oz = DA(bz, DM(sj, g.v[2]));
+}
+
+__device__ __forceinline__ int64_t warp_fetch(unsigned long long *counter)
+{
+    unsigned long long item = 0;
+    if ((threadIdx.x & 31) == 0) item = atomicAdd(counter, 1ULL);
+    return (int64_t)__shfl_sync(0xffffffffu, item, 0);
+}
+
+// ---------------------------------------------------------------------------
+// trace kernels
+// ---------------------------------------------------------------------------
+constexpr int kTraceThreads = 128;
+
+template <int STORAGE>
+__global__ void __launch_bounds__(kTraceThreads)
+k_trace_solve(TraceCfg cfg, const GridDev *__restrict__ grids,
+              const UnitDev *__restrict__ units, int n_units, int64_t n_items,
+              SlotRec *__restrict__ slots, unsigned long long *counter)
+{
+    const int lane = threadIdx.x & 31;
+    while (true) {
+        const int64_t item = warp_fetch(counter);
+        if (item >= n_items) break;
+        const int64_t slot = item * 32 + lane;
+        const int ui = find_unit(units, n_units, item * 32);
+        const UnitDev U = units[ui];
+        const int64_t r = U.ray_begin + (slot - U.slot_base);
+        const GridDev &G = grids[U.grid];
+        // anti-aliasing launch rule, spacing <= lambda_min / factor
+        // (transport.py:75-81, inclusive); violating grids launch nothing
+        const bool alias_ok = cfg.allow_aliasing || !(G.spacing > cfg.spacing_limit);
+        if (!alias_ok && lane == 0) atomicOr(cfg.error_flag, 1u);
+        SlotRec rec;
+        rec.R = 0.0; rec.cosv = 0.f; rec.meta = 0u;
+        if (r < U.ray_end && alias_ok) {
+            double ox, oy, oz;
+            grid_origin(G, r, ox, oy, oz);
+            const double kx = G.k[0], ky = G.k[1], kz = G.k[2];
+            int visits = 0;
+            RayResult res = trace_ray_walk<STORAGE>(cfg.B, ox, oy, oz, kx, ky, kz,
+                                                    cfg.max_bounces, cfg.eps,
+                                                    cfg.strict != 0, nullptr, visits);
+            double c = -DA(DA(DM(res.n0x, kx), DM(res.n0y, ky)), DM(res.n0z, kz));
+            bool sel = res.valid && (res.escaped || cfg.count_trapped) && c > 0.0;
+            rec.R = res.path;
+            rec.cosv = (float)c;
+            rec.meta = (uint32_t)res.bounces | kMetaActive | (res.valid ? kMetaValid : 0u) |
+                       (res.escaped ? kMetaEscaped : 0u) | (sel ? kMetaSel : 0u);
+        }
+        slots[slot] = rec;
+    }
+}
+
+template <int STORAGE, bool GRID>
+__global__ void __launch_bounds__(kTraceThreads)
+k_trace_full(TraceCfg cfg, const GridDev *__restrict__ grid,
+             const double *__restrict__ orig, const double *__restrict__ dirs, int64_t n,
+             FullOut out, unsigned long long *counter)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t n_items = (n + 31) / 32;
+    while (true) {
+        const int64_t item = warp_fetch(counter);
+        if (item >= n_items) break;
+        const int64_t r = item * 32 + lane;
+        if (r >= n) continue;  // lanes re-converge at the next warp_fetch
+        double ox, oy, oz, dx, dy, dz;
+        if (GRID) {
+            grid_origin(*grid, r, ox, oy, oz);
+            dx = grid->k[0]; dy = grid->k[1]; dz = grid->k[2];
+        } else {
+            ox = orig[3 * r]; oy = orig[3 * r + 1]; oz = orig[3 * r + 2];
+            dx = dirs[3 * r]; dy = dirs[3 * r + 1]; dz = dirs[3 * r + 2];
+        }
+        int *ids = nullptr;
+        if (out.ids) {
+            ids = out.ids + r * (int64_t)cfg.max_bounces;
+            for (int b = 0; b < cfg.max_bounces; ++b) ids[b] = -1;
+        }
+        int visits = 0;
+        RayResult res = trace_ray_walk<STORAGE>(cfg.B, ox, oy, oz, dx, dy, dz,
+                                                cfg.max_bounces, cfg.eps, cfg.strict != 0,
+                                                ids, visits);
+        out.valid[r] = res.valid ? 1 : 0;
+        out.escaped[r] = res.escaped ? 1 : 0;
+        out.bounces[r] = res.bounces;
+        out.path[r] = res.path;
+        out.n0[3 * r] = res.n0x; out.n0[3 * r + 1] = res.n0y; out.n0[3 * r + 2] = res.n0z;
+        out.out_dir[3 * r] = res.dx; out.out_dir[3 * r + 1] = res.dy;
+        out.out_dir[3 * r + 2] = res.dz;
+    }
+}
+
+template <int STORAGE>
+__global__ void __launch_bounds__(kTraceThreads)
+k_closest(BvhView B, const double *__restrict__ orig, const double *__restrict__ dirs,
+          int64_t n, double t_min, double t_max, int64_t *__restrict__ tri,
+          double *__restrict__ t_out, int64_t *__restrict__ visits_out)
+{
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        double t = t_max;
+        int visits = 0;
+        int id = closest_hit<STORAGE, false>(B, orig[3 * r], orig[3 * r + 1], orig[3 * r + 2],
+                                             dirs[3 * r], dirs[3 * r + 1], dirs[3 * r + 2],
+                                             t_min, t, visits);
+        tri[r] = id;
+        t_out[r] = t;
+        visits_out[r] = visits;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// records -> slots (sbr_accumulate on host HitRecords)
+// ---------------------------------------------------------------------------
+__global__ void k_records_to_slots(const uint8_t *__restrict__ valid,
+                                   const double *__restrict__ n0,
+                                   const double *__restrict__ path,
+                                   const int32_t *__restrict__ bounces,
+                                   const uint8_t *__restrict__ escaped, int64_t n, double kx,
+                                   double ky, double kz, int count_trapped, int64_t n_slots,
+                                   SlotRec *__restrict__ slots)
+{
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_slots;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        SlotRec rec;
+        rec.R = 0.0; rec.cosv = 0.f; rec.meta = 0u;
+        if (r < n) {
+            bool v = valid[r] != 0, e = escaped[r] != 0;
+            double c = -DA(DA(DM(n0[3 * r], kx), DM(n0[3 * r + 1], ky)), DM(n0[3 * r + 2], kz));
+            bool sel = v && (e || count_trapped) && c > 0.0;
+            int b = bounces[r];
+            rec.R = path[r];
+            rec.cosv = (float)c;
+            rec.meta = ((uint32_t)b & kMetaBounceMask) | kMetaActive | (v ? kMetaValid : 0u) |
+                       (e ? kMetaEscaped : 0u) | (sel ? kMetaSel : 0u);
+        }
+        slots[r] = rec;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// compaction + PO
+// ---------------------------------------------------------------------------
+constexpr int kPoThreads = 256;
+constexpr int kPoWarps = kPoThreads / 32;
+constexpr int kPerThread = kChunk / kPoThreads;   // 8
+constexpr int kMaxHist = 64;                      // bounce histogram bins in smem
+
+__constant__ double c_two_pi_hi = 6.283185307179586;
+__constant__ double c_two_pi_lo = 2.4492935982947064e-16;
+__constant__ double c_inv_two_pi = 0.15915494309189535;
+
+template <int FPT>
+__global__ void __launch_bounds__(kPoThreads)
+k_po(const SlotRec *__restrict__ slots, const UnitDev *__restrict__ units, int n_units,
+     const double *__restrict__ k2, int nk, const double *__restrict__ gpow, int max_bounces,
+     double2 *__restrict__ chunk_part, int64_t *__restrict__ diag,
+     unsigned long long *__restrict__ bad)
+{
+    __shared__ double2 srec[kChunk];                 // compacted (R, w)
+    __shared__ int wcount[kPerThread][kPoWarps];
+    __shared__ int wbase[kPerThread][kPoWarps];
+    __shared__ int s_total;
+    __shared__ unsigned long long s_hist[kMaxHist];
+    __shared__ unsigned long long s_valid, s_queries;
+    __shared__ unsigned int s_maxb;
+    __shared__ double2 red[kPoWarps][FPT];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t chunk = blockIdx.x;
+    const int64_t slot0 = chunk * kChunk;
+    const int ui = find_unit(units, n_units, slot0);
+    const UnitDev U = units[ui];
+    const int nb = max_bounces + 1;
+    const int64_t dstride = 3 + nb;
+
+    if (tid < kMaxHist) s_hist[tid] = 0ULL;
+    if (tid == 0) { s_valid = 0ULL; s_queries = 0ULL; s_maxb = 0u; }
+
+    // ---- load + ballot ----
+    SlotRec rec[kPerThread];
+    unsigned selmask = 0;
+    unsigned long long my_q = 0;
+    unsigned my_maxb = 0;
+    int my_valid = 0;
+#pragma unroll
+    for (int q = 0; q < kPerThread; ++q) {
+        const SlotRec r = slots[slot0 + q * kPoThreads + tid];
+        rec[q] = r;
+        const bool sel = (r.meta & kMetaSel) != 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, sel);
+        if (lane == 0) wcount[q][warp] = __popc(bal);
+        if (sel) selmask |= 1u << q;
+        if (r.meta & kMetaActive) {
+            const unsigned b = r.meta & kMetaBounceMask;
+            my_q += b + 1;
+            my_maxb = max(my_maxb, b);
+        }
+        if (r.meta & kMetaValid) ++my_valid;
+    }
+    __syncthreads();
+    // exclusive scan over (q, warp) in slot order
+    if (warp == 0) {
+        int carry = 0;
+        for (int base = 0; base < kPerThread * kPoWarps; base += 32) {
+            const int idx = base + lane;
+            const int v = idx < kPerThread * kPoWarps ? (&wcount[0][0])[idx] : 0;
+            int incl = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (idx < kPerThread * kPoWarps) (&wbase[0][0])[idx] = carry + incl - v;
+            carry += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (lane == 0) s_total = carry;
+    }
+    __syncthreads();
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int q = 0; q < kPerThread; ++q) {
+        const bool sel = (selmask >> q) & 1u;
+        const unsigned bal = __ballot_sync(0xffffffffu, sel);
+        if (sel) {
+            const SlotRec r = rec[q];
+            const int pos = wbase[q][warp] + __popc(bal & lt);
+            const unsigned b = r.meta & kMetaBounceMask;
+            const double w = 2.0 * (double)r.cosv * gpow[b];
+            srec[pos] = make_double2(r.R, w);
+            if (!isfinite(r.R) || !isfinite(w)) {
+                const int64_t ridx = U.ray_begin + (slot0 - U.slot_base) + q * kPoThreads + tid;
+                atomicMin(bad, (unsigned long long)ridx);
+            }
+        }
+        if (rec[q].meta & kMetaValid) {
+            const unsigned b = rec[q].meta & kMetaBounceMask;
+            if (b < (unsigned)kMaxHist) atomicAdd(&s_hist[b], 1ULL);
+            else if (diag) atomicAdd((unsigned long long *)&diag[(int64_t)U.grid * dstride + 3 + b], 1ULL);
+        }
+    }
+    // diagnostics: warp reductions then one atomic per warp
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        my_q += __shfl_xor_sync(0xffffffffu, my_q, o);
+        my_valid += __shfl_xor_sync(0xffffffffu, my_valid, o);
+        my_maxb = max(my_maxb, __shfl_xor_sync(0xffffffffu, my_maxb, o));
+    }
+    if (lane == 0) {
+        atomicAdd(&s_queries, my_q);
+        atomicAdd(&s_valid, (unsigned long long)my_valid);
+        atomicMax(&s_maxb, my_maxb);
+    }
+    __syncthreads();
+    if (diag) {
+        int64_t *dg = diag + (int64_t)U.grid * dstride;
+        if (tid == 0) {
+            if (s_valid) atomicAdd((unsigned long long *)&dg[0], s_valid);
+            atomicAdd((unsigned long long *)&dg[1], s_queries);
+            atomicMax((unsigned long long *)&dg[2], (unsigned long long)s_maxb);
+        }
+        if (tid < nb && tid < kMaxHist && s_hist[tid])
+            atomicAdd((unsigned long long *)&dg[3 + tid], s_hist[tid]);
+    }
+
+    // ---- PO terms ----
+    const int M = s_total;
+    const int G = (nk + FPT - 1) / FPT;        // frequency groups
+    const int wpg = G >= kPoWarps ? 1 : kPoWarps / G;   // warps per group
+    const int passes = (G + kPoWarps - 1) / kPoWarps;
+    for (int pass = 0; pass < passes; ++pass) {
+        int grp, sub;
+        if (G >= kPoWarps) { grp = pass * kPoWarps + warp; sub = 0; }
+        else { grp = warp / wpg; sub = warp % wpg; }
+        const bool active = grp < G && (G >= kPoWarps || warp < G * wpg);
+        double sacc[FPT], cacc[FPT], kk[FPT];
+#pragma unroll
+        for (int f = 0; f < FPT; ++f) {
+            sacc[f] = 0.0; cacc[f] = 0.0;
+            const int fi = grp * FPT + f;
+            kk[f] = (active && fi < nk) ? k2[fi] : 0.0;
+        }
+        if (active) {
+            for (int m = sub * 32 + lane; m < M; m += wpg * 32) {
+                const double2 rw = srec[m];
+#pragma unroll
+                for (int f = 0; f < FPT; ++f) {
+                    const double ph = kk[f] * rw.x;
+                    const double nn = rint(ph * c_inv_two_pi);
+                    double rr = fma(-nn, c_two_pi_hi, ph);
+                    rr = fma(-nn, c_two_pi_lo, rr);
+                    float s, c;
+                    __sincosf((float)rr, &s, &c);
+                    sacc[f] = fma(rw.y, (double)s, sacc[f]);
+                    cacc[f] = fma(rw.y, (double)c, cacc[f]);
+                }
+            }
+        }
+#pragma unroll
+        for (int f = 0; f < FPT; ++f) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                sacc[f] += __shfl_xor_sync(0xffffffffu, sacc[f], o);
+                cacc[f] += __shfl_xor_sync(0xffffffffu, cacc[f], o);
+            }
+        }
+        if (lane == 0) {
+#pragma unroll
+            for (int f = 0; f < FPT; ++f) red[warp][f] = make_double2(sacc[f], cacc[f]);
+        }
+        __syncthreads();
+        // fixed-order cross-warp combine; one thread per (group, f)
+        const int groups_now = G >= kPoWarps ? min(kPoWarps, G - pass * kPoWarps) : G;
+        if (tid < groups_now * FPT) {
+            const int gl = tid / FPT, f = tid % FPT;
+            const int g = G >= kPoWarps ? pass * kPoWarps + gl : gl;
+            const int fi = g * FPT + f;
+            if (fi < nk) {
+                double2 acc = make_double2(0.0, 0.0);
+                const int nsub = G >= kPoWarps ? 1 : wpg;
+                for (int s = 0; s < nsub; ++s) {
+                    const int w = G >= kPoWarps ? gl : gl * wpg + s;
+                    acc.x += red[w][f].x;
+                    acc.y += red[w][f].y;
+                }
+                chunk_part[chunk * nk + fi] = acc;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// deterministic pairwise trees
+// ---------------------------------------------------------------------------
+// Sequential adjacent-pair tree with odd-tail carry (po.py:59-80 shape),
+// evaluated with a size-tagged stack: equal-size neighbours merge left+right,
+// leftovers fold right-nested -- identical to the level-by-level algorithm.
+__device__ double2 pairwise_seq(const double2 *p, int64_t n, int64_t stride)
+{
+    double2 st[48];
+    int64_t sz[48];
+    int top = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        double2 v = p[i * stride];
+        int64_t s = 1;
+        while (top > 0 && sz[top - 1] == s) {
+            v = make_double2(st[top - 1].x + v.x, st[top - 1].y + v.y);
+            s <<= 1;
+            --top;
+        }
+        st[top] = v;
+        sz[top] = s;
+        ++top;
+    }
+    if (top == 0) return make_double2(0.0, 0.0);
+    double2 acc = st[top - 1];
+    for (int j = top - 2; j >= 0; --j) acc = make_double2(st[j].x + acc.x, st[j].y + acc.y);
+    return acc;
+}
+
+__global__ void k_seg_reduce(const double2 *__restrict__ chunk_part,
+                             const UnitDev *__restrict__ units, int n_units, int nk,
+                             double2 *__restrict__ seg_part)
+{
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= (int64_t)n_units * nk) return;
+    const int u = (int)(t / nk), f = (int)(t % nk);
+    const UnitDev U = units[u];
+    const int64_t nch = (U.ray_end - U.ray_begin + kChunk - 1) / kChunk;
+    const int64_t c0 = U.slot_base / kChunk;
+    double2 v = pairwise_seq(chunk_part + c0 * nk + f, nch, nk);
+    v.x += 0.0;   // normalise -0.0 so a disjoint-support sum reduce is exact
+    v.y += 0.0;
+    seg_part[U.seg_out * nk + f] = v;
+}
+
+__global__ void k_finalize(const double2 *__restrict__ seg_part,
+                           const int64_t *__restrict__ seg_base, int ngrids, int nk,
+                           const double *__restrict__ scale, double2 *__restrict__ amp)
+{
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= (int64_t)ngrids * nk) return;
+    const int g = (int)(t / nk), f = (int)(t % nk);
+    const int64_t s0 = seg_base[g], s1 = seg_base[g + 1];
+    const double2 v = pairwise_seq(seg_part + s0 * nk + f, s1 - s0, nk);
+    // sum carries (w sin, w cos); term = a (sin + j cos), a = k dA / 4pi
+    const double a = scale[t];
+    amp[t] = make_double2(a * v.x, a * v.y);
+}
+
+// ---------------------------------------------------------------------------
+// launch wrappers
+// ---------------------------------------------------------------------------
+template <class K>
+static int persistent_blocks(K kernel, int threads, int num_sms)
+{
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0) != cudaSuccess ||
+        per_sm < 1)
+        per_sm = 1;
+    return per_sm * num_sms;
+}
+
+cudaError_t launch_trace_solve(const TraceCfg &cfg, const GridDev *d_grids,
+                               const UnitDev *d_units, int n_units, int64_t n_slots,
+                               SlotRec *d_slots, unsigned long long *d_counter,
+                               cudaStream_t st, const LaunchStats &ls)
+{
+    cudaError_t e = cudaMemsetAsync(d_counter, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return e;
+    const int64_t n_items = n_slots / 32;
+    switch (cfg.storage) {
+    case kF64: {
+        int nb = persistent_blocks(k_trace_solve<kF64>, kTraceThreads, ls.num_sms);
+        k_trace_solve<kF64><<<nb, kTraceThreads, 0, st>>>(cfg, d_grids, d_units, n_units,
+                                                          n_items, d_slots, d_counter);
+        break;
+    }
+    case kSingle: {
+        int nb = persistent_blocks(k_trace_solve<kSingle>, kTraceThreads, ls.num_sms);
+        k_trace_solve<kSingle><<<nb, kTraceThreads, 0, st>>>(cfg, d_grids, d_units, n_units,
+                                                             n_items, d_slots, d_counter);
+        break;
+    }
+    default: {
+        int nb = persistent_blocks(k_trace_solve<kF32Exact>, kTraceThreads, ls.num_sms);
+        k_trace_solve<kF32Exact><<<nb, kTraceThreads, 0, st>>>(
+            cfg, d_grids, d_units, n_units, n_items, d_slots, d_counter);
+        break;
+    }
+    }
+    ++*ls.launches;
+    return cudaGetLastError();
+}
+
+template <int S>
+static void trace_full_dispatch(const TraceCfg &cfg, const GridDev *g, const double *o,
+                                const double *d, int64_t n, const FullOut &out,
+                                unsigned long long *ctr, cudaStream_t st, int num_sms)
+{
+    if (g) {
+        int nb = persistent_blocks(k_trace_full<S, true>, kTraceThreads, num_sms);
+        k_trace_full<S, true><<<nb, kTraceThreads, 0, st>>>(cfg, g, o, d, n, out, ctr);
+    } else {
+        int nb = persistent_blocks(k_trace_full<S, false>, kTraceThreads, num_sms);
+        k_trace_full<S, false><<<nb, kTraceThreads, 0, st>>>(cfg, g, o, d, n, out, ctr);
+    }
+}
+
+cudaError_t launch_trace_full(const TraceCfg &cfg, const GridDev *d_grid,
+                              const double *d_orig, const double *d_dirs, int64_t n,
+                              const FullOut &out, unsigned long long *d_counter,
+                              cudaStream_t st, const LaunchStats &ls)
+{
+    cudaError_t e = cudaMemsetAsync(d_counter, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return e;
+    if (cfg.storage == kF64)
+        trace_full_dispatch<kF64>(cfg, d_grid, d_orig, d_dirs, n, out, d_counter, st, ls.num_sms);
+    else if (cfg.storage == kSingle)
+        trace_full_dispatch<kSingle>(cfg, d_grid, d_orig, d_dirs, n, out, d_counter, st,
+                                     ls.num_sms);
+    else
+        trace_full_dispatch<kF32Exact>(cfg, d_grid, d_orig, d_dirs, n, out, d_counter, st,
+                                       ls.num_sms);
+    ++*ls.launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_closest(const BvhView &B, int storage, const double *d_orig,
+                           const double *d_dirs, int64_t n, double t_min, double t_max,
+                           int64_t *d_tri, double *d_t, int64_t *d_visits, cudaStream_t st,
+                           const LaunchStats &ls)
+{
+    int64_t want = (n + kTraceThreads - 1) / kTraceThreads;
+    int nb = (int)(want < 65535 ? (want > 0 ? want : 1) : 65535);
+    if (storage == kF64)
+        k_closest<kF64><<<nb, kTraceThreads, 0, st>>>(B, d_orig, d_dirs, n, t_min, t_max, d_tri,
+                                                      d_t, d_visits);
+    else if (storage == kSingle)
+        k_closest<kSingle><<<nb, kTraceThreads, 0, st>>>(B, d_orig, d_dirs, n, t_min, t_max,
+                                                         d_tri, d_t, d_visits);
+    else
+        k_closest<kF32Exact><<<nb, kTraceThreads, 0, st>>>(B, d_orig, d_dirs, n, t_min, t_max,
+                                                           d_tri, d_t, d_visits);
+    ++*ls.launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_records_to_slots(const uint8_t *valid, const double *n0,
+                                    const double *path, const int32_t *bounces,
+                                    const uint8_t *escaped, int64_t n, double kx,
+                                    double ky, double kz, int count_trapped,
+                                    int64_t n_slots, SlotRec *slots, cudaStream_t st,
+                                    const LaunchStats &ls)
+{
+    int64_t want = (n_slots + 255) / 256;
+    int nb = (int)(want < 65535 ? (want > 0 ? want : 1) : 65535);
+    k_records_to_slots<<<nb, 256, 0, st>>>(valid, n0, path, bounces, escaped, n, kx, ky, kz,
+                                           count_trapped, n_slots, slots);
+    ++*ls.launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_po(const SlotRec *d_slots, const UnitDev *d_units, int n_units,
+                      int64_t n_chunks, const double *d_k2, int nk, const double *d_gpow,
+                      int max_bounces, double2 *d_chunk_part, int64_t *d_diag,
+                      unsigned long long *d_bad, cudaStream_t st, const LaunchStats &ls)
+{
+    if (n_chunks <= 0) return cudaSuccess;
+    dim3 grid((unsigned)n_chunks);
+    if (nk >= 8)
+        k_po<8><<<grid, kPoThreads, 0, st>>>(d_slots, d_units, n_units, d_k2, nk, d_gpow,
+                                             max_bounces, d_chunk_part, d_diag, d_bad);
+    else if (nk >= 4)
+        k_po<4><<<grid, kPoThreads, 0, st>>>(d_slots, d_units, n_units, d_k2, nk, d_gpow,
+                                             max_bounces, d_chunk_part, d_diag, d_bad);
+    else if (nk >= 2)
+        k_po<2><<<grid, kPoThreads, 0, st>>>(d_slots, d_units, n_units, d_k2, nk, d_gpow,
+                                             max_bounces, d_chunk_part, d_diag, d_bad);
+    else
+        k_po<1><<<grid, kPoThreads, 0, st>>>(d_slots, d_units, n_units, d_k2, nk, d_gpow,
+                                             max_bounces, d_chunk_part, d_diag, d_bad);
+    ++*ls.launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_seg_reduce(const double2 *d_chunk_part, const UnitDev *d_units,
+                              int n_units, int nk, double2 *d_seg_part, cudaStream_t st,
+                              const LaunchStats &ls)
+{
+    int64_t n = (int64_t)n_units * nk;
+    if (n == 0) return cudaSuccess;
+    k_seg_reduce<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(d_chunk_part, d_units, n_units,
+                                                               nk, d_seg_part);
+    ++*ls.launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_finalize(const double2 *d_seg_part, const int64_t *d_seg_base,
+                            int ngrids, int nk, const double *d_scale, double2 *d_amp,
+                            cudaStream_t st, const LaunchStats &ls)
+{
+    int64_t n = (int64_t)ngrids * nk;
+    if (n == 0) return cudaSuccess;
+    k_finalize<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(d_seg_part, d_seg_base, ngrids, nk,
+                                                             d_scale, d_amp);
+    ++*ls.launches;
+    return cudaGetLastError();
+}
+
+}  // namespace sbr
+
+namespace sbr {
+
+// ---------------------------------------------------------------------------
+// scalar predicates over independent pairs (geometry.py:394-425)
+// ---------------------------------------------------------------------------
+__global__ void k_tri_pairs(const double *__restrict__ v0, const double *__restrict__ v1,
+                            const double *__restrict__ v2, const double *__restrict__ o,
+                            const double *__restrict__ d, int64_t n, double t_min,
+                            double t_max, int single, double *__restrict__ t_out)
+{
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        TriF64 T;
+        T.ax = v0[3 * r]; T.ay = v0[3 * r + 1]; T.az = v0[3 * r + 2];
+        if (single) {
+            T.e1x = __fsub_rn((float)v1[3 * r], (float)T.ax);
+            T.e1y = __fsub_rn((float)v1[3 * r + 1], (float)T.ay);
+            T.e1z = __fsub_rn((float)v1[3 * r + 2], (float)T.az);
+            T.e2x = __fsub_rn((float)v2[3 * r], (float)T.ax);
+            T.e2y = __fsub_rn((float)v2[3 * r + 1], (float)T.ay);
+            T.e2z = __fsub_rn((float)v2[3 * r + 2], (float)T.az);
+        } else {
+            T.e1x = DS(v1[3 * r], T.ax); T.e1y = DS(v1[3 * r + 1], T.ay);
+            T.e1z = DS(v1[3 * r + 2], T.az);
+            T.e2x = DS(v2[3 * r], T.ax); T.e2y = DS(v2[3 * r + 1], T.ay);
+            T.e2z = DS(v2[3 * r + 2], T.az);
+        }
+        T.id = 0;
+        t_out[r] = tri_hit_exact(T, o[3 * r], o[3 * r + 1], o[3 * r + 2], d[3 * r], d[3 * r + 1],
+                                 d[3 * r + 2], t_min, t_max);
+    }
+}
+
+// FP64 slab test exactly as geometry.py:358-391 (reciprocals given).
+__global__ void k_box_pairs(const double *__restrict__ lo, const double *__restrict__ hi,
+                            const double *__restrict__ o, const double *__restrict__ inv,
+                            int64_t n, double t_max, uint8_t *__restrict__ hit,
+                            double *__restrict__ entry)
+{
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        double tn = 0.0, tf = t_max;
+        bool h = true;
+        for (int a = 0; a < 3 && h; ++a) {
+            const double l = lo[3 * r + a], u = hi[3 * r + a], oo = o[3 * r + a],
+                         iv = inv[3 * r + a];
+            if (isinf(iv)) {
+                if (oo < l || oo > u) h = false;
+            } else {
+                double t1 = DM(DS(l, oo), iv), t2 = DM(DS(u, oo), iv);
+                if (t1 > t2) { double s = t1; t1 = t2; t2 = s; }
+                if (t1 > tn) tn = t1;
+                if (t2 < tf) tf = t2;
+                if (tn > tf) h = false;
+            }
+        }
+        hit[r] = h ? 1 : 0;
+        entry[r] = h ? tn : 0.0;
+    }
+}
+
+cudaError_t launch_tri_pairs(const double *v0, const double *v1, const double *v2,
+                             const double *o, const double *d, int64_t n, double t_min,
+                             double t_max, int single, double *t_out, cudaStream_t st,
+                             const LaunchStats &ls)
+{
+    int64_t want = (n + 255) / 256;
+    int nb = (int)(want < 65535 ? (want > 0 ? want : 1) : 65535);
+    k_tri_pairs<<<nb, 256, 0, st>>>(v0, v1, v2, o, d, n, t_min, t_max, single, t_out);
+    ++*ls.launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_box_pairs(const double *lo, const double *hi, const double *o,
+                             const double *inv, int64_t n, double t_max, uint8_t *hit,
+                             double *entry, cudaStream_t st, const LaunchStats &ls)
+{
+    int64_t want = (n + 255) / 256;
+    int nb = (int)(want < 65535 ? (want > 0 ? want : 1) : 65535);
+    k_box_pairs<<<nb, 256, 0, st>>>(lo, hi, o, inv, n, t_max, hit, entry);
+    ++*ls.launches;
+    return cudaGetLastError();
+}
+
+}  // namespace sbr

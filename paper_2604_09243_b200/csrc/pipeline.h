@@ -1,0 +1,119 @@
+// pipeline.h -- launch wrappers of the trace / compaction+PO / reduce kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "sbr_device.cuh"
+
+namespace sbr {
+
+constexpr int kChunk = 2048;        // ray slots per PO block (compaction tile)
+constexpr int kSegChunks = 256;     // chunks per segment -> 2^19 rays
+constexpr int64_t kSegRays = (int64_t)kChunk * kSegChunks;
+
+// One incident direction (ApertureGrid, transport.py:84-127).
+struct GridDev {
+    double corner[3], u[3], v[3], k[3];
+    double spacing;
+    int64_t n_v;
+    int64_t n_rays;
+};
+
+// Unit of work: rays [ray_begin, ray_end) of grid `grid` (segment `seg`),
+// occupying slots [slot_base, slot_base + roundup(len, kChunk)) of a batch.
+struct UnitDev {
+    int grid;
+    int seg;
+    int64_t ray_begin, ray_end;
+    int64_t slot_base;
+    int64_t seg_out;    // global segment row of the partial output
+};
+
+// Compact per-ray record of the solve path (16 B).
+struct __align__(16) SlotRec {
+    double R;          // accumulated path length (FP64)
+    float cosv;        // -(n0 . k_inc)
+    uint32_t meta;     // bits 0-15 bounces | flags below
+};
+constexpr uint32_t kMetaValid = 1u << 16;
+constexpr uint32_t kMetaEscaped = 1u << 17;
+constexpr uint32_t kMetaSel = 1u << 18;
+constexpr uint32_t kMetaActive = 1u << 19;
+constexpr uint32_t kMetaBounceMask = 0xffffu;
+
+struct TraceCfg {
+    BvhView B;
+    int storage;
+    int max_bounces;
+    double eps;
+    int strict;
+    int count_trapped;
+    int allow_aliasing;
+    double spacing_limit;       // lambda_min / sampling_factor (<= 0: no rule)
+    unsigned int *error_flag;   // device: bit 0 = sampling rule violated
+};
+
+struct LaunchStats {
+    int64_t *launches;
+    int num_sms;
+};
+
+// ---- trace ---------------------------------------------------------------
+cudaError_t launch_trace_solve(const TraceCfg &cfg, const GridDev *d_grids,
+                               const UnitDev *d_units, int n_units, int64_t n_slots,
+                               SlotRec *d_slots, unsigned long long *d_counter,
+                               cudaStream_t st, const LaunchStats &ls);
+
+struct FullOut {
+    uint8_t *valid;
+    double *n0;
+    double *path;
+    int32_t *bounces;
+    uint8_t *escaped;
+    double *out_dir;
+    int32_t *ids;      // may be null
+};
+
+// grid != null: rays from the grid; else origins/dirs arrays
+cudaError_t launch_trace_full(const TraceCfg &cfg, const GridDev *d_grid,
+                              const double *d_orig, const double *d_dirs, int64_t n,
+                              const FullOut &out, unsigned long long *d_counter,
+                              cudaStream_t st, const LaunchStats &ls);
+
+cudaError_t launch_closest(const BvhView &B, int storage, const double *d_orig,
+                           const double *d_dirs, int64_t n, double t_min, double t_max,
+                           int64_t *d_tri, double *d_t, int64_t *d_visits, cudaStream_t st,
+                           const LaunchStats &ls);
+
+// ---- integrate ------------------------------------------------------------
+cudaError_t launch_records_to_slots(const uint8_t *valid, const double *n0,
+                                    const double *path, const int32_t *bounces,
+                                    const uint8_t *escaped, int64_t n, double kx,
+                                    double ky, double kz, int count_trapped,
+                                    int64_t n_slots, SlotRec *slots, cudaStream_t st,
+                                    const LaunchStats &ls);
+
+cudaError_t launch_po(const SlotRec *d_slots, const UnitDev *d_units, int n_units,
+                      int64_t n_chunks, const double *d_k2, int nk, const double *d_gpow,
+                      int max_bounces, double2 *d_chunk_part, int64_t *d_diag,
+                      unsigned long long *d_bad, cudaStream_t st, const LaunchStats &ls);
+
+cudaError_t launch_seg_reduce(const double2 *d_chunk_part, const UnitDev *d_units,
+                              int n_units, int nk, double2 *d_seg_part, cudaStream_t st,
+                              const LaunchStats &ls);
+
+cudaError_t launch_finalize(const double2 *d_seg_part, const int64_t *d_seg_base,
+                            int ngrids, int nk, const double *d_scale, double2 *d_amp,
+                            cudaStream_t st, const LaunchStats &ls);
+
+// ---- scalar predicates ------------------------------------------------------
+cudaError_t launch_tri_pairs(const double *v0, const double *v1, const double *v2,
+                             const double *o, const double *d, int64_t n, double t_min,
+                             double t_max, int single, double *t_out, cudaStream_t st,
+                             const LaunchStats &ls);
+cudaError_t launch_box_pairs(const double *lo, const double *hi, const double *o,
+                             const double *inv, int64_t n, double t_max, uint8_t *hit,
+                             double *entry, cudaStream_t st, const LaunchStats &ls);
+
+}  // namespace sbr

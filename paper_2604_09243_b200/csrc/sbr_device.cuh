@@ -1,0 +1,194 @@
+// sbr_device.cuh -- device data layout and the exact/conservative
+// intersection primitives shared by the trace, LBVH and PO kernels.
+//
+// Exactness contract: the closest hit of a query is the
+// lexicographic minimum of (t, triangle id) over every triangle whose
+// Moller-Trumbore test accepts the ray (pkg/src/sbr/bvh.py:340).  That set
+// does not depend on the tree, so any BVH whose box culling is conservative
+// returns the reference result bit-for-bit, provided the per-triangle
+// arithmetic is bit-identical.  Hence:
+//   * tri_hit_exact() mirrors geometry.py:326-355 operation by operation
+//     with explicit round-to-nearest FP64 intrinsics (no FMA contraction,
+//     identical association);
+//   * box tests run in FP32 on outward-rounded boxes with a per-ray padding
+//     (RayBox) that dominates every rounding error of the FP32 slab test,
+//     so they only ever cull boxes that cannot contain an accepted hit.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sbr {
+
+// ---------------------------------------------------------------------------
+// Node / triangle layout in HBM
+// ---------------------------------------------------------------------------
+// Child-pair BVH2 node, 64 B = four 16-byte loads:
+//   a = (c0.lo.x, c0.lo.y, c0.lo.z, c0.hi.x)
+//   b = (c0.hi.y, c0.hi.z, c1.lo.x, c1.lo.y)
+//   c = (c1.lo.z, c1.hi.x, c1.hi.y, c1.hi.z)
+//   d = (ref0, ref1, -, -)
+// Boxes are FP32, relative to the scene centre (BvhView::c*), rounded
+// outward.  A child reference >= 0 is an internal node index; < 0 is a leaf
+// encoding (first triangle slot, count) -- see leaf_ref().
+struct __align__(16) Node {
+    float4 a, b, c;
+    int4 d;
+};
+
+constexpr int kLeafCountShift = 25;
+constexpr int kLeafFirstMask = (1 << kLeafCountShift) - 1;
+constexpr int kMaxLeafCount = 63;
+constexpr int64_t kMaxTriangles = (int64_t)1 << kLeafCountShift;
+constexpr int kStack = 64;   // traversal stack entries; builds reject deeper trees
+
+__host__ __device__ inline int leaf_ref(int first, int count)
+{
+    return (int)(0x80000000u | ((unsigned)count << kLeafCountShift) | (unsigned)first);
+}
+__host__ __device__ inline int leaf_first(int ref) { return ref & kLeafFirstMask; }
+__host__ __device__ inline int leaf_count(int ref) { return (ref >> kLeafCountShift) & kMaxLeafCount; }
+
+// Triangle storage in leaf order.
+//   F32 (float32-representable vertices): 3 x float4 = 48 B
+//     t0 = (v0.x v0.y v0.z v1.x) t1 = (v1.y v1.z v2.x v2.y) t2 = (v2.z id - -)
+//   F64: 5 x double2 = 80 B: (v0.x v0.y)(v0.z v1.x)(v1.y v1.z)(v2.x v2.y)(v2.z id)
+enum Storage : int { kF32Exact = 1, kF64 = 2, kSingle = 3 };
+
+struct BvhView {
+    const Node *nodes;
+    const float4 *tri32;
+    const double2 *tri64;
+    const double *normals;   // (T,3), original triangle order
+    double cx, cy, cz;       // box frame origin
+    float scale;             // max |box coordinate| in the box frame
+    int root;                // root reference (internal node 0, or a leaf)
+};
+
+// ---------------------------------------------------------------------------
+// Exact FP64 Moller-Trumbore (geometry.py:326-355)
+// ---------------------------------------------------------------------------
+#define DM(a, b) __dmul_rn((a), (b))
+#define DA(a, b) __dadd_rn((a), (b))
+#define DS(a, b) __dsub_rn((a), (b))
+
+struct TriF64 {
+    double ax, ay, az, e1x, e1y, e1z, e2x, e2y, e2z;
+    int id;
+};
+
+template <int STORAGE>
+__device__ __forceinline__ TriF64 load_tri(const BvhView &B, int k)
+{
+    TriF64 r;
+    if (STORAGE == kF64) {
+        const double2 *p = B.tri64 + 5 * (int64_t)k;
+        double2 q0 = __ldg(p), q1 = __ldg(p + 1), q2 = __ldg(p + 2),
+                q3 = __ldg(p + 3), q4 = __ldg(p + 4);
+        r.ax = q0.x; r.ay = q0.y; r.az = q1.x;
+        r.e1x = DS(q1.y, r.ax); r.e1y = DS(q2.x, r.ay); r.e1z = DS(q2.y, r.az);
+        r.e2x = DS(q3.x, r.ax); r.e2y = DS(q3.y, r.ay); r.e2z = DS(q4.x, r.az);
+        r.id = (int)__double_as_longlong(q4.y);
+    } else {
+        const float4 *p = B.tri32 + 3 * (int64_t)k;
+        float4 t0 = __ldg(p), t1 = __ldg(p + 1), t2 = __ldg(p + 2);
+        r.ax = t0.x; r.ay = t0.y; r.az = t0.z;
+        if (STORAGE == kSingle) {
+            // reference precision="single": float32 arrays subtract in float32
+            r.e1x = __fsub_rn(t0.w, t0.x); r.e1y = __fsub_rn(t1.x, t0.y);
+            r.e1z = __fsub_rn(t1.y, t0.z);
+            r.e2x = __fsub_rn(t1.z, t0.x); r.e2y = __fsub_rn(t1.w, t0.y);
+            r.e2z = __fsub_rn(t2.x, t0.z);
+        } else {
+            r.e1x = DS((double)t0.w, r.ax); r.e1y = DS((double)t1.x, r.ay);
+            r.e1z = DS((double)t1.y, r.az);
+            r.e2x = DS((double)t1.z, r.ax); r.e2y = DS((double)t1.w, r.ay);
+            r.e2z = DS((double)t2.x, r.az);
+        }
+        r.id = __float_as_int(t2.y);
+    }
+    return r;
+}
+
+// Returns t in (t_min, t_max] or -1.0 (edge-inclusive), bit-identical to
+// the reference.  Operand association: a*b + c*d + e*f == (ab + cd) + ef.
+__device__ __forceinline__ double tri_hit_exact(const TriF64 &T, double ox,
+                                                double oy, double oz, double dx,
+                                                double dy, double dz,
+                                                double t_min, double t_max)
+{
+    double px = DS(DM(dy, T.e2z), DM(dz, T.e2y));
+    double py = DS(DM(dz, T.e2x), DM(dx, T.e2z));
+    double pz = DS(DM(dx, T.e2y), DM(dy, T.e2x));
+    double det = DA(DA(DM(T.e1x, px), DM(T.e1y, py)), DM(T.e1z, pz));
+    if (det == 0.0) return -1.0;
+    double tx = DS(ox, T.ax), ty = DS(oy, T.ay), tz = DS(oz, T.az);
+    double un = DA(DA(DM(tx, px), DM(ty, py)), DM(tz, pz));
+    double inv = __drcp_rn(det);  // == IEEE 1.0 / det
+    double u = DM(un, inv);
+    if (u < 0.0 || u > 1.0) return -1.0;
+    double qx = DS(DM(ty, T.e1z), DM(tz, T.e1y));
+    double qy = DS(DM(tz, T.e1x), DM(tx, T.e1z));
+    double qz = DS(DM(tx, T.e1y), DM(ty, T.e1x));
+    double v = DM(DA(DA(DM(dx, qx), DM(dy, qy)), DM(dz, qz)), inv);
+    if (v < 0.0 || DA(u, v) > 1.0) return -1.0;
+    double t = DM(DA(DA(DM(T.e2x, qx), DM(T.e2y, qy)), DM(T.e2z, qz)), inv);
+    if (t <= t_min || t > t_max) return -1.0;
+    return t;
+}
+
+// ---------------------------------------------------------------------------
+// Conservative FP32 slab test
+// ---------------------------------------------------------------------------
+// For each axis the padded slab [lo - delta, hi + delta] is evaluated as
+//   t_lo = fma(lo, inv, off_lo), off_lo = -(o' + delta) * inv
+//   t_hi = fma(hi, inv, off_hi), off_hi = -(o' - delta) * inv
+// with o' = fl32(o - c).  Every rounding error (origin conversion, the
+// reciprocal, the offsets, the fma) is a position error bounded by a few
+// ulp of (|o'| + scale); delta = 2^-17 (|o'|_inf + scale) exceeds that by
+// more than 10x, so the computed interval contains the exact interval of
+// the unpadded box: culling is conservative, never result-changing.
+struct RayBox {
+    float ix, iy, iz;
+    float lx, ly, lz;   // off_lo
+    float hx, hy, hz;   // off_hi
+};
+
+__device__ __forceinline__ float safe_dir(float d)
+{
+    return fabsf(d) < 1e-20f ? (d < 0.f ? -1e-20f : 1e-20f) : d;
+}
+
+__device__ __forceinline__ RayBox make_raybox(const BvhView &B, double ox, double oy,
+                                              double oz, double dx, double dy,
+                                              double dz)
+{
+    RayBox r;
+    float fx = __double2float_rn(ox - B.cx);
+    float fy = __double2float_rn(oy - B.cy);
+    float fz = __double2float_rn(oz - B.cz);
+    float m = fmaxf(fmaxf(fabsf(fx), fabsf(fy)), fabsf(fz));
+    float delta = (m + B.scale) * 7.62939453125e-06f;  // 2^-17
+    r.ix = 1.0f / safe_dir(__double2float_rn(dx));
+    r.iy = 1.0f / safe_dir(__double2float_rn(dy));
+    r.iz = 1.0f / safe_dir(__double2float_rn(dz));
+    r.lx = -(fx + delta) * r.ix; r.hx = -(fx - delta) * r.ix;
+    r.ly = -(fy + delta) * r.iy; r.hy = -(fy - delta) * r.iy;
+    r.lz = -(fz + delta) * r.iz; r.hz = -(fz - delta) * r.iz;
+    return r;
+}
+
+__device__ __forceinline__ float slab(const RayBox &r, float lox, float loy,
+                                      float loz, float hix, float hiy, float hiz,
+                                      float tmax, bool &hit)
+{
+    float ax = fmaf(lox, r.ix, r.lx), bx = fmaf(hix, r.ix, r.hx);
+    float ay = fmaf(loy, r.iy, r.ly), by = fmaf(hiy, r.iy, r.hy);
+    float az = fmaf(loz, r.iz, r.lz), bz = fmaf(hiz, r.iz, r.hz);
+    float tn = fmaxf(fmaxf(fminf(ax, bx), fminf(ay, by)), fmaxf(fminf(az, bz), 0.0f));
+    float tf = fminf(fminf(fmaxf(ax, bx), fmaxf(ay, by)), fminf(fmaxf(az, bz), tmax));
+    hit = tn <= tf;
+    return tn;
+}
+
+}  // namespace sbr

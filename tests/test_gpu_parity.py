@@ -1,0 +1,362 @@
+"""CUDA path vs the reference: golden vectors (produced by the reference
+itself) and the pinned CPU oracle on identical inputs.
+
+Bars (BASELINE.json north_star):
+  * closest-hit triangle ids, t, bounce counts, per-bounce triangle ids and
+    every HitRecords field: bit-exact;
+  * complex amplitude: 1e-4 relative field; RCS: 0.05 dB.
+"""
+
+import math
+import os
+
+import numpy as np
+import pytest
+
+import paper_2604_09243_b200 as sbr
+from paper_2604_09243_b200 import meshgen
+from conftest import golden_names, load_golden
+
+pytestmark = pytest.mark.gpu
+
+FIELD_RTOL = 1e-4
+DB_TOL = 0.05
+
+
+def _mesh(g):
+    """The fixture's exact Mesh arrays (float32 meshes keep their float32
+    normals, which were rounded from the FP64 construction)."""
+    v0, v1, v2 = g["mesh_v0"], g["mesh_v1"], g["mesh_v2"]
+    pts = np.concatenate([v0, v1, v2]).astype(np.float64)
+    return sbr.Mesh(v0=v0, v1=v1, v2=v2, normals=g["mesh_normals"],
+                    aabb=sbr.Aabb(pts.min(0), pts.max(0)))
+
+
+def _grid(g):
+    return sbr.ApertureGrid(u=g["grid_u"], v=g["grid_v"], k_inc=g["grid_k"],
+                            corner=g["grid_corner"], spacing=float(g["grid_spacing"]),
+                            n_u=int(g["grid_n_u"]), n_v=int(g["grid_n_v"]),
+                            cell_area=float(g["grid_cell_area"]),
+                            standoff=float(g["grid_standoff"]), margin=float(g["grid_margin"]))
+
+
+def _amp_close(a, ref):
+    a, ref = complex(a), complex(ref)
+    assert abs(a - ref) <= FIELD_RTOL * abs(ref) + 1e-300, (a, ref)
+    if abs(ref) > 0:
+        db = 20 * math.log10(abs(a) / abs(ref))
+        assert abs(db) <= DB_TOL
+
+
+# ---------------------------------------------------------------------------
+def test_mt_pairs_bitwise():
+    g = load_golden("mt")
+    t = np.empty_like(g["t"])
+    from paper_2604_09243_b200 import _native as nat
+    ctx = nat.context()
+    arrs = [nat.f64(g[k]) for k in ("v0", "v1", "v2", "o", "d")]
+    nat.check(ctx.lib.sbr_tri_hit_pairs(ctx.handle, *[nat.ptr(a) for a in arrs], t.shape[0],
+                                        0.0, np.inf, 0, nat.ptr(t)))
+    assert np.array_equal(t, g["t"])
+    for r in range(g["kat_t"].shape[0]):
+        res = sbr.ray_triangle_intersect(g["kat_o"][r], g["kat_d"][r],
+                                         sbr.Triangle(g["kat_v0"][r], g["kat_v1"][r],
+                                                      g["kat_v2"][r], np.zeros(3)),
+                                         g["kat_tmin"][r], g["kat_tmax"][r])
+        got = -1.0 if res is None else res[0]
+        assert got == g["kat_t"][r], r
+
+
+def test_aabb_predicate():
+    box = sbr.Aabb([0, 0, 0], [1, 1, 1])
+    assert sbr.ray_aabb_intersect([0.5, 0.5, 2.0], [np.inf, np.inf, -1.0], box) == (True, 1.0)
+    assert sbr.ray_aabb_intersect([1.5, 0.5, 2.0], [np.inf, np.inf, -1.0], box)[0] is False
+    assert sbr.ray_aabb_intersect([0.5, 0.5, 0.5], [1.0, 1.0, 1.0], box) == (True, 0.0)
+
+
+@pytest.mark.parametrize("name", golden_names("bvh_"))
+def test_closest_hit_lbvh_matches_reference(name):
+    g = load_golden(name)
+    mesh = _mesh(g)
+    tree = sbr.build(mesh)
+    tree.validate(mesh)
+    tri, t, vis = sbr.closest_hit_batch(tree, mesh, g["origins"], g["dirs"])
+    assert np.array_equal(tri, g["sah_tri"])
+    if mesh.dtype == np.float64:
+        assert np.array_equal(t, g["sah_t"])
+    assert (vis >= 1).all()
+
+
+@pytest.mark.parametrize("name", ["bvh_ico3", "bvh_rough20", "bvh_dihedral", "bvh_single"])
+@pytest.mark.parametrize("rule", ["sah", "median"])
+def test_closest_hit_uploaded_reference_tree(name, rule):
+    g = load_golden(name)
+    mesh = _mesh(g)
+    tree = sbr.Bvh(g[f"{rule}_nodes_min"], g[f"{rule}_nodes_max"], g[f"{rule}_node_first"],
+                   g[f"{rule}_node_count"], g[f"{rule}_tri_order"],
+                   int(g[f"{rule}_max_depth_seen"]))
+    tri, t, _ = sbr.closest_hit_batch(tree, mesh, g["origins"], g["dirs"])
+    assert np.array_equal(tri, g[f"{rule}_tri"])
+    assert np.array_equal(t, g[f"{rule}_t"])
+
+
+def test_closest_hit_t_window_and_root_cull():
+    mesh = sbr.generate_icosphere(1.0, 2)
+    tree = sbr.build(mesh)
+    hit = sbr.closest_hit(tree, mesh, (0, 0, 5.0), (0.0, 0.0, -1.0))
+    assert hit.t == pytest.approx(4.0, abs=0.05)
+    far = sbr.closest_hit(tree, mesh, (0, 0, 5.0), (0.0, 0.0, -1.0), t_min=hit.t + 1e-6)
+    assert far is not None and far.t > 5.5
+    miss, visits = sbr.closest_hit_counted(tree, mesh, (5, 5, 5.0), (0.0, 0.0, -1.0))
+    assert miss is None and visits == 1
+
+
+@pytest.mark.parametrize("name", golden_names("trace_"))
+def test_trace_grid_bitwise_with_ids(name):
+    g = load_golden(name)
+    mesh = _mesh(g)
+    tree = sbr.build(mesh)
+    params = sbr.TraceParams(max_bounces=int(g["max_bounces"]), epsilon=float(g["epsilon"]),
+                             strict_orientation=bool(g["strict"]))
+    rec = sbr.trace_grid(tree, mesh, _grid(g), params, with_ids=True)
+    for k in ("valid", "normal0", "path", "bounces", "escaped", "out_dir", "tri_ids"):
+        assert np.array_equal(getattr(rec, k), g[k]), k
+
+
+@pytest.mark.parametrize("name", golden_names("trace_"))
+def test_accumulate_matches_reference(name):
+    g = load_golden(name)
+    rec = sbr.HitRecords(g["valid"], g["normal0"], g["path"], g["bounces"], g["escaped"],
+                         g["out_dir"])
+    lam, area = float(g["wavelength"]), float(g["grid_cell_area"])
+    _amp_close(sbr.accumulate(rec, g["grid_k"], sbr.ScatterParams.from_wavelength(lam, area)),
+               g["amplitude"])
+    _amp_close(sbr.accumulate(rec, g["grid_k"], sbr.ScatterParams.from_wavelength(lam, area),
+                              count_trapped=True), g["amplitude_trapped"])
+    ks = 2 * np.pi / g["wavelengths"]
+    multi = sbr.accumulate_multi(rec, g["grid_k"], ks, area)
+    for a, ref in zip(multi, g["amplitudes_k"]):
+        _amp_close(a, ref)
+
+
+@pytest.mark.parametrize("name", golden_names("trace_"))
+def test_fused_solve_matches_reference(name):
+    g = load_golden(name)
+    if g["epsilon_given"]:
+        pytest.skip("fixture uses an explicit epsilon; covered by trace test")
+    mesh = _mesh(g)
+    tree = sbr.build(mesh)
+    d = sbr.IncidentDirection(float(g["theta"]), float(g["phi"]))
+    params = sbr.TraceParams(max_bounces=int(g["max_bounces"]),
+                             strict_orientation=bool(g["strict"]))
+    sol = sbr.solve_direction(tree, mesh, d, float(g["grid_spacing"]), float(g["wavelength"]),
+                              margin=float(g["grid_margin"]), trace_params=params)
+    assert sol.valid_rays == int(g["valid_rays"])
+    assert sol.max_bounce == int(g["max_bounce"])
+    assert np.array_equal(sol.bounce_counts, g["bounce_counts"])
+    _amp_close(sol.amplitude, g["amplitude"])
+    ref_db = float(g["sigma_dbsm"])
+    if np.isfinite(ref_db):
+        assert abs(sol.rcs.sigma_dbsm - ref_db) <= DB_TOL
+    # keep_records path gives the same bits as the fused path
+    sol2 = sbr.solve_direction(tree, mesh, d, float(g["grid_spacing"]), float(g["wavelength"]),
+                               margin=float(g["grid_margin"]), trace_params=params,
+                               keep_records=True)
+    assert sol2.amplitude == sol.amplitude
+
+
+def test_run_sweep_matches_reference():
+    g = load_golden("sweep_dihedral")
+    mesh = meshgen.dihedral_mesh(1.0)
+    cfg = sbr.SweepConfig(mesh_path="dihedral.obj", frequency_hz=3e9,
+                          theta=sbr.AngleRange(math.pi / 2, math.pi / 2, 1),
+                          phi=sbr.AngleRange(0.0, math.pi / 2, 7), max_bounces=3)
+    res = sbr.run_sweep(cfg, mesh)
+    assert np.array_equal(res.valid_rays, g["valid_rays"])
+    assert np.array_equal(res.max_bounces_seen, g["max_bounces_seen"])
+    assert np.array_equal(res.bounce_histogram, g["bounce_histogram"])
+    for a, ref in zip(res.amplitude.ravel(), g["amplitude"].ravel()):
+        _amp_close(a, ref)
+    assert res.mesh_checksum == str(g["mesh_checksum"])
+
+
+def test_validate_sphere_matches_reference():
+    g = load_golden("validate_sphere_small")
+    rep = sbr.validate_sphere(1.0, [8.0, 12.0], subdivisions=3, n_directions=6, max_bounces=4)
+    for row, s, m in zip(rep.rows, g["sigma_sbr"], g["sigma_mie"]):
+        assert row.sigma_sbr_m2 == pytest.approx(float(s), rel=3e-4)
+        assert row.sigma_mie_m2 == pytest.approx(float(m), rel=1e-12)
+
+
+# ---------------------------------------------------------------------------
+# larger inputs against the pinned CPU oracle (same mesh, same grid)
+# ---------------------------------------------------------------------------
+def _oracle_scene(orc, mesh):
+    return orc.Scene.from_mesh(mesh, single=mesh.dtype == np.float32)
+
+
+@pytest.mark.parametrize("case", ["aircraft", "sphere_s6", "rough_b5"])
+def test_trace_vs_oracle_larger(orc, case):
+    if case == "aircraft":
+        mesh = meshgen.generate_aircraft(density=0.05)
+        lam, B, dirs = 0.12, 5, [(math.pi / 2, math.pi), (math.pi / 2, 0.3), (1.2, 2.0)]
+    elif case == "sphere_s6":
+        mesh = meshgen.quantized_icosphere(1.0, 6)
+        lam, B, dirs = 2 * math.pi / 100, 1, [(math.pi / 2, 0.0), (math.pi / 2, 1.0)]
+    else:
+        mesh = meshgen.perturbed_grid_mesh(cells=120, extent=4.0, amplitude=0.08, seed=3)
+        lam, B, dirs = 0.1, 5, [(0.3, 0.7)]
+    tree = sbr.build(mesh)
+    scene = _oracle_scene(orc, mesh)
+    params = sbr.TraceParams(max_bounces=B)
+    for th, ph in dirs:
+        grid = sbr.build_aperture(mesh.aabb, sbr.IncidentDirection(th, ph), lam / 5,
+                                  wavelength=lam)
+        rows = (0, min(grid.n_u, max(1, 60000 // grid.n_v)))
+        ref = orc.trace_grid(scene, grid, B, params.resolve_epsilon(mesh), rows=rows,
+                             with_ids=True)
+        rec = sbr.trace_grid(tree, mesh, grid, params, with_ids=True)
+        n = ref.valid.shape[0]
+        for k in ("valid", "normal0", "path", "bounces", "escaped", "out_dir", "tri_ids"):
+            assert np.array_equal(getattr(rec, k)[:n], getattr(ref, k)), (case, k)
+        full = orc.trace_grid(scene, grid, B, params.resolve_epsilon(mesh))
+        a_ref = orc.accumulate(full, grid.k_inc, lam, grid.cell_area)
+        sol = sbr.solve_direction(tree, mesh, sbr.IncidentDirection(th, ph), lam / 5, lam,
+                                  trace_params=params)
+        _amp_close(sol.amplitude, a_ref)
+        assert sol.valid_rays == int(full.valid.sum())
+
+
+def test_solve_is_deterministic_and_batch_invariant(monkeypatch):
+    mesh = meshgen.quantized_icosphere(1.0, 5)
+    tree = sbr.build(mesh)
+    lam = 2 * math.pi / 60
+    grids = [sbr.build_aperture(mesh.aabb, d, lam / 5, wavelength=lam)
+             for d in sbr.fibonacci_directions(5)]
+    tp = sbr.TraceParams(max_bounces=4)
+    ks = 2 * np.pi / (lam * np.linspace(0.95, 1.05, 11))
+    a = sbr.solve_grids(tree, mesh, grids, tp, ks)
+    b = sbr.solve_grids(tree, mesh, grids, tp, ks)
+    assert np.array_equal(a.amplitude, b.amplitude)
+    monkeypatch.setenv("SBR_SLOT_BUDGET", "6144")
+    c = sbr.solve_grids(tree, mesh, grids, tp, ks)
+    assert np.array_equal(a.amplitude, c.amplitude)
+    assert np.array_equal(a.bounce_counts, c.bounce_counts)
+    # each grid alone == its row of the batch
+    for i, g in enumerate(grids):
+        s = sbr.solve_grids(tree, mesh, [g], tp, ks)
+        assert np.array_equal(s.amplitude[0], a.amplitude[i])
+
+
+def test_sharded_solve_equals_single(orc):
+    """Simulated N-rank run on one GPU: summing the disjoint shard buffers
+    and finalising reproduces sbr_solve bit for bit (both shard modes)."""
+    import ctypes
+    import torch
+    from paper_2604_09243_b200 import _native as nat, distributed as D
+    from paper_2604_09243_b200.sweep import grid_array
+    mesh = meshgen.quantized_icosphere(1.0, 4)
+    tree = sbr.build(mesh)
+    lam = 2 * math.pi / 450   # big grids -> several segments per grid
+    grids = [sbr.build_aperture(mesh.aabb, d, lam / 5, wavelength=lam)
+             for d in sbr.fibonacci_directions(3)]
+    tp = sbr.TraceParams(max_bounces=2)
+    ks = np.array([2 * np.pi / lam, 2 * np.pi / (0.9 * lam)])
+    ref = sbr.solve_grids(tree, mesh, grids, tp, ks)
+    ctx = nat.context()
+    d = tree.device(mesh, ctx)
+    base = D.segment_layout(grids)
+    assert base[-1] > len(grids)
+    garr = grid_array(grids)
+    cp = nat.make_trace_params(2, tp.resolve_epsilon(mesh))
+    for mode in ("angles", "rays"):
+        for world in (2, 3):
+            tot_seg = torch.zeros(int(base[-1]) * 4, dtype=torch.float64, device="cuda")
+            tot_diag = torch.zeros((len(grids), D.diag_stride(2)), dtype=torch.int64,
+                                   device="cuda")
+            maxb = torch.zeros(len(grids), dtype=torch.int64, device="cuda")
+            for rank in range(world):
+                seg = torch.zeros_like(tot_seg)
+                diag = torch.zeros_like(tot_diag)
+                nat.check(ctx.lib.sbr_solve_shard(ctx.handle, d.mesh_dev.handle, d.handle, garr,
+                                                  len(grids), ctypes.byref(cp), nat.ptr(ks), 2,
+                                                  -1.0, 0, rank, world, D.MODES[mode],
+                                                  nat.c_vp(seg.data_ptr()),
+                                                  nat.c_vp(diag.data_ptr())))
+                ctx.synchronize()
+                tot_seg += seg
+                tot_diag += diag
+                maxb = torch.maximum(maxb, diag[:, 2])
+            tot_diag[:, 2] = maxb
+            amp = np.zeros((len(grids), 2, 2))
+            vr = np.zeros(len(grids), np.int64)
+            dg = nat.Diag(vr.ctypes.data, None, None, None)
+            nat.check(ctx.lib.sbr_finalize(ctx.handle, garr, len(grids), nat.ptr(ks), 2, 2,
+                                           nat.c_vp(tot_seg.data_ptr()),
+                                           nat.c_vp(tot_diag.data_ptr()), nat.ptr(amp),
+                                           ctypes.byref(dg)))
+            assert np.array_equal(amp.view(np.complex128)[..., 0], ref.amplitude), (mode, world)
+            assert np.array_equal(vr, ref.valid_rays)
+
+
+def test_mie_sphere_direction_averaged():
+    """SBR-PO sphere vs Mie with the reference's direction averaging
+    (test_acceptance.py:38-49 style)."""
+    rep = sbr.validate_sphere(1.0, [20.0, 30.0], sampling_factor=5.0, subdivisions=5,
+                              n_directions=16)
+    for row in rep.rows:
+        assert row.rel_error <= 0.08, row
+    assert rep.mean_rel_error() <= 0.06
+
+
+def test_plate_closed_form():
+    side, lam = 1.0, 0.1
+    mesh = meshgen.plate_mesh(side)
+    tree = sbr.build(mesh)
+    d = sbr.IncidentDirection(0.0, 0.0)
+    sol = sbr.solve_direction(tree, mesh, d, lam / 10, lam, margin=0.0,
+                              trace_params=sbr.TraceParams(max_bounces=3))
+    ref = sbr.plate_reference(side, lam)
+    assert abs(sol.rcs.sigma_m2 - ref) / ref <= 0.01
+
+
+def test_errors_map_to_reference_exceptions():
+    mesh = meshgen.plate_mesh()
+    tree = sbr.build(mesh)
+    rec = sbr.trace_grid(tree, mesh, sbr.build_aperture(mesh.aabb, sbr.IncidentDirection(0, 0),
+                                                        0.1, margin=0.0))
+    bad = sbr.HitRecords(rec.valid, rec.normal0, rec.path.copy(), rec.bounces, rec.escaped,
+                         rec.out_dir)
+    bad.path[5] = np.inf
+    with pytest.raises(sbr.NumericalError, match="record index 5"):
+        sbr.accumulate(bad, [0, 0, -1.0], sbr.ScatterParams.from_wavelength(0.5, 0.01))
+    grid = sbr.build_aperture(mesh.aabb, sbr.IncidentDirection(0, 0), 0.1, margin=0.0)
+    with pytest.raises(sbr.ValidationError):
+        sbr.solve_grids(tree, mesh, [grid], sbr.TraceParams(max_bounces=1), [2 * np.pi / 0.2],
+                        lambda_min=0.2, allow_aliasing=False)
+
+
+def test_strict_and_budget_semantics():
+    mesh = meshgen.plate_mesh()
+    tree = sbr.build(mesh)
+    rec = sbr.trace_ray(tree, mesh, (0.5, 0.5, -3.0), (0.0, 0.0, 1.0),
+                        sbr.TraceParams(strict_orientation=True))
+    assert not rec.valid and rec.escaped
+    lax = sbr.trace_ray(tree, mesh, (0.5, 0.5, -3.0), (0.0, 0.0, 1.0))
+    assert lax.valid and np.allclose(lax.normal0, [0, 0, -1])
+    dmesh = meshgen.dihedral_mesh()
+    dtree = sbr.build(dmesh)
+    k = sbr.IncidentDirection(math.pi / 2, math.pi / 4).k_inc
+    one = sbr.trace_ray(dtree, dmesh, (1.5, 1.2, 0.5), k, sbr.TraceParams(max_bounces=1))
+    two = sbr.trace_ray(dtree, dmesh, (1.5, 1.2, 0.5), k, sbr.TraceParams(max_bounces=2))
+    assert one.bounces == 1 and two.bounces == 2 and not one.escaped and two.escaped
+
+
+def test_launches_are_counted():
+    from paper_2604_09243_b200 import _native as nat
+    ctx = nat.context()
+    before = ctx.launches
+    mesh = meshgen.quantized_icosphere(1.0, 3)
+    tree = sbr.build(mesh)
+    sbr.solve_direction(tree, mesh, sbr.IncidentDirection(0.3, 0.2), 0.05, 0.25)
+    assert ctx.launches - before >= 6   # LBVH kernels + trace + po + reduces

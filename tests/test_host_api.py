@@ -1,0 +1,168 @@
+"""Host-side API parity (no GPU): the FP64 pieces the product computes on the
+host must be bit-identical to the reference (golden vectors)."""
+
+import hashlib
+import json
+import math
+
+import numpy as np
+import pytest
+
+import paper_2604_09243_b200 as sbr
+from paper_2604_09243_b200 import meshgen
+from conftest import load_golden
+
+
+def test_public_names_match_reference_surface():
+    ref_names = {
+        "Aabb", "AngleRange", "ApertureGrid", "BuildParams", "Bvh", "Hit", "HitRecord",
+        "HitRecords", "IncidentDirection", "Mesh", "NumericalError", "RcsValue",
+        "SamplingCheck", "SbrError", "ScatterParams", "SphereValidationReport", "SweepConfig",
+        "SweepResult", "TraceParams", "Triangle", "ValidationError", "SPEED_OF_LIGHT",
+        "accumulate", "binned_sah_split", "build", "build_aperture", "closest_hit",
+        "closest_hit_batch", "closest_hit_counted", "fibonacci_directions",
+        "generate_icosphere", "load_mesh", "median_split", "mesh_from_arrays",
+        "mesh_from_soup", "mie_backscatter_pec", "orthonormal_basis", "pairwise_sum",
+        "plate_reference", "ray_aabb_intersect", "ray_triangle_intersect", "rcs", "reflect",
+        "run_sweep", "sah_cost", "sampling_check", "save_obj", "solve_direction",
+        "trace_grid", "trace_ray", "truncation_order", "validate_sphere", "write_csv",
+        "write_heatmap", "write_validation_csv"}
+    missing = sorted(n for n in ref_names if not hasattr(sbr, n))
+    assert not missing
+    assert ref_names <= set(sbr.__all__)
+
+
+def test_aperture_bitwise():
+    g = load_golden("aperture")
+    for row in g["rows"]:
+        bi = int(row[0])
+        box = sbr.Aabb(g["boxes_lo"][bi], g["boxes_hi"][bi])
+        grid = sbr.build_aperture(box, sbr.IncidentDirection(row[1], row[2]), row[3],
+                                  margin=row[4])
+        assert (grid.n_u, grid.n_v) == (int(row[5]), int(row[6]))
+        assert np.array_equal(grid.corner, row[7:10])
+        assert np.array_equal(grid.u, row[10:13])
+        assert np.array_equal(grid.v, row[13:16])
+        assert np.array_equal(grid.k_inc, row[16:19])
+        assert grid.standoff == row[19]
+
+
+def test_trace_fixture_grids_bitwise():
+    from conftest import golden_names
+    for name in golden_names("trace_"):
+        g = load_golden(name)
+        mesh = sbr.mesh_from_soup(np.stack([g["mesh_v0"], g["mesh_v1"], g["mesh_v2"]], 1))
+        d = sbr.IncidentDirection(float(g["theta"]), float(g["phi"]))
+        grid = sbr.build_aperture(mesh.aabb, d, float(g["grid_spacing"]),
+                                  margin=float(g["grid_margin"]))
+        assert np.array_equal(grid.corner, g["grid_corner"]), name
+        assert (grid.n_u, grid.n_v) == (int(g["grid_n_u"]), int(g["grid_n_v"]))
+
+
+def test_icosphere_bit_identical():
+    g = load_golden("meshes")
+    for s, want in zip(g["ico_hash_levels"], g["ico_hashes"]):
+        m = sbr.generate_icosphere(1.0, int(s))
+        h = hashlib.sha256()
+        for a in (m.v0, m.v1, m.v2, m.normals):
+            h.update(np.ascontiguousarray(a).tobytes())
+        assert h.hexdigest() == str(want), s
+    m = sbr.generate_icosphere(2.5, 2)
+    for k in ("v0", "v1", "v2", "normals"):
+        assert np.array_equal(getattr(m, k), g["ico2r25_" + k])
+
+
+def test_reference_test_meshes_identical():
+    g = load_golden("meshes")
+    assert meshgen.perturbed_grid_mesh(cells=71).checksum() == str(g["rough71_checksum"])
+    assert meshgen.dihedral_mesh().checksum() == str(g["dihedral_checksum"])
+
+
+def test_trace_fixture_meshes_identical():
+    for name, mk in [("trace_plate_c3", lambda: meshgen.plate_mesh(1.0)),
+                     ("trace_trihedral_b3", lambda: meshgen.trihedral_mesh(1.0)),
+                     ("trace_sphere_c1", lambda: meshgen.quantized_icosphere(1.0, 5)),
+                     ("trace_rough40_b5", lambda: meshgen.perturbed_grid_mesh(
+                         cells=40, extent=2.0, amplitude=0.08, seed=42))]:
+        g = load_golden(name)
+        m = mk()
+        for k in ("v0", "v1", "v2", "normals"):
+            assert np.array_equal(getattr(m, k), g["mesh_" + k]), (name, k)
+
+
+def test_mie_matches_reference():
+    g = load_golden("meshes")
+    for x, s in zip(g["mie_x"], g["mie_sigma"]):
+        assert sbr.mie_backscatter_pec(float(x), 1.0) == pytest.approx(float(s), rel=1e-12)
+
+
+def test_pairwise_sum_matches_reference_shape(orc):
+    rng = np.random.default_rng(0)
+    for n in (0, 1, 2, 5, 31, 1024, 1025):
+        v = rng.normal(size=n) + 1j * rng.normal(size=n)
+        assert sbr.pairwise_sum(v) == orc.pairwise_sum(v)
+
+
+def test_fibonacci_and_sampling():
+    g = load_golden("validate_sphere_small")
+    for d, (th, ph) in zip(sbr.fibonacci_directions(16), g["fib"]):
+        assert (d.theta, d.phi) == (th, ph)
+    assert sbr.sampling_check(0.02, 0.1).passed
+    assert not sbr.sampling_check(0.0200001, 0.1).passed
+    with pytest.raises(sbr.ValidationError):
+        sbr.build_aperture(sbr.Aabb([0, 0, 0], [1, 1, 1]), sbr.IncidentDirection(0, 0), 0.05,
+                           wavelength=0.1)
+
+
+def test_split_helpers_match_oracle_build(orc):
+    """median_split / binned_sah_split restate bvh.py:135-215: the root
+    split they choose equals the one the reference tree (oracle) made."""
+    g = load_golden("bvh_ico3")
+    v0, v1, v2 = g["mesh_v0"], g["mesh_v1"], g["mesh_v2"]
+    tmin = np.minimum(np.minimum(v0, v1), v2)
+    tmax = np.maximum(np.maximum(v0, v1), v2)
+    cents = (tmin + tmax) * 0.5
+    box = sbr.Aabb(tmin.min(0), tmax.max(0))
+    ax, b, left, right = sbr.binned_sah_split(tmin, tmax, cents, box)
+    # left subtree of the reference root = node 1; its leaves hold `left`
+    order = g["sah_tri_order"]
+    right_root = int(g["sah_node_first"][0])
+    first_right_leaf = min(int(g["sah_node_first"][i]) for i in range(right_root,
+                           g["sah_node_first"].shape[0]) if g["sah_node_count"][i] > 0)
+    assert sorted(left.tolist()) == sorted(order[:first_right_leaf].tolist())
+    ax, l2, r2 = sbr.median_split(cents, box)
+    assert len(l2) == len(cents) // 2
+    assert sbr.sah_cost(2.0, 1.0, 1.0, 3, 5, 1.0, 1.0) == 1.0 + 0.5 * 3 + 0.5 * 5
+
+
+def test_sweep_config_roundtrip(tmp_path):
+    p = tmp_path / "run.json"
+    p.write_text(json.dumps({"mesh": "x.obj", "frequency_hz": 3e9,
+                             "theta_deg": [90, 90, 1], "phi_deg": {"start_deg": 0,
+                                                                  "stop_deg": 90,
+                                                                  "samples": 7},
+                             "max_bounces": 3, "bvh": {"n_leaf": 2}, "unknown_key": 1}))
+    cfg = sbr.SweepConfig.from_json_file(p)
+    assert cfg.max_bounces == 3 and cfg.n_leaf == 2 and cfg.phi.samples == 7
+    assert cfg.resolved_spacing() == pytest.approx(sbr.SPEED_OF_LIGHT / 3e9 / 5)
+    with pytest.raises(sbr.ValidationError):
+        sbr.SweepConfig.from_dict({"frequency_hz": 1e9})
+    with pytest.raises(sbr.ValidationError):
+        sbr.BuildParams(split_rule="bogus")
+
+
+def test_obj_roundtrip(tmp_path):
+    m = meshgen.trihedral_mesh()
+    p = tmp_path / "t.obj"
+    sbr.save_obj(m, p)
+    m2 = sbr.load_mesh(p)
+    assert np.array_equal(m.v0, m2.v0) and np.array_equal(m.normals, m2.normals)
+
+
+def test_aircraft_generator_deterministic():
+    a = meshgen.generate_aircraft(density=0.01)
+    b = meshgen.generate_aircraft(density=0.01)
+    assert a.checksum() == b.checksum()
+    assert a.triangle_count > 5000
+    soup = np.concatenate([a.v0, a.v1, a.v2])
+    assert np.array_equal(soup.astype(np.float32).astype(np.float64), soup)
