@@ -1,0 +1,357 @@
+#!/usr/bin/env python
+"""Benchmark: 360-angle monostatic RCS sweep of the ~1M-triangle procedural
+aircraft at 10 GHz with 5 bounces (BASELINE.json configs[3], the workload the
+north-star target "1e9 ray-bounce intersections/s per B200 on a 1M-triangle
+mesh" is quoted on).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...     (one rank per GPU)
+
+A step = one full 360-angle sweep (launcher + 5-bounce trace + compaction +
+PO + reduction) over the resident mesh/BVH.  metric = closest-hit queries
+per second, sum_i (N_i + 1) over all rays of the step (the reference's
+_traverse calls), whole job over all GPUs.  Angles are sharded
+across ranks (strong scaling: the sweep is fixed) and combined with one
+NCCL reduce.  ``--impl reference`` times the reference algorithm (the CPU
+oracle port of the numba kernels, all host cores) on a bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ray-bounce intersections/s per GPU & monostatic RCS sweep angles/s at 1/2/4/8 B200"
+UNIT = "intersections/s"
+FREQ_HZ = 10e9
+MAX_BOUNCES = 5
+N_ANGLES = 360
+C = 299792458.0
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--density", type=float, default=1.0, help="mesh density (1.0 = ~1M tris)")
+    p.add_argument("--angles", type=int, default=N_ANGLES)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    return p.parse_args()
+
+
+def workload(density, n_angles):
+    import paper_2604_09243_b200 as sbr
+    from paper_2604_09243_b200 import meshgen
+    mesh = meshgen.generate_aircraft(density=density)
+    lam = C / FREQ_HZ
+    cfg = sbr.SweepConfig(mesh_path="<procedural aircraft>", frequency_hz=FREQ_HZ,
+                          theta=sbr.AngleRange(math.pi / 2, math.pi / 2, 1),
+                          phi=sbr.AngleRange(0.0, math.radians(n_angles - 1), n_angles),
+                          max_bounces=MAX_BOUNCES)
+    return mesh, lam, cfg
+
+
+def config_dict(mesh, n_angles, world):
+    return {"workload": "C4: procedural aircraft, 360-angle monostatic sweep, 10 GHz, "
+                        "5 bounces, lambda/5 ray spacing",
+            "triangles": int(mesh.triangle_count), "angles": n_angles,
+            "theta_deg": 90, "phi_deg": [0, n_angles - 1], "frequency_hz": FREQ_HZ,
+            "max_bounces": MAX_BOUNCES, "spacing": "lambda/5 (5.996 mm)",
+            "parallelism": f"angle-sharded x{world}, one NCCL reduce" if world > 1 else "1 GPU",
+            "l2": "flushed (512 MB write) between timed steps"}
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class Clocks:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, index):
+        self.index = str(index)
+        self.lines = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9 or f[0] != self.index:
+                continue
+            try:
+                sm.append(float(f[1])); mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for name, val in zip(self.NAMES, f[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the reference algorithm (oracle port) on the host cores
+# ---------------------------------------------------------------------------
+def cpu_sample(mesh, lam, cfg, n_angles_sample=4, bands=8, band_rows=8):
+    """Bounded sample of the same workload through the CPU port of the
+    reference kernels (oracle/, test infrastructure): reference SAH tree,
+    then trace + PO on row bands of a few azimuths; returns a dict."""
+    from oracle import oracle as orc
+    import paper_2604_09243_b200 as sbr
+    t0 = time.perf_counter()
+    tree = orc.build(mesh.v0, mesh.v1, mesh.v2, split_rule="sah", n_leaf=4)
+    build_s = time.perf_counter() - t0
+    scene = orc.Scene(mesh.v0, mesh.v1, mesh.v2, mesh.normals, tree)
+    eps = 1e-6 * mesh.aabb.diagonal()
+    phis = cfg.phi.values()
+    picks = np.linspace(0, len(phis) - 1, n_angles_sample).astype(int)
+    return scene, eps, build_s, [(phis[i]) for i in picks]
+
+
+def cpu_run(scene, eps, lam, phis, bands, band_rows):
+    from oracle import oracle as orc
+    import paper_2604_09243_b200 as sbr
+    mesh_box = sbr.Aabb(scene.aabb_min, scene.aabb_max)
+    queries = rays = 0
+    t0 = time.perf_counter()
+    for ph in phis:
+        g = sbr.build_aperture(mesh_box, sbr.IncidentDirection(math.pi / 2, float(ph)),
+                               lam / 5, wavelength=lam)
+        for b in range(bands):
+            r0 = (2 * b + 1) * g.n_u // (2 * bands)
+            rows = (r0, min(g.n_u, r0 + band_rows))
+            rec = orc.trace_grid(scene, g, MAX_BOUNCES, eps, rows=rows)
+            orc.accumulate(rec, g.k_inc, lam, g.cell_area)
+            queries += int((rec.bounces.astype(np.int64) + 1).sum())
+            rays += rec.valid.shape[0]
+    return queries, rays, time.perf_counter() - t0
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    mesh, lam, cfg = workload(args.density, args.angles)
+    scene, eps, build_s, phis = cpu_sample(mesh, lam, cfg)
+    cores = os.cpu_count() or 1
+    for _ in range(max(args.warmup, 0)):
+        cpu_run(scene, eps, lam, phis[:1], 4, 8)
+    q = r = 0
+    t = 0.0
+    for s in range(args.steps):
+        qq, rr, tt = cpu_run(scene, eps, lam, [phis[s % len(phis)]], 8, 8)
+        q += qq; r += rr; t += tt
+    value = q / t
+    sample = (f"{args.steps} steps x 1 azimuth x 8 row bands of 8 rows ({r} rays, {q} queries) "
+              f"of the C4 sweep; reference SAH tree built in {build_s:.2f} s (not timed)")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_dict(mesh, args.angles, 1),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+    import paper_2604_09243_b200 as sbr
+    from paper_2604_09243_b200 import _native as nat
+    from paper_2604_09243_b200 import distributed as D
+    from paper_2604_09243_b200.sweep import sweep_grids
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctx = nat.context(local)
+
+    mesh, lam, cfg = workload(args.density, args.angles)
+    tree = sbr.build(mesh)
+    th, ph, cells, grids = sweep_grids(cfg, mesh)
+    tp = cfg.trace_params()
+    k = [2 * math.pi / lam]
+    stats = {}
+
+    def step():
+        if world == 1:
+            return sbr.solve_grids(tree, mesh, grids, tp, k, cfg.gamma, lambda_min=lam,
+                                   allow_aliasing=False)
+        return D.solve_grids_distributed(tree, mesh, grids, tp, k, cfg.gamma,
+                                         shard_mode="angles", lambda_min=lam,
+                                         allow_aliasing=False, stats=stats)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    ctx.profile(True)
+    clocks = Clocks(torch.cuda.current_device() if "CUDA_VISIBLE_DEVICES" not in os.environ
+                    else os.environ["CUDA_VISIBLE_DEVICES"].split(",")[local])
+    clocks.start()
+    launches0 = ctx.launches
+    total_ms = 0.0
+    queries = 0
+    local_queries = 0
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        res = step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        total_ms += e0.elapsed_time(e1)
+        if res is not None:
+            queries += int(res.queries.sum())
+        local_queries += stats.get("local_queries", int(res.queries.sum()) if res else 0)
+    launches = ctx.launches - launches0
+    clk = clocks.stop()
+    kst = ctx.kernel_stats()
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+
+    # ---- e2e through the public API with host buffers -------------------
+    e2e = None
+    if not args.no_e2e:
+        import dataclasses
+        e2e_s = 0.0
+        e2e_q = 0
+        reps = max(1, min(args.steps, 3))
+        for _ in range(reps):
+            fresh = dataclasses.replace(mesh, _dev={})     # nothing resident
+            torch.cuda.synchronize()
+            barrier()
+            t0 = time.perf_counter()
+            if world == 1:
+                out = sbr.run_sweep(cfg, fresh)
+            else:
+                out = D.run_sweep_distributed(cfg, fresh)
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            if world > 1:
+                tt = torch.tensor([dt], dtype=torch.float64, device="cuda")
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                dt = float(tt.item())
+            e2e_s += dt
+            if out is not None:
+                e2e_q += int(out.queries_total)
+        if rank == 0:
+            h2d = (mesh.triangle_count * 12 * 8 + len(grids) * 128) // 1
+            d2h = len(grids) * (16 + 8 * (3 + MAX_BOUNCES + 1))
+            e2e = {"value": e2e_q / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                   "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * e2e_s / reps,
+                   "path": "paper_2604_09243_b200.run_sweep(config, mesh) from host arrays: "
+                           "mesh upload + GPU LBVH + 360 apertures + fused solve + readback"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    value = queries / (total_ms / 1e3)
+    ab = json.load(open(os.path.join(ROOT, "profiles", "algorithmic_bytes_c4.json")))
+    bpq = ab["bytes_per_query"]
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak = peaks.get("hbm_gbs", 6650.0)
+    achieved = bpq * local_queries / (kst["trace_ms"] / 1e3) / 1e9 if kst["trace_ms"] else None
+    traffic = None
+    ncu_path = os.path.join(ROOT, "profiles", "ncu_trace_summary.json")
+    if os.path.exists(ncu_path):
+        traffic = json.load(open(ncu_path)).get("dram_bytes_per_launch")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(mesh, args.angles, world),
+        "angles_per_s": args.angles * args.steps / (total_ms / 1e3),
+        "queries_per_step": queries // max(args.steps, 1),
+        "gpu_launches": launches,
+        "kernel_ms": {"trace": kst["trace_ms"] / args.steps, "compact_po": kst["po_ms"] / args.steps,
+                      "trace_launches_per_step": kst["trace_launches"] / args.steps},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "kernel": "k_trace_solve (launcher + 5-bounce traversal)",
+                     "bytes_per_query": bpq,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
+        "clocks": clk,
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if world == 1 and not args.no_cpu:
+        scene, eps, build_s, phis = cpu_sample(mesh, lam, cfg)
+        q, r, t = cpu_run(scene, eps, lam, phis, 8, 16)
+        line["cpu_baseline"] = {
+            "value": q / t, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port",
+            "sample": f"{len(phis)} azimuths x 8 row bands of 16 rows ({r} rays, {q} queries) "
+                      f"of the same sweep, reference SAH tree (built in {build_s:.2f} s, not "
+                      "timed), oracle/ C port of the numba kernels, OpenMP all cores"}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -112,6 +112,12 @@ int sbr_ctx_stream(sbr_ctx *ctx, void **stream_out);
 /* Number of kernels this context has launched (instrumentation). */
 int sbr_ctx_launch_count(sbr_ctx *ctx, int64_t *count_out);
 
+/* Per-kernel CUDA-event timing of the solve pipeline (trace kernel and
+ * compaction+PO kernel), accumulated over calls; enabling resets it. */
+int sbr_ctx_profile(sbr_ctx *ctx, int32_t enable);
+int sbr_ctx_kernel_stats(sbr_ctx *ctx, double *trace_ms, int64_t *trace_launches,
+                         double *po_ms, int64_t *po_launches);
+
 /* ---- mesh: geometry.py:130-180 mesh_from_soup output -> device --------- */
 int sbr_mesh_create(sbr_ctx *ctx, const double *v0, const double *v1,
                     const double *v2, const double *normals, int64_t ntri,

@@ -64,6 +64,9 @@ _SIGS = {
     "sbr_ctx_synchronize": (ctypes.c_int, [c_vp]),
     "sbr_ctx_stream": (ctypes.c_int, [c_vp, ctypes.POINTER(c_vp)]),
     "sbr_ctx_launch_count": (ctypes.c_int, [c_vp, ctypes.POINTER(c_i64)]),
+    "sbr_ctx_profile": (ctypes.c_int, [c_vp, c_i32]),
+    "sbr_ctx_kernel_stats": (ctypes.c_int, [c_vp, ctypes.POINTER(c_dbl), ctypes.POINTER(c_i64),
+                                            ctypes.POINTER(c_dbl), ctypes.POINTER(c_i64)]),
     "sbr_mesh_create": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i32,
                                        ctypes.POINTER(c_vp)]),
     "sbr_mesh_destroy": (ctypes.c_int, [c_vp]),
@@ -175,6 +178,16 @@ class Context:
         n = c_i64()
         check(self.lib.sbr_ctx_launch_count(self.handle, ctypes.byref(n)))
         return int(n.value)
+
+    def profile(self, enable: bool = True):
+        check(self.lib.sbr_ctx_profile(self.handle, int(bool(enable))))
+
+    def kernel_stats(self) -> dict:
+        tm, tn, pm, pn = c_dbl(), c_i64(), c_dbl(), c_i64()
+        check(self.lib.sbr_ctx_kernel_stats(self.handle, ctypes.byref(tm), ctypes.byref(tn),
+                                            ctypes.byref(pm), ctypes.byref(pn)))
+        return {"trace_ms": tm.value, "trace_launches": int(tn.value), "po_ms": pm.value,
+                "po_launches": int(pn.value)}
 
     @property
     def stream(self) -> int:

@@ -69,7 +69,17 @@ struct sbr_ctx {
     DevBuf<int64_t> seg_base;
     DevBuf<double> k2, gpow, scale;
     DevBuf<double2> amp;
+    // optional per-kernel CUDA-event timing of the solve pipeline
+    bool profile = false;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    double trace_ms = 0.0, po_ms = 0.0;
+    int64_t trace_n = 0, po_n = 0;
     LaunchStats stats() { return LaunchStats{&launches, num_sms}; }
+    ~sbr_ctx()
+    {
+        for (auto &e : ev)
+            if (e) cudaEventDestroy(e);
+    }
 };
 
 struct sbr_mesh {
@@ -778,15 +788,27 @@ static int run_units(sbr_ctx *ctx, const sbr_bvh *bvh, const std::vector<UnitDev
         CUDA_TRY(ctx->chunk_part.reserve((size_t)(slots / kChunk) * nk));
         CUDA_TRY(cudaMemcpyAsync(ctx->units.p, batch.data(), sizeof(UnitDev) * batch.size(),
                                  cudaMemcpyHostToDevice, st));
+        if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev[0], st));
         CUDA_TRY(launch_trace_solve(cfg, ctx->grids.p, ctx->units.p, (int)batch.size(), slots,
                                     ctx->slots.p, ctx->counter.p, st, ctx->stats()));
+        if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev[1], st));
         CUDA_TRY(launch_po(ctx->slots.p, ctx->units.p, (int)batch.size(), slots / kChunk,
                            ctx->k2.p, nk, ctx->gpow.p, cfg.max_bounces, ctx->chunk_part.p,
                            diag_dev, ctx->bad.p, st, ctx->stats()));
+        if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev[2], st));
         CUDA_TRY(launch_seg_reduce(ctx->chunk_part.p, ctx->units.p, (int)batch.size(), nk,
                                    seg_dev, st, ctx->stats()));
         // the units buffer is rewritten by the next batch: keep batches ordered
         CUDA_TRY(cudaStreamSynchronize(st));
+        if (ctx->profile) {
+            float a = 0.f, b = 0.f;
+            CUDA_TRY(cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]));
+            CUDA_TRY(cudaEventElapsedTime(&b, ctx->ev[1], ctx->ev[2]));
+            ctx->trace_ms += a;
+            ctx->po_ms += b;
+            ctx->trace_n += 1;
+            ctx->po_n += 1;
+        }
         u0 = u1;
     }
     return SBR_OK;
@@ -1121,5 +1143,32 @@ extern "C" int sbr_aabb_hit_pairs(sbr_ctx *ctx, const double *box_min, const dou
     CUDA_TRY(cudaMemcpyAsync(hit, h.p, n, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaMemcpyAsync(entry, en.p, 8 * n, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
+    return SBR_OK;
+}
+
+// ---------------------------------------------------------------------------
+// instrumentation
+// ---------------------------------------------------------------------------
+extern "C" int sbr_ctx_profile(sbr_ctx *ctx, int32_t enable)
+{
+    REQUIRE(ctx, "ctx is NULL");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (int rc = set_device(ctx)) return rc;
+    if (enable && !ctx->ev[0])
+        for (auto &e : ctx->ev) CUDA_TRY(cudaEventCreate(&e));
+    ctx->profile = enable != 0;
+    ctx->trace_ms = ctx->po_ms = 0.0;
+    ctx->trace_n = ctx->po_n = 0;
+    return SBR_OK;
+}
+
+extern "C" int sbr_ctx_kernel_stats(sbr_ctx *ctx, double *trace_ms, int64_t *trace_launches,
+                                    double *po_ms, int64_t *po_launches)
+{
+    REQUIRE(ctx, "ctx is NULL");
+    if (trace_ms) *trace_ms = ctx->trace_ms;
+    if (trace_launches) *trace_launches = ctx->trace_n;
+    if (po_ms) *po_ms = ctx->po_ms;
+    if (po_launches) *po_launches = ctx->po_n;
     return SBR_OK;
 }

@@ -1,10 +1,10 @@
 // pipeline.cu -- the hot path: ray launch + multi-bounce traversal,
 // warp-ballot compaction + physical-optics integral, deterministic reduce.
 //
-//   k_trace_solve  persistent warps fetch 32-ray work items with one atomic
-//                  per warp; each lane computes its ray origin on the fly
-//                  from the grid scalars (transport.py:339-345, no record of
-//                  the launch is materialised), walks up to B bounces
+//   k_trace_persistent (trace_persistent.cuh) persistent warps with per-lane
+//                  ray refill; each lane computes its ray origin on the fly
+//                  from the grid scalars (transport.py:339-345, no launch
+//                  record is materialised), walks up to B bounces
 //                  (transport.py:276-327) and stores a 16-byte SlotRec.
 //   k_po           one block per 2048-slot chunk: coalesced SlotRec loads,
 //                  warp __ballot_sync + popc + block scan compact the
@@ -17,6 +17,8 @@
 //   k_seg_reduce / k_finalize  fixed pairwise trees (po.py:59-80 shape)
 //                  over chunk -> segment -> grid partials: results are
 //                  bit-stable and independent of GPU count.
+#include <cstdlib>
+
 #include "pipeline.h"
 #include "traverse.cuh"
 
@@ -61,85 +63,9 @@ __device__ __forceinline__ int64_t warp_fetch(unsigned long long *counter)
 // ---------------------------------------------------------------------------
 constexpr int kTraceThreads = 128;
 
-template <int STORAGE>
-__global__ void __launch_bounds__(kTraceThreads)
-k_trace_solve(TraceCfg cfg, const GridDev *__restrict__ grids,
-              const UnitDev *__restrict__ units, int n_units, int64_t n_items,
-              SlotRec *__restrict__ slots, unsigned long long *counter)
-{
-    const int lane = threadIdx.x & 31;
-    while (true) {
-        const int64_t item = warp_fetch(counter);
-        if (item >= n_items) break;
-        const int64_t slot = item * 32 + lane;
-        const int ui = find_unit(units, n_units, item * 32);
-        const UnitDev U = units[ui];
-        const int64_t r = U.ray_begin + (slot - U.slot_base);
-        const GridDev &G = grids[U.grid];
-        // anti-aliasing launch rule, spacing <= lambda_min / factor
-        // (transport.py:75-81, inclusive); violating grids launch nothing
-        const bool alias_ok = cfg.allow_aliasing || !(G.spacing > cfg.spacing_limit);
-        if (!alias_ok && lane == 0) atomicOr(cfg.error_flag, 1u);
-        SlotRec rec;
-        rec.R = 0.0; rec.cosv = 0.f; rec.meta = 0u;
-        if (r < U.ray_end && alias_ok) {
-            double ox, oy, oz;
-            grid_origin(G, r, ox, oy, oz);
-            const double kx = G.k[0], ky = G.k[1], kz = G.k[2];
-            int visits = 0;
-            RayResult res = trace_ray_walk<STORAGE>(cfg.B, ox, oy, oz, kx, ky, kz,
-                                                    cfg.max_bounces, cfg.eps,
-                                                    cfg.strict != 0, nullptr, visits);
-            double c = -DA(DA(DM(res.n0x, kx), DM(res.n0y, ky)), DM(res.n0z, kz));
-            bool sel = res.valid && (res.escaped || cfg.count_trapped) && c > 0.0;
-            rec.R = res.path;
-            rec.cosv = (float)c;
-            rec.meta = (uint32_t)res.bounces | kMetaActive | (res.valid ? kMetaValid : 0u) |
-                       (res.escaped ? kMetaEscaped : 0u) | (sel ? kMetaSel : 0u);
-        }
-        slots[slot] = rec;
-    }
-}
-
-template <int STORAGE, bool GRID>
-__global__ void __launch_bounds__(kTraceThreads)
-k_trace_full(TraceCfg cfg, const GridDev *__restrict__ grid,
-             const double *__restrict__ orig, const double *__restrict__ dirs, int64_t n,
-             FullOut out, unsigned long long *counter)
-{
-    const int lane = threadIdx.x & 31;
-    const int64_t n_items = (n + 31) / 32;
-    while (true) {
-        const int64_t item = warp_fetch(counter);
-        if (item >= n_items) break;
-        const int64_t r = item * 32 + lane;
-        if (r >= n) continue;  // lanes re-converge at the next warp_fetch
-        double ox, oy, oz, dx, dy, dz;
-        if (GRID) {
-            grid_origin(*grid, r, ox, oy, oz);
-            dx = grid->k[0]; dy = grid->k[1]; dz = grid->k[2];
-        } else {
-            ox = orig[3 * r]; oy = orig[3 * r + 1]; oz = orig[3 * r + 2];
-            dx = dirs[3 * r]; dy = dirs[3 * r + 1]; dz = dirs[3 * r + 2];
-        }
-        int *ids = nullptr;
-        if (out.ids) {
-            ids = out.ids + r * (int64_t)cfg.max_bounces;
-            for (int b = 0; b < cfg.max_bounces; ++b) ids[b] = -1;
-        }
-        int visits = 0;
-        RayResult res = trace_ray_walk<STORAGE>(cfg.B, ox, oy, oz, dx, dy, dz,
-                                                cfg.max_bounces, cfg.eps, cfg.strict != 0,
-                                                ids, visits);
-        out.valid[r] = res.valid ? 1 : 0;
-        out.escaped[r] = res.escaped ? 1 : 0;
-        out.bounces[r] = res.bounces;
-        out.path[r] = res.path;
-        out.n0[3 * r] = res.n0x; out.n0[3 * r + 1] = res.n0y; out.n0[3 * r + 2] = res.n0z;
-        out.out_dir[3 * r] = res.dx; out.out_dir[3 * r + 1] = res.dy;
-        out.out_dir[3 * r + 2] = res.dz;
-    }
-}
+}  // namespace sbr
+#include "trace_persistent.cuh"
+namespace sbr {
 
 template <int STORAGE>
 __global__ void __launch_bounds__(kTraceThreads)
@@ -453,6 +379,36 @@ static int persistent_blocks(K kernel, int threads, int num_sms)
     return per_sm * num_sms;
 }
 
+template <int S, int M>
+static void trace_dispatch(const TraceArgs &a, cudaStream_t st, int num_sms)
+{
+    // occupancy experiment knob (solve path, FP32-exact storage only)
+    static const int occ = getenv("SBR_TRACE_OCC") ? atoi(getenv("SBR_TRACE_OCC")) : 0;
+    if (S == kF32Exact && M == kModeSolve && occ >= 6) {
+        if (occ == 6) {
+            int nb = persistent_blocks(k_trace_persistent<S, M, 6>, kTraceThreads, num_sms);
+            k_trace_persistent<S, M, 6><<<nb, kTraceThreads, 0, st>>>(a);
+        } else if (occ == 7) {
+            int nb = persistent_blocks(k_trace_persistent<S, M, 7>, kTraceThreads, num_sms);
+            k_trace_persistent<S, M, 7><<<nb, kTraceThreads, 0, st>>>(a);
+        } else {
+            int nb = persistent_blocks(k_trace_persistent<S, M, 8>, kTraceThreads, num_sms);
+            k_trace_persistent<S, M, 8><<<nb, kTraceThreads, 0, st>>>(a);
+        }
+        return;
+    }
+    int nb = persistent_blocks(k_trace_persistent<S, M>, kTraceThreads, num_sms);
+    k_trace_persistent<S, M><<<nb, kTraceThreads, 0, st>>>(a);
+}
+
+template <int M>
+static void trace_storage_dispatch(const TraceArgs &a, cudaStream_t st, int num_sms)
+{
+    if (a.cfg.storage == kF64) trace_dispatch<kF64, M>(a, st, num_sms);
+    else if (a.cfg.storage == kSingle) trace_dispatch<kSingle, M>(a, st, num_sms);
+    else trace_dispatch<kF32Exact, M>(a, st, num_sms);
+}
+
 cudaError_t launch_trace_solve(const TraceCfg &cfg, const GridDev *d_grids,
                                const UnitDev *d_units, int n_units, int64_t n_slots,
                                SlotRec *d_slots, unsigned long long *d_counter,
@@ -460,43 +416,17 @@ cudaError_t launch_trace_solve(const TraceCfg &cfg, const GridDev *d_grids,
 {
     cudaError_t e = cudaMemsetAsync(d_counter, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
-    const int64_t n_items = n_slots / 32;
-    switch (cfg.storage) {
-    case kF64: {
-        int nb = persistent_blocks(k_trace_solve<kF64>, kTraceThreads, ls.num_sms);
-        k_trace_solve<kF64><<<nb, kTraceThreads, 0, st>>>(cfg, d_grids, d_units, n_units,
-                                                          n_items, d_slots, d_counter);
-        break;
-    }
-    case kSingle: {
-        int nb = persistent_blocks(k_trace_solve<kSingle>, kTraceThreads, ls.num_sms);
-        k_trace_solve<kSingle><<<nb, kTraceThreads, 0, st>>>(cfg, d_grids, d_units, n_units,
-                                                             n_items, d_slots, d_counter);
-        break;
-    }
-    default: {
-        int nb = persistent_blocks(k_trace_solve<kF32Exact>, kTraceThreads, ls.num_sms);
-        k_trace_solve<kF32Exact><<<nb, kTraceThreads, 0, st>>>(
-            cfg, d_grids, d_units, n_units, n_items, d_slots, d_counter);
-        break;
-    }
-    }
+    TraceArgs a = {};
+    a.cfg = cfg;
+    a.grids = d_grids;
+    a.units = d_units;
+    a.n_units = n_units;
+    a.n_work = n_slots;
+    a.counter = d_counter;
+    a.slots = d_slots;
+    trace_storage_dispatch<kModeSolve>(a, st, ls.num_sms);
     ++*ls.launches;
     return cudaGetLastError();
-}
-
-template <int S>
-static void trace_full_dispatch(const TraceCfg &cfg, const GridDev *g, const double *o,
-                                const double *d, int64_t n, const FullOut &out,
-                                unsigned long long *ctr, cudaStream_t st, int num_sms)
-{
-    if (g) {
-        int nb = persistent_blocks(k_trace_full<S, true>, kTraceThreads, num_sms);
-        k_trace_full<S, true><<<nb, kTraceThreads, 0, st>>>(cfg, g, o, d, n, out, ctr);
-    } else {
-        int nb = persistent_blocks(k_trace_full<S, false>, kTraceThreads, num_sms);
-        k_trace_full<S, false><<<nb, kTraceThreads, 0, st>>>(cfg, g, o, d, n, out, ctr);
-    }
 }
 
 cudaError_t launch_trace_full(const TraceCfg &cfg, const GridDev *d_grid,
@@ -506,14 +436,16 @@ cudaError_t launch_trace_full(const TraceCfg &cfg, const GridDev *d_grid,
 {
     cudaError_t e = cudaMemsetAsync(d_counter, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
-    if (cfg.storage == kF64)
-        trace_full_dispatch<kF64>(cfg, d_grid, d_orig, d_dirs, n, out, d_counter, st, ls.num_sms);
-    else if (cfg.storage == kSingle)
-        trace_full_dispatch<kSingle>(cfg, d_grid, d_orig, d_dirs, n, out, d_counter, st,
-                                     ls.num_sms);
-    else
-        trace_full_dispatch<kF32Exact>(cfg, d_grid, d_orig, d_dirs, n, out, d_counter, st,
-                                       ls.num_sms);
+    TraceArgs a = {};
+    a.cfg = cfg;
+    a.grids = d_grid;
+    a.orig = d_orig;
+    a.dirs = d_dirs;
+    a.n_work = n;
+    a.counter = d_counter;
+    a.full = out;
+    if (d_grid) trace_storage_dispatch<kModeGrid>(a, st, ls.num_sms);
+    else trace_storage_dispatch<kModeList>(a, st, ls.num_sms);
     ++*ls.launches;
     return cudaGetLastError();
 }

@@ -124,13 +124,24 @@ __device__ __forceinline__ double tri_hit_exact(const TriF64 &T, double ox,
     if (det == 0.0) return -1.0;
     double tx = DS(ox, T.ax), ty = DS(oy, T.ay), tz = DS(oz, T.az);
     double un = DA(DA(DM(tx, px), DM(ty, py)), DM(tz, pz));
-    double inv = __drcp_rn(det);  // == IEEE 1.0 / det
-    double u = DM(un, inv);
-    if (u < 0.0 || u > 1.0) return -1.0;
+    // Division-free pre-filters.  They only reject rays the exact test below
+    // rejects too: with 1e-150 < |un|, |det| < 1e150 the rounded product
+    // un * fl(1/det) is a normal number carrying the sign of un*det, so
+    // opposite signs mean u < 0; |un| > 2|det| means u > 1 after rounding.
+    const double adet = fabs(det);
+    const bool safe = adet < 1e150;
+    if (safe && fabs(un) > 1e-150 && ((un < 0.0) != (det < 0.0))) return -1.0;
+    if (safe && fabs(un) > 2.0 * adet) return -1.0;
     double qx = DS(DM(ty, T.e1z), DM(tz, T.e1y));
     double qy = DS(DM(tz, T.e1x), DM(tx, T.e1z));
     double qz = DS(DM(tx, T.e1y), DM(ty, T.e1x));
-    double v = DM(DA(DA(DM(dx, qx), DM(dy, qy)), DM(dz, qz)), inv);
+    double vn = DA(DA(DM(dx, qx), DM(dy, qy)), DM(dz, qz));
+    if (safe && fabs(vn) > 1e-150 && ((vn < 0.0) != (det < 0.0))) return -1.0;
+    // exact reference sequence (geometry.py:340-352)
+    double inv = __drcp_rn(det);  // == IEEE 1.0 / det
+    double u = DM(un, inv);
+    if (u < 0.0 || u > 1.0) return -1.0;
+    double v = DM(vn, inv);
     if (v < 0.0 || DA(u, v) > 1.0) return -1.0;
     double t = DM(DA(DA(DM(T.e2x, qx), DM(T.e2y, qy)), DM(T.e2z, qz)), inv);
     if (t <= t_min || t > t_max) return -1.0;

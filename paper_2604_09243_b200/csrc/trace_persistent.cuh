@@ -1,0 +1,347 @@
+// trace_persistent.cuh -- persistent, warp-cooperative multi-bounce tracer.
+//
+// Every lane is a small state machine over (ray, query, traversal step):
+//
+//   IDLE  -> fetch a ray index from the warp's private chunk of the global
+//            work counter (one atomic per kChunkRays rays per warp), build
+//            its origin on the fly (transport.py:339-345) and start query 0
+//   TRAV  -> one BVH node per step: conservative FP32 slab tests of both
+//            children (child-pair node, four 16-byte loads), near child
+//            next, far child onto the stack
+//   LEAF  -> exact FP64 Moller-Trumbore on the leaf's triangles
+//   DONE  -> query finished: the bounce logic of transport.py:293-326
+//            (flip / strict / reflect / epsilon offset / escape probe) and
+//            either the next query or the ray's output record
+//
+// The warp loop is "while-while" (Aila & Laine 2009): node steps repeat
+// while any lane is traversing, lanes that reached a leaf wait, then all
+// pending leaves are intersected together, then finished queries advance
+// and idle lanes are refilled.  A lane never waits for a whole other ray
+// (bounce counts and miss/hit mixes no longer serialise the warp), only for
+// the current traversal phase.
+//
+// Results are bit-identical to trace_ray_walk() / the reference: every
+// query still returns the lexicographic (t, id) minimum over accepted
+// triangles, and the per-bounce FP64 arithmetic is unchanged.
+#pragma once
+
+#include "pipeline.h"
+#include "traverse.cuh"
+
+namespace sbr {
+
+constexpr int kChunkRays = 128;   // rays claimed per warp-level atomic
+
+enum LaneState : int { kIdle = 0, kTrav = 1, kLeaf = 2, kDone = 3 };
+enum TraceMode : int { kModeSolve = 0, kModeGrid = 1, kModeList = 2 };
+
+struct TraceArgs {
+    TraceCfg cfg;
+    // work source
+    const GridDev *grids;     // solve: all grids; grid mode: the one grid
+    const UnitDev *units;     // solve only
+    int n_units;
+    const double *orig, *dirs;  // list mode
+    int64_t n_work;           // solve: slots; grid/list: rays
+    unsigned long long *counter;
+    // outputs
+    SlotRec *slots;           // solve
+    FullOut full;             // grid / list
+};
+
+struct LaneRay {
+    // ray + walk state (FP64, transport.py:276-327)
+    double ox, oy, oz, dx, dy, dz;
+    double path, n0x, n0y, n0z;
+    double cosd;     // solve mode: -(n0 . k_inc) of the first hit
+    double best_t;
+    int best;
+    int bounces;
+    bool valid, probe;
+    // traversal state
+    RayBox rb;
+    float tmax;
+    int ref, sp;
+    int pend;        // parked leaf reference (0: none)
+    // bookkeeping
+    int64_t r;       // ray index within its grid / list
+    int64_t slot;    // output slot (solve) or ray index
+    int grid;
+};
+
+template <int STORAGE>
+__device__ __forceinline__ void start_query(const BvhView &B, LaneRay &L, int &state)
+{
+    L.rb = make_raybox(B, L.ox, L.oy, L.oz, L.dx, L.dy, L.dz);
+    L.best_t = __longlong_as_double(0x7ff0000000000000LL);
+    L.best = -1;
+    L.tmax = __int_as_float(0x7f800000);
+    L.sp = 0;
+    L.pend = 0;
+    L.ref = B.root;
+    state = L.ref >= 0 ? kTrav : kLeaf;
+}
+
+// exact test of one leaf's triangles; true = any-hit probe satisfied
+template <int STORAGE>
+__device__ __forceinline__ bool leaf_test(const BvhView &B, LaneRay &L, int leaf)
+{
+    const int first = leaf_first(leaf), cnt = leaf_count(leaf);
+    for (int k = first; k < first + cnt; ++k) {
+        const TriF64 T = load_tri<STORAGE>(B, k);
+        const double t = tri_hit_exact(T, L.ox, L.oy, L.oz, L.dx, L.dy, L.dz, 0.0, L.best_t);
+        if (t > 0.0 && (t < L.best_t || (t == L.best_t && T.id < L.best))) {
+            L.best_t = t;
+            L.best = T.id;
+            L.tmax = __double2float_ru(t);
+            if (L.probe) return true;   // escape probe: any hit decides
+        }
+    }
+    return false;
+}
+
+// pop the next stack entry whose entry distance can still beat best_t
+__device__ __forceinline__ bool pop_next(StackEntry *stack, LaneRay &L)
+{
+    while (L.sp > 0) {
+        --L.sp;
+        if (stack[L.sp].tn <= L.tmax) {
+            L.ref = stack[L.sp].ref;
+            return true;
+        }
+    }
+    return false;
+}
+
+// MINB = 8 caps registers at 64 (32 resident warps per SM): measured
+// faster than unconstrained 80-92 registers despite a few spills, since the
+// traversal is latency-bound.
+template <int STORAGE, int MODE, int MINB = 8>
+__global__ void __launch_bounds__(128, MINB)
+k_trace_persistent(TraceArgs a)
+{
+    const TraceCfg &cfg = a.cfg;
+    const BvhView &B = cfg.B;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1u;
+
+    StackEntry stack[kStack];
+    LaneRay L;
+    int state = kIdle;
+    bool exhausted = false;
+    int64_t chunk_next = 0, chunk_end = 0;   // warp-uniform private work range
+
+    while (true) {
+        // ---------------- refill idle lanes -------------------------------
+        const unsigned want = __ballot_sync(0xffffffffu, state == kIdle && !exhausted);
+        if (want) {
+            // warp-uniform bookkeeping: [chunk_next, chunk_end) is this warp's
+            // private slice of the global work counter
+            const int need = __popc(want);
+            const int64_t avail = chunk_end - chunk_next;
+            int64_t fresh = 0;
+            if (avail < need) {
+                unsigned long long base = 0;
+                if (lane == 0) base = atomicAdd(a.counter, (unsigned long long)kChunkRays);
+                fresh = (int64_t)__shfl_sync(0xffffffffu, base, 0);
+            }
+            if (want & (1u << lane)) {
+                const int rank = __popc(want & lt_mask);
+                const int64_t w = rank < avail ? chunk_next + rank : fresh + (rank - avail);
+                if (w < a.n_work) L.slot = w; else exhausted = true;
+            }
+            if (avail >= need) {
+                chunk_next += need;
+            } else {
+                chunk_next = fresh + (need - avail);
+                chunk_end = fresh + kChunkRays;
+            }
+            if (state == kIdle && !exhausted && (want & (1u << lane))) {
+                // ---------------- ray setup -------------------------------
+                bool real = true;
+                const GridDev *G = nullptr;
+                if (MODE == kModeSolve) {
+                    const int ui = find_unit(a.units, a.n_units, L.slot);
+                    const UnitDev U = a.units[ui];
+                    L.r = U.ray_begin + (L.slot - U.slot_base);
+                    L.grid = U.grid;
+                    G = a.grids + U.grid;
+                    real = L.r < U.ray_end;
+                    const bool alias_ok = cfg.allow_aliasing || !(G->spacing > cfg.spacing_limit);
+                    if (!alias_ok) {
+                        atomicOr(cfg.error_flag, 1u);
+                        real = false;
+                    }
+                    if (!real) {
+                        SlotRec z;
+                        z.R = 0.0; z.cosv = 0.f; z.meta = 0u;
+                        a.slots[L.slot] = z;
+                    }
+                } else if (MODE == kModeGrid) {
+                    L.r = L.slot;
+                    G = a.grids;
+                } else {
+                    L.r = L.slot;
+                }
+                if (real) {
+                    if (MODE == kModeList) {
+                        L.ox = a.orig[3 * L.r]; L.oy = a.orig[3 * L.r + 1];
+                        L.oz = a.orig[3 * L.r + 2];
+                        L.dx = a.dirs[3 * L.r]; L.dy = a.dirs[3 * L.r + 1];
+                        L.dz = a.dirs[3 * L.r + 2];
+                    } else {
+                        grid_origin(*G, L.r, L.ox, L.oy, L.oz);
+                        L.dx = G->k[0]; L.dy = G->k[1]; L.dz = G->k[2];
+                    }
+                    if (MODE != kModeSolve && a.full.ids) {
+                        int *ids = a.full.ids + L.r * (int64_t)cfg.max_bounces;
+                        for (int b = 0; b < cfg.max_bounces; ++b) ids[b] = -1;
+                    }
+                    L.path = 0.0; L.n0x = L.n0y = L.n0z = 0.0; L.cosd = 0.0;
+                    L.bounces = 0; L.valid = false; L.probe = false;
+                    start_query<STORAGE>(B, L, state);
+                }
+            }
+        }
+        if (!__any_sync(0xffffffffu, state != kIdle || !exhausted)) break;
+
+        // ---------------- traversal phase ---------------------------------
+        // Speculative while-while: a lane that reaches its first leaf parks
+        // it in L.pend and keeps traversing; the phase ends once every
+        // traversing lane has a parked leaf (or stopped at a second leaf).
+        while (__any_sync(0xffffffffu, state == kTrav && L.pend == 0)) {
+            if (state == kTrav) {
+                const Node *np = B.nodes + L.ref;
+                const float4 na = __ldg(&np->a), nb = __ldg(&np->b), nc = __ldg(&np->c);
+                const int4 nd = __ldg(&np->d);
+                bool h0, h1;
+                const float t0 = slab(L.rb, na.x, na.y, na.z, na.w, nb.x, nb.y, L.tmax, h0);
+                const float t1 = slab(L.rb, nb.z, nb.w, nc.x, nc.y, nc.z, nc.w, L.tmax, h1);
+                bool have = true;
+                if (h0 && h1) {
+                    int nr = nd.x, fr = nd.y;
+                    float ft = t1;
+                    if (t1 < t0) { nr = nd.y; fr = nd.x; ft = t0; }
+                    stack[L.sp].ref = fr;
+                    stack[L.sp].tn = ft;
+                    ++L.sp;
+                    L.ref = nr;
+                } else if (h0 || h1) {
+                    L.ref = h0 ? nd.x : nd.y;
+                } else {
+                    have = pop_next(stack, L);
+                }
+                if (!have) {
+                    state = L.pend ? kLeaf : kDone;   // kLeaf with ref < 0 unset: pend only
+                    L.ref = 0;
+                } else if (L.ref < 0) {
+                    if (L.pend == 0) {
+                        L.pend = L.ref;               // park the first leaf
+                        if (!pop_next(stack, L)) { state = kLeaf; L.ref = 0; }
+                        else if (L.ref < 0) state = kLeaf;   // second leaf: stop here
+                    } else {
+                        state = kLeaf;                // parked leaf + this one
+                    }
+                }
+            }
+        }
+
+        // ---------------- leaf phase --------------------------------------
+        // parked leaf first, then (kLeaf lanes) the leaf in L.ref and any
+        // further leaves popped straight off the stack
+        if (L.pend != 0 && (state == kTrav || state == kLeaf)) {
+            const int leaf = L.pend;
+            L.pend = 0;
+            if (leaf_test<STORAGE>(B, L, leaf)) state = kDone;
+        }
+        while (state == kLeaf) {
+            if (L.ref < 0) {
+                if (leaf_test<STORAGE>(B, L, L.ref)) { state = kDone; break; }
+            }
+            if (!pop_next(stack, L)) state = kDone;
+            else if (L.ref >= 0) state = kTrav;
+        }
+
+        // ---------------- query completion (transport.py:293-326) ---------
+        if (state == kDone) {
+            bool finish = false, escaped = false;
+            if (L.probe) {
+                escaped = L.best < 0;
+                finish = true;
+            } else if (L.best < 0) {
+                escaped = true;
+                finish = true;
+            } else {
+                const double t = L.best_t;
+                const double *n = B.normals + 3 * (int64_t)L.best;
+                double nx = __ldg(n), ny = __ldg(n + 1), nz = __ldg(n + 2);
+                double ndd = DA(DA(DM(nx, L.dx), DM(ny, L.dy)), DM(nz, L.dz));
+                bool strict_out = false;
+                if (ndd > 0.0) {
+                    if (cfg.strict && L.bounces == 0) {
+                        strict_out = true;
+                    } else {
+                        nx = -nx; ny = -ny; nz = -nz; ndd = -ndd;
+                    }
+                }
+                if (strict_out) {
+                    // transport.py:306-307: invalid, escaped, direction kept
+                    L.valid = false;
+                    L.bounces = 0;
+                    L.path = 0.0;
+                    L.n0x = L.n0y = L.n0z = 0.0;
+                    escaped = true;
+                    finish = true;
+                } else {
+                    if (MODE != kModeSolve && a.full.ids)
+                        a.full.ids[L.r * (int64_t)cfg.max_bounces + L.bounces] = L.best;
+                    const double hx = DA(L.ox, DM(t, L.dx)), hy = DA(L.oy, DM(t, L.dy)),
+                                 hz = DA(L.oz, DM(t, L.dz));
+                    L.path = DA(L.path, t);
+                    L.bounces += 1;
+                    if (L.bounces == 1) {
+                        L.valid = true;
+                        // solve mode keeps only cos = -(n0 . k_inc) (po.py:99);
+                        // d == k_inc here, so -ndd is that dot product exactly
+                        if (MODE == kModeSolve) L.cosd = -ndd;
+                        else { L.n0x = nx; L.n0y = ny; L.n0z = nz; }
+                    }
+                    const double s = DM(2.0, ndd);
+                    L.dx = DS(L.dx, DM(s, nx));
+                    L.dy = DS(L.dy, DM(s, ny));
+                    L.dz = DS(L.dz, DM(s, nz));
+                    L.ox = DA(hx, DM(cfg.eps, nx));
+                    L.oy = DA(hy, DM(cfg.eps, ny));
+                    L.oz = DA(hz, DM(cfg.eps, nz));
+                    if (L.bounces == cfg.max_bounces) L.probe = true;  // budget spent
+                    start_query<STORAGE>(B, L, state);
+                }
+            }
+            if (finish) {
+                if (MODE == kModeSolve) {
+                    const double c = L.valid ? L.cosd : 0.0;
+                    const bool sel = L.valid && (escaped || cfg.count_trapped) && c > 0.0;
+                    SlotRec rec;
+                    rec.R = L.path;
+                    rec.cosv = (float)c;
+                    rec.meta = (uint32_t)L.bounces | kMetaActive | (L.valid ? kMetaValid : 0u) |
+                               (escaped ? kMetaEscaped : 0u) | (sel ? kMetaSel : 0u);
+                    a.slots[L.slot] = rec;
+                } else {
+                    const int64_t r = L.r;
+                    a.full.valid[r] = L.valid ? 1 : 0;
+                    a.full.escaped[r] = escaped ? 1 : 0;
+                    a.full.bounces[r] = L.bounces;
+                    a.full.path[r] = L.path;
+                    a.full.n0[3 * r] = L.n0x; a.full.n0[3 * r + 1] = L.n0y;
+                    a.full.n0[3 * r + 2] = L.n0z;
+                    a.full.out_dir[3 * r] = L.dx; a.full.out_dir[3 * r + 1] = L.dy;
+                    a.full.out_dir[3 * r + 2] = L.dz;
+                }
+                state = kIdle;
+            }
+        }
+    }
+}
+
+}  // namespace sbr

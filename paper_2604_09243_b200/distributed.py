@@ -72,9 +72,10 @@ def solve_grids_distributed(tree, mesh, grids: Sequence, trace_params, wavenumbe
                             gamma: float = -1.0, count_trapped: bool = False,
                             shard_mode: str = "angles", root: int = 0, group=None,
                             lambda_min: Optional[float] = None, allow_aliasing: bool = True,
-                            timer: Optional[Callable] = None):
+                            timer: Optional[Callable] = None, stats: Optional[dict] = None):
     """Sharded fused solve; returns the sweep.SolveResult on ``root`` and
-    None elsewhere.  Every rank must call it with identical arguments."""
+    None elsewhere.  Every rank must call it with identical arguments.
+    ``stats`` (optional) receives this rank's own query count."""
     import torch
     import torch.distributed as dist
     from .sweep import SolveResult, grid_array
@@ -103,6 +104,8 @@ def solve_grids_distributed(tree, mesh, grids: Sequence, trace_params, wavenumbe
     ctx.synchronize()   # library stream -> visible to NCCL on torch's stream
     if timer:
         timer("traced")
+    if stats is not None:
+        stats["local_queries"] = int(diag[:, 1].sum().item())
     reduce_partials(seg, diag, root, group)
     if rank != root:
         return None
@@ -117,3 +120,21 @@ def solve_grids_distributed(tree, mesh, grids: Sequence, trace_params, wavenumbe
                                    nat.c_vp(seg.data_ptr()), nat.c_vp(diag.data_ptr()),
                                    nat.ptr(amp), ctypes.byref(dg)), "sbr_finalize")
     return SolveResult(amp.view(np.complex128)[..., 0], valid, maxb, hist, queries)
+
+
+def run_sweep_distributed(config, mesh=None, shard_mode: str = "angles", root: int = 0,
+                          group=None):
+    """``sweep.run_sweep`` across the ranks of the process group: every rank
+    builds the (replicated) BVH on its GPU and traces its shard of the
+    cells; the SweepResult is returned on ``root`` (None elsewhere)."""
+    from . import sweep as S
+    from .geometry import load_mesh
+    if mesh is None:
+        mesh = load_mesh(config.mesh_path, dtype=config.dtype())
+
+    def solver(tree, m, grids, tp, ks, gamma, count_trapped, lambda_min=None,
+               allow_aliasing=True):
+        return solve_grids_distributed(tree, m, grids, tp, ks, gamma, count_trapped,
+                                       shard_mode=shard_mode, root=root, group=group,
+                                       lambda_min=lambda_min, allow_aliasing=allow_aliasing)
+    return S._run_sweep(config, mesh, solver)
