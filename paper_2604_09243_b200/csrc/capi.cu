@@ -69,6 +69,8 @@ struct sbr_ctx {
     DevBuf<int64_t> seg_base;
     DevBuf<double> k2, gpow, scale;
     DevBuf<double2> amp;
+    DevBuf<double> stage;        // host->device staging (mesh ingest, records)
+    Arena ws;                    // LBVH build workspace
     // optional per-kernel CUDA-event timing of the solve pipeline
     bool profile = false;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -175,8 +177,6 @@ extern "C" int sbr_ctx_launch_count(sbr_ctx *ctx, int64_t *count_out)
 // ---------------------------------------------------------------------------
 // mesh
 // ---------------------------------------------------------------------------
-static bool f32_exact(double x) { return (double)(float)x == x; }
-
 extern "C" int sbr_mesh_create(sbr_ctx *ctx, const double *v0, const double *v1,
                                const double *v2, const double *normals, int64_t ntri,
                                int32_t storage, sbr_mesh **out)
@@ -189,55 +189,48 @@ extern "C" int sbr_mesh_create(sbr_ctx *ctx, const double *v0, const double *v1,
             storage);
     std::lock_guard<std::mutex> lk(ctx->mu);
     if (int rc = set_device(ctx)) return rc;
-    std::vector<double> verts((size_t)ntri * 9);
-    bool all_f32 = true, finite = true;
-    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
-    double clo[3] = {INFINITY, INFINITY, INFINITY}, chi[3] = {-INFINITY, -INFINITY, -INFINITY};
-    for (int64_t t = 0; t < ntri; ++t) {
-        const double *src[3] = {v0 + 3 * t, v1 + 3 * t, v2 + 3 * t};
-        for (int c = 0; c < 3; ++c)
-            for (int a = 0; a < 3; ++a) {
-                double x = src[c][a];
-                verts[9 * t + 3 * c + a] = x;
-                all_f32 &= f32_exact(x);
-                finite &= std::isfinite(x);
-            }
-        for (int a = 0; a < 3; ++a) {
-            double mn = fmin(fmin(src[0][a], src[1][a]), src[2][a]);
-            double mx = fmax(fmax(src[0][a], src[1][a]), src[2][a]);
-            lo[a] = fmin(lo[a], mn);
-            hi[a] = fmax(hi[a], mx);
-            double cc = (mn + mx) * 0.5;
-            clo[a] = fmin(clo[a], cc);
-            chi[a] = fmax(chi[a], cc);
-        }
-    }
-    REQUIRE(finite, "mesh has non-finite vertex coordinates");
-    int st = storage;
-    if (st == SBR_STORAGE_AUTO) st = all_f32 ? SBR_STORAGE_F32_EXACT : SBR_STORAGE_F64;
-    REQUIRE(!(st == SBR_STORAGE_F32_EXACT || st == SBR_STORAGE_SINGLE) || all_f32,
-            "storage requires float32-representable vertices");
+    // Raw SoA upload, then one device pass interleaves the (T,9) vertex
+    // records and reduces the AABB, centroid bounds and the finite /
+    // float32-representable flags (no host-side loop over the mesh).
     sbr_mesh *m = new sbr_mesh();
     m->ctx = ctx;
     m->ntri = ntri;
-    m->storage = st;
-    for (int a = 0; a < 3; ++a) {
-        m->aabb[a] = lo[a]; m->aabb[3 + a] = hi[a];
-        m->cmin[a] = clo[a]; m->cmax[a] = chi[a];
-    }
+    MeshIngest ing;
     cudaError_t e = m->verts.alloc((size_t)ntri * 9);
     if (e == cudaSuccess) e = m->normals.alloc((size_t)ntri * 3);
+    if (e == cudaSuccess) e = ctx->stage.reserve((size_t)ntri * 9);
     if (e == cudaSuccess)
-        e = cudaMemcpyAsync(m->verts.p, verts.data(), sizeof(double) * 9 * ntri,
-                            cudaMemcpyHostToDevice, ctx->stream);
+        e = cudaMemcpyAsync(ctx->stage.p, v0, 24 * ntri, cudaMemcpyHostToDevice, ctx->stream);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(ctx->stage.p + 3 * ntri, v1, 24 * ntri, cudaMemcpyHostToDevice,
+                            ctx->stream);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(ctx->stage.p + 6 * ntri, v2, 24 * ntri, cudaMemcpyHostToDevice,
+                            ctx->stream);
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(m->normals.p, normals, sizeof(double) * 3 * ntri,
                             cudaMemcpyHostToDevice, ctx->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e == cudaSuccess)
+        e = mesh_ingest(ctx->stage.p, ntri, m->verts.p, ing, ctx->stream, &ctx->launches);
     if (e != cudaSuccess) {
         delete m;
         return fail(e == cudaErrorMemoryAllocation ? SBR_ENOMEM : SBR_ECUDA, "mesh upload: %s",
                     cudaGetErrorString(e));
+    }
+    if (!ing.finite) {
+        delete m;
+        return fail(SBR_EINVAL, "mesh has non-finite vertex coordinates");
+    }
+    int st = storage;
+    if (st == SBR_STORAGE_AUTO) st = ing.all_f32 ? SBR_STORAGE_F32_EXACT : SBR_STORAGE_F64;
+    if ((st == SBR_STORAGE_F32_EXACT || st == SBR_STORAGE_SINGLE) && !ing.all_f32) {
+        delete m;
+        return fail(SBR_EINVAL, "storage requires float32-representable vertices");
+    }
+    m->storage = st;
+    for (int a = 0; a < 3; ++a) {
+        m->aabb[a] = ing.lo[a]; m->aabb[3 + a] = ing.hi[a];
+        m->cmin[a] = ing.clo[a]; m->cmax[a] = ing.chi[a];
     }
     *out = m;
     return SBR_OK;
@@ -297,7 +290,7 @@ extern "C" int sbr_bvh_build(sbr_ctx *ctx, const sbr_mesh *mesh,
         in.frame[a] = b->frame[a];
     }
     memcpy(in.aabb, mesh->aabb, sizeof(in.aabb));
-    cudaError_t e = lbvh_build(in, b->out, ctx->stream, &ctx->launches);
+    cudaError_t e = lbvh_build(in, b->out, ctx->ws, ctx->stream, &ctx->launches);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     if (e != cudaSuccess) {
         delete b;

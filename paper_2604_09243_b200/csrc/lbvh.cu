@@ -19,6 +19,8 @@
 //                    outward.
 //   6. k_pack_tris : triangles gathered into leaf order (48 B FP32-exact or
 //                    80 B FP64 records with the original id embedded).
+#include <cstring>
+
 #include <cub/cub.cuh>
 
 #include "lbvh.h"
@@ -243,32 +245,135 @@ static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / 
         if (e_ != cudaSuccess) return e_;                         \
     } while (0)
 
-cudaError_t lbvh_build(const LbvhInput &in, LbvhOutput &out, cudaStream_t st,
+// ---------------------------------------------------------------------------
+// mesh ingest: SoA -> (T,9) records + bounds / flags reductions
+// ---------------------------------------------------------------------------
+// order-preserving map double -> uint64 so atomicMin/Max work on doubles
+__device__ __forceinline__ unsigned long long ord_of(double x)
+{
+    const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+}
+static inline double unord(unsigned long long u)
+{
+    const unsigned long long b = (u >> 63) ? (u & 0x7fffffffffffffffULL) : ~u;
+    double x;
+    memcpy(&x, &b, sizeof(x));
+    return x;
+}
+
+// red[0..5] = min (lo xyz, centroid lo xyz), red[6..11] = max, red[12] =
+// non-finite flag, red[13] = not-float32-representable flag
+__global__ void k_ingest(const double *__restrict__ soa, int64_t n, double *__restrict__ verts,
+                         unsigned long long *__restrict__ red)
+{
+    double mn[6], mx[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) { mn[q] = INFINITY; mx[q] = -INFINITY; }
+    bool bad = false, not32 = false;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        double v[9];
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const double x = soa[c * 3 * n + 3 * t + a];
+                v[3 * c + a] = x;
+                bad |= !isfinite(x);
+                not32 |= (double)(float)x != x;
+            }
+#pragma unroll
+        for (int q = 0; q < 9; ++q) verts[9 * t + q] = v[q];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const double lo = fmin(fmin(v[a], v[3 + a]), v[6 + a]);
+            const double hi = fmax(fmax(v[a], v[3 + a]), v[6 + a]);
+            const double cc = (lo + hi) * 0.5;
+            mn[a] = fmin(mn[a], lo); mx[a] = fmax(mx[a], hi);
+            mn[3 + a] = fmin(mn[3 + a], cc); mx[3 + a] = fmax(mx[3 + a], cc);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+            mn[q] = fmin(mn[q], __shfl_xor_sync(0xffffffffu, mn[q], o));
+            mx[q] = fmax(mx[q], __shfl_xor_sync(0xffffffffu, mx[q], o));
+        }
+    }
+    bad = __any_sync(0xffffffffu, bad);
+    not32 = __any_sync(0xffffffffu, not32);
+    if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+            atomicMin(&red[q], ord_of(mn[q]));
+            atomicMax(&red[6 + q], ord_of(mx[q]));
+        }
+        if (bad) atomicOr(&red[12], 1ULL);
+        if (not32) atomicOr(&red[13], 1ULL);
+    }
+}
+
+cudaError_t mesh_ingest(const double *d_soa, int64_t ntri, double *d_verts, MeshIngest &out,
+                        cudaStream_t st, int64_t *launches)
+{
+    DevBuf<unsigned long long> red(14);
+    CK(red.status());
+    unsigned long long init[14];
+    for (int q = 0; q < 6; ++q) { init[q] = ~0ULL; init[6 + q] = 0ULL; }
+    init[12] = init[13] = 0ULL;
+    CK(cudaMemcpyAsync(red.p, init, sizeof(init), cudaMemcpyHostToDevice, st));
+    int64_t want = (ntri + 255) / 256;
+    unsigned nb = (unsigned)(want < 4096 ? (want > 0 ? want : 1) : 4096);
+    k_ingest<<<nb, 256, 0, st>>>(d_soa, ntri, d_verts, red.p);
+    ++*launches;
+    CK(cudaGetLastError());
+    unsigned long long res[14];
+    CK(cudaMemcpyAsync(res, red.p, sizeof(res), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int a = 0; a < 3; ++a) {
+        out.lo[a] = unord(res[a]);
+        out.clo[a] = unord(res[3 + a]);
+        out.hi[a] = unord(res[6 + a]);
+        out.chi[a] = unord(res[9 + a]);
+    }
+    out.finite = res[12] == 0ULL;
+    out.all_f32 = res[13] == 0ULL;
+    return cudaSuccess;
+}
+
+cudaError_t lbvh_build(const LbvhInput &in, LbvhOutput &out, Arena &ws, cudaStream_t st,
                        int64_t *launches)
 {
     const int64_t n = in.ntri;
     const int T = 256;
-    DevBuf<double> tri_box(6 * n);
-    DevBuf<uint64_t> keys(n), keys2(n);
-    DevBuf<int> vals(n), order(n);
-    CK(tri_box.status()); CK(keys.status()); CK(keys2.status());
-    CK(vals.status()); CK(order.status());
+    const int64_t ni = n > 1 ? n - 1 : 1;
+    // one grow-only workspace for every temporary (no per-build cudaMalloc)
+    size_t sort_bytes = 0, scan_bytes = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (uint64_t *)nullptr,
+                                       (uint64_t *)nullptr, (int *)nullptr, (int *)nullptr,
+                                       (int)n, 0, 63, st));
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (int *)nullptr, (int *)nullptr,
+                                     (int)ni, st));
+    const size_t need = 256 * 20 + 48 * n + 16 * n + 8 * n + sort_bytes + 16 * ni + 8 * n +
+                        12 * ni + 48 * ni + 4 + scan_bytes;
+    CK(ws.reserve(need));
+    double *tri_box = ws.take<double>(6 * n);
+    uint64_t *keys = ws.take<uint64_t>(n), *keys2 = ws.take<uint64_t>(n);
+    int *vals = ws.take<int>(n), *order = ws.take<int>(n);
+    unsigned char *sort_tmp = ws.take<unsigned char>(sort_bytes);
 
     double3 cmin = make_double3(in.cmin[0], in.cmin[1], in.cmin[2]);
     double ext[3] = {in.cmax[0] - in.cmin[0], in.cmax[1] - in.cmin[1], in.cmax[2] - in.cmin[2]};
     double3 cinv = make_double3(ext[0] > 0 ? 1.0 / ext[0] : 0.0, ext[1] > 0 ? 1.0 / ext[1] : 0.0,
                                 ext[2] > 0 ? 1.0 / ext[2] : 0.0);
-    k_morton<<<nblk(n, T), T, 0, st>>>(in.d_verts, n, cmin, cinv, tri_box.p, keys.p, vals.p);
+    k_morton<<<nblk(n, T), T, 0, st>>>(in.d_verts, n, cmin, cinv, tri_box, keys, vals);
     ++*launches;
     CK(cudaGetLastError());
 
-    size_t tmp_bytes = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys.p, keys2.p, vals.p, order.p,
-                                       (int)n, 0, 63, st));
-    DevBuf<unsigned char> tmp(tmp_bytes);
-    CK(tmp.status());
-    CK(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, keys.p, keys2.p, vals.p, order.p,
-                                       (int)n, 0, 63, st));
+    CK(cub::DeviceRadixSort::SortPairs(sort_tmp, sort_bytes, keys, keys2, vals, order, (int)n,
+                                       0, 63, st));
     ++*launches;
 
     out.n_leaf_slots = n;
@@ -281,12 +386,12 @@ cudaError_t lbvh_build(const LbvhInput &in, LbvhOutput &out, cudaStream_t st,
     } else {
         CK(out.tri32.alloc(3 * n));
     }
-    k_pack_tris<<<nblk(n, T), T, 0, st>>>(in.d_verts, order.p, n, in.storage, out.tri32.p,
+    k_pack_tris<<<nblk(n, T), T, 0, st>>>(in.d_verts, order, n, in.storage, out.tri32.p,
                                           out.tri64.p);
     ++*launches;
     CK(cudaGetLastError());
     CK(out.leaf_ids.alloc(n));
-    CK(cudaMemcpyAsync(out.leaf_ids.p, order.p, sizeof(int) * n, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(out.leaf_ids.p, order, sizeof(int) * n, cudaMemcpyDeviceToDevice, st));
 
     if (n <= in.n_leaf) {
         // single leaf: node 0 carries the leaf in both child slots
@@ -314,47 +419,41 @@ cudaError_t lbvh_build(const LbvhInput &in, LbvhOutput &out, cudaStream_t st,
         return cudaSuccess;
     }
 
-    const int64_t ni = n - 1;
-    DevBuf<int2> child(ni), range(ni);
-    DevBuf<int> parent(2 * n - 1), arrive(ni), keep(ni), relabel(ni), dmax(1);
-    DevBuf<double> node_box(6 * ni);
-    CK(child.status()); CK(range.status()); CK(parent.status()); CK(arrive.status());
-    CK(keep.status()); CK(relabel.status()); CK(node_box.status()); CK(dmax.status());
+    int2 *child = ws.take<int2>(ni), *range = ws.take<int2>(ni);
+    int *parent = ws.take<int>(2 * n - 1), *arrive = ws.take<int>(ni);
+    int *keep = ws.take<int>(ni), *relabel = ws.take<int>(ni), *dmax = ws.take<int>(1);
+    double *node_box = ws.take<double>(6 * ni);
+    unsigned char *scan_tmp = ws.take<unsigned char>(scan_bytes);
 
-    k_karras<<<nblk(ni, T), T, 0, st>>>(keys2.p, n, child.p, range.p, parent.p);
+    k_karras<<<nblk(ni, T), T, 0, st>>>(keys2, n, child, range, parent);
     ++*launches;
     CK(cudaGetLastError());
-    CK(cudaMemsetAsync(arrive.p, 0, sizeof(int) * ni, st));
-    k_refit<<<nblk(n, T), T, 0, st>>>(tri_box.p, order.p, n, child.p, parent.p, node_box.p,
-                                      arrive.p);
+    CK(cudaMemsetAsync(arrive, 0, sizeof(int) * ni, st));
+    k_refit<<<nblk(n, T), T, 0, st>>>(tri_box, order, n, child, parent, node_box, arrive);
     ++*launches;
     CK(cudaGetLastError());
-    k_keep<<<nblk(ni, T), T, 0, st>>>(range.p, n, in.n_leaf, keep.p);
+    k_keep<<<nblk(ni, T), T, 0, st>>>(range, n, in.n_leaf, keep);
     ++*launches;
     CK(cudaGetLastError());
 
-    size_t scan_bytes = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, keep.p, relabel.p, (int)ni, st));
-    DevBuf<unsigned char> scan_tmp(scan_bytes);
-    CK(scan_tmp.status());
-    CK(cub::DeviceScan::ExclusiveSum(scan_tmp.p, scan_bytes, keep.p, relabel.p, (int)ni, st));
+    CK(cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, keep, relabel, (int)ni, st));
     ++*launches;
     int last_keep = 0, last_rel = 0;
-    CK(cudaMemcpyAsync(&last_keep, keep.p + ni - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&last_rel, relabel.p + ni - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&last_keep, keep + ni - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&last_rel, relabel + ni - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     const int64_t nk = (int64_t)last_keep + last_rel;
     CK(out.nodes.alloc(nk));
-    k_emit<<<nblk(ni, T), T, 0, st>>>(child.p, range.p, keep.p, relabel.p, node_box.p,
-                                      tri_box.p, order.p, n, c, out.nodes.p);
+    k_emit<<<nblk(ni, T), T, 0, st>>>(child, range, keep, relabel, node_box, tri_box, order, n,
+                                      c, out.nodes.p);
     ++*launches;
     CK(cudaGetLastError());
-    CK(cudaMemsetAsync(dmax.p, 0, sizeof(int), st));
-    k_depth<<<nblk(ni, T), T, 0, st>>>(keep.p, parent.p, n, dmax.p);
+    CK(cudaMemsetAsync(dmax, 0, sizeof(int), st));
+    k_depth<<<nblk(ni, T), T, 0, st>>>(keep, parent, n, dmax);
     ++*launches;
     CK(cudaGetLastError());
     int depth = 0;
-    CK(cudaMemcpyAsync(&depth, dmax.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&depth, dmax, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     out.nnodes = nk;
     out.root = 0;

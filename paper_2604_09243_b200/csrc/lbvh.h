@@ -58,6 +58,24 @@ struct DevBuf {
     size_t bytes() const { return n * sizeof(T); }
 };
 
+// Grow-only device workspace carved into 256-byte aligned sub-buffers.
+struct Arena {
+    DevBuf<unsigned char> buf;
+    size_t off = 0;
+    cudaError_t reserve(size_t bytes)
+    {
+        off = 0;
+        return buf.reserve(bytes);
+    }
+    template <class T>
+    T *take(size_t count)
+    {
+        const size_t at = (off + 255) & ~(size_t)255;
+        off = at + count * sizeof(T);
+        return reinterpret_cast<T *>(buf.p + at);
+    }
+};
+
 struct LbvhInput {
     const double *d_verts;   // (T, 9): v0 xyz, v1 xyz, v2 xyz (original order)
     int64_t ntri;
@@ -80,7 +98,16 @@ struct LbvhOutput {
     int storage = 0;
 };
 
-cudaError_t lbvh_build(const LbvhInput &in, LbvhOutput &out, cudaStream_t st,
+// Device-side mesh ingest: soa = [v0 (T,3) | v1 (T,3) | v2 (T,3)] -> verts
+// (T,9) plus the reductions the builder needs; synchronises the stream.
+struct MeshIngest {
+    double lo[3], hi[3], clo[3], chi[3];
+    bool finite, all_f32;
+};
+cudaError_t mesh_ingest(const double *d_soa, int64_t ntri, double *d_verts, MeshIngest &out,
+                        cudaStream_t st, int64_t *launches);
+
+cudaError_t lbvh_build(const LbvhInput &in, LbvhOutput &out, Arena &ws, cudaStream_t st,
                        int64_t *launches);
 cudaError_t pack_tris(const double *d_verts, const int *d_order, int64_t n, int storage,
                       LbvhOutput &out, cudaStream_t st, int64_t *launches);

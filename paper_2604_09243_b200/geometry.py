@@ -130,10 +130,14 @@ class Mesh:
         return 0.5 * np.linalg.norm(c, axis=1)
 
     def checksum(self) -> str:
-        h = hashlib.sha256()
-        for a in (self.v0, self.v1, self.v2):
-            h.update(np.ascontiguousarray(a, dtype=np.float64).tobytes())
-        return h.hexdigest()
+        """SHA-256 over the FP64 vertex data (cached: the mesh is immutable)."""
+        cached = self._dev.get("checksum")
+        if cached is None:
+            h = hashlib.sha256()
+            for a in (self.v0, self.v1, self.v2):
+                h.update(np.ascontiguousarray(a, dtype=np.float64).tobytes())
+            cached = self._dev["checksum"] = h.hexdigest()
+        return cached
 
     def device(self, ctx: Optional[nat.Context] = None) -> _DeviceMesh:
         ctx = ctx or nat.context()
