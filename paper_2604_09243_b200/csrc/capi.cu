@@ -104,6 +104,7 @@ struct sbr_bvh {
     {
         BvhView v;
         v.nodes = out.nodes.p;
+        v.nodes4 = out.nodes4.p;
         v.tri32 = out.tri32.p;
         v.tri64 = out.tri64.p;
         v.normals = mesh->normals.p;
@@ -118,6 +119,17 @@ static int set_device(sbr_ctx *ctx)
 {
     CUDA_TRY(cudaSetDevice(ctx->device));
     return SBR_OK;
+}
+
+// the 4-wide traversal pushes <= 3 entries per level: bound the depth by the
+// per-thread stack (kStack); deletes the handle on failure
+static int check_depth(sbr_bvh *b)
+{
+    if (b->out.depth4 <= kMaxDepth4) return SBR_OK;
+    const int d = b->out.depth4;
+    delete b;
+    return fail(SBR_EINVAL, "BVH4 depth %d exceeds the traversal stack limit (%d)", d,
+                kMaxDepth4);
 }
 
 extern "C" int sbr_ctx_create(int device, sbr_ctx **out)
@@ -292,16 +304,13 @@ extern "C" int sbr_bvh_build(sbr_ctx *ctx, const sbr_mesh *mesh,
     memcpy(in.aabb, mesh->aabb, sizeof(in.aabb));
     cudaError_t e = lbvh_build(in, b->out, ctx->ws, ctx->stream, &ctx->launches);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e == cudaSuccess) e = collapse_bvh4(b->out, ctx->ws, ctx->stream, &ctx->launches);
     if (e != cudaSuccess) {
         delete b;
         return fail(e == cudaErrorMemoryAllocation ? SBR_ENOMEM : SBR_ECUDA, "LBVH build: %s",
                     cudaGetErrorString(e));
     }
-    if (b->out.max_depth + 1 >= kStack) {
-        int d = b->out.max_depth;
-        delete b;
-        return fail(SBR_EINVAL, "BVH depth %d exceeds the traversal stack (%d)", d, kStack);
-    }
+    if (int rc = check_depth(b)) return rc;
     *out = b;
     return SBR_OK;
 }
@@ -417,11 +426,6 @@ extern "C" int sbr_bvh_upload(sbr_ctx *ctx, const sbr_mesh *mesh, const double *
         delete b;
         return fail(SBR_EINVAL, "invalid BVH: %s", U.why.c_str());
     }
-    if (U.max_depth + 1 >= kStack) {
-        delete b;
-        return fail(SBR_EINVAL, "BVH depth %d exceeds the traversal stack (%d)", U.max_depth,
-                    kStack);
-    }
     DevBuf<int> order(mesh->ntri);
     cudaError_t e = order.status();
     if (e == cudaSuccess)
@@ -448,6 +452,12 @@ extern "C" int sbr_bvh_upload(sbr_ctx *ctx, const sbr_mesh *mesh, const double *
     b->out.root = 0;
     b->out.max_depth = U.max_depth;
     b->out.storage = mesh->storage;
+    e = collapse_bvh4(b->out, ctx->ws, ctx->stream, &ctx->launches);
+    if (e != cudaSuccess) {
+        delete b;
+        return fail(SBR_ECUDA, "BVH upload: %s", cudaGetErrorString(e));
+    }
+    if (int rc = check_depth(b)) return rc;
     *out = b;
     return SBR_OK;
 }

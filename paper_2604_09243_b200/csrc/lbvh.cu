@@ -475,4 +475,145 @@ cudaError_t pack_tris(const double *d_verts, const int *d_order, int64_t n, int 
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// BVH2 -> BVH4 collapse (level by level, deterministic)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void child_box(const Node &n, int which, float b[6])
+{
+    if (which == 0) {
+        b[0] = n.a.x; b[1] = n.a.y; b[2] = n.a.z; b[3] = n.a.w; b[4] = n.b.x; b[5] = n.b.y;
+    } else {
+        b[0] = n.b.z; b[1] = n.b.w; b[2] = n.c.x; b[3] = n.c.y; b[4] = n.c.z; b[5] = n.c.w;
+    }
+}
+
+__device__ __forceinline__ float half_area(const float b[6])
+{
+    const float dx = b[3] - b[0], dy = b[4] - b[1], dz = b[5] - b[2];
+    return dx * dy + dy * dz + dz * dx;
+}
+
+// pass A: open up to four descendants of each item, count internal ones
+__global__ void k_collapse_open(const Node *__restrict__ bvh2, const int *__restrict__ items,
+                                int n_items, int *__restrict__ cref, float *__restrict__ cbox,
+                                int *__restrict__ cnt)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_items) return;
+    const Node x = bvh2[items[i]];
+    int ref[4];
+    float box[4][6];
+    ref[0] = x.d.x;
+    ref[1] = x.d.y;
+    child_box(x, 0, box[0]);
+    child_box(x, 1, box[1]);
+    int n = 2;
+    while (n < 4) {
+        int pick = -1;
+        float best = -1.f;
+        for (int k = 0; k < n; ++k)
+            if (ref[k] >= 0) {
+                const float a = half_area(box[k]);
+                if (a > best) { best = a; pick = k; }
+            }
+        if (pick < 0) break;
+        const Node y = bvh2[ref[pick]];
+        ref[pick] = y.d.x;
+        child_box(y, 0, box[pick]);
+        ref[n] = y.d.y;
+        child_box(y, 1, box[n]);
+        ++n;
+    }
+    int internal = 0;
+    for (int k = 0; k < 4; ++k) {
+        const bool have = k < n;
+        cref[4 * i + k] = have ? ref[k] : kEmptyRef;
+        for (int q = 0; q < 6; ++q) cbox[24 * i + 6 * k + q] = have ? box[k][q] : 0.f;
+        internal += (have && ref[k] >= 0) ? 1 : 0;
+    }
+    cnt[i] = internal;
+}
+
+// pass B: write the BVH4 nodes, allocate (by prefix offset) and enqueue the
+// internal children as the next level
+__global__ void k_collapse_emit(const int *__restrict__ cref, const float *__restrict__ cbox,
+                                const int *__restrict__ off, const int *__restrict__ out_idx,
+                                int n_items, int next_base, Node4 *__restrict__ out,
+                                int *__restrict__ next_items, int *__restrict__ next_out)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_items) return;
+    Node4 nd;
+    int r[4];
+    float lo[3][4], hi[3][4];
+    int j = off[i];
+    for (int k = 0; k < 4; ++k) {
+        int c = cref[4 * i + k];
+        for (int a = 0; a < 3; ++a) {
+            lo[a][k] = cbox[24 * i + 6 * k + a];
+            hi[a][k] = cbox[24 * i + 6 * k + 3 + a];
+        }
+        if (c >= 0 && c != kEmptyRef) {
+            next_items[j] = c;
+            next_out[j] = next_base + j;
+            c = next_base + j;
+            ++j;
+        }
+        r[k] = c;
+    }
+    nd.lox = make_float4(lo[0][0], lo[0][1], lo[0][2], lo[0][3]);
+    nd.loy = make_float4(lo[1][0], lo[1][1], lo[1][2], lo[1][3]);
+    nd.loz = make_float4(lo[2][0], lo[2][1], lo[2][2], lo[2][3]);
+    nd.hix = make_float4(hi[0][0], hi[0][1], hi[0][2], hi[0][3]);
+    nd.hiy = make_float4(hi[1][0], hi[1][1], hi[1][2], hi[1][3]);
+    nd.hiz = make_float4(hi[2][0], hi[2][1], hi[2][2], hi[2][3]);
+    nd.ref = make_int4(r[0], r[1], r[2], r[3]);
+    nd.pad = make_int4(0, 0, 0, 0);
+    out[out_idx[i]] = nd;
+}
+
+cudaError_t collapse_bvh4(LbvhOutput &out, Arena &ws, cudaStream_t st, int64_t *launches)
+{
+    const int n2 = (int)out.nnodes;
+    size_t scan_bytes = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (int *)nullptr, (int *)nullptr, n2,
+                                     st));
+    CK(ws.reserve(256 * 12 + (size_t)n2 * (4 * 4 + 4 * 4 + 24 * 4 + 4 * 2) + scan_bytes + 64));
+    int *items[2] = {ws.take<int>(n2), ws.take<int>(n2)};
+    int *outs[2] = {ws.take<int>(n2), ws.take<int>(n2)};
+    int *cref = ws.take<int>(4 * (size_t)n2);
+    float *cbox = ws.take<float>(24 * (size_t)n2);
+    int *cnt = ws.take<int>(n2), *off = ws.take<int>(n2);
+    unsigned char *scan_tmp = ws.take<unsigned char>(scan_bytes);
+    CK(out.nodes4.alloc(n2));
+    const int zero = 0;
+    CK(cudaMemcpyAsync(items[0], &out.root, sizeof(int), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(outs[0], &zero, sizeof(int), cudaMemcpyHostToDevice, st));
+    int n_items = 1, next_base = 1, level = 0, cur = 0;
+    while (n_items > 0) {
+        const unsigned nb = (unsigned)((n_items + 127) / 128);
+        k_collapse_open<<<nb, 128, 0, st>>>(out.nodes.p, items[cur], n_items, cref, cbox, cnt);
+        ++*launches;
+        CK(cudaGetLastError());
+        CK(cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, cnt, off, n_items, st));
+        ++*launches;
+        k_collapse_emit<<<nb, 128, 0, st>>>(cref, cbox, off, outs[cur], n_items, next_base,
+                                            out.nodes4.p, items[cur ^ 1], outs[cur ^ 1]);
+        ++*launches;
+        CK(cudaGetLastError());
+        int last_off = 0, last_cnt = 0;
+        CK(cudaMemcpyAsync(&last_off, off + n_items - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&last_cnt, cnt + n_items - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        const int total = last_off + last_cnt;
+        next_base += total;
+        n_items = total;
+        cur ^= 1;
+        ++level;
+    }
+    out.nnodes4 = next_base;
+    out.depth4 = level - 1;
+    return cudaSuccess;
+}
+
 }  // namespace sbr

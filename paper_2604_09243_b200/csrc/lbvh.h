@@ -96,7 +96,16 @@ struct LbvhOutput {
     int root = 0;
     int max_depth = 0;
     int storage = 0;
+    // 4-wide traversal tree collapsed from `nodes` (level order, root 0)
+    DevBuf<Node4> nodes4;
+    int64_t nnodes4 = 0;
+    int depth4 = 0;
 };
+
+// Collapse the binary tree in out.nodes into out.nodes4: every BVH4 node
+// adopts up to four descendants, greedily opening the child with the
+// largest box surface area; deterministic (prefix-sum allocation).
+cudaError_t collapse_bvh4(LbvhOutput &out, Arena &ws, cudaStream_t st, int64_t *launches);
 
 // Device-side mesh ingest: soa = [v0 (T,3) | v1 (T,3) | v2 (T,3)] -> verts
 // (T,9) plus the reductions the builder needs; synchronises the stream.

@@ -36,11 +36,23 @@ struct __align__(16) Node {
     int4 d;
 };
 
+// 4-wide node, 128 B = one cache line = eight 16-byte loads, boxes SoA by
+// axis so the four slab tests vectorise naturally:
+//   lox, loy, loz, hix, hiy, hiz (4 children each), ref (4 child refs)
+// An absent child has ref == kEmptyRef and is never hit.
+struct __align__(128) Node4 {
+    float4 lox, loy, loz, hix, hiy, hiz;
+    int4 ref;
+    int4 pad;
+};
+constexpr int kEmptyRef = 0x7fffffff;
+
 constexpr int kLeafCountShift = 25;
 constexpr int kLeafFirstMask = (1 << kLeafCountShift) - 1;
 constexpr int kMaxLeafCount = 63;
 constexpr int64_t kMaxTriangles = (int64_t)1 << kLeafCountShift;
-constexpr int kStack = 64;   // traversal stack entries; builds reject deeper trees
+constexpr int kStack = 96;   // traversal stack entries (<= 3 per BVH4 level)
+constexpr int kMaxDepth4 = 31;  // deepest BVH4 level accepted (3 * 31 + 1 < kStack)
 
 __host__ __device__ inline int leaf_ref(int first, int count)
 {
@@ -56,7 +68,8 @@ __host__ __device__ inline int leaf_count(int ref) { return (ref >> kLeafCountSh
 enum Storage : int { kF32Exact = 1, kF64 = 2, kSingle = 3 };
 
 struct BvhView {
-    const Node *nodes;
+    const Node *nodes;       // binary tree (build / export)
+    const Node4 *nodes4;     // 4-wide tree (traversal)
     const float4 *tri32;
     const double2 *tri64;
     const double *normals;   // (T,3), original triangle order
@@ -200,6 +213,46 @@ __device__ __forceinline__ float slab(const RayBox &r, float lox, float loy,
     float tf = fminf(fminf(fmaxf(ax, bx), fmaxf(ay, by)), fminf(fmaxf(az, bz), tmax));
     hit = tn <= tf;
     return tn;
+}
+
+// Visit one BVH4 node: slab-test its four children and return the hit
+// children ordered near -> far (entry distance), count in the result.
+__device__ __forceinline__ void cswap(float &ka, int &va, float &kb, int &vb)
+{
+    const bool s = kb < ka;
+    const float k = s ? kb : ka;
+    kb = s ? ka : kb;
+    ka = k;
+    const int v = s ? vb : va;
+    vb = s ? va : vb;
+    va = v;
+}
+
+__device__ __forceinline__ int node4_visit(const Node4 *np, const RayBox &r, float tmax,
+                                           int ref[4], float tn[4])
+{
+    const float4 lx = __ldg(&np->lox), ly = __ldg(&np->loy), lz = __ldg(&np->loz);
+    const float4 hx = __ldg(&np->hix), hy = __ldg(&np->hiy), hz = __ldg(&np->hiz);
+    const int4 rf = __ldg(&np->ref);
+    const float inf = __int_as_float(0x7f800000);
+    bool h;
+    tn[0] = slab(r, lx.x, ly.x, lz.x, hx.x, hy.x, hz.x, tmax, h);
+    tn[0] = (h && rf.x != kEmptyRef) ? tn[0] : inf;
+    tn[1] = slab(r, lx.y, ly.y, lz.y, hx.y, hy.y, hz.y, tmax, h);
+    tn[1] = (h && rf.y != kEmptyRef) ? tn[1] : inf;
+    tn[2] = slab(r, lx.z, ly.z, lz.z, hx.z, hy.z, hz.z, tmax, h);
+    tn[2] = (h && rf.z != kEmptyRef) ? tn[2] : inf;
+    tn[3] = slab(r, lx.w, ly.w, lz.w, hx.w, hy.w, hz.w, tmax, h);
+    tn[3] = (h && rf.w != kEmptyRef) ? tn[3] : inf;
+    const int n = (tn[0] != inf) + (tn[1] != inf) + (tn[2] != inf) + (tn[3] != inf);
+    ref[0] = rf.x; ref[1] = rf.y; ref[2] = rf.z; ref[3] = rf.w;
+    // 4-element sorting network, misses (+inf) sink to the end
+    cswap(tn[0], ref[0], tn[1], ref[1]);
+    cswap(tn[2], ref[2], tn[3], ref[3]);
+    cswap(tn[0], ref[0], tn[2], ref[2]);
+    cswap(tn[1], ref[1], tn[3], ref[3]);
+    cswap(tn[1], ref[1], tn[2], ref[2]);
+    return n;
 }
 
 }  // namespace sbr

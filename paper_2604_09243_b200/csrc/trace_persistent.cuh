@@ -211,23 +211,19 @@ k_trace_persistent(TraceArgs a)
         // traversing lane has a parked leaf (or stopped at a second leaf).
         while (__any_sync(0xffffffffu, state == kTrav && L.pend == 0)) {
             if (state == kTrav) {
-                const Node *np = B.nodes + L.ref;
-                const float4 na = __ldg(&np->a), nb = __ldg(&np->b), nc = __ldg(&np->c);
-                const int4 nd = __ldg(&np->d);
-                bool h0, h1;
-                const float t0 = slab(L.rb, na.x, na.y, na.z, na.w, nb.x, nb.y, L.tmax, h0);
-                const float t1 = slab(L.rb, nb.z, nb.w, nc.x, nc.y, nc.z, nc.w, L.tmax, h1);
+                int rr[4];
+                float tt[4];
+                const int n = node4_visit(B.nodes4 + L.ref, L.rb, L.tmax, rr, tt);
                 bool have = true;
-                if (h0 && h1) {
-                    int nr = nd.x, fr = nd.y;
-                    float ft = t1;
-                    if (t1 < t0) { nr = nd.y; fr = nd.x; ft = t0; }
-                    stack[L.sp].ref = fr;
-                    stack[L.sp].tn = ft;
-                    ++L.sp;
-                    L.ref = nr;
-                } else if (h0 || h1) {
-                    L.ref = h0 ? nd.x : nd.y;
+                if (n > 0) {
+#pragma unroll
+                    for (int c = 3; c >= 1; --c)   // farther hits first: nearest pops first
+                        if (c < n) {
+                            stack[L.sp].ref = rr[c];
+                            stack[L.sp].tn = tt[c];
+                            ++L.sp;
+                        }
+                    L.ref = rr[0];
                 } else {
                     have = pop_next(stack, L);
                 }

@@ -35,24 +35,18 @@ __device__ __forceinline__ int closest_hit(const BvhView &B, double ox, double o
     while (true) {
         if (ref >= 0) {
             ++visits;
-            const Node *np = B.nodes + ref;
-            float4 a = __ldg(&np->a), b = __ldg(&np->b), c = __ldg(&np->c);
-            int4 d = __ldg(&np->d);
-            bool h0, h1;
-            float t0 = slab(rb, a.x, a.y, a.z, a.w, b.x, b.y, tmax, h0);
-            float t1 = slab(rb, b.z, b.w, c.x, c.y, c.z, c.w, tmax, h1);
-            if (h0 && h1) {
-                int nr = d.x, fr = d.y;
-                float ft = t1;
-                if (t1 < t0) { nr = d.y; fr = d.x; ft = t0; }
-                stack[sp].ref = fr;
-                stack[sp].tn = ft;
-                ++sp;
-                ref = nr;
-                continue;
-            }
-            if (h0 || h1) {
-                ref = h0 ? d.x : d.y;
+            int rr[4];
+            float tt[4];
+            const int n = node4_visit(B.nodes4 + ref, rb, tmax, rr, tt);
+            if (n > 0) {
+#pragma unroll
+                for (int c = 3; c >= 1; --c)
+                    if (c < n) {
+                        stack[sp].ref = rr[c];
+                        stack[sp].tn = tt[c];
+                        ++sp;
+                    }
+                ref = rr[0];
                 continue;
             }
         } else {
