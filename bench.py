@@ -51,6 +51,7 @@ def parse():
     p.add_argument("--angles", type=int, default=N_ANGLES)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--n-leaf", type=int, default=4, help="BVH leaf size (BuildParams.n_leaf)")
     return p.parse_args()
 
 
@@ -219,7 +220,7 @@ def main():
     ctx = nat.context(local)
 
     mesh, lam, cfg = workload(args.density, args.angles)
-    tree = sbr.build(mesh)
+    tree = sbr.build(mesh, sbr.BuildParams(n_leaf=args.n_leaf))
     th, ph, cells, grids = sweep_grids(cfg, mesh)
     tp = cfg.trace_params()
     k = [2 * math.pi / lam]

@@ -167,6 +167,7 @@ __device__ __forceinline__ double tri_hit_exact(const TriF64 &T, double ox,
 // For each axis the padded slab [lo - delta, hi + delta] is evaluated as
 //   t_lo = fma(lo, inv, off_lo), off_lo = -(o' + delta) * inv
 //   t_hi = fma(hi, inv, off_hi), off_hi = -(o' - delta) * inv
+// (the near plane of the pair is lo for inv >= 0, hi otherwise)
 // with o' = fl32(o - c).  Every rounding error (origin conversion, the
 // reciprocal, the offsets, the fma) is a position error bounded by a few
 // ulp of (|o'| + scale); delta = 2^-17 (|o'|_inf + scale) exceeds that by
@@ -174,8 +175,9 @@ __device__ __forceinline__ double tri_hit_exact(const TriF64 &T, double ox,
 // the unpadded box: culling is conservative, never result-changing.
 struct RayBox {
     float ix, iy, iz;
-    float lx, ly, lz;   // off_lo
-    float hx, hy, hz;   // off_hi
+    float nx, ny, nz;   // offsets of the near planes (off_lo if inv >= 0 else off_hi)
+    float fx, fy, fz;   // offsets of the far planes
+    int sel;            // float4 index of the near plane per axis: x | y << 3 | z << 6
 };
 
 __device__ __forceinline__ float safe_dir(float d)
@@ -188,35 +190,28 @@ __device__ __forceinline__ RayBox make_raybox(const BvhView &B, double ox, doubl
                                               double dz)
 {
     RayBox r;
-    float fx = __double2float_rn(ox - B.cx);
-    float fy = __double2float_rn(oy - B.cy);
-    float fz = __double2float_rn(oz - B.cz);
-    float m = fmaxf(fmaxf(fabsf(fx), fabsf(fy)), fabsf(fz));
-    float delta = (m + B.scale) * 7.62939453125e-06f;  // 2^-17
+    const float fx = __double2float_rn(ox - B.cx);
+    const float fy = __double2float_rn(oy - B.cy);
+    const float fz = __double2float_rn(oz - B.cz);
+    const float m = fmaxf(fmaxf(fabsf(fx), fabsf(fy)), fabsf(fz));
+    const float delta = (m + B.scale) * 7.62939453125e-06f;  // 2^-17
     r.ix = 1.0f / safe_dir(__double2float_rn(dx));
     r.iy = 1.0f / safe_dir(__double2float_rn(dy));
     r.iz = 1.0f / safe_dir(__double2float_rn(dz));
-    r.lx = -(fx + delta) * r.ix; r.hx = -(fx - delta) * r.ix;
-    r.ly = -(fy + delta) * r.iy; r.hy = -(fy - delta) * r.iy;
-    r.lz = -(fz + delta) * r.iz; r.hz = -(fz - delta) * r.iz;
+    const float lx = -(fx + delta) * r.ix, hx = -(fx - delta) * r.ix;
+    const float ly = -(fy + delta) * r.iy, hy = -(fy - delta) * r.iy;
+    const float lz = -(fz + delta) * r.iz, hz = -(fz - delta) * r.iz;
+    // near plane = lo for a positive component, hi for a negative one;
+    // Node4 float4 order: lox loy loz hix hiy hiz -> indices 0..5
+    const bool sx = r.ix < 0.f, sy = r.iy < 0.f, sz = r.iz < 0.f;
+    r.nx = sx ? hx : lx; r.fx = sx ? lx : hx;
+    r.ny = sy ? hy : ly; r.fy = sy ? ly : hy;
+    r.nz = sz ? hz : lz; r.fz = sz ? lz : hz;
+    r.sel = (sx ? 3 : 0) | (sy ? 4 : 1) << 3 | (sz ? 5 : 2) << 6;
     return r;
 }
 
-__device__ __forceinline__ float slab(const RayBox &r, float lox, float loy,
-                                      float loz, float hix, float hiy, float hiz,
-                                      float tmax, bool &hit)
-{
-    float ax = fmaf(lox, r.ix, r.lx), bx = fmaf(hix, r.ix, r.hx);
-    float ay = fmaf(loy, r.iy, r.ly), by = fmaf(hiy, r.iy, r.hy);
-    float az = fmaf(loz, r.iz, r.lz), bz = fmaf(hiz, r.iz, r.hz);
-    float tn = fmaxf(fmaxf(fminf(ax, bx), fminf(ay, by)), fmaxf(fminf(az, bz), 0.0f));
-    float tf = fminf(fminf(fmaxf(ax, bx), fmaxf(ay, by)), fminf(fmaxf(az, bz), tmax));
-    hit = tn <= tf;
-    return tn;
-}
-
-// Visit one BVH4 node: slab-test its four children and return the hit
-// children ordered near -> far (entry distance), count in the result.
+// 4-element compare-exchange on (key, ref) pairs
 __device__ __forceinline__ void cswap(float &ka, int &va, float &kb, int &vb)
 {
     const bool s = kb < ka;
@@ -228,22 +223,33 @@ __device__ __forceinline__ void cswap(float &ka, int &va, float &kb, int &vb)
     va = v;
 }
 
+// Visit one BVH4 node: slab-test its four children against the padded
+// boxes (only the ray's near planes give entry distances and its far planes
+// exit distances, so no per-axis min/max) and return the hit children
+// ordered near -> far by entry distance; the count is the return value.
 __device__ __forceinline__ int node4_visit(const Node4 *np, const RayBox &r, float tmax,
                                            int ref[4], float tn[4])
 {
-    const float4 lx = __ldg(&np->lox), ly = __ldg(&np->loy), lz = __ldg(&np->loz);
-    const float4 hx = __ldg(&np->hix), hy = __ldg(&np->hiy), hz = __ldg(&np->hiz);
+    const float4 *q = reinterpret_cast<const float4 *>(np);
+    const int nxi = r.sel & 7, nyi = (r.sel >> 3) & 7, nzi = (r.sel >> 6) & 7;
+    const float4 nxv = __ldg(q + nxi), fxv = __ldg(q + (3 - nxi));
+    const float4 nyv = __ldg(q + nyi), fyv = __ldg(q + (5 - nyi));
+    const float4 nzv = __ldg(q + nzi), fzv = __ldg(q + (7 - nzi));
     const int4 rf = __ldg(&np->ref);
     const float inf = __int_as_float(0x7f800000);
-    bool h;
-    tn[0] = slab(r, lx.x, ly.x, lz.x, hx.x, hy.x, hz.x, tmax, h);
-    tn[0] = (h && rf.x != kEmptyRef) ? tn[0] : inf;
-    tn[1] = slab(r, lx.y, ly.y, lz.y, hx.y, hy.y, hz.y, tmax, h);
-    tn[1] = (h && rf.y != kEmptyRef) ? tn[1] : inf;
-    tn[2] = slab(r, lx.z, ly.z, lz.z, hx.z, hy.z, hz.z, tmax, h);
-    tn[2] = (h && rf.z != kEmptyRef) ? tn[2] : inf;
-    tn[3] = slab(r, lx.w, ly.w, lz.w, hx.w, hy.w, hz.w, tmax, h);
-    tn[3] = (h && rf.w != kEmptyRef) ? tn[3] : inf;
+#define SBR_SLAB(c, k)                                                                     \
+    {                                                                                      \
+        const float a = fmaxf(fmaxf(fmaf(nxv.c, r.ix, r.nx), fmaf(nyv.c, r.iy, r.ny)),     \
+                              fmaxf(fmaf(nzv.c, r.iz, r.nz), 0.0f));                       \
+        const float b = fminf(fminf(fmaf(fxv.c, r.ix, r.fx), fmaf(fyv.c, r.iy, r.fy)),     \
+                              fminf(fmaf(fzv.c, r.iz, r.fz), tmax));                       \
+        tn[k] = (a <= b && rf.c != kEmptyRef) ? a : inf;                                   \
+    }
+    SBR_SLAB(x, 0)
+    SBR_SLAB(y, 1)
+    SBR_SLAB(z, 2)
+    SBR_SLAB(w, 3)
+#undef SBR_SLAB
     const int n = (tn[0] != inf) + (tn[1] != inf) + (tn[2] != inf) + (tn[3] != inf);
     ref[0] = rf.x; ref[1] = rf.y; ref[2] = rf.z; ref[3] = rf.w;
     // 4-element sorting network, misses (+inf) sink to the end
