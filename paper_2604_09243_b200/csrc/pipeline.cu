@@ -120,7 +120,7 @@ __global__ void k_records_to_slots(const uint8_t *__restrict__ valid,
 // ---------------------------------------------------------------------------
 constexpr int kPoThreads = 256;
 constexpr int kPoWarps = kPoThreads / 32;
-constexpr int kPerThread = kChunk / kPoThreads;   // 8
+constexpr int kPerThread = kChunk / kPoThreads;   // 4
 constexpr int kMaxHist = 64;                      // bounce histogram bins in smem
 
 __constant__ double c_two_pi_hi = 6.283185307179586;
@@ -382,21 +382,6 @@ static int persistent_blocks(K kernel, int threads, int num_sms)
 template <int S, int M>
 static void trace_dispatch(const TraceArgs &a, cudaStream_t st, int num_sms)
 {
-    // occupancy experiment knob (solve path, FP32-exact storage only)
-    static const int occ = getenv("SBR_TRACE_OCC") ? atoi(getenv("SBR_TRACE_OCC")) : 0;
-    if (S == kF32Exact && M == kModeSolve && occ >= 6) {
-        if (occ == 6) {
-            int nb = persistent_blocks(k_trace_persistent<S, M, 6>, kTraceThreads, num_sms);
-            k_trace_persistent<S, M, 6><<<nb, kTraceThreads, 0, st>>>(a);
-        } else if (occ == 7) {
-            int nb = persistent_blocks(k_trace_persistent<S, M, 7>, kTraceThreads, num_sms);
-            k_trace_persistent<S, M, 7><<<nb, kTraceThreads, 0, st>>>(a);
-        } else {
-            int nb = persistent_blocks(k_trace_persistent<S, M, 8>, kTraceThreads, num_sms);
-            k_trace_persistent<S, M, 8><<<nb, kTraceThreads, 0, st>>>(a);
-        }
-        return;
-    }
     int nb = persistent_blocks(k_trace_persistent<S, M>, kTraceThreads, num_sms);
     k_trace_persistent<S, M><<<nb, kTraceThreads, 0, st>>>(a);
 }

@@ -8,8 +8,8 @@
 
 namespace sbr {
 
-constexpr int kChunk = 2048;        // ray slots per PO block (compaction tile)
-constexpr int kSegChunks = 256;     // chunks per segment -> 2^19 rays
+constexpr int kChunk = 1024;        // ray slots per PO block (compaction tile)
+constexpr int kSegChunks = 512;     // chunks per segment -> 2^19 rays
 constexpr int64_t kSegRays = (int64_t)kChunk * kSegChunks;
 
 // One incident direction (ApertureGrid, transport.py:84-127).

@@ -195,9 +195,9 @@ __device__ __forceinline__ RayBox make_raybox(const BvhView &B, double ox, doubl
     const float fz = __double2float_rn(oz - B.cz);
     const float m = fmaxf(fmaxf(fabsf(fx), fabsf(fy)), fabsf(fz));
     const float delta = (m + B.scale) * 7.62939453125e-06f;  // 2^-17
-    r.ix = 1.0f / safe_dir(__double2float_rn(dx));
-    r.iy = 1.0f / safe_dir(__double2float_rn(dy));
-    r.iz = 1.0f / safe_dir(__double2float_rn(dz));
+    r.ix = __frcp_rn(safe_dir(__double2float_rn(dx)));   // correctly rounded 1/d
+    r.iy = __frcp_rn(safe_dir(__double2float_rn(dy)));
+    r.iz = __frcp_rn(safe_dir(__double2float_rn(dz)));
     const float lx = -(fx + delta) * r.ix, hx = -(fx - delta) * r.ix;
     const float ly = -(fy + delta) * r.iy, hy = -(fy - delta) * r.iy;
     const float lz = -(fz + delta) * r.iz, hz = -(fz - delta) * r.iz;

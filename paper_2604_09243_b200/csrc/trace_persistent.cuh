@@ -20,7 +20,7 @@
 // (bounce counts and miss/hit mixes no longer serialise the warp), only for
 // the current traversal phase.
 //
-// Results are bit-identical to trace_ray_walk() / the reference: every
+// Results are bit-identical to the reference (transport.py:276-327): every
 // query still returns the lexicographic (t, id) minimum over accepted
 // triangles, and the per-bounce FP64 arithmetic is unchanged.
 #pragma once

@@ -3,9 +3,8 @@
 //
 // Reference semantics:
 //   closest_hit()  == bvh.py:306-362 _traverse (result only; the visit
-//                     count is this tree's node fetches);
-//   trace_ray_walk == transport.py:276-327 _trace_one, operation for
-//                     operation in FP64 round-to-nearest intrinsics.
+//                     count is this tree's node fetches).  The multi-bounce
+//                     walk lives in trace_persistent.cuh.
 #pragma once
 
 #include "sbr_device.cuh"
@@ -76,66 +75,6 @@ __device__ __forceinline__ int closest_hit(const BvhView &B, double ox, double o
         if (!found) break;
     }
     return best;
-}
-
-struct RayResult {
-    bool valid, escaped;
-    int bounces;
-    double n0x, n0y, n0z, path, dx, dy, dz;
-    int queries;
-};
-
-// transport.py:276-327.  ids (optional, stride 1) receives the hit
-// triangle of every accepted bounce.
-template <int STORAGE>
-__device__ __forceinline__ RayResult trace_ray_walk(const BvhView &B, double ox,
-                                                    double oy, double oz,
-                                                    double dx, double dy,
-                                                    double dz, int max_bounces,
-                                                    double eps, bool strict,
-                                                    int *ids, int &visits)
-{
-    RayResult R;
-    R.valid = false; R.escaped = false; R.bounces = 0;
-    R.n0x = R.n0y = R.n0z = 0.0; R.path = 0.0; R.queries = 0;
-    for (int it = 0; it < max_bounces; ++it) {
-        double t = __longlong_as_double(0x7ff0000000000000LL);  // +inf
-        ++R.queries;
-        int tri = closest_hit<STORAGE, false>(B, ox, oy, oz, dx, dy, dz, 0.0, t, visits);
-        if (tri < 0) { R.escaped = true; break; }
-        const double *n = B.normals + 3 * (int64_t)tri;
-        double nx = __ldg(n), ny = __ldg(n + 1), nz = __ldg(n + 2);
-        double nd = DA(DA(DM(nx, dx), DM(ny, dy)), DM(nz, dz));
-        if (nd > 0.0) {
-            if (strict && R.bounces == 0) {
-                R.valid = false; R.escaped = true; R.bounces = 0;
-                R.n0x = R.n0y = R.n0z = 0.0; R.path = 0.0;
-                R.dx = dx; R.dy = dy; R.dz = dz;
-                return R;
-            }
-            nx = -nx; ny = -ny; nz = -nz; nd = -nd;
-        }
-        if (ids) ids[it] = tri;
-        double hx = DA(ox, DM(t, dx)), hy = DA(oy, DM(t, dy)), hz = DA(oz, DM(t, dz));
-        R.path = DA(R.path, t);
-        R.bounces += 1;
-        if (R.bounces == 1) { R.n0x = nx; R.n0y = ny; R.n0z = nz; R.valid = true; }
-        double s = DM(2.0, nd);
-        dx = DS(dx, DM(s, nx));
-        dy = DS(dy, DM(s, ny));
-        dz = DS(dz, DM(s, nz));
-        ox = DA(hx, DM(eps, nx));
-        oy = DA(hy, DM(eps, ny));
-        oz = DA(hz, DM(eps, nz));
-    }
-    if (R.valid && !R.escaped) {
-        double t = __longlong_as_double(0x7ff0000000000000LL);
-        ++R.queries;
-        int tri = closest_hit<STORAGE, true>(B, ox, oy, oz, dx, dy, dz, 0.0, t, visits);
-        R.escaped = tri < 0;
-    }
-    R.dx = dx; R.dy = dy; R.dz = dz;
-    return R;
 }
 
 }  // namespace sbr
