@@ -16,7 +16,8 @@ import numpy as np
 from .errors import NumericalError, SbrError, ValidationError
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libsbr200.so")
+# SBR_LIB points at an alternative build (e.g. an instrumented variant)
+LIB_PATH = os.environ.get("SBR_LIB") or os.path.join(_PKG, "libsbr200.so")
 
 SBR_OK, SBR_EINVAL, SBR_EIO, SBR_ENUMERIC, SBR_ECUDA, SBR_ENOMEM = 0, 2, 3, 4, 10, 12
 STORAGE_AUTO, STORAGE_F32_EXACT, STORAGE_F64, STORAGE_SINGLE = 0, 1, 2, 3
