@@ -68,6 +68,7 @@ struct sbr_ctx {
     DevBuf<int64_t> diag;
     DevBuf<int64_t> seg_base;
     DevBuf<double> k2, gpow, scale;
+    double dkturn = 0.0;         // uniform wavenumber step in turns (0: not uniform)
     DevBuf<double2> amp;
     DevBuf<double> stage;        // host->device staging (mesh ingest, records)
     Arena ws;                    // LBVH build workspace
@@ -753,7 +754,17 @@ static int64_t slot_budget()
 static int upload_freqs(sbr_ctx *ctx, const double *k, int nk, double gamma, int B)
 {
     std::vector<double> k2(nk), gp(B + 1);
-    for (int f = 0; f < nk; ++f) k2[f] = 2.0 * k[f];
+    for (int f = 0; f < nk; ++f) k2[f] = k[f] / M_PI;   // phase 2kR in turns = (k/pi) R
+    // equally spaced wavenumbers (a linspace frequency sweep) enable the
+    // rotation recurrence of k_po
+    ctx->dkturn = 0.0;
+    if (nk > 1) {
+        const double dk = (k[nk - 1] - k[0]) / (nk - 1);
+        bool uniform = dk != 0.0;
+        for (int f = 0; f < nk && uniform; ++f)
+            uniform = std::fabs(k[f] - (k[0] + f * dk)) <= 1e-13 * std::fabs(k[f]);
+        if (uniform) ctx->dkturn = dk / M_PI;
+    }
     for (int b = 0; b <= B; ++b) gp[b] = pow(gamma, (double)b);
     CUDA_TRY(ctx->k2.reserve(nk));
     CUDA_TRY(ctx->gpow.reserve(B + 1));
@@ -796,7 +807,7 @@ static int run_units(sbr_ctx *ctx, const sbr_bvh *bvh, const std::vector<UnitDev
                                     ctx->slots.p, ctx->counter.p, st, ctx->stats()));
         if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev[1], st));
         CUDA_TRY(launch_po(ctx->slots.p, ctx->units.p, (int)batch.size(), slots / kChunk,
-                           ctx->k2.p, nk, ctx->gpow.p, cfg.max_bounces, ctx->chunk_part.p,
+                           ctx->k2.p, nk, ctx->dkturn, ctx->gpow.p, cfg.max_bounces, ctx->chunk_part.p,
                            diag_dev, ctx->bad.p, st, ctx->stats()));
         if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev[2], st));
         CUDA_TRY(launch_seg_reduce(ctx->chunk_part.p, ctx->units.p, (int)batch.size(), nk,
@@ -1073,7 +1084,7 @@ extern "C" int sbr_accumulate(sbr_ctx *ctx, const uint8_t *valid, const double *
                                      k_inc[2], count_trapped, slots_used, ctx->slots.p, st,
                                      ctx->stats()));
     CUDA_TRY(launch_po(ctx->slots.p, ctx->units.p, (int)nseg, slots_used / kChunk, ctx->k2.p, nk,
-                       ctx->gpow.p, maxb, ctx->chunk_part.p, ctx->diag.p, ctx->bad.p, st,
+                       ctx->dkturn, ctx->gpow.p, maxb, ctx->chunk_part.p, ctx->diag.p, ctx->bad.p, st,
                        ctx->stats()));
     CUDA_TRY(launch_seg_reduce(ctx->chunk_part.p, ctx->units.p, (int)nseg, nk, ctx->seg_part.p, st,
                                ctx->stats()));

@@ -11,9 +11,9 @@
 //                  selected records (po.py:96-101) into shared memory in
 //                  slot order, then evaluates (po.py:105-108)
 //                    term_f = j k_f dA/4pi * 2 cos Gamma^N exp(-2j k_f R)
-//                  for nk wavenumbers: phase reduced mod 2pi in FP64,
-//                  FP32 __sincosf on the SFU, FP64 accumulation, warp
-//                  shuffle tree then a fixed cross-warp order.
+//                  for nk wavenumbers: phase in turns reduced exactly in
+//                  FP64, FP32 __sincosf on the SFU, per-lane FP32 then FP64
+//                  accumulation, warp shuffle tree, fixed cross-warp order.
 //   k_seg_reduce / k_finalize  fixed pairwise trees (po.py:59-80 shape)
 //                  over chunk -> segment -> grid partials: results are
 //                  bit-stable and independent of GPU count.
@@ -123,14 +123,11 @@ constexpr int kPoWarps = kPoThreads / 32;
 constexpr int kPerThread = kChunk / kPoThreads;   // 4
 constexpr int kMaxHist = 64;                      // bounce histogram bins in smem
 
-__constant__ double c_two_pi_hi = 6.283185307179586;
-__constant__ double c_two_pi_lo = 2.4492935982947064e-16;
-__constant__ double c_inv_two_pi = 0.15915494309189535;
-
 template <int FPT>
 __global__ void __launch_bounds__(kPoThreads)
 k_po(const SlotRec *__restrict__ slots, const UnitDev *__restrict__ units, int n_units,
-     const double *__restrict__ k2, int nk, const double *__restrict__ gpow, int max_bounces,
+     const double *__restrict__ kturn, int nk, double dkturn, const double *__restrict__ gpow,
+     int max_bounces,
      double2 *__restrict__ chunk_part, int64_t *__restrict__ diag,
      unsigned long long *__restrict__ bad)
 {
@@ -138,9 +135,10 @@ k_po(const SlotRec *__restrict__ slots, const UnitDev *__restrict__ units, int n
     __shared__ int wcount[kPerThread][kPoWarps];
     __shared__ int wbase[kPerThread][kPoWarps];
     __shared__ int s_total;
-    __shared__ unsigned long long s_hist[kMaxHist];
-    __shared__ unsigned long long s_valid, s_queries;
-    __shared__ unsigned int s_maxb;
+    // per-chunk counters fit 32 bits: native shared atomics (64-bit shared
+    // atomics are CAS loops -- measured as the top PO stall)
+    __shared__ unsigned int s_hist[kMaxHist];
+    __shared__ unsigned int s_valid, s_queries, s_maxb;
     __shared__ double2 red[kPoWarps][FPT];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -151,8 +149,8 @@ k_po(const SlotRec *__restrict__ slots, const UnitDev *__restrict__ units, int n
     const int nb = max_bounces + 1;
     const int64_t dstride = 3 + nb;
 
-    if (tid < kMaxHist) s_hist[tid] = 0ULL;
-    if (tid == 0) { s_valid = 0ULL; s_queries = 0ULL; s_maxb = 0u; }
+    if (tid < kMaxHist) s_hist[tid] = 0u;
+    if (tid == 0) { s_valid = 0u; s_queries = 0u; s_maxb = 0u; }
 
     // ---- load + ballot ----
     SlotRec rec[kPerThread];
@@ -210,10 +208,16 @@ k_po(const SlotRec *__restrict__ slots, const UnitDev *__restrict__ units, int n
                 atomicMin(bad, (unsigned long long)ridx);
             }
         }
-        if (rec[q].meta & kMetaValid) {
-            const unsigned b = rec[q].meta & kMetaBounceMask;
-            if (b < (unsigned)kMaxHist) atomicAdd(&s_hist[b], 1ULL);
-            else if (diag) atomicAdd((unsigned long long *)&diag[(int64_t)U.grid * dstride + 3 + b], 1ULL);
+        {   // bounce histogram of valid rays: one atomic per distinct value
+            const bool v = (rec[q].meta & kMetaValid) != 0;
+            const unsigned b = v ? (rec[q].meta & kMetaBounceMask) : 0xffffffffu;
+            const unsigned peers = __match_any_sync(0xffffffffu, b);
+            if (v && lane == __ffs(peers) - 1) {
+                if (b < (unsigned)kMaxHist) atomicAdd(&s_hist[b], (unsigned)__popc(peers));
+                else if (diag)
+                    atomicAdd((unsigned long long *)&diag[(int64_t)U.grid * dstride + 3 + b],
+                              (unsigned long long)__popc(peers));
+            }
         }
     }
     // diagnostics: warp reductions then one atomic per warp
@@ -224,20 +228,20 @@ k_po(const SlotRec *__restrict__ slots, const UnitDev *__restrict__ units, int n
         my_maxb = max(my_maxb, __shfl_xor_sync(0xffffffffu, my_maxb, o));
     }
     if (lane == 0) {
-        atomicAdd(&s_queries, my_q);
-        atomicAdd(&s_valid, (unsigned long long)my_valid);
+        atomicAdd(&s_queries, (unsigned)my_q);
+        atomicAdd(&s_valid, (unsigned)my_valid);
         atomicMax(&s_maxb, my_maxb);
     }
     __syncthreads();
     if (diag) {
         int64_t *dg = diag + (int64_t)U.grid * dstride;
         if (tid == 0) {
-            if (s_valid) atomicAdd((unsigned long long *)&dg[0], s_valid);
-            atomicAdd((unsigned long long *)&dg[1], s_queries);
+            if (s_valid) atomicAdd((unsigned long long *)&dg[0], (unsigned long long)s_valid);
+            atomicAdd((unsigned long long *)&dg[1], (unsigned long long)s_queries);
             atomicMax((unsigned long long *)&dg[2], (unsigned long long)s_maxb);
         }
         if (tid < nb && tid < kMaxHist && s_hist[tid])
-            atomicAdd((unsigned long long *)&dg[3 + tid], s_hist[tid]);
+            atomicAdd((unsigned long long *)&dg[3 + tid], (unsigned long long)s_hist[tid]);
     }
 
     // ---- PO terms ----
@@ -250,40 +254,67 @@ k_po(const SlotRec *__restrict__ slots, const UnitDev *__restrict__ units, int n
         if (G >= kPoWarps) { grp = pass * kPoWarps + warp; sub = 0; }
         else { grp = warp / wpg; sub = warp % wpg; }
         const bool active = grp < G && (G >= kPoWarps || warp < G * wpg);
-        double sacc[FPT], cacc[FPT], kk[FPT];
+        // phase 2 k R in turns: tau = (k / pi) R, reduced exactly in FP64
+        // (tau - rint(tau) has no rounding error), then one float conversion
+        // and __sincosf on the SFU; a lane's <= 32 terms per chunk accumulate
+        // in FP32 (error comparable to the SFU's), cross-lane sums in FP64
+        float sacc[FPT], cacc[FPT];
+        double kk[FPT];
 #pragma unroll
         for (int f = 0; f < FPT; ++f) {
-            sacc[f] = 0.0; cacc[f] = 0.0;
+            sacc[f] = 0.f; cacc[f] = 0.f;
             const int fi = grp * FPT + f;
-            kk[f] = (active && fi < nk) ? k2[fi] : 0.0;
+            kk[f] = (active && fi < nk) ? kturn[fi] : 0.0;
         }
-        if (active) {
+        if (active && FPT > 1 && dkturn != 0.0) {
+            // equally spaced wavenumbers: one SFU sincos for the group's first
+            // phase and one for the step, then FPT-1 exact-phase rotations
+            // (FP32 complex products, error <= FPT ulps), re-anchored per group
             for (int m = sub * 32 + lane; m < M; m += wpg * 32) {
                 const double2 rw = srec[m];
+                const float wf = (float)rw.y;
+                const double t0 = kk[0] * rw.x, dt = dkturn * rw.x;
+                float sn, cs, ds, dc;
+                __sincosf((float)(t0 - rint(t0)) * 6.28318530717958648f, &sn, &cs);
+                __sincosf((float)(dt - rint(dt)) * 6.28318530717958648f, &ds, &dc);
 #pragma unroll
                 for (int f = 0; f < FPT; ++f) {
-                    const double ph = kk[f] * rw.x;
-                    const double nn = rint(ph * c_inv_two_pi);
-                    double rr = fma(-nn, c_two_pi_hi, ph);
-                    rr = fma(-nn, c_two_pi_lo, rr);
-                    float s, c;
-                    __sincosf((float)rr, &s, &c);
-                    sacc[f] = fma(rw.y, (double)s, sacc[f]);
-                    cacc[f] = fma(rw.y, (double)c, cacc[f]);
+                    sacc[f] = fmaf(wf, sn, sacc[f]);
+                    cacc[f] = fmaf(wf, cs, cacc[f]);
+                    const float s2 = fmaf(sn, dc, cs * ds);
+                    cs = fmaf(cs, dc, -sn * ds);
+                    sn = s2;
+                }
+            }
+        } else if (active) {
+            for (int m = sub * 32 + lane; m < M; m += wpg * 32) {
+                const double2 rw = srec[m];
+                const float wf = (float)rw.y;
+#pragma unroll
+                for (int f = 0; f < FPT; ++f) {
+                    const double tau = kk[f] * rw.x;
+                    const float fr = (float)(tau - rint(tau));
+                    float sn, cs;
+                    __sincosf(fr * 6.28318530717958648f, &sn, &cs);
+                    sacc[f] = fmaf(wf, sn, sacc[f]);
+                    cacc[f] = fmaf(wf, cs, cacc[f]);
                 }
             }
         }
+        double sred[FPT], cred[FPT];
 #pragma unroll
         for (int f = 0; f < FPT; ++f) {
+            sred[f] = (double)sacc[f];
+            cred[f] = (double)cacc[f];
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
-                sacc[f] += __shfl_xor_sync(0xffffffffu, sacc[f], o);
-                cacc[f] += __shfl_xor_sync(0xffffffffu, cacc[f], o);
+                sred[f] += __shfl_xor_sync(0xffffffffu, sred[f], o);
+                cred[f] += __shfl_xor_sync(0xffffffffu, cred[f], o);
             }
         }
         if (lane == 0) {
 #pragma unroll
-            for (int f = 0; f < FPT; ++f) red[warp][f] = make_double2(sacc[f], cacc[f]);
+            for (int f = 0; f < FPT; ++f) red[warp][f] = make_double2(sred[f], cred[f]);
         }
         __syncthreads();
         // fixed-order cross-warp combine; one thread per (group, f)
@@ -471,23 +502,24 @@ cudaError_t launch_records_to_slots(const uint8_t *valid, const double *n0,
 }
 
 cudaError_t launch_po(const SlotRec *d_slots, const UnitDev *d_units, int n_units,
-                      int64_t n_chunks, const double *d_k2, int nk, const double *d_gpow,
+                      int64_t n_chunks, const double *d_k2, int nk, double dkturn,
+                      const double *d_gpow,
                       int max_bounces, double2 *d_chunk_part, int64_t *d_diag,
                       unsigned long long *d_bad, cudaStream_t st, const LaunchStats &ls)
 {
     if (n_chunks <= 0) return cudaSuccess;
     dim3 grid((unsigned)n_chunks);
     if (nk >= 8)
-        k_po<8><<<grid, kPoThreads, 0, st>>>(d_slots, d_units, n_units, d_k2, nk, d_gpow,
+        k_po<8><<<grid, kPoThreads, 0, st>>>(d_slots, d_units, n_units, d_k2, nk, dkturn, d_gpow,
                                              max_bounces, d_chunk_part, d_diag, d_bad);
     else if (nk >= 4)
-        k_po<4><<<grid, kPoThreads, 0, st>>>(d_slots, d_units, n_units, d_k2, nk, d_gpow,
+        k_po<4><<<grid, kPoThreads, 0, st>>>(d_slots, d_units, n_units, d_k2, nk, dkturn, d_gpow,
                                              max_bounces, d_chunk_part, d_diag, d_bad);
     else if (nk >= 2)
-        k_po<2><<<grid, kPoThreads, 0, st>>>(d_slots, d_units, n_units, d_k2, nk, d_gpow,
+        k_po<2><<<grid, kPoThreads, 0, st>>>(d_slots, d_units, n_units, d_k2, nk, dkturn, d_gpow,
                                              max_bounces, d_chunk_part, d_diag, d_bad);
     else
-        k_po<1><<<grid, kPoThreads, 0, st>>>(d_slots, d_units, n_units, d_k2, nk, d_gpow,
+        k_po<1><<<grid, kPoThreads, 0, st>>>(d_slots, d_units, n_units, d_k2, nk, dkturn, d_gpow,
                                              max_bounces, d_chunk_part, d_diag, d_bad);
     ++*ls.launches;
     return cudaGetLastError();

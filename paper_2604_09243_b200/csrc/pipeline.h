@@ -94,8 +94,10 @@ cudaError_t launch_records_to_slots(const uint8_t *valid, const double *n0,
                                     int64_t n_slots, SlotRec *slots, cudaStream_t st,
                                     const LaunchStats &ls);
 
+// dkturn != 0: the nk wavenumbers are equally spaced, (k[f+1]-k[f]) / pi
 cudaError_t launch_po(const SlotRec *d_slots, const UnitDev *d_units, int n_units,
-                      int64_t n_chunks, const double *d_k2, int nk, const double *d_gpow,
+                      int64_t n_chunks, const double *d_k2, int nk, double dkturn,
+                      const double *d_gpow,
                       int max_bounces, double2 *d_chunk_part, int64_t *d_diag,
                       unsigned long long *d_bad, cudaStream_t st, const LaunchStats &ls);
 

@@ -360,3 +360,25 @@ def test_launches_are_counted():
     tree = sbr.build(mesh)
     sbr.solve_direction(tree, mesh, sbr.IncidentDirection(0.3, 0.2), 0.05, 0.25)
     assert ctx.launches - before >= 6   # LBVH kernels + trace + po + reduces
+
+
+@pytest.mark.parametrize("uniform", [True, False])
+def test_multifrequency_po_vs_oracle(orc, uniform):
+    """C5-style frequency sweep: 64 wavenumbers (linspace -> rotation
+    recurrence in k_po; perturbed -> direct SFU sincos per term)."""
+    mesh = meshgen.quantized_icosphere(1.0, 4)
+    tree = sbr.build(mesh)
+    ka = np.linspace(60.0, 64.0, 64)
+    if not uniform:
+        ka[5] += 1e-3
+    lam_min = 2 * math.pi / ka.max()
+    d = sbr.IncidentDirection(math.pi / 2, 0.3)
+    grid = sbr.build_aperture(mesh.aabb, d, lam_min / 6, wavelength=lam_min)
+    tp = sbr.TraceParams(max_bounces=2)
+    res = sbr.solve_grids(tree, mesh, [grid], tp, ka)
+    rec = sbr.trace_grid(tree, mesh, grid, tp)
+    multi = sbr.accumulate_multi(rec, grid.k_inc, ka, grid.cell_area)
+    for f in range(0, 64, 7):
+        ref = orc.accumulate(rec, grid.k_inc, 2 * math.pi / ka[f], grid.cell_area)
+        _amp_close(res.amplitude[0, f], ref)
+        _amp_close(multi[f], ref)
