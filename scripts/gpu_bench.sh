@@ -9,7 +9,7 @@ tail -2 gpurun_out/bench.err; cat gpurun_out/bench.json
 if [ -n "$NCU" ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 0 --angles 36 --no-e2e --no-cpu > gpurun_out/ncu_launch.log 2>&1
-  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_trace_solve -c 1 \
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_trace_persistent -c 1 \
     -o gpurun_out/prof_trace -f python bench.py --steps 1 --warmup 0 --angles 8 --no-e2e --no-cpu > gpurun_out/ncu_full.log 2>&1
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_po -c 1 \
     -o gpurun_out/prof_po -f python bench.py --steps 1 --warmup 0 --angles 8 --no-e2e --no-cpu > gpurun_out/ncu_po.log 2>&1
