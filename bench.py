@@ -52,10 +52,12 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--n-leaf", type=int, default=4, help="BVH leaf size (BuildParams.n_leaf)")
+    p.add_argument("--bounces", type=int, default=MAX_BOUNCES,
+                   help="max bounces (experiments only; the C4 workload is 5)")
     return p.parse_args()
 
 
-def workload(density, n_angles):
+def workload(density, n_angles, bounces=MAX_BOUNCES):
     import paper_2604_09243_b200 as sbr
     from paper_2604_09243_b200 import meshgen
     mesh = meshgen.generate_aircraft(density=density)
@@ -63,16 +65,16 @@ def workload(density, n_angles):
     cfg = sbr.SweepConfig(mesh_path="<procedural aircraft>", frequency_hz=FREQ_HZ,
                           theta=sbr.AngleRange(math.pi / 2, math.pi / 2, 1),
                           phi=sbr.AngleRange(0.0, math.radians(n_angles - 1), n_angles),
-                          max_bounces=MAX_BOUNCES)
+                          max_bounces=bounces)
     return mesh, lam, cfg
 
 
-def config_dict(mesh, n_angles, world):
+def config_dict(mesh, n_angles, world, bounces=MAX_BOUNCES):
     return {"workload": "C4: procedural aircraft, 360-angle monostatic sweep, 10 GHz, "
                         "5 bounces, lambda/5 ray spacing",
             "triangles": int(mesh.triangle_count), "angles": n_angles,
             "theta_deg": 90, "phi_deg": [0, n_angles - 1], "frequency_hz": FREQ_HZ,
-            "max_bounces": MAX_BOUNCES, "spacing": "lambda/5 (5.996 mm)",
+            "max_bounces": bounces, "spacing": "lambda/5 (5.996 mm)",
             "parallelism": f"angle-sharded x{world}, one NCCL reduce" if world > 1 else "1 GPU",
             "l2": "flushed (512 MB write) between timed steps"}
 
@@ -219,7 +221,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ctx = nat.context(local)
 
-    mesh, lam, cfg = workload(args.density, args.angles)
+    mesh, lam, cfg = workload(args.density, args.angles, args.bounces)
     tree = sbr.build(mesh, sbr.BuildParams(n_leaf=args.n_leaf))
     th, ph, cells, grids = sweep_grids(cfg, mesh)
     tp = cfg.trace_params()
@@ -326,7 +328,7 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_dict(mesh, args.angles, world),
+        "config": config_dict(mesh, args.angles, world, args.bounces),
         "angles_per_s": args.angles * args.steps / (total_ms / 1e3),
         "queries_per_step": queries // max(args.steps, 1),
         "gpu_launches": launches,

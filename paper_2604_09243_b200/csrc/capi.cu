@@ -739,12 +739,25 @@ extern "C" int sbr_segment_layout(const sbr_grid *grids, int32_t ngrids, int64_t
     return SBR_OK;
 }
 
-// slots (16 B each) staged per batch; SBR_SLOT_BUDGET overrides (tests use
-// tiny budgets to prove results do not depend on batching)
+// slots (16 B each) staged per batch: up to 2^30 (16 GB, a whole C4 sweep in
+// one persistent launch, so the kernel drains once per solve), capped at an
+// eighth of the free device memory.  SBR_SLOT_BUDGET overrides (tests use
+// tiny budgets to prove results do not depend on batching).
 static int64_t slot_budget()
 {
     const char *s = getenv("SBR_SLOT_BUDGET");
-    int64_t v = s ? atoll(s) : ((int64_t)1 << 25);
+    int64_t v;
+    if (s) {
+        v = atoll(s);
+    } else {
+        size_t free_b = 0, total_b = 0;
+        v = (int64_t)1 << 30;
+        if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+            const int64_t cap = (int64_t)(free_b / 8 / sizeof(SlotRec));
+            if (cap < v) v = cap;
+        }
+        if (v < ((int64_t)1 << 22)) v = (int64_t)1 << 22;
+    }
     if (v < kChunk) v = kChunk;
     return round_chunk(v);
 }
@@ -924,7 +937,7 @@ static int validate_solve(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *bvh
     if (int rc = check_pair(ctx, mesh, bvh)) return rc;
     if (int rc = check_params(params)) return rc;
     if (int rc = check_grids(grids, ngrids)) return rc;
-    REQUIRE(k && nk >= 1, "need at least one wavenumber");
+    REQUIRE(k && nk >= 1 && nk <= 65535, "need 1..65535 wavenumbers");
     for (int f = 0; f < nk; ++f) REQUIRE(k[f] > 0.0 && std::isfinite(k[f]), "bad wavenumber");
     REQUIRE(std::fabs(gamma) <= 1.0, "|gamma| must be <= 1");
     return check_sampling(grids, ngrids, params);
@@ -993,7 +1006,7 @@ extern "C" int sbr_finalize(sbr_ctx *ctx, const sbr_grid *grids, int32_t ngrids,
 {
     REQUIRE(ctx && amp && seg_dev && diag_dev, "NULL argument");
     if (int rc = check_grids(grids, ngrids)) return rc;
-    REQUIRE(k && nk >= 1, "need at least one wavenumber");
+    REQUIRE(k && nk >= 1 && nk <= 65535, "need 1..65535 wavenumbers");
     REQUIRE(max_bounces >= 1, "max_bounces must be >= 1");
     std::lock_guard<std::mutex> lk(ctx->mu);
     if (int rc = set_device(ctx)) return rc;
@@ -1028,6 +1041,7 @@ extern "C" int sbr_accumulate(sbr_ctx *ctx, const uint8_t *valid, const double *
                               int64_t *bad_index)
 {
     REQUIRE(ctx && amp && k_inc && k && nk >= 1, "NULL argument");
+    REQUIRE(nk <= 65535, "at most 65535 wavenumbers");
     REQUIRE(n >= 0, "negative record count");
     REQUIRE(cell_area > 0.0, "cell_area must be positive");
     REQUIRE(std::fabs(gamma) <= 1.0, "|gamma| must be <= 1");

@@ -367,20 +367,40 @@ __device__ double2 pairwise_seq(const double2 *p, int64_t n, int64_t stride)
     return acc;
 }
 
-__global__ void k_seg_reduce(const double2 *__restrict__ chunk_part,
-                             const UnitDev *__restrict__ units, int n_units, int nk,
-                             double2 *__restrict__ seg_part)
+// One block per (unit, wavenumber): the unit's <= kSegChunks chunk partials
+// are summed level by level in shared memory (adjacent pairs, odd tail
+// carried -- the same tree as pairwise_seq / po.py:59-80).
+constexpr int kSegThreads = 256;
+__global__ void __launch_bounds__(kSegThreads)
+k_seg_reduce(const double2 *__restrict__ chunk_part, const UnitDev *__restrict__ units,
+             int n_units, int nk, double2 *__restrict__ seg_part)
 {
-    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (t >= (int64_t)n_units * nk) return;
-    const int u = (int)(t / nk), f = (int)(t % nk);
+    __shared__ double2 buf[2][kSegChunks];
+    const int u = blockIdx.x, f = blockIdx.y;
     const UnitDev U = units[u];
-    const int64_t nch = (U.ray_end - U.ray_begin + kChunk - 1) / kChunk;
+    int n = (int)((U.ray_end - U.ray_begin + kChunk - 1) / kChunk);
     const int64_t c0 = U.slot_base / kChunk;
-    double2 v = pairwise_seq(chunk_part + c0 * nk + f, nch, nk);
-    v.x += 0.0;   // normalise -0.0 so a disjoint-support sum reduce is exact
-    v.y += 0.0;
-    seg_part[U.seg_out * nk + f] = v;
+    for (int i = threadIdx.x; i < n; i += kSegThreads)
+        buf[0][i] = chunk_part[(c0 + i) * nk + f];
+    __syncthreads();
+    int cur = 0;
+    while (n > 1) {
+        const int half = n >> 1;
+        for (int i = threadIdx.x; i < half; i += kSegThreads) {
+            const double2 a = buf[cur][2 * i], b = buf[cur][2 * i + 1];
+            buf[cur ^ 1][i] = make_double2(a.x + b.x, a.y + b.y);
+        }
+        if ((n & 1) && threadIdx.x == 0) buf[cur ^ 1][half] = buf[cur][n - 1];
+        n = half + (n & 1);
+        cur ^= 1;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        double2 v = n ? buf[cur][0] : make_double2(0.0, 0.0);
+        v.x += 0.0;   // normalise -0.0 so a disjoint-support sum reduce is exact
+        v.y += 0.0;
+        seg_part[U.seg_out * nk + f] = v;
+    }
 }
 
 __global__ void k_finalize(const double2 *__restrict__ seg_part,
@@ -529,10 +549,9 @@ cudaError_t launch_seg_reduce(const double2 *d_chunk_part, const UnitDev *d_unit
                               int n_units, int nk, double2 *d_seg_part, cudaStream_t st,
                               const LaunchStats &ls)
 {
-    int64_t n = (int64_t)n_units * nk;
-    if (n == 0) return cudaSuccess;
-    k_seg_reduce<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(d_chunk_part, d_units, n_units,
-                                                               nk, d_seg_part);
+    if ((int64_t)n_units * nk == 0) return cudaSuccess;
+    k_seg_reduce<<<dim3((unsigned)n_units, (unsigned)nk), kSegThreads, 0, st>>>(
+        d_chunk_part, d_units, n_units, nk, d_seg_part);
     ++*ls.launches;
     return cudaGetLastError();
 }
