@@ -319,7 +319,8 @@ def main():
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     peak = peaks.get("hbm_gbs", 6650.0)
-    achieved = bpq * local_queries / (kst["trace_ms"] / 1e3) / 1e9 if kst["trace_ms"] else None
+    stage_ms = kst["trace_ms"] + kst["raster_ms"]   # query 0 (raster) + bounces (trace)
+    achieved = bpq * local_queries / (stage_ms / 1e3) / 1e9 if stage_ms else None
     traffic = None
     ncu_path = os.path.join(ROOT, "profiles", "ncu_trace_summary.json")
     if os.path.exists(ncu_path):
@@ -332,11 +333,13 @@ def main():
         "angles_per_s": args.angles * args.steps / (total_ms / 1e3),
         "queries_per_step": queries // max(args.steps, 1),
         "gpu_launches": launches,
-        "kernel_ms": {"trace": kst["trace_ms"] / args.steps, "compact_po": kst["po_ms"] / args.steps,
+        "kernel_ms": {"raster": kst["raster_ms"] / args.steps,
+                      "trace": kst["trace_ms"] / args.steps, "compact_po": kst["po_ms"] / args.steps,
                       "trace_launches_per_step": kst["trace_launches"] / args.steps},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                     "kernel": "k_trace_solve (launcher + 5-bounce traversal)",
+                     "kernel": "trace stage: k_raster (query 0 of every ray) + k_trace_persistent "
+                               "(launcher + 5-bounce traversal)",
                      "bytes_per_query": bpq,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
         "clocks": clk,

@@ -117,6 +117,9 @@ int sbr_ctx_launch_count(sbr_ctx *ctx, int64_t *count_out);
 int sbr_ctx_profile(sbr_ctx *ctx, int32_t enable);
 int sbr_ctx_kernel_stats(sbr_ctx *ctx, double *trace_ms, int64_t *trace_launches,
                          double *po_ms, int64_t *po_launches);
+/* Accumulated time of the primary-visibility raster pass (memset + two
+ * sweeps) that precedes each trace launch; trace_ms excludes it. */
+int sbr_ctx_raster_stats(sbr_ctx *ctx, double *raster_ms);
 
 /* ---- mesh: geometry.py:130-180 mesh_from_soup output -> device --------- */
 int sbr_mesh_create(sbr_ctx *ctx, const double *v0, const double *v1,

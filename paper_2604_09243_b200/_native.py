@@ -68,6 +68,7 @@ _SIGS = {
     "sbr_ctx_profile": (ctypes.c_int, [c_vp, c_i32]),
     "sbr_ctx_kernel_stats": (ctypes.c_int, [c_vp, ctypes.POINTER(c_dbl), ctypes.POINTER(c_i64),
                                             ctypes.POINTER(c_dbl), ctypes.POINTER(c_i64)]),
+    "sbr_ctx_raster_stats": (ctypes.c_int, [c_vp, ctypes.POINTER(c_dbl)]),
     "sbr_mesh_create": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i32,
                                        ctypes.POINTER(c_vp)]),
     "sbr_mesh_destroy": (ctypes.c_int, [c_vp]),
@@ -187,8 +188,10 @@ class Context:
         tm, tn, pm, pn = c_dbl(), c_i64(), c_dbl(), c_i64()
         check(self.lib.sbr_ctx_kernel_stats(self.handle, ctypes.byref(tm), ctypes.byref(tn),
                                             ctypes.byref(pm), ctypes.byref(pn)))
+        rm = c_dbl()
+        check(self.lib.sbr_ctx_raster_stats(self.handle, ctypes.byref(rm)))
         return {"trace_ms": tm.value, "trace_launches": int(tn.value), "po_ms": pm.value,
-                "po_launches": int(pn.value)}
+                "po_launches": int(pn.value), "raster_ms": rm.value}
 
     @property
     def stream(self) -> int:

@@ -67,6 +67,8 @@ struct sbr_ctx {
     DevBuf<double2> seg_part;
     DevBuf<int64_t> diag;
     DevBuf<int64_t> seg_base;
+    DevBuf<int64_t> seg_slot;    // raster pass: global segment row -> slot offset
+    DevBuf<int> bgrids;          // raster pass: grids of the current batch
     DevBuf<double> k2, gpow, scale;
     double dkturn = 0.0;         // uniform wavenumber step in turns (0: not uniform)
     DevBuf<double2> amp;
@@ -75,7 +77,7 @@ struct sbr_ctx {
     // optional per-kernel CUDA-event timing of the solve pipeline
     bool profile = false;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
-    double trace_ms = 0.0, po_ms = 0.0;
+    double trace_ms = 0.0, po_ms = 0.0, raster_ms = 0.0;
     int64_t trace_n = 0, po_n = 0;
     LaunchStats stats() { return LaunchStats{&launches, num_sms}; }
     ~sbr_ctx()
@@ -144,7 +146,7 @@ extern "C" int sbr_ctx_create(int device, sbr_ctx **out)
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
-    if (e == cudaSuccess) e = ctx->counter.alloc(1);
+    if (e == cudaSuccess) e = ctx->counter.alloc(2);   // [0] trace, [1] raster
     if (e == cudaSuccess) e = ctx->err_flag.alloc(1);
     if (e == cudaSuccess) e = ctx->bad.alloc(1);
     if (e != cudaSuccess) {
@@ -594,6 +596,33 @@ static int check_pair(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *bvh)
     return SBR_OK;
 }
 
+// Query 0 of aperture rays: rasterised per triangle (default) or traced
+// through the BVH like every other query (SBR_PRIMARY=bvh).  Both give the
+// same bits; the switch exists for A/B measurement and parity tests.
+static bool raster_primary()
+{
+    const char *s = getenv("SBR_PRIMARY");
+    return !(s && std::strcmp(s, "bvh") == 0);
+}
+
+static RasterArgs raster_args(const sbr_bvh *bvh, const GridDev *grids, const int *bgrids,
+                              int nbg, const int64_t *seg_base, const int64_t *seg_slot,
+                              PrimHit *prim)
+{
+    RasterArgs r;
+    r.B = bvh->view();
+    r.storage = bvh->mesh->storage;
+    r.ntri = bvh->mesh->ntri;
+    r.grids = grids;
+    r.bgrids = bgrids;
+    r.nbg = nbg;
+    r.seg_base = seg_base;
+    r.seg_slot = seg_slot;
+    r.prim = prim;
+    r.counter = nullptr;
+    return r;
+}
+
 static TraceCfg make_cfg(const sbr_bvh *bvh, const sbr_trace_params *p, sbr_ctx *ctx)
 {
     TraceCfg c;
@@ -687,7 +716,27 @@ static int trace_full_common(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *
     }
     TraceCfg cfg = make_cfg(bvh, params, ctx);
     FullOut fo{dv.p, dn.p, dp.p, db.p, de.p, dd.p, tri_ids ? di.p : nullptr};
-    CUDA_TRY(launch_trace_full(cfg, dg.p, o.p, d.p, n, fo, ctx->counter.p, st, ctx->stats()));
+    DevBuf<PrimHit> prim;
+    if (grid && raster_primary()) {
+        // one grid, slot == ray index: every segment maps with offset 0
+        const int64_t nseg = (n + kSegRays - 1) / kSegRays;
+        std::vector<int64_t> sb{0, nseg}, ss(nseg, 0);
+        const int bg = 0;
+        DevBuf<int64_t> dsb(2), dss(nseg);
+        DevBuf<int> dbg(1);
+        CUDA_TRY(prim.alloc(n));
+        CUDA_TRY(dsb.status()); CUDA_TRY(dss.status()); CUDA_TRY(dbg.status());
+        CUDA_TRY(cudaMemcpyAsync(dsb.p, sb.data(), 16, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaMemcpyAsync(dss.p, ss.data(), 8 * nseg, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaMemcpyAsync(dbg.p, &bg, 4, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaMemsetAsync(prim.p, 0xff, sizeof(PrimHit) * n, st));
+        RasterArgs ra = raster_args(bvh, dg.p, dbg.p, 1, dsb.p, dss.p, prim.p);
+        ra.counter = ctx->counter.p + 1;
+        CUDA_TRY(launch_raster(ra, st, ctx->stats()));
+        CUDA_TRY(cudaStreamSynchronize(st));   // scratch tables die with this scope
+    }
+    CUDA_TRY(launch_trace_full(cfg, dg.p, o.p, d.p, n, fo, prim.p, ctx->counter.p, st,
+                               ctx->stats()));
     CUDA_TRY(cudaMemcpyAsync(valid, dv.p, n, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaMemcpyAsync(escaped, de.p, n, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaMemcpyAsync(normal0, dn.p, 24 * n, cudaMemcpyDeviceToHost, st));
@@ -791,10 +840,22 @@ static int upload_freqs(sbr_ctx *ctx, const double *k, int nk, double gamma, int
 // ctx->stream); writes segment partials into seg_dev and diagnostics into
 // diag_dev (both pre-zeroed by the caller).
 static int run_units(sbr_ctx *ctx, const sbr_bvh *bvh, const std::vector<UnitDev> &all_units,
-                     int nk, const TraceCfg &cfg, double2 *seg_dev, int64_t *diag_dev)
+                     const std::vector<int64_t> &seg_base, int nk, const TraceCfg &cfg,
+                     double2 *seg_dev, int64_t *diag_dev)
 {
     cudaStream_t st = ctx->stream;
     const int64_t budget = slot_budget();
+    const bool raster = raster_primary();
+    const int ngrids = (int)seg_base.size() - 1;
+    std::vector<int64_t> seg_slot;
+    std::vector<int> bgrids;
+    if (raster) {
+        CUDA_TRY(ctx->seg_base.reserve(seg_base.size()));
+        CUDA_TRY(cudaMemcpyAsync(ctx->seg_base.p, seg_base.data(), 8 * seg_base.size(),
+                                 cudaMemcpyHostToDevice, st));
+        CUDA_TRY(ctx->seg_slot.reserve(seg_base[ngrids]));
+        CUDA_TRY(ctx->bgrids.reserve(ngrids));
+    }
     size_t u0 = 0;
     std::vector<UnitDev> batch;
     while (u0 < all_units.size()) {
@@ -816,8 +877,27 @@ static int run_units(sbr_ctx *ctx, const sbr_bvh *bvh, const std::vector<UnitDev
         CUDA_TRY(cudaMemcpyAsync(ctx->units.p, batch.data(), sizeof(UnitDev) * batch.size(),
                                  cudaMemcpyHostToDevice, st));
         if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev[0], st));
+        if (raster) {
+            seg_slot.assign(seg_base[ngrids], kNoSlot);
+            bgrids.clear();
+            for (const UnitDev &u : batch) {
+                seg_slot[u.seg_out] = u.slot_base - u.ray_begin;
+                if (bgrids.empty() || bgrids.back() != u.grid) bgrids.push_back(u.grid);
+            }
+            CUDA_TRY(cudaMemcpyAsync(ctx->seg_slot.p, seg_slot.data(), 8 * seg_slot.size(),
+                                     cudaMemcpyHostToDevice, st));
+            CUDA_TRY(cudaMemcpyAsync(ctx->bgrids.p, bgrids.data(), 4 * bgrids.size(),
+                                     cudaMemcpyHostToDevice, st));
+            CUDA_TRY(cudaMemsetAsync(ctx->slots.p, 0xff, sizeof(SlotRec) * slots, st));
+            RasterArgs ra = raster_args(bvh, ctx->grids.p, ctx->bgrids.p, (int)bgrids.size(),
+                                        ctx->seg_base.p, ctx->seg_slot.p,
+                                        reinterpret_cast<PrimHit *>(ctx->slots.p));
+            ra.counter = ctx->counter.p + 1;
+            CUDA_TRY(launch_raster(ra, st, ctx->stats()));
+        }
+        if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev[3], st));
         CUDA_TRY(launch_trace_solve(cfg, ctx->grids.p, ctx->units.p, (int)batch.size(), slots,
-                                    ctx->slots.p, ctx->counter.p, st, ctx->stats()));
+                                    ctx->slots.p, ctx->counter.p, raster, st, ctx->stats()));
         if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev[1], st));
         CUDA_TRY(launch_po(ctx->slots.p, ctx->units.p, (int)batch.size(), slots / kChunk,
                            ctx->k2.p, nk, ctx->dkturn, ctx->gpow.p, cfg.max_bounces, ctx->chunk_part.p,
@@ -829,8 +909,11 @@ static int run_units(sbr_ctx *ctx, const sbr_bvh *bvh, const std::vector<UnitDev
         CUDA_TRY(cudaStreamSynchronize(st));
         if (ctx->profile) {
             float a = 0.f, b = 0.f;
-            CUDA_TRY(cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]));
+            float c = 0.f;
+            CUDA_TRY(cudaEventElapsedTime(&c, ctx->ev[0], ctx->ev[3]));
+            CUDA_TRY(cudaEventElapsedTime(&a, ctx->ev[3], ctx->ev[1]));
             CUDA_TRY(cudaEventElapsedTime(&b, ctx->ev[1], ctx->ev[2]));
+            ctx->raster_ms += c;
             ctx->trace_ms += a;
             ctx->po_ms += b;
             ctx->trace_n += 1;
@@ -918,7 +1001,7 @@ static int solve_shard_locked(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh 
     }
     TraceCfg cfg = make_cfg(bvh, params, ctx);
     cfg.count_trapped = count_trapped;
-    if (int rc = run_units(ctx, bvh, units, nk, cfg, seg_dev, diag_dev)) return rc;
+    if (int rc = run_units(ctx, bvh, units, seg_base, nk, cfg, seg_dev, diag_dev)) return rc;
     unsigned int flag = 0;
     unsigned long long bad = 0;
     CUDA_TRY(cudaMemcpyAsync(&flag, ctx->err_flag.p, sizeof(flag), cudaMemcpyDeviceToHost, st));
@@ -1185,8 +1268,15 @@ extern "C" int sbr_ctx_profile(sbr_ctx *ctx, int32_t enable)
     if (enable && !ctx->ev[0])
         for (auto &e : ctx->ev) CUDA_TRY(cudaEventCreate(&e));
     ctx->profile = enable != 0;
-    ctx->trace_ms = ctx->po_ms = 0.0;
+    ctx->trace_ms = ctx->po_ms = ctx->raster_ms = 0.0;
     ctx->trace_n = ctx->po_n = 0;
+    return SBR_OK;
+}
+
+extern "C" int sbr_ctx_raster_stats(sbr_ctx *ctx, double *raster_ms)
+{
+    REQUIRE(ctx && raster_ms, "NULL argument");
+    *raster_ms = ctx->raster_ms;
     return SBR_OK;
 }
 

@@ -448,7 +448,7 @@ static void trace_storage_dispatch(const TraceArgs &a, cudaStream_t st, int num_
 cudaError_t launch_trace_solve(const TraceCfg &cfg, const GridDev *d_grids,
                                const UnitDev *d_units, int n_units, int64_t n_slots,
                                SlotRec *d_slots, unsigned long long *d_counter,
-                               cudaStream_t st, const LaunchStats &ls)
+                               bool prim_from_slots, cudaStream_t st, const LaunchStats &ls)
 {
     cudaError_t e = cudaMemsetAsync(d_counter, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
@@ -460,6 +460,7 @@ cudaError_t launch_trace_solve(const TraceCfg &cfg, const GridDev *d_grids,
     a.n_work = n_slots;
     a.counter = d_counter;
     a.slots = d_slots;
+    a.prim = prim_from_slots ? reinterpret_cast<const PrimHit *>(d_slots) : nullptr;
     trace_storage_dispatch<kModeSolve>(a, st, ls.num_sms);
     ++*ls.launches;
     return cudaGetLastError();
@@ -467,8 +468,9 @@ cudaError_t launch_trace_solve(const TraceCfg &cfg, const GridDev *d_grids,
 
 cudaError_t launch_trace_full(const TraceCfg &cfg, const GridDev *d_grid,
                               const double *d_orig, const double *d_dirs, int64_t n,
-                              const FullOut &out, unsigned long long *d_counter,
-                              cudaStream_t st, const LaunchStats &ls)
+                              const FullOut &out, const PrimHit *d_prim,
+                              unsigned long long *d_counter, cudaStream_t st,
+                              const LaunchStats &ls)
 {
     cudaError_t e = cudaMemsetAsync(d_counter, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
@@ -480,6 +482,7 @@ cudaError_t launch_trace_full(const TraceCfg &cfg, const GridDev *d_grid,
     a.n_work = n;
     a.counter = d_counter;
     a.full = out;
+    a.prim = d_grid ? d_prim : nullptr;
     if (d_grid) trace_storage_dispatch<kModeGrid>(a, st, ls.num_sms);
     else trace_storage_dispatch<kModeList>(a, st, ls.num_sms);
     ++*ls.launches;

@@ -42,6 +42,18 @@ constexpr uint32_t kMetaSel = 1u << 18;
 constexpr uint32_t kMetaActive = 1u << 19;
 constexpr uint32_t kMetaBounceMask = 0xffffu;
 
+// Primary-visibility result of one ray (query 0), written by the raster
+// pass with two atomicMin sweeps and read by the trace kernel.  Aliases the
+// SlotRec of the same slot in the fused solve: tbits <-> R, id <-> meta.
+// All-ones = no hit (the buffer is memset to 0xff before the pass).
+struct __align__(16) PrimHit {
+    unsigned long long tbits;   // bits of the closest accepted t (> 0, finite)
+    unsigned int pad;
+    unsigned int id;            // smallest triangle id among hits at that t
+};
+static_assert(sizeof(PrimHit) == sizeof(SlotRec), "PrimHit aliases SlotRec");
+constexpr unsigned long long kNoHitBits = ~0ULL;
+
 struct TraceCfg {
     BvhView B;
     int storage;
@@ -60,10 +72,12 @@ struct LaunchStats {
 };
 
 // ---- trace ---------------------------------------------------------------
+// prim_from_slots: query 0 of every ray was resolved by launch_raster into
+// the slots (PrimHit aliasing), the kernel starts at the first bounce.
 cudaError_t launch_trace_solve(const TraceCfg &cfg, const GridDev *d_grids,
                                const UnitDev *d_units, int n_units, int64_t n_slots,
                                SlotRec *d_slots, unsigned long long *d_counter,
-                               cudaStream_t st, const LaunchStats &ls);
+                               bool prim_from_slots, cudaStream_t st, const LaunchStats &ls);
 
 struct FullOut {
     uint8_t *valid;
@@ -76,15 +90,41 @@ struct FullOut {
 };
 
 // grid != null: rays from the grid; else origins/dirs arrays
+// d_prim (grid mode only, may be null): query-0 results from launch_raster
 cudaError_t launch_trace_full(const TraceCfg &cfg, const GridDev *d_grid,
                               const double *d_orig, const double *d_dirs, int64_t n,
-                              const FullOut &out, unsigned long long *d_counter,
-                              cudaStream_t st, const LaunchStats &ls);
+                              const FullOut &out, const PrimHit *d_prim,
+                              unsigned long long *d_counter, cudaStream_t st,
+                              const LaunchStats &ls);
 
 cudaError_t launch_closest(const BvhView &B, int storage, const double *d_orig,
                            const double *d_dirs, int64_t n, double t_min, double t_max,
                            int64_t *d_tri, double *d_t, int64_t *d_visits, cudaStream_t st,
                            const LaunchStats &ls);
+
+// ---- primary visibility (raster pass) -------------------------------------
+// The primary rays of an aperture form a regular orthographic grid with one
+// direction, so query 0 of every ray is answered per TRIANGLE instead of per
+// ray: each (grid, triangle) pair enumerates the grid cells inside the
+// triangle's projected bounding box (plus a margin) and runs the same exact
+// FP64 Moller-Trumbore test on each (origin built exactly as the launcher
+// builds it).  Pass 0 atomicMin's the t bits, pass 1 atomicMin's the id
+// among triangles that reached that t: the lexicographic (t, id) minimum of
+// bvh.py:340, independent of execution order.
+struct RasterArgs {
+    BvhView B;
+    int storage;
+    int64_t ntri;              // triangles (leaf-order slots)
+    const GridDev *grids;
+    const int *bgrids;         // grids of this batch
+    int nbg;
+    const int64_t *seg_base;   // (ngrids+1) first global segment row of each grid
+    const int64_t *seg_slot;   // per global segment row: slot - ray index, or kNoSlot
+    PrimHit *prim;
+    unsigned long long *counter;   // work counter (zeroed by launch_raster)
+};
+constexpr int64_t kNoSlot = INT64_MIN;   // segment not in this batch / shard
+cudaError_t launch_raster(const RasterArgs &a, cudaStream_t st, const LaunchStats &ls);
 
 // ---- integrate ------------------------------------------------------------
 cudaError_t launch_records_to_slots(const uint8_t *valid, const double *n0,

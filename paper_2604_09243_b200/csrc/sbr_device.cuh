@@ -123,20 +123,35 @@ __device__ __forceinline__ TriF64 load_tri(const BvhView &B, int k)
     return r;
 }
 
-// Returns t in (t_min, t_max] or -1.0 (edge-inclusive), bit-identical to
-// the reference.  Operand association: a*b + c*d + e*f == (ab + cd) + ef.
-__device__ __forceinline__ double tri_hit_exact(const TriF64 &T, double ox,
-                                                double oy, double oz, double dx,
-                                                double dy, double dz,
-                                                double t_min, double t_max)
+// Direction-only part of the test: p = d x e2 and det = e1 . p
+// (geometry.py:336-339).  Identical for every ray of one aperture, so the
+// primary-visibility pass hoists it out of its per-cell loop.
+struct TriDir {
+    double px, py, pz, det;
+};
+
+__device__ __forceinline__ TriDir tri_dir(const TriF64 &T, double dx, double dy, double dz)
 {
-    double px = DS(DM(dy, T.e2z), DM(dz, T.e2y));
-    double py = DS(DM(dz, T.e2x), DM(dx, T.e2z));
-    double pz = DS(DM(dx, T.e2y), DM(dy, T.e2x));
-    double det = DA(DA(DM(T.e1x, px), DM(T.e1y, py)), DM(T.e1z, pz));
-    if (det == 0.0) return -1.0;
+    TriDir r;
+    r.px = DS(DM(dy, T.e2z), DM(dz, T.e2y));
+    r.py = DS(DM(dz, T.e2x), DM(dx, T.e2z));
+    r.pz = DS(DM(dx, T.e2y), DM(dy, T.e2x));
+    r.det = DA(DA(DM(T.e1x, r.px), DM(T.e1y, r.py)), DM(T.e1z, r.pz));
+    return r;
+}
+
+// Origin-dependent part (geometry.py:340-355) for det != 0.  HAVE_INV: the
+// caller passes inv == __drcp_rn(det) (== IEEE 1.0 / det); otherwise it is
+// computed here, after the division-free pre-filters.
+template <bool HAVE_INV>
+__device__ __forceinline__ double tri_hit_origin(const TriF64 &T, const TriDir &P, double inv,
+                                                 double ox, double oy, double oz, double dx,
+                                                 double dy, double dz, double t_min,
+                                                 double t_max)
+{
+    const double det = P.det;
     double tx = DS(ox, T.ax), ty = DS(oy, T.ay), tz = DS(oz, T.az);
-    double un = DA(DA(DM(tx, px), DM(ty, py)), DM(tz, pz));
+    double un = DA(DA(DM(tx, P.px), DM(ty, P.py)), DM(tz, P.pz));
     // Division-free pre-filters.  They only reject rays the exact test below
     // rejects too: with 1e-150 < |un|, |det| < 1e150 the rounded product
     // un * fl(1/det) is a normal number carrying the sign of un*det, so
@@ -151,7 +166,7 @@ __device__ __forceinline__ double tri_hit_exact(const TriF64 &T, double ox,
     double vn = DA(DA(DM(dx, qx), DM(dy, qy)), DM(dz, qz));
     if (safe && fabs(vn) > 1e-150 && ((vn < 0.0) != (det < 0.0))) return -1.0;
     // exact reference sequence (geometry.py:340-352)
-    double inv = __drcp_rn(det);  // == IEEE 1.0 / det
+    if (!HAVE_INV) inv = __drcp_rn(det);  // == IEEE 1.0 / det
     double u = DM(un, inv);
     if (u < 0.0 || u > 1.0) return -1.0;
     double v = DM(vn, inv);
@@ -159,6 +174,18 @@ __device__ __forceinline__ double tri_hit_exact(const TriF64 &T, double ox,
     double t = DM(DA(DA(DM(T.e2x, qx), DM(T.e2y, qy)), DM(T.e2z, qz)), inv);
     if (t <= t_min || t > t_max) return -1.0;
     return t;
+}
+
+// Returns t in (t_min, t_max] or -1.0 (edge-inclusive), bit-identical to
+// the reference.  Operand association: a*b + c*d + e*f == (ab + cd) + ef.
+__device__ __forceinline__ double tri_hit_exact(const TriF64 &T, double ox,
+                                                double oy, double oz, double dx,
+                                                double dy, double dz,
+                                                double t_min, double t_max)
+{
+    const TriDir P = tri_dir(T, dx, dy, dz);
+    if (P.det == 0.0) return -1.0;
+    return tri_hit_origin<false>(T, P, 0.0, ox, oy, oz, dx, dy, dz, t_min, t_max);
 }
 
 // ---------------------------------------------------------------------------

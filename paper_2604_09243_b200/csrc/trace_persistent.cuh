@@ -44,6 +44,9 @@ struct TraceArgs {
     const double *orig, *dirs;  // list mode
     int64_t n_work;           // solve: slots; grid/list: rays
     unsigned long long *counter;
+    // query-0 results of the raster pass (solve: aliases `slots`, indexed by
+    // slot; grid: indexed by ray); null = trace query 0 through the BVH
+    const PrimHit *prim;
     // outputs
     SlotRec *slots;           // solve
     FullOut full;             // grid / list
@@ -199,7 +202,17 @@ k_trace_persistent(TraceArgs a)
                     }
                     L.path = 0.0; L.n0x = L.n0y = L.n0z = 0.0; L.cosd = 0.0;
                     L.bounces = 0; L.valid = false; L.probe = false;
-                    start_query<STORAGE>(B, L, state);
+                    if (MODE != kModeList && a.prim) {
+                        // query 0 already answered by the raster pass
+                        const PrimHit h = a.prim[MODE == kModeSolve ? L.slot : L.r];
+                        const bool hit = h.tbits != kNoHitBits;
+                        L.best_t = hit ? __longlong_as_double((long long)h.tbits)
+                                       : __longlong_as_double(0x7ff0000000000000LL);
+                        L.best = hit ? (int)h.id : -1;
+                        state = kDone;
+                    } else {
+                        start_query<STORAGE>(B, L, state);
+                    }
                 }
             }
         }

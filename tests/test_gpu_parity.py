@@ -40,6 +40,13 @@ def _grid(g):
                             standoff=float(g["grid_standoff"]), margin=float(g["grid_margin"]))
 
 
+@pytest.fixture(params=["raster", "bvh"])
+def primary(request, monkeypatch):
+    """Query 0 answered by the raster pass (default) or by BVH traversal."""
+    monkeypatch.setenv("SBR_PRIMARY", request.param)
+    return request.param
+
+
 def _amp_close(a, ref):
     a, ref = complex(a), complex(ref)
     assert abs(a - ref) <= FIELD_RTOL * abs(ref) + 1e-300, (a, ref)
@@ -112,7 +119,7 @@ def test_closest_hit_t_window_and_root_cull():
 
 
 @pytest.mark.parametrize("name", golden_names("trace_"))
-def test_trace_grid_bitwise_with_ids(name):
+def test_trace_grid_bitwise_with_ids(name, primary):
     g = load_golden(name)
     mesh = _mesh(g)
     tree = sbr.build(mesh)
@@ -140,7 +147,7 @@ def test_accumulate_matches_reference(name):
 
 
 @pytest.mark.parametrize("name", golden_names("trace_"))
-def test_fused_solve_matches_reference(name):
+def test_fused_solve_matches_reference(name, primary):
     g = load_golden(name)
     if g["epsilon_given"]:
         pytest.skip("fixture uses an explicit epsilon; covered by trace test")
@@ -196,7 +203,7 @@ def _oracle_scene(orc, mesh):
 
 
 @pytest.mark.parametrize("case", ["aircraft", "sphere_s6", "rough_b5"])
-def test_trace_vs_oracle_larger(orc, case):
+def test_trace_vs_oracle_larger(orc, case, primary):
     if case == "aircraft":
         mesh = meshgen.generate_aircraft(density=0.05)
         lam, B, dirs = 0.12, 5, [(math.pi / 2, math.pi), (math.pi / 2, 0.3), (1.2, 2.0)]
@@ -227,7 +234,7 @@ def test_trace_vs_oracle_larger(orc, case):
         assert sol.valid_rays == int(full.valid.sum())
 
 
-def test_solve_is_deterministic_and_batch_invariant(monkeypatch):
+def test_solve_is_deterministic_and_batch_invariant(monkeypatch, primary):
     mesh = meshgen.quantized_icosphere(1.0, 5)
     tree = sbr.build(mesh)
     lam = 2 * math.pi / 60
@@ -248,7 +255,7 @@ def test_solve_is_deterministic_and_batch_invariant(monkeypatch):
         assert np.array_equal(s.amplitude[0], a.amplitude[i])
 
 
-def test_sharded_solve_equals_single(orc):
+def test_sharded_solve_equals_single(orc, primary):
     """Simulated N-rank run on one GPU: summing the disjoint shard buffers
     and finalising reproduces sbr_solve bit for bit (both shard modes)."""
     import ctypes
@@ -382,3 +389,28 @@ def test_multifrequency_po_vs_oracle(orc, uniform):
         ref = orc.accumulate(rec, grid.k_inc, 2 * math.pi / ka[f], grid.cell_area)
         _amp_close(res.amplitude[0, f], ref)
         _amp_close(multi[f], ref)
+
+
+def test_raster_primary_equals_bvh_primary(monkeypatch):
+    """The raster pass answers query 0 with the same bits as BVH traversal:
+    a multi-angle aircraft solve gives bitwise-identical amplitudes and
+    diagnostics in both modes (also with tiny batches and ray-tile shards)."""
+    mesh = meshgen.generate_aircraft(density=0.03)
+    tree = sbr.build(mesh)
+    lam = 0.1
+    grids = [sbr.build_aperture(mesh.aabb, sbr.IncidentDirection(th, ph), lam / 5,
+                                wavelength=lam)
+             for th, ph in [(math.pi / 2, 0.0), (math.pi / 2, 2.0), (1.1, 4.0), (0.2, 1.0)]]
+    tp = sbr.TraceParams(max_bounces=5)
+    ks = [2 * math.pi / lam]
+    out = {}
+    for mode in ("bvh", "raster"):
+        monkeypatch.setenv("SBR_PRIMARY", mode)
+        out[mode] = sbr.solve_grids(tree, mesh, grids, tp, ks)
+    monkeypatch.setenv("SBR_SLOT_BUDGET", "5120")
+    out["raster_small"] = sbr.solve_grids(tree, mesh, grids, tp, ks)
+    for k in ("raster", "raster_small"):
+        assert np.array_equal(out[k].amplitude, out["bvh"].amplitude), k
+        assert np.array_equal(out[k].bounce_counts, out["bvh"].bounce_counts), k
+        assert np.array_equal(out[k].valid_rays, out["bvh"].valid_rays), k
+        assert np.array_equal(out[k].queries, out["bvh"].queries), k
