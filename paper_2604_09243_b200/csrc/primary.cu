@@ -44,9 +44,9 @@ struct __align__(16) U128 {
 __device__ __forceinline__ void prim_min(PrimHit *h, unsigned long long bits, unsigned int id)
 {
     U128 *p = reinterpret_cast<U128 *>(h);
-    U128 cur;
-    cur.lo = *reinterpret_cast<volatile unsigned long long *>(&p->lo);
-    cur.hi = *reinterpret_cast<volatile unsigned long long *>(&p->hi);
+    // pre-check with one plain 16-byte load; a stale (cached) value is safe:
+    // entries only ever decrease, and the CAS re-validates
+    U128 cur = *p;
     U128 nv;
     nv.lo = bits;
     nv.hi = 0xffffffffULL | ((unsigned long long)id << 32);
