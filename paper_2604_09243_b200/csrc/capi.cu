@@ -69,6 +69,8 @@ struct sbr_ctx {
     DevBuf<int64_t> seg_base;
     DevBuf<int64_t> seg_slot;    // raster pass: global segment row -> slot offset
     DevBuf<int> bgrids;          // raster pass: grids of the current batch
+    DevBuf<unsigned int> worklist;          // raster pass: slots whose query 0 hit
+    DevBuf<unsigned long long> nwork;
     DevBuf<double> k2, gpow, scale;
     double dkturn = 0.0;         // uniform wavenumber step in turns (0: not uniform)
     DevBuf<double2> amp;
@@ -895,9 +897,18 @@ static int run_units(sbr_ctx *ctx, const sbr_bvh *bvh, const std::vector<UnitDev
             ra.counter = ctx->counter.p + 1;
             CUDA_TRY(launch_raster(ra, st, ctx->stats()));
         }
+        if (raster) {
+            CUDA_TRY(ctx->worklist.reserve(slots));
+            CUDA_TRY(ctx->nwork.reserve(1));
+            CUDA_TRY(launch_prim_compact(cfg, ctx->grids.p, ctx->units.p, (int)batch.size(),
+                                         slots, ctx->slots.p, ctx->worklist.p, ctx->nwork.p, st,
+                                         ctx->stats()));
+        }
         if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev[3], st));
         CUDA_TRY(launch_trace_solve(cfg, ctx->grids.p, ctx->units.p, (int)batch.size(), slots,
-                                    ctx->slots.p, ctx->counter.p, raster, st, ctx->stats()));
+                                    ctx->slots.p, ctx->counter.p, raster,
+                                    raster ? ctx->worklist.p : nullptr,
+                                    raster ? ctx->nwork.p : nullptr, st, ctx->stats()));
         if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev[1], st));
         CUDA_TRY(launch_po(ctx->slots.p, ctx->units.p, (int)batch.size(), slots / kChunk,
                            ctx->k2.p, nk, ctx->dkturn, ctx->gpow.p, cfg.max_bounces, ctx->chunk_part.p,

@@ -339,6 +339,101 @@ k_po(const SlotRec *__restrict__ slots, const UnitDev *__restrict__ units, int n
 }
 
 // ---------------------------------------------------------------------------
+// hit-list compaction after the raster pass
+// ---------------------------------------------------------------------------
+// A slot whose primary ray missed is finished (transport.py:294-296: miss on
+// query 0 -> escaped, invalid, N = 0); write its record here so the trace
+// kernel only ever receives rays with work left.  Hits are appended to the
+// work list 32 slots (one warp ballot) at a time, so consecutive list entries
+// are neighbouring rays of one aperture: coherent first bounces.
+constexpr int kCompactThreads = 256;
+constexpr int kCompactPer = 4;                        // slots per thread per tile
+constexpr int kCompactTile = kCompactThreads * kCompactPer;   // == kChunk
+
+__global__ void __launch_bounds__(kCompactThreads)
+k_prim_compact(TraceCfg cfg, const GridDev *__restrict__ grids,
+               const UnitDev *__restrict__ units, int n_units, int64_t n_slots,
+               SlotRec *__restrict__ slots, unsigned int *__restrict__ list,
+               unsigned long long *__restrict__ nlist)
+{
+    constexpr int W = kCompactThreads / 32;
+    __shared__ int cnt[kCompactPer][W];
+    __shared__ int pos[kCompactPer][W];
+    __shared__ unsigned long long s_at;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int64_t tile = (int64_t)blockIdx.x * kCompactTile; tile < n_slots;
+         tile += (int64_t)gridDim.x * kCompactTile) {
+        // slots are chunk-aligned per unit and kCompactTile == kChunk: one unit
+        const UnitDev U = units[find_unit(units, n_units, tile)];
+        const bool alias_ok =
+            cfg.allow_aliasing || !(grids[U.grid].spacing > cfg.spacing_limit);
+        if (!alias_ok && tid == 0) atomicOr(cfg.error_flag, 1u);
+        unsigned hitmask = 0;
+#pragma unroll
+        for (int q = 0; q < kCompactPer; ++q) {
+            const int64_t slot = tile + q * kCompactThreads + tid;
+            bool hit = false;
+            if (slot < n_slots) {
+                const int64_t r = U.ray_begin + (slot - U.slot_base);
+                const bool real = r < U.ray_end && alias_ok;
+                const PrimHit h = reinterpret_cast<const PrimHit *>(slots)[slot];
+                hit = real && h.tbits != kNoHitBits;
+                if (!hit) {
+                    SlotRec z;
+                    z.R = 0.0;
+                    z.cosv = 0.f;
+                    z.meta = real ? (kMetaActive | kMetaEscaped) : 0u;
+                    slots[slot] = z;
+                }
+            }
+            const unsigned bal = __ballot_sync(0xffffffffu, hit);
+            if (lane == 0) cnt[q][warp] = __popc(bal);
+            hitmask |= (hit ? 1u : 0u) << q;
+        }
+        __syncthreads();
+        if (tid == 0) {   // exclusive scan in slot order + one atomic per tile
+            int run = 0;
+            for (int q = 0; q < kCompactPer; ++q)
+                for (int w = 0; w < W; ++w) {
+                    pos[q][w] = run;
+                    run += cnt[q][w];
+                }
+            s_at = run ? atomicAdd(nlist, (unsigned long long)run) : 0ULL;
+        }
+        __syncthreads();
+        const unsigned long long at = s_at;
+#pragma unroll
+        for (int q = 0; q < kCompactPer; ++q) {
+            const bool hit = (hitmask >> q) & 1u;
+            const unsigned bal = __ballot_sync(0xffffffffu, hit);
+            if (hit)
+                list[at + pos[q][warp] + __popc(bal & ((1u << lane) - 1u))] =
+                    (unsigned int)(tile + q * kCompactThreads + tid);
+        }
+        __syncthreads();
+    }
+}
+
+cudaError_t launch_prim_compact(const TraceCfg &cfg, const GridDev *d_grids,
+                                const UnitDev *d_units, int n_units, int64_t n_slots,
+                                SlotRec *d_slots, unsigned int *d_worklist,
+                                unsigned long long *d_nwork, cudaStream_t st,
+                                const LaunchStats &ls)
+{
+    cudaError_t e = cudaMemsetAsync(d_nwork, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return e;
+    static_assert(kCompactTile == kChunk, "tiles must not straddle units");
+    int64_t blocks = (n_slots + kCompactTile - 1) / kCompactTile;
+    const int64_t cap = (int64_t)ls.num_sms * 8;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    k_prim_compact<<<(unsigned)blocks, kCompactThreads, 0, st>>>(
+        cfg, d_grids, d_units, n_units, n_slots, d_slots, d_worklist, d_nwork);
+    ++*ls.launches;
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // deterministic pairwise trees
 // ---------------------------------------------------------------------------
 // Sequential adjacent-pair tree with odd-tail carry (po.py:59-80 shape),
@@ -448,7 +543,9 @@ static void trace_storage_dispatch(const TraceArgs &a, cudaStream_t st, int num_
 cudaError_t launch_trace_solve(const TraceCfg &cfg, const GridDev *d_grids,
                                const UnitDev *d_units, int n_units, int64_t n_slots,
                                SlotRec *d_slots, unsigned long long *d_counter,
-                               bool prim_from_slots, cudaStream_t st, const LaunchStats &ls)
+                               bool prim_from_slots, const unsigned int *d_worklist,
+                               const unsigned long long *d_nwork, cudaStream_t st,
+                               const LaunchStats &ls)
 {
     cudaError_t e = cudaMemsetAsync(d_counter, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
@@ -461,6 +558,8 @@ cudaError_t launch_trace_solve(const TraceCfg &cfg, const GridDev *d_grids,
     a.counter = d_counter;
     a.slots = d_slots;
     a.prim = prim_from_slots ? reinterpret_cast<const PrimHit *>(d_slots) : nullptr;
+    a.worklist = d_worklist;
+    a.n_work_dev = d_nwork;
     trace_storage_dispatch<kModeSolve>(a, st, ls.num_sms);
     ++*ls.launches;
     return cudaGetLastError();

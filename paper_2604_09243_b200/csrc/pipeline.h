@@ -74,10 +74,21 @@ struct LaunchStats {
 // ---- trace ---------------------------------------------------------------
 // prim_from_slots: query 0 of every ray was resolved by launch_raster into
 // the slots (PrimHit aliasing), the kernel starts at the first bounce.
+// worklist (raster mode): slots still to trace, count in *d_nwork.
 cudaError_t launch_trace_solve(const TraceCfg &cfg, const GridDev *d_grids,
                                const UnitDev *d_units, int n_units, int64_t n_slots,
                                SlotRec *d_slots, unsigned long long *d_counter,
-                               bool prim_from_slots, cudaStream_t st, const LaunchStats &ls);
+                               bool prim_from_slots, const unsigned int *d_worklist,
+                               const unsigned long long *d_nwork, cudaStream_t st,
+                               const LaunchStats &ls);
+
+// After the raster pass: final records for padding / aliasing-rejected /
+// missed slots, and the list of slots whose query 0 hit (warp-ordered).
+cudaError_t launch_prim_compact(const TraceCfg &cfg, const GridDev *d_grids,
+                                const UnitDev *d_units, int n_units, int64_t n_slots,
+                                SlotRec *d_slots, unsigned int *d_worklist,
+                                unsigned long long *d_nwork, cudaStream_t st,
+                                const LaunchStats &ls);
 
 struct FullOut {
     uint8_t *valid;

@@ -47,6 +47,10 @@ struct TraceArgs {
     // query-0 results of the raster pass (solve: aliases `slots`, indexed by
     // slot; grid: indexed by ray); null = trace query 0 through the BVH
     const PrimHit *prim;
+    // solve + raster: the slots whose query 0 hit (k_prim_compact); the other
+    // slots already hold their final records.  n_work is read from n_work_dev.
+    const unsigned int *worklist;
+    const unsigned long long *n_work_dev;
     // outputs
     SlotRec *slots;           // solve
     FullOut full;             // grid / list
@@ -131,6 +135,7 @@ k_trace_persistent(TraceArgs a)
     StackEntry stack[kStack];
     LaneRay L;
     int state = kIdle;
+    const int64_t n_work = a.worklist ? (int64_t)*a.n_work_dev : a.n_work;
     bool exhausted = false;
     int64_t chunk_next = 0, chunk_end = 0;   // warp-uniform private work range
 
@@ -151,7 +156,8 @@ k_trace_persistent(TraceArgs a)
             if (want & (1u << lane)) {
                 const int rank = __popc(want & lt_mask);
                 const int64_t w = rank < avail ? chunk_next + rank : fresh + (rank - avail);
-                if (w < a.n_work) L.slot = w; else exhausted = true;
+                if (w < n_work) L.slot = a.worklist ? (int64_t)__ldg(&a.worklist[w]) : w;
+                else exhausted = true;
             }
             if (avail >= need) {
                 chunk_next += need;
