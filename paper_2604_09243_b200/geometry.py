@@ -135,7 +135,7 @@ class Mesh:
         if cached is None:
             h = hashlib.sha256()
             for a in (self.v0, self.v1, self.v2):
-                h.update(np.ascontiguousarray(a, dtype=np.float64).tobytes())
+                h.update(np.ascontiguousarray(a, dtype=np.float64).data)
             cached = self._dev["checksum"] = h.hexdigest()
         return cached
 

@@ -42,14 +42,23 @@ class IncidentDirection:
                    math.atan2(-k[1], -k[0]) % (2.0 * math.pi))
 
 
+def _cross3(a, b) -> np.ndarray:
+    """numpy.cross for two 3-vectors with the same per-component rounding
+    (a1*b2 - a2*b1, ...: one product rounding each, then one subtraction),
+    without numpy.cross's per-call axis bookkeeping."""
+    a0, a1, a2 = float(a[0]), float(a[1]), float(a[2])
+    b0, b1, b2 = float(b[0]), float(b[1]), float(b[2])
+    return np.array([a1 * b2 - a2 * b1, a2 * b0 - a0 * b2, a0 * b1 - a1 * b0])
+
+
 def orthonormal_basis(k_inc) -> tuple[np.ndarray, np.ndarray]:
     """Right-handed (u, v, k): u = normalize(seed x k), v = k x u; the seed is
     the world axis least aligned with k (ties x -> y -> z)."""
     k = np.asarray(k_inc, dtype=np.float64)
     seed = np.eye(3)[int(np.argmin(np.abs(k)))]
-    u = np.cross(seed, k)
+    u = _cross3(seed, k)
     u /= np.linalg.norm(u)
-    return u, np.cross(k, u)
+    return u, _cross3(k, u)
 
 
 class SamplingCheck(NamedTuple):
