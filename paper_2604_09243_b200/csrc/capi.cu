@@ -598,13 +598,18 @@ static int check_pair(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *bvh)
     return SBR_OK;
 }
 
-// Query 0 of aperture rays: rasterised per triangle (default) or traced
-// through the BVH like every other query (SBR_PRIMARY=bvh).  Both give the
-// same bits; the switch exists for A/B measurement and parity tests.
-static bool raster_primary()
+// Query 0 of aperture rays: rasterised per triangle or traced through the
+// BVH like every other query.  Both give the same bits.  The raster pass
+// hands each warp 32 triangles of one grid, so it needs many (grid,
+// triangle) pairs to fill the GPU: below ~16k warps of work (a handful of
+// large triangles, e.g. corner reflectors) the BVH path is faster.
+// SBR_PRIMARY=raster|bvh forces a path (A/B measurement, parity tests).
+static bool raster_primary(int64_t ntri, int64_t ngrids)
 {
     const char *s = getenv("SBR_PRIMARY");
-    return !(s && std::strcmp(s, "bvh") == 0);
+    if (s && std::strcmp(s, "bvh") == 0) return false;
+    if (s && std::strcmp(s, "raster") == 0) return true;
+    return ngrids * ((ntri + 31) / 32) >= 16384;
 }
 
 static RasterArgs raster_args(const sbr_bvh *bvh, const GridDev *grids, const int *bgrids,
@@ -719,7 +724,7 @@ static int trace_full_common(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *
     TraceCfg cfg = make_cfg(bvh, params, ctx);
     FullOut fo{dv.p, dn.p, dp.p, db.p, de.p, dd.p, tri_ids ? di.p : nullptr};
     DevBuf<PrimHit> prim;
-    if (grid && raster_primary()) {
+    if (grid && raster_primary(mesh->ntri, 1)) {
         // one grid, slot == ray index: every segment maps with offset 0
         const int64_t nseg = (n + kSegRays - 1) / kSegRays;
         std::vector<int64_t> sb{0, nseg}, ss(nseg, 0);
@@ -847,8 +852,8 @@ static int run_units(sbr_ctx *ctx, const sbr_bvh *bvh, const std::vector<UnitDev
 {
     cudaStream_t st = ctx->stream;
     const int64_t budget = slot_budget();
-    const bool raster = raster_primary();
     const int ngrids = (int)seg_base.size() - 1;
+    const bool raster = raster_primary(bvh->mesh->ntri, ngrids);
     std::vector<int64_t> seg_slot;
     std::vector<int> bgrids;
     if (raster) {

@@ -65,7 +65,7 @@ def report(name, mesh, grids, res, t, kst, nk, extra):
     out = {"config": name, "triangles": mesh.triangle_count, "angles": len(grids),
            "rays": rays, "queries": q, "seconds": t,
            "intersections_per_s": q / t, "angles_per_s": len(grids) / t,
-           "trace_ms": kst["trace_ms"], "po_ms": kst["po_ms"],
+           "raster_ms": kst["raster_ms"], "trace_ms": kst["trace_ms"], "po_ms": kst["po_ms"],
            "po_terms": sel * nk,
            "po_terms_per_s": sel * nk / (kst["po_ms"] / 1e3) if kst["po_ms"] else None}
     out.update(extra)
