@@ -42,6 +42,8 @@ typedef enum {
     SBR_EINVAL = 2,    /* ValidationError (errors.py:12) */
     SBR_EIO = 3,       /* OSError */
     SBR_ENUMERIC = 4,  /* NumericalError (errors.py:16) */
+    SBR_ENOTSUP = 5,   /* input outside the native fast path (caller falls back to the
+                          reference-equivalent Python reader; host I/O only) */
     SBR_ECUDA = 10,    /* CUDA runtime failure */
     SBR_ENOMEM = 12    /* device or host allocation failure */
 } sbr_status;
@@ -232,6 +234,25 @@ int sbr_finalize(sbr_ctx *ctx, const sbr_grid *grids, int32_t ngrids,
                  const double *k, int32_t nk, int32_t max_bounces,
                  const double *seg_dev, const int64_t *diag_dev, double *amp,
                  sbr_diag *diag);
+
+/* ---- mesh I/O (host only, no GPU needed) ---------------------------------
+ * geometry.py:190-241 load_mesh: parse a Wavefront OBJ ("v"/"f" records,
+ * 1-based or negative indices, polygons fan-triangulated).  `label` is the
+ * path text used in error messages (reference wording).  SBR_EINVAL carries
+ * the reference's ValidationError message; SBR_ENOTSUP means the file uses
+ * number syntax only Python's float()/int() define (underscores, hex,
+ * non-ASCII) and must be read by the Python loop. */
+typedef struct sbr_obj sbr_obj;
+int sbr_obj_read(const char *path, const char *label, sbr_obj **out);
+int sbr_obj_info(const sbr_obj *obj, int64_t *nverts, int64_t *ntris);
+/* verts (nverts,3) f64, tris (ntris,3) i64 vertex indices, labels (ntris) i64
+ * source face numbers; any pointer may be NULL. */
+int sbr_obj_copy(const sbr_obj *obj, double *verts, int64_t *tris, int64_t *labels);
+int sbr_obj_free(sbr_obj *obj);
+/* geometry.py:244-265 save_obj: exactly-equal corners share a "v" line
+ * (first-seen order, "%.17g"), then one "f a b c" per triangle. */
+int sbr_obj_write(const char *path, const double *v0, const double *v1, const double *v2,
+                  int64_t ntri);
 
 #ifdef __cplusplus
 }

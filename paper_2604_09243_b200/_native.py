@@ -19,7 +19,8 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 # SBR_LIB points at an alternative build (e.g. an instrumented variant)
 LIB_PATH = os.environ.get("SBR_LIB") or os.path.join(_PKG, "libsbr200.so")
 
-SBR_OK, SBR_EINVAL, SBR_EIO, SBR_ENUMERIC, SBR_ECUDA, SBR_ENOMEM = 0, 2, 3, 4, 10, 12
+SBR_OK, SBR_EINVAL, SBR_EIO, SBR_ENUMERIC, SBR_ENOTSUP, SBR_ECUDA, SBR_ENOMEM = \
+    0, 2, 3, 4, 5, 10, 12
 STORAGE_AUTO, STORAGE_F32_EXACT, STORAGE_F64, STORAGE_SINGLE = 0, 1, 2, 3
 SEGMENT_RAYS = 1 << 19
 
@@ -99,6 +100,11 @@ _SIGS = {
     "sbr_solve": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_i32, ctypes.POINTER(TraceParams),
                                  c_vp, c_i32, c_dbl, c_i32, c_vp, ctypes.POINTER(Diag)]),
     "sbr_segment_layout": (ctypes.c_int, [c_vp, c_i32, c_vp]),
+    "sbr_obj_read": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(c_vp)]),
+    "sbr_obj_info": (ctypes.c_int, [c_vp, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),
+    "sbr_obj_copy": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
+    "sbr_obj_free": (ctypes.c_int, [c_vp]),
+    "sbr_obj_write": (ctypes.c_int, [ctypes.c_char_p, c_vp, c_vp, c_vp, c_i64]),
     "sbr_solve_shard": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_i32,
                                        ctypes.POINTER(TraceParams), c_vp, c_i32, c_dbl, c_i32,
                                        c_i32, c_i32, c_i32, c_vp, c_vp]),
@@ -145,6 +151,40 @@ def check(rc: int, what: str = ""):
     if rc == SBR_ENOMEM:
         raise MemoryError(text)
     raise CudaError(f"[{rc}] {text}")
+
+
+def obj_read(path):
+    """Native OBJ parse (sbr_obj_read): (verts (V,3) f64, tris (T,3) i64,
+    labels (T,) i64), or None when the file must be read by the Python loop
+    (SBR_ENOTSUP: number syntax only Python defines; SBR_EIO: let Python's
+    open() raise its own exception).  ValidationError as the reference."""
+    import os
+    lib = load_library()
+    h = c_vp()
+    rc = lib.sbr_obj_read(os.fsencode(path), str(path).encode("utf-8", "surrogateescape"),
+                          ctypes.byref(h))
+    if rc in (SBR_ENOTSUP, SBR_EIO):
+        return None
+    check(rc)
+    try:
+        nv, nt = c_i64(), c_i64()
+        check(lib.sbr_obj_info(h, ctypes.byref(nv), ctypes.byref(nt)))
+        verts = np.empty((nv.value, 3), np.float64)
+        tris = np.empty((nt.value, 3), np.int64)
+        labels = np.empty(nt.value, np.int64)
+        check(lib.sbr_obj_copy(h, ptr(verts), ptr(tris), ptr(labels)))
+    finally:
+        lib.sbr_obj_free(h)
+    return verts, tris, labels
+
+
+def obj_write(path, v0, v1, v2) -> None:
+    """Native save_obj (sbr_obj_write)."""
+    import os
+    lib = load_library()
+    a = [f64(x, (-1, 3)) for x in (v0, v1, v2)]
+    check(lib.sbr_obj_write(os.fsencode(path), *[ptr(x) for x in a], a[0].shape[0]),
+          "sbr_obj_write")
 
 
 def ptr(a) -> c_vp:

@@ -19,15 +19,31 @@ using namespace sbr;
 // ---------------------------------------------------------------------------
 static thread_local std::string g_err;
 
-static int fail(int code, const char *fmt, ...)
+static int vfail(int code, const char *fmt, va_list ap)
 {
     char buf[1024];
-    va_list ap;
-    va_start(ap, fmt);
     vsnprintf(buf, sizeof(buf), fmt, ap);
-    va_end(ap);
     g_err = buf;
     return code;
+}
+
+static int fail(int code, const char *fmt, ...)
+{
+    va_list ap;
+    va_start(ap, fmt);
+    const int rc = vfail(code, fmt, ap);
+    va_end(ap);
+    return rc;
+}
+
+// shared with the other translation units (objio.cpp)
+int sbr_fail(int code, const char *fmt, ...)
+{
+    va_list ap;
+    va_start(ap, fmt);
+    const int rc = vfail(code, fmt, ap);
+    va_end(ap);
+    return rc;
 }
 
 #define CUDA_TRY(x)                                                                     \

@@ -30,7 +30,13 @@
 
 namespace sbr {
 
-constexpr int kChunkRays = 128;   // rays claimed per warp-level atomic
+#ifndef SBR_CHUNK_RAYS
+#define SBR_CHUNK_RAYS 128
+#endif
+#ifndef SBR_TRACE_MINB
+#define SBR_TRACE_MINB 8
+#endif
+constexpr int kChunkRays = SBR_CHUNK_RAYS;   // rays claimed per warp-level atomic
 
 enum LaneState : int { kIdle = 0, kTrav = 1, kLeaf = 2, kDone = 3 };
 enum TraceMode : int { kModeSolve = 0, kModeGrid = 1, kModeList = 2 };
@@ -123,7 +129,7 @@ __device__ __forceinline__ bool pop_next(StackEntry *stack, LaneRay &L)
 // MINB = 8 caps registers at 64 (32 resident warps per SM): measured
 // faster than unconstrained 80-92 registers despite a few spills, since the
 // traversal is latency-bound.
-template <int STORAGE, int MODE, int MINB = 8>
+template <int STORAGE, int MODE, int MINB = SBR_TRACE_MINB>
 __global__ void __launch_bounds__(128, MINB)
 k_trace_persistent(TraceArgs a)
 {

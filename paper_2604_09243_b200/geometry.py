@@ -196,7 +196,20 @@ def mesh_from_arrays(vertices: np.ndarray, faces: np.ndarray, **kwargs) -> Mesh:
 
 def load_mesh(path, strict: bool = False, dtype=np.float64) -> Mesh:
     """Wavefront OBJ subset (geometry.py:190-241): ``v`` and ``f`` records,
-    1-based or negative (relative) indices, polygons fan-triangulated."""
+    1-based or negative (relative) indices, polygons fan-triangulated.
+
+    Parsed by the native reader (sbr_obj_read); files using number syntax
+    only Python's float()/int() define go through the equivalent Python
+    loop, so every input behaves exactly as in the reference."""
+    got = nat.obj_read(path)
+    if got is None:
+        return _load_mesh_py(path, strict, dtype)
+    v, f, labels = got
+    return mesh_from_soup(v[f], path=str(path), strict=strict, dtype=dtype, face_labels=labels)
+
+
+def _load_mesh_py(path, strict: bool = False, dtype=np.float64) -> Mesh:
+    """The reference reader loop (geometry.py:199-241)."""
     verts: list = []
     tris: list = []
     labels: list = []
@@ -238,7 +251,12 @@ def load_mesh(path, strict: bool = False, dtype=np.float64) -> Mesh:
 
 
 def save_obj(mesh: Mesh, path) -> None:
-    """OBJ writer; bit-equal vertices are shared (geometry.py:244-265)."""
+    """OBJ writer; equal vertices are shared (geometry.py:244-265), native."""
+    nat.obj_write(path, mesh.v0, mesh.v1, mesh.v2)
+
+
+def _save_obj_py(mesh: Mesh, path) -> None:
+    """The reference writer loop (geometry.py:244-265), kept as the test oracle."""
     corners = np.stack([np.asarray(mesh.v0, np.float64), np.asarray(mesh.v1, np.float64),
                         np.asarray(mesh.v2, np.float64)], axis=1).reshape(-1, 3)
     lookup: dict = {}
