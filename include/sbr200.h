@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SBR200_ABI_VERSION 1
+#define SBR200_ABI_VERSION 2
 
 typedef enum {
     SBR_OK = 0,
@@ -61,14 +61,20 @@ typedef struct sbr_ctx sbr_ctx;
 typedef struct sbr_mesh sbr_mesh;
 typedef struct sbr_bvh sbr_bvh;
 
-/* Replaces bvh.py:22-49 BuildParams.  split_rule is accepted for API
- * parity; the GPU always builds an LBVH (closest-hit results are tree-
- * independent).  n_leaf bounds the leaf size. */
+/* Replaces bvh.py:22-49 BuildParams.
+ *  SBR_SPLIT_SAH:  the reference's binned-SAH tree (bvh.py:154-299), built on
+ *                  the GPU level by level and identical node for node
+ *                  (sbr_bvh_export returns it verbatim);
+ *  SBR_SPLIT_LBVH: a GPU LBVH (Morton order; fastest build);
+ *  SBR_SPLIT_MEDIAN: accepted for API parity, built as an LBVH.
+ * Closest-hit results do not depend on the tree. */
+enum { SBR_SPLIT_MEDIAN = 0, SBR_SPLIT_SAH = 1, SBR_SPLIT_LBVH = 2 };
 typedef struct {
-    int32_t split_rule;   /* 0 median, 1 sah (informational) */
-    int32_t n_leaf;       /* >= 1 */
-    int32_t max_depth;    /* reference default 64; informational */
-    int32_t reserved;
+    int32_t split_rule;     /* SBR_SPLIT_* */
+    int32_t n_leaf;         /* >= 1 (LBVH: <= 63) */
+    int32_t max_depth;      /* SAH: depth limit, reference default 64 */
+    int32_t bins_per_axis;  /* SAH: 2..64, 0 -> 16 */
+    double c_t, c_i;        /* SAH cost constants, <= 0 -> 1.0 */
 } sbr_build_params;
 
 /* One incident direction's launch grid (transport.py:84-127 ApertureGrid).

@@ -48,9 +48,12 @@ class TraceParams(ctypes.Structure):
                 ("lambda_min", c_dbl), ("sampling_factor", c_dbl)]
 
 
+SPLIT_MEDIAN, SPLIT_SAH, SPLIT_LBVH = 0, 1, 2
+
+
 class BuildParams(ctypes.Structure):
     _fields_ = [("split_rule", c_i32), ("n_leaf", c_i32), ("max_depth", c_i32),
-                ("reserved", c_i32)]
+                ("bins_per_axis", c_i32), ("c_t", c_dbl), ("c_i", c_dbl)]
 
 
 class Diag(ctypes.Structure):

@@ -40,7 +40,7 @@ class BuildParams:
     max_depth: int = 64
 
     def __post_init__(self):
-        if self.split_rule not in ("median", "sah"):
+        if self.split_rule not in ("median", "sah", "lbvh"):
             raise ValidationError(f"unknown split rule {self.split_rule!r}")
         if self.n_leaf < 1:
             raise ValidationError("n_leaf must be >= 1")
@@ -113,6 +113,12 @@ class Bvh:
                    tri_order=np.empty(mesh.triangle_count, np.int32))
         nat.check(lib.sbr_bvh_export(dbvh.handle, *[nat.ptr(out[k]) for k in self._FIELDS]),
                   "sbr_bvh_export")
+        if np.dtype(mesh.dtype) == np.float32:
+            # bvh.py:286-290: float32 meshes get outward-rounded float32 boxes
+            out["nodes_min"] = np.nextafter(out["nodes_min"].astype(np.float32),
+                                            np.float32(-np.inf))
+            out["nodes_max"] = np.nextafter(out["nodes_max"].astype(np.float32),
+                                            np.float32(np.inf))
         self._host = out
         return out
 
@@ -279,15 +285,25 @@ def binned_sah_split(tri_min: np.ndarray, tri_max: np.ndarray, centroids: np.nda
 
 
 def build(mesh: Mesh, params: BuildParams = BuildParams()) -> Bvh:
-    """GPU LBVH over the mesh triangles (replaces bvh.py:218-299)."""
-    if params.n_leaf > 63:
-        raise ValidationError("the GPU builder supports n_leaf <= 63")
+    """BVH over the mesh triangles on the GPU (replaces bvh.py:218-299).
+
+    ``split_rule="sah"`` (the reference default) builds the reference's
+    binned-SAH tree on the GPU, node for node identical to bvh.build;
+    ``"lbvh"`` builds a Morton-order LBVH (fastest build); ``"median"`` is
+    accepted for parity and built as an LBVH.  Closest hits are identical
+    for every tree."""
+    if params.split_rule != "sah" and params.n_leaf > 63:
+        raise ValidationError("the LBVH builder supports n_leaf <= 63")
     ctx = nat.context()
     dm = mesh.device(ctx)
     bp = nat.BuildParams()
-    bp.split_rule = 1 if params.split_rule == "sah" else 0
+    bp.split_rule = {"median": nat.SPLIT_MEDIAN, "sah": nat.SPLIT_SAH,
+                     "lbvh": nat.SPLIT_LBVH}[params.split_rule]
     bp.n_leaf = int(params.n_leaf)
     bp.max_depth = int(params.max_depth)
+    bp.bins_per_axis = int(params.bins_per_axis)
+    bp.c_t = float(params.c_t)
+    bp.c_i = float(params.c_i)
     handle = nat.c_vp()
     nat.check(ctx.lib.sbr_bvh_build(ctx.handle, dm.handle, ctypes.byref(bp),
                                     ctypes.byref(handle)), "sbr_bvh_build")

@@ -11,6 +11,7 @@
 #include "../../include/sbr200.h"
 #include "lbvh.h"
 #include "pipeline.h"
+#include "sahbuild.h"
 
 using namespace sbr;
 
@@ -119,6 +120,11 @@ struct sbr_bvh {
     sbr_ctx *ctx = nullptr;
     const sbr_mesh *mesh = nullptr;
     LbvhOutput out;
+    // reference-layout tree when this BVH IS a reference tree (GPU SAH build
+    // or upload): exported verbatim; ref_depth < 0 otherwise
+    std::vector<double> ref_nmin, ref_nmax;
+    std::vector<int32_t> ref_first, ref_count, ref_order;
+    int ref_depth = -1;
     double frame[3];
     float scale = 0.f;
     BvhView view() const
@@ -300,18 +306,34 @@ static void set_frame(sbr_bvh *b, const sbr_mesh *m)
     b->scale = (float)s * 1.0001f + 1e-30f;
 }
 
+static int build_sah(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_build_params *params,
+                     sbr_bvh *b);
+
 extern "C" int sbr_bvh_build(sbr_ctx *ctx, const sbr_mesh *mesh,
                              const sbr_build_params *params, sbr_bvh **out)
 {
     REQUIRE(ctx && mesh && out, "NULL argument");
     int n_leaf = params ? params->n_leaf : 4;
-    REQUIRE(n_leaf >= 1 && n_leaf <= kMaxLeafCount, "n_leaf must be in [1, %d], got %d",
-            kMaxLeafCount, n_leaf);
+    REQUIRE(n_leaf >= 1, "n_leaf must be >= 1, got %d", n_leaf);
+    const int rule = params ? params->split_rule : SBR_SPLIT_SAH;
+    REQUIRE(rule == SBR_SPLIT_MEDIAN || rule == SBR_SPLIT_SAH || rule == SBR_SPLIT_LBVH,
+            "unknown split rule %d", rule);
     std::lock_guard<std::mutex> lk(ctx->mu);
     if (int rc = set_device(ctx)) return rc;
     sbr_bvh *b = new sbr_bvh();
     b->ctx = ctx;
     b->mesh = mesh;
+    if (rule == SBR_SPLIT_SAH) {
+        sbr_build_params p = *params;
+        if (int rc = build_sah(ctx, mesh, &p, b)) {
+            delete b;
+            return rc;
+        }
+        *out = b;
+        return SBR_OK;
+    }
+    REQUIRE(n_leaf <= kMaxLeafCount, "the LBVH builder supports n_leaf <= %d, got %d",
+            kMaxLeafCount, n_leaf);
     set_frame(b, mesh);
     LbvhInput in;
     in.d_verts = mesh->verts.p;
@@ -405,6 +427,63 @@ struct UploadBuilder {
     }
 };
 
+// reference-layout tree -> device BVH2 (+ BVH4) into a fresh sbr_bvh;
+// the caller holds ctx->mu and has validated the permutation
+static int upload_ref_tree(sbr_ctx *ctx, const sbr_mesh *mesh, const double *nodes_min,
+                           const double *nodes_max, const int32_t *node_first,
+                           const int32_t *node_count, const int32_t *tri_order,
+                           int64_t nnodes, sbr_bvh *b)
+{
+    set_frame(b, mesh);
+    UploadBuilder U{nodes_min, nodes_max, node_first, node_count, nnodes,
+                    {b->frame[0], b->frame[1], b->frame[2]}};
+    if (node_count[0] > 0) {
+        // root is a leaf: wrap it in a node carrying the leaf twice
+        float box[6];
+        U.rel(nodes_min, nodes_max, box);
+        U.nodes.push_back(Node());
+        int r = U.leaf_range(node_first[0], node_count[0], box, 1);
+        Node nd;
+        nd.a = make_float4(box[0], box[1], box[2], box[3]);
+        nd.b = make_float4(box[4], box[5], box[0], box[1]);
+        nd.c = make_float4(box[2], box[3], box[4], box[5]);
+        nd.d = make_int4(r, r, 0, 0);
+        U.nodes[0] = nd;
+    } else {
+        U.internal(0, 0);
+    }
+    if (!U.ok) return fail(SBR_EINVAL, "invalid BVH: %s", U.why.c_str());
+    DevBuf<int> order(mesh->ntri);
+    cudaError_t e = order.status();
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(order.p, tri_order, sizeof(int) * mesh->ntri, cudaMemcpyHostToDevice,
+                            ctx->stream);
+    if (e == cudaSuccess)
+        e = pack_tris(mesh->verts.p, order.p, mesh->ntri, mesh->storage, b->out, ctx->stream,
+                      &ctx->launches);
+    if (e == cudaSuccess) e = b->out.leaf_ids.alloc(mesh->ntri);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(b->out.leaf_ids.p, order.p, sizeof(int) * mesh->ntri,
+                            cudaMemcpyDeviceToDevice, ctx->stream);
+    if (e == cudaSuccess) e = b->out.nodes.alloc(U.nodes.size());
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(b->out.nodes.p, U.nodes.data(), sizeof(Node) * U.nodes.size(),
+                            cudaMemcpyHostToDevice, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) return fail(SBR_ECUDA, "BVH upload: %s", cudaGetErrorString(e));
+    b->out.nnodes = (int64_t)U.nodes.size();
+    b->out.n_leaf_slots = mesh->ntri;
+    b->out.root = 0;
+    b->out.max_depth = U.max_depth;
+    b->out.storage = mesh->storage;
+    e = collapse_bvh4(b->out, ctx->ws, ctx->stream, &ctx->launches);
+    if (e != cudaSuccess) return fail(SBR_ECUDA, "BVH upload: %s", cudaGetErrorString(e));
+    if (b->out.depth4 > kMaxDepth4)
+        return fail(SBR_EINVAL, "BVH4 depth %d exceeds the traversal stack limit (%d)",
+                    b->out.depth4, kMaxDepth4);
+    return SBR_OK;
+}
+
 extern "C" int sbr_bvh_upload(sbr_ctx *ctx, const sbr_mesh *mesh, const double *nodes_min,
                               const double *nodes_max, const int32_t *node_first,
                               const int32_t *node_count, const int32_t *tri_order,
@@ -425,62 +504,54 @@ extern "C" int sbr_bvh_upload(sbr_ctx *ctx, const sbr_mesh *mesh, const double *
     sbr_bvh *b = new sbr_bvh();
     b->ctx = ctx;
     b->mesh = mesh;
-    set_frame(b, mesh);
-    UploadBuilder U{nodes_min, nodes_max, node_first, node_count, nnodes,
-                    {b->frame[0], b->frame[1], b->frame[2]}};
-    if (node_count[0] > 0) {
-        // root is a leaf: wrap it in a node carrying the leaf twice
-        float box[6];
-        U.rel(nodes_min, nodes_max, box);
-        U.nodes.push_back(Node());
-        int r = U.leaf_range(node_first[0], node_count[0], box, 1);
-        Node nd;
-        nd.a = make_float4(box[0], box[1], box[2], box[3]);
-        nd.b = make_float4(box[4], box[5], box[0], box[1]);
-        nd.c = make_float4(box[2], box[3], box[4], box[5]);
-        nd.d = make_int4(r, r, 0, 0);
-        U.nodes[0] = nd;
-    } else {
-        U.internal(0, 0);
-    }
-    if (!U.ok) {
+    if (int rc = upload_ref_tree(ctx, mesh, nodes_min, nodes_max, node_first, node_count,
+                                 tri_order, nnodes, b)) {
         delete b;
-        return fail(SBR_EINVAL, "invalid BVH: %s", U.why.c_str());
+        return rc;
     }
-    DevBuf<int> order(mesh->ntri);
-    cudaError_t e = order.status();
-    if (e == cudaSuccess)
-        e = cudaMemcpyAsync(order.p, tri_order, sizeof(int) * mesh->ntri, cudaMemcpyHostToDevice,
-                            ctx->stream);
-    if (e == cudaSuccess)
-        e = pack_tris(mesh->verts.p, order.p, mesh->ntri, mesh->storage, b->out, ctx->stream,
-                      &ctx->launches);
-    if (e == cudaSuccess) e = b->out.leaf_ids.alloc(mesh->ntri);
-    if (e == cudaSuccess)
-        e = cudaMemcpyAsync(b->out.leaf_ids.p, order.p, sizeof(int) * mesh->ntri,
-                            cudaMemcpyDeviceToDevice, ctx->stream);
-    if (e == cudaSuccess) e = b->out.nodes.alloc(U.nodes.size());
-    if (e == cudaSuccess)
-        e = cudaMemcpyAsync(b->out.nodes.p, U.nodes.data(), sizeof(Node) * U.nodes.size(),
-                            cudaMemcpyHostToDevice, ctx->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-    if (e != cudaSuccess) {
-        delete b;
-        return fail(SBR_ECUDA, "BVH upload: %s", cudaGetErrorString(e));
-    }
-    b->out.nnodes = (int64_t)U.nodes.size();
-    b->out.n_leaf_slots = mesh->ntri;
-    b->out.root = 0;
-    b->out.max_depth = U.max_depth;
-    b->out.storage = mesh->storage;
-    e = collapse_bvh4(b->out, ctx->ws, ctx->stream, &ctx->launches);
-    if (e != cudaSuccess) {
-        delete b;
-        return fail(SBR_ECUDA, "BVH upload: %s", cudaGetErrorString(e));
-    }
-    if (int rc = check_depth(b)) return rc;
     *out = b;
     return SBR_OK;
+}
+
+// GPU build of the reference binned-SAH tree (sahbuild.cu), kept verbatim
+// for export and uploaded as the traversal tree
+static int build_sah(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_build_params *params,
+                     sbr_bvh *b)
+{
+    SahParams P;
+    P.n_leaf = params->n_leaf;
+    P.max_depth = params->max_depth > 0 ? params->max_depth : 64;
+    P.bins = params->bins_per_axis > 0 ? params->bins_per_axis : 16;
+    P.c_t = params->c_t > 0.0 ? params->c_t : 1.0;
+    P.c_i = params->c_i > 0.0 ? params->c_i : 1.0;
+    REQUIRE(P.bins >= 2 && P.bins <= kSahMaxBins, "bins_per_axis must be in [2, %d]",
+            kSahMaxBins);
+    SahTree T;
+    cudaError_t e = sah_build(mesh->verts.p, mesh->ntri, P, T, ctx->stream, &ctx->launches);
+    if (e != cudaSuccess)
+        return fail(e == cudaErrorMemoryAllocation ? SBR_ENOMEM : SBR_ECUDA, "SAH build: %s",
+                    cudaGetErrorString(e));
+    const size_t N = (size_t)T.nnodes;
+    b->ref_nmin.resize(3 * N);
+    b->ref_nmax.resize(3 * N);
+    b->ref_first.resize(N);
+    b->ref_count.resize(N);
+    b->ref_order.resize((size_t)mesh->ntri);
+    CUDA_TRY(cudaMemcpyAsync(b->ref_nmin.data(), T.nmin.p, 24 * N, cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(b->ref_nmax.data(), T.nmax.p, 24 * N, cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(b->ref_first.data(), T.first.p, 4 * N, cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(b->ref_count.data(), T.count.p, 4 * N, cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(b->ref_order.data(), T.order.p, 4 * (size_t)mesh->ntri,
+                             cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    b->ref_depth = T.max_depth;
+    return upload_ref_tree(ctx, mesh, b->ref_nmin.data(), b->ref_nmax.data(),
+                           b->ref_first.data(), b->ref_count.data(), b->ref_order.data(),
+                           (int64_t)N, b);
 }
 
 // ---- export to the reference preorder layout -------------------------------
@@ -564,6 +635,11 @@ extern "C" int sbr_bvh_info(const sbr_bvh *bvh, int64_t *nnodes_export, int64_t 
 {
     REQUIRE(bvh, "bvh is NULL");
     if (nnodes_device) *nnodes_device = bvh->out.nnodes;
+    if (bvh->ref_depth >= 0) {
+        if (max_depth) *max_depth = bvh->ref_depth;
+        if (nnodes_export) *nnodes_export = (int64_t)bvh->ref_first.size();
+        return SBR_OK;
+    }
     if (max_depth) *max_depth = bvh->out.max_depth + 1;
     if (nnodes_export) {
         if (int rc = set_device(bvh->ctx)) return rc;
@@ -581,6 +657,14 @@ extern "C" int sbr_bvh_export(const sbr_bvh *bvh, double *nodes_min, double *nod
 {
     REQUIRE(bvh && nodes_min && nodes_max && node_first && node_count && tri_order,
             "NULL argument");
+    if (bvh->ref_depth >= 0) {
+        memcpy(nodes_min, bvh->ref_nmin.data(), sizeof(double) * bvh->ref_nmin.size());
+        memcpy(nodes_max, bvh->ref_nmax.data(), sizeof(double) * bvh->ref_nmax.size());
+        memcpy(node_first, bvh->ref_first.data(), sizeof(int32_t) * bvh->ref_first.size());
+        memcpy(node_count, bvh->ref_count.data(), sizeof(int32_t) * bvh->ref_count.size());
+        memcpy(tri_order, bvh->ref_order.data(), sizeof(int32_t) * bvh->ref_order.size());
+        return SBR_OK;
+    }
     if (int rc = set_device(bvh->ctx)) return rc;
     std::vector<Node> nodes;
     Exporter *E = nullptr;

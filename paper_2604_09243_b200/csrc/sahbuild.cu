@@ -1,0 +1,515 @@
+// sahbuild.cu -- the reference's binned-SAH BVH (bvh.py:124-299), built on
+// the GPU level by level, node for node identical to the reference tree.
+//
+// The reference recursion (emit -> binned_sah_split -> stable partition,
+// preorder numbering) is order-independent except for the partition, which
+// is stable.  Every per-node quantity is a min/max/count reduction (exact in
+// any order) or a short FP64 formula evaluated once per node, so the tree can
+// be built breadth-first with all nodes of a level in parallel:
+//   level loop (host):
+//     k_seg_of       element -> active segment (binary search on begins)
+//     k_bounds       node box + centroid bounds per segment (ordered-int
+//                    atomicMin/Max on doubles: exact)
+//     k_bin          per (segment, axis, bin) counts + child-box bounds
+//     k_select       one thread per segment: the reference's SAH sweep,
+//                    cost formula with the reference's association, tie to
+//                    the lowest (axis, boundary), leaf rule (bvh.py:154-215)
+//     scan           stable partition ranks (CUB exclusive sum over flags)
+//     k_partition    left block first, both order-preserving (bvh.py:213-214)
+//     k_children     BFS node ids of the children, next level's segments
+//   then subtree sizes bottom-up and preorder ids top-down give the
+//   reference's node numbering (left child = i + 1, node_first = right child
+//   or leaf start); leaves' triangle ranges are already in preorder.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "sahbuild.h"
+
+namespace sbr {
+
+#define CK(x)                                                     \
+    do {                                                          \
+        cudaError_t e_ = (x);                                     \
+        if (e_ != cudaSuccess) return e_;                         \
+    } while (0)
+
+static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+__device__ __forceinline__ unsigned long long ordd(double x)
+{
+    const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+}
+__device__ __forceinline__ double unordd(unsigned long long u)
+{
+    const unsigned long long b = (u >> 63) ? (u & 0x7fffffffffffffffULL) : ~u;
+    return __longlong_as_double((long long)b);
+}
+constexpr unsigned long long kOrdPosInf = 0xfff0000000000000ULL;   // ordd(+inf)
+constexpr unsigned long long kOrdNegInf = 0x000fffffffffffffULL;   // ordd(-inf)
+
+// per-triangle bounds: tri_min, tri_max, centroid = (min + max) * 0.5
+// (bvh.py:227-231), AoS of 9 doubles
+__global__ void k_tri_bounds(const double *__restrict__ verts, int64_t n,
+                             double *__restrict__ tb, int *__restrict__ idx)
+{
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const double *v = verts + 9 * t;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double lo = fmin(fmin(v[a], v[3 + a]), v[6 + a]);
+        const double hi = fmax(fmax(v[a], v[3 + a]), v[6 + a]);
+        tb[9 * t + a] = lo;
+        tb[9 * t + 3 + a] = hi;
+        tb[9 * t + 6 + a] = __dmul_rn(__dadd_rn(lo, hi), 0.5);
+    }
+    idx[t] = (int)t;
+}
+
+struct SegAcc {                      // per active segment (node)
+    unsigned long long box[6];       // lo xyz (min), hi xyz (max), ordered
+    unsigned long long cb[6];        // centroid lo xyz, hi xyz
+};
+
+__global__ void k_seg_init(SegAcc *__restrict__ acc, unsigned int *__restrict__ cnt,
+                           unsigned long long *__restrict__ bbox, int S, int nbins)
+{
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t per = 3 * nbins;
+    if (i < S) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            acc[i].box[q] = kOrdPosInf; acc[i].box[3 + q] = kOrdNegInf;
+            acc[i].cb[q] = kOrdPosInf; acc[i].cb[3 + q] = kOrdNegInf;
+        }
+    }
+    if (i < (int64_t)S * per) {
+        cnt[i] = 0u;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            bbox[6 * i + q] = kOrdPosInf;
+            bbox[6 * i + 3 + q] = kOrdNegInf;
+        }
+    }
+}
+
+__global__ void k_seg_of(const int64_t *__restrict__ sb, const int64_t *__restrict__ sc, int S,
+                         int64_t n, int *__restrict__ eseg)
+{
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int lo = 0, hi = S - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (sb[mid] <= i) lo = mid; else hi = mid - 1;
+    }
+    eseg[i] = (S > 0 && sb[lo] <= i && i < sb[lo] + sc[lo]) ? lo : -1;
+}
+
+// node box + centroid bounds, one warp-segmented pre-reduction per run of
+// equal segment ids (segments are contiguous in element order)
+__global__ void k_bounds(const double *__restrict__ tb, const int *__restrict__ idx,
+                         const int *__restrict__ eseg, int64_t n, SegAcc *__restrict__ acc)
+{
+    const int lane = threadIdx.x & 31;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i - lane < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int s = i < n ? eseg[i] : -1;
+        unsigned long long v[12];
+        if (s >= 0) {
+            const double *b = tb + 9 * (int64_t)idx[i];
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                v[q] = ordd(b[q]);            // tri_min   -> min
+                v[3 + q] = ordd(b[3 + q]);    // tri_max   -> max
+                v[6 + q] = ordd(b[6 + q]);    // centroid  -> min
+                v[9 + q] = v[6 + q];          // centroid  -> max
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                v[q] = kOrdPosInf; v[3 + q] = kOrdNegInf;
+                v[6 + q] = kOrdPosInf; v[9 + q] = kOrdNegInf;
+            }
+        }
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int so = __shfl_down_sync(0xffffffffu, s, o);
+            const bool same = lane + o < 32 && so == s;
+#pragma unroll
+            for (int q = 0; q < 12; ++q) {
+                const unsigned long long w = __shfl_down_sync(0xffffffffu, v[q], o);
+                if (same) {
+                    const bool is_min = (q < 3) || (q >= 6 && q < 9);
+                    v[q] = is_min ? (w < v[q] ? w : v[q]) : (w > v[q] ? w : v[q]);
+                }
+            }
+        }
+        const int sp = __shfl_up_sync(0xffffffffu, s, 1);
+        if (s >= 0 && (lane == 0 || sp != s)) {      // head of its run
+            SegAcc &A = acc[s];
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                atomicMin(&A.box[q], v[q]);
+                atomicMax(&A.box[3 + q], v[3 + q]);
+                atomicMin(&A.cb[q], v[6 + q]);
+                atomicMax(&A.cb[3 + q], v[9 + q]);
+            }
+        }
+    }
+}
+
+// bin index of a centroid coordinate (bvh.py:181-182): min(int64(scale *
+// (c - c_lo)), bins - 1), scale = bins / (c_hi - c_lo)
+__device__ __forceinline__ int bin_of(double c, double c_lo, double scale, int nbins)
+{
+    const long long b = (long long)__dmul_rn(scale, __dsub_rn(c, c_lo));
+    return b > nbins - 1 ? nbins - 1 : (int)b;
+}
+
+__global__ void k_bin(const double *__restrict__ tb, const int *__restrict__ idx,
+                      const int *__restrict__ eseg, int64_t n, const SegAcc *__restrict__ acc,
+                      int nbins, unsigned int *__restrict__ cnt,
+                      unsigned long long *__restrict__ bbox)
+{
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int s = eseg[i];
+    if (s < 0) return;
+    const double *b = tb + 9 * (int64_t)idx[i];
+    const SegAcc &A = acc[s];
+#pragma unroll
+    for (int axis = 0; axis < 3; ++axis) {
+        const double c_lo = unordd(A.cb[axis]), c_hi = unordd(A.cb[3 + axis]);
+        if (!(c_hi > c_lo)) continue;                       // bvh.py:177-178
+        const double scale = __ddiv_rn((double)nbins, __dsub_rn(c_hi, c_lo));
+        const int bi = bin_of(b[6 + axis], c_lo, scale, nbins);
+        const int64_t slot = ((int64_t)s * 3 + axis) * nbins + bi;
+        atomicAdd(&cnt[slot], 1u);
+        unsigned long long *bb = bbox + 6 * slot;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            atomicMin(&bb[q], ordd(b[q]));
+            atomicMax(&bb[3 + q], ordd(b[3 + q]));
+        }
+    }
+}
+
+// _box_surface_area (bvh.py:130-132): 2 * (d0 d1 + d1 d2 + d2 d0)
+__device__ __forceinline__ double sa_of(const double lo[3], const double hi[3])
+{
+    const double d0 = __dsub_rn(hi[0], lo[0]), d1 = __dsub_rn(hi[1], lo[1]),
+                 d2 = __dsub_rn(hi[2], lo[2]);
+    return __dmul_rn(2.0, __dadd_rn(__dadd_rn(__dmul_rn(d0, d1), __dmul_rn(d1, d2)),
+                                    __dmul_rn(d2, d0)));
+}
+
+struct SegSplit {
+    int split;          // 1: internal (children at the next level)
+    int axis, boundary;
+    double c_lo, scale;
+    int64_t nl;
+};
+
+// one thread per segment: node box out, split decision (bvh.py:154-215 and
+// the leaf test of bvh.py:253-262)
+__global__ void k_select(const SegAcc *__restrict__ acc, const unsigned int *__restrict__ cnt,
+                         const unsigned long long *__restrict__ bbox,
+                         const int64_t *__restrict__ sc, const int *__restrict__ snode, int S,
+                         int depth, SahParams P, double *__restrict__ node_box,
+                         SegSplit *__restrict__ out, int *__restrict__ split_flag)
+{
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= S) return;
+    const SegAcc &A = acc[s];
+    double lo[3], hi[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        lo[q] = unordd(A.box[q]);
+        hi[q] = unordd(A.box[3 + q]);
+    }
+    double *nb = node_box + 6 * (int64_t)snode[s];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) { nb[q] = lo[q]; nb[3 + q] = hi[q]; }
+    SegSplit r;
+    r.split = 0; r.axis = -1; r.boundary = -1; r.c_lo = 0.0; r.scale = 0.0; r.nl = 0;
+    const int64_t n = sc[s];
+    if (n > P.n_leaf && depth < P.max_depth) {
+        double sa_p = sa_of(lo, hi);
+        if (!(sa_p >= 1e-300)) sa_p = 1e-300;          // max(sa, 1e-300)
+        bool have = false;
+        double best = 0.0;
+        const int B = P.bins;
+        for (int axis = 0; axis < 3; ++axis) {
+            const double c_lo = unordd(A.cb[axis]), c_hi = unordd(A.cb[3 + axis]);
+            if (!(c_hi > c_lo)) continue;
+            const int64_t base = ((int64_t)s * 3 + axis) * B;
+            // suffix sweep first (right side of boundary b is bins b+1..B-1)
+            double rlo[3][kSahMaxBins], rhi[3][kSahMaxBins];
+            int64_t rn[kSahMaxBins];
+            {
+                double l3[3] = {INFINITY, INFINITY, INFINITY}, h3[3] = {-INFINITY, -INFINITY, -INFINITY};
+                int64_t acc_n = 0;
+                for (int b = B - 1; b >= 0; --b) {
+                    const unsigned long long *bb = bbox + 6 * (base + b);
+                    acc_n += cnt[base + b];
+                    for (int q = 0; q < 3; ++q) {
+                        l3[q] = fmin(l3[q], unordd(bb[q]));
+                        h3[q] = fmax(h3[q], unordd(bb[3 + q]));
+                        rlo[q][b] = l3[q];
+                        rhi[q][b] = h3[q];
+                    }
+                    rn[b] = acc_n;
+                }
+            }
+            double l3[3] = {INFINITY, INFINITY, INFINITY}, h3[3] = {-INFINITY, -INFINITY, -INFINITY};
+            int64_t ln = 0;
+            for (int b = 0; b < B - 1; ++b) {
+                const unsigned long long *bb = bbox + 6 * (base + b);
+                ln += cnt[base + b];
+                for (int q = 0; q < 3; ++q) {
+                    l3[q] = fmin(l3[q], unordd(bb[q]));
+                    h3[q] = fmax(h3[q], unordd(bb[3 + q]));
+                }
+                const int64_t nr = rn[b + 1];
+                if (ln == 0 || nr == 0) continue;
+                double rl[3] = {rlo[0][b + 1], rlo[1][b + 1], rlo[2][b + 1]};
+                double rh[3] = {rhi[0][b + 1], rhi[1][b + 1], rhi[2][b + 1]};
+                const double sal = sa_of(l3, h3), sar = sa_of(rl, rh);
+                // sah_cost (bvh.py:124-127): c_t + (sal/sa_p) n_l c_i + (sar/sa_p) n_r c_i
+                const double cost = __dadd_rn(
+                    __dadd_rn(P.c_t, __dmul_rn(__dmul_rn(__ddiv_rn(sal, sa_p), (double)ln), P.c_i)),
+                    __dmul_rn(__dmul_rn(__ddiv_rn(sar, sa_p), (double)nr), P.c_i));
+                if (!have || cost < best) {
+                    have = true;
+                    best = cost;
+                    r.axis = axis;
+                    r.boundary = b;
+                    r.c_lo = c_lo;
+                    r.scale = __ddiv_rn((double)B, __dsub_rn(c_hi, c_lo));
+                    r.nl = ln;
+                }
+            }
+        }
+        // bvh.py:210-211: no admissible split, or not worth it for a small node
+        if (have && !(best >= __dmul_rn((double)n, P.c_i) && n <= 4 * (int64_t)P.n_leaf))
+            r.split = 1;
+    }
+    out[s] = r;
+    split_flag[s] = r.split;
+}
+
+__global__ void k_flags(const double *__restrict__ tb, const int *__restrict__ idx,
+                        const int *__restrict__ eseg, int64_t n,
+                        const SegSplit *__restrict__ sp, int nbins, int *__restrict__ flag)
+{
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int s = eseg[i];
+    int f = 0;
+    if (s >= 0 && sp[s].split) {
+        const SegSplit &r = sp[s];
+        const double c = tb[9 * (int64_t)idx[i] + 6 + r.axis];
+        f = bin_of(c, r.c_lo, r.scale, nbins) <= r.boundary;
+    }
+    flag[i] = f;
+}
+
+__global__ void k_partition(const int *__restrict__ idx, const int *__restrict__ eseg,
+                            int64_t n, const SegSplit *__restrict__ sp,
+                            const int64_t *__restrict__ sb, const int *__restrict__ flag,
+                            const int *__restrict__ rank, int *__restrict__ out)
+{
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int s = eseg[i];
+    int64_t dst = i;
+    if (s >= 0 && sp[s].split) {
+        const int64_t b = sb[s];
+        const int64_t left = (int64_t)rank[i] - rank[b];       // flags before i in segment
+        dst = flag[i] ? b + left : b + sp[s].nl + ((i - b) - left);
+    }
+    out[dst] = idx[i];
+}
+
+// children of split segments -> next level; leaves recorded
+__global__ void k_children(int S, const SegSplit *__restrict__ sp, const int *__restrict__ crank,
+                           const int64_t *__restrict__ sb, const int64_t *__restrict__ sc,
+                           const int *__restrict__ snode, int node_base,
+                           int *__restrict__ left, int *__restrict__ right,
+                           int64_t *__restrict__ leaf_first, int64_t *__restrict__ leaf_count,
+                           int64_t *__restrict__ nsb, int64_t *__restrict__ nsc,
+                           int *__restrict__ nsnode)
+{
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= S) return;
+    const int me = snode[s];
+    if (!sp[s].split) {
+        left[me] = -1;
+        right[me] = -1;
+        leaf_first[me] = sb[s];
+        leaf_count[me] = sc[s];
+        return;
+    }
+    const int k = crank[s];                 // index among split segments
+    const int l = node_base + 2 * k, r = l + 1;
+    left[me] = l;
+    right[me] = r;
+    leaf_count[me] = 0;
+    nsb[2 * k] = sb[s];
+    nsc[2 * k] = sp[s].nl;
+    nsnode[2 * k] = l;
+    nsb[2 * k + 1] = sb[s] + sp[s].nl;
+    nsc[2 * k + 1] = sc[s] - sp[s].nl;
+    nsnode[2 * k + 1] = r;
+}
+
+__global__ void k_sizes(int a, int b, const int *__restrict__ left, const int *__restrict__ right,
+                        int64_t *__restrict__ size)
+{
+    const int i = a + blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= b) return;
+    size[i] = left[i] < 0 ? 1 : 1 + size[left[i]] + size[right[i]];
+}
+
+__global__ void k_preorder(int a, int b, const int *__restrict__ left,
+                           const int *__restrict__ right, const int64_t *__restrict__ size,
+                           int64_t *__restrict__ pre)
+{
+    const int i = a + blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= b || left[i] < 0) return;
+    pre[left[i]] = pre[i] + 1;
+    pre[right[i]] = pre[i] + 1 + size[left[i]];
+}
+
+__global__ void k_emit_ref(int N, const int64_t *__restrict__ pre, const double *__restrict__ box,
+                           const int *__restrict__ right, const int64_t *__restrict__ lf,
+                           const int64_t *__restrict__ lc, double *__restrict__ nmin,
+                           double *__restrict__ nmax, int32_t *__restrict__ first,
+                           int32_t *__restrict__ count)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const int64_t p = pre[i];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        nmin[3 * p + q] = box[6 * (int64_t)i + q];
+        nmax[3 * p + q] = box[6 * (int64_t)i + 3 + q];
+    }
+    if (right[i] < 0) {
+        first[p] = (int32_t)lf[i];
+        count[p] = (int32_t)lc[i];
+    } else {
+        first[p] = (int32_t)pre[right[i]];
+        count[p] = 0;
+    }
+}
+
+cudaError_t sah_build(const double *d_verts, int64_t n, const SahParams &P, SahTree &out,
+                      cudaStream_t st, int64_t *launches)
+{
+    if (n < 1 || P.bins < 2 || P.bins > kSahMaxBins) return cudaErrorInvalidValue;
+    const int T = 256;
+    const int B = P.bins;
+    DevBuf<double> tb(9 * (size_t)n);
+    DevBuf<int> idx(n), idx2(n), eseg(n), flag(n), rank(n + 1);
+    CK(tb.status()); CK(idx.status()); CK(idx2.status()); CK(eseg.status());
+    CK(flag.status()); CK(rank.status());
+    const int64_t max_nodes = 2 * n;   // binary tree with >= 1 triangle per leaf
+    DevBuf<double> node_box(6 * (size_t)max_nodes);
+    DevBuf<int> left(max_nodes), right(max_nodes);
+    DevBuf<int64_t> lf(max_nodes), lc(max_nodes);
+    CK(node_box.status()); CK(left.status()); CK(right.status()); CK(lf.status());
+    CK(lc.status());
+    // segment buffers (double-buffered), accumulators, splits
+    DevBuf<int64_t> sb(n), sc(n), nsb(n), nsc(n);
+    DevBuf<int> snode(n), nsnode(n), crank(n + 1), sflag(n + 1);
+    CK(sb.status()); CK(sc.status()); CK(nsb.status()); CK(nsc.status());
+    CK(snode.status()); CK(nsnode.status()); CK(crank.status()); CK(sflag.status());
+    size_t scan_bytes = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (int *)nullptr, (int *)nullptr,
+                                     (int)(n + 1), st));
+    DevBuf<unsigned char> scan_tmp(scan_bytes);
+    CK(scan_tmp.status());
+
+    k_tri_bounds<<<nblk(n, T), T, 0, st>>>(d_verts, n, tb.p, idx.p);
+    ++*launches;
+    // root segment
+    const int64_t zero64 = 0;
+    const int zero = 0;
+    CK(cudaMemcpyAsync(sb.p, &zero64, 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(sc.p, &n, 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(snode.p, &zero, 4, cudaMemcpyHostToDevice, st));
+    int S = 1, node_count = 1, depth = 0;
+    std::vector<int> level_start{0};
+    DevBuf<SegAcc> acc;
+    DevBuf<unsigned int> cnt;
+    DevBuf<unsigned long long> bbox;
+    DevBuf<SegSplit> sp;
+    while (S > 0) {
+        CK(acc.reserve(S));
+        CK(cnt.reserve((size_t)S * 3 * B));
+        CK(bbox.reserve((size_t)S * 3 * B * 6));
+        CK(sp.reserve(S));
+        k_seg_init<<<nblk((int64_t)S * 3 * B, T), T, 0, st>>>(acc.p, cnt.p, bbox.p, S, B);
+        k_seg_of<<<nblk(n, T), T, 0, st>>>(sb.p, sc.p, S, n, eseg.p);
+        k_bounds<<<nblk(n, T), T, 0, st>>>(tb.p, idx.p, eseg.p, n, acc.p);
+        k_bin<<<nblk(n, T), T, 0, st>>>(tb.p, idx.p, eseg.p, n, acc.p, B, cnt.p, bbox.p);
+        CK(cudaMemsetAsync(sflag.p + S, 0, sizeof(int), st));
+        k_select<<<nblk(S, 128), 128, 0, st>>>(acc.p, cnt.p, bbox.p, sc.p, snode.p, S, depth, P,
+                                               node_box.p, sp.p, sflag.p);
+        k_flags<<<nblk(n, T), T, 0, st>>>(tb.p, idx.p, eseg.p, n, sp.p, B, flag.p);
+        CK(cub::DeviceScan::ExclusiveSum(scan_tmp.p, scan_bytes, flag.p, rank.p, (int)n, st));
+        k_partition<<<nblk(n, T), T, 0, st>>>(idx.p, eseg.p, n, sp.p, sb.p, flag.p, rank.p,
+                                              idx2.p);
+        std::swap(idx.p, idx2.p);
+        // split flags of the segments -> child slots (exclusive scan; the
+        // extra element S receives the total)
+        CK(cub::DeviceScan::ExclusiveSum(scan_tmp.p, scan_bytes, sflag.p, crank.p, S + 1, st));
+        k_children<<<nblk(S, 128), 128, 0, st>>>(S, sp.p, crank.p, sb.p, sc.p, snode.p,
+                                                 node_count, left.p, right.p, lf.p, lc.p, nsb.p,
+                                                 nsc.p, nsnode.p);
+        *launches += 9;
+        CK(cudaGetLastError());
+        int nsplit = 0;
+        CK(cudaMemcpyAsync(&nsplit, crank.p + S, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        std::swap(sb.p, nsb.p);
+        std::swap(sc.p, nsc.p);
+        std::swap(snode.p, nsnode.p);
+        level_start.push_back(node_count);
+        node_count += 2 * nsplit;
+        S = 2 * nsplit;
+        if (S > 0) ++depth;
+    }
+    // level_start: first BFS id of each level, plus the end
+    const int N = node_count;
+    DevBuf<int64_t> size(N), pre(N);
+    CK(size.status()); CK(pre.status());
+    const int L = (int)level_start.size() - 1;
+    for (int l = L - 1; l >= 0; --l) {
+        const int a = level_start[l], b = level_start[l + 1];
+        if (b > a) k_sizes<<<nblk(b - a, T), T, 0, st>>>(a, b, left.p, right.p, size.p);
+    }
+    CK(cudaMemsetAsync(pre.p, 0, 8, st));
+    for (int l = 0; l < L; ++l) {
+        const int a = level_start[l], b = level_start[l + 1];
+        if (b > a) k_preorder<<<nblk(b - a, T), T, 0, st>>>(a, b, left.p, right.p, size.p, pre.p);
+    }
+    CK(out.nmin.alloc(3 * (size_t)N)); CK(out.nmax.alloc(3 * (size_t)N));
+    CK(out.first.alloc(N)); CK(out.count.alloc(N)); CK(out.order.alloc(n));
+    k_emit_ref<<<nblk(N, T), T, 0, st>>>(N, pre.p, node_box.p, right.p, lf.p, lc.p, out.nmin.p,
+                                         out.nmax.p, out.first.p, out.count.p);
+    CK(cudaMemcpyAsync(out.order.p, idx.p, sizeof(int) * n, cudaMemcpyDeviceToDevice, st));
+    *launches += 2 * L + 1;
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    out.nnodes = N;
+    out.max_depth = depth;
+    return cudaSuccess;
+}
+
+}  // namespace sbr

@@ -414,3 +414,53 @@ def test_raster_primary_equals_bvh_primary(monkeypatch):
         assert np.array_equal(out[k].bounce_counts, out["bvh"].bounce_counts), k
         assert np.array_equal(out[k].valid_rays, out["bvh"].valid_rays), k
         assert np.array_equal(out[k].queries, out["bvh"].queries), k
+
+
+# ---------------------------------------------------------------------------
+# GPU binned-SAH build == the reference tree, node for node
+# ---------------------------------------------------------------------------
+_TREE_KEYS = ("nodes_min", "nodes_max", "node_first", "node_count", "tri_order")
+
+
+@pytest.mark.parametrize("name", golden_names("bvh_"))
+def test_gpu_sah_build_is_the_reference_tree(name):
+    g = load_golden(name)
+    mesh = _mesh(g)
+    tree = sbr.build(mesh, sbr.BuildParams(split_rule="sah"))
+    for k in _TREE_KEYS:
+        ref = g[f"sah_{k}"]
+        got = getattr(tree, k)
+        assert got.dtype == ref.dtype or k in ("node_first", "node_count", "tri_order"), k
+        assert np.array_equal(got, ref), k
+    assert tree.max_depth_seen == int(g["sah_max_depth_seen"])
+    tree.validate(mesh)
+
+
+@pytest.mark.parametrize("case", ["aircraft", "sphere_s6", "rough", "bins8_leaf2"])
+def test_gpu_sah_build_matches_oracle_large(orc, case):
+    params = sbr.BuildParams(split_rule="sah")
+    if case == "aircraft":
+        mesh = meshgen.generate_aircraft(density=0.08)
+    elif case == "sphere_s6":
+        mesh = meshgen.quantized_icosphere(1.0, 6)
+    elif case == "rough":
+        mesh = meshgen.perturbed_grid_mesh(cells=150, extent=4.0, amplitude=0.08, seed=3)
+    else:
+        mesh = meshgen.generate_aircraft(density=0.03)
+        params = sbr.BuildParams(split_rule="sah", bins_per_axis=8, n_leaf=2, c_t=0.5, c_i=2.0)
+    tree = sbr.build(mesh, params)
+    ref = orc.build(mesh.v0, mesh.v1, mesh.v2, split_rule="sah", n_leaf=params.n_leaf,
+                    bins_per_axis=params.bins_per_axis, c_t=params.c_t, c_i=params.c_i)
+    for k in _TREE_KEYS:
+        assert np.array_equal(getattr(tree, k), getattr(ref, k)), (case, k)
+    assert tree.max_depth_seen == ref.max_depth_seen
+    # and the traversal results are those of the LBVH (tree independence)
+    lam = 0.1
+    grid = sbr.build_aperture(mesh.aabb, sbr.IncidentDirection(1.1, 0.7), lam / 5,
+                              wavelength=lam)
+    tp = sbr.TraceParams(max_bounces=4)
+    a = sbr.trace_grid(tree, mesh, grid, tp, with_ids=True)
+    b = sbr.trace_grid(sbr.build(mesh, sbr.BuildParams(split_rule="lbvh")), mesh, grid, tp,
+                       with_ids=True)
+    for k in ("valid", "path", "bounces", "tri_ids", "out_dir"):
+        assert np.array_equal(getattr(a, k), getattr(b, k)), (case, k)
