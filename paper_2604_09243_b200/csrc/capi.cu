@@ -1,5 +1,6 @@
 // capi.cu -- the extern "C" boundary (include/sbr200.h): handles, argument
 // validation, host<->device staging and the batched solve orchestration.
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -93,6 +94,7 @@ struct sbr_ctx {
     DevBuf<double2> amp;
     DevBuf<double> stage;        // host->device staging (mesh ingest, records)
     Arena ws;                    // LBVH build workspace
+    SahWork sah;                 // SAH build workspace
     // optional per-kernel CUDA-event timing of the solve pipeline
     bool profile = false;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -122,6 +124,8 @@ struct sbr_bvh {
     LbvhOutput out;
     // reference-layout tree when this BVH IS a reference tree (GPU SAH build
     // or upload): exported verbatim; ref_depth < 0 otherwise
+    // (host copies filled lazily from ref_dev on export)
+    SahTree ref_dev;
     std::vector<double> ref_nmin, ref_nmax;
     std::vector<int32_t> ref_first, ref_count, ref_order;
     int ref_depth = -1;
@@ -513,8 +517,11 @@ extern "C" int sbr_bvh_upload(sbr_ctx *ctx, const sbr_mesh *mesh, const double *
     return SBR_OK;
 }
 
-// GPU build of the reference binned-SAH tree (sahbuild.cu), kept verbatim
-// for export and uploaded as the traversal tree
+// GPU build of the reference binned-SAH tree (sahbuild.cu): the reference
+// layout stays on the device (exported verbatim on request) and is converted
+// to traversal nodes on the device
+static int ref_download(const sbr_bvh *bvh);
+
 static int build_sah(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_build_params *params,
                      sbr_bvh *b)
 {
@@ -526,32 +533,69 @@ static int build_sah(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_build_params 
     P.c_i = params->c_i > 0.0 ? params->c_i : 1.0;
     REQUIRE(P.bins >= 2 && P.bins <= kSahMaxBins, "bins_per_axis must be in [2, %d]",
             kSahMaxBins);
-    SahTree T;
-    cudaError_t e = sah_build(mesh->verts.p, mesh->ntri, P, T, ctx->stream, &ctx->launches);
+    const bool timing = getenv("SBR_SAH_TIMING") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto ms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point z) {
+        return std::chrono::duration<double, std::milli>(z - a).count();
+    };
+    const auto t0 = now();
+    SahTree &T = b->ref_dev;
+    cudaError_t e = sah_build(mesh->verts.p, mesh->ntri, P, T, ctx->sah, ctx->stream,
+                              &ctx->launches);
     if (e != cudaSuccess)
         return fail(e == cudaErrorMemoryAllocation ? SBR_ENOMEM : SBR_ECUDA, "SAH build: %s",
                     cudaGetErrorString(e));
-    const size_t N = (size_t)T.nnodes;
+    b->ref_depth = T.max_depth;
+    set_frame(b, mesh);
+    bool host = false;
+    e = ref_to_bvh2(T, b->frame, ctx->sah, b->out, host, ctx->stream, &ctx->launches);
+    if (e != cudaSuccess) return fail(SBR_ECUDA, "SAH build: %s", cudaGetErrorString(e));
+    const auto t1 = now();
+    if (host) {   // big leaves / leaf root: the host converter splits them
+        if (int rc = ref_download(b)) return rc;
+        const int rc = upload_ref_tree(ctx, mesh, b->ref_nmin.data(), b->ref_nmax.data(),
+                                       b->ref_first.data(), b->ref_count.data(),
+                                       b->ref_order.data(), (int64_t)b->ref_first.size(), b);
+        b->out.max_depth = T.max_depth;
+        return rc;
+    }
+    e = pack_tris(mesh->verts.p, T.order.p, mesh->ntri, mesh->storage, b->out, ctx->stream,
+                  &ctx->launches);
+    if (e == cudaSuccess) e = b->out.leaf_ids.alloc(mesh->ntri);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(b->out.leaf_ids.p, T.order.p, sizeof(int) * mesh->ntri,
+                            cudaMemcpyDeviceToDevice, ctx->stream);
+    b->out.n_leaf_slots = mesh->ntri;
+    b->out.storage = mesh->storage;
+    if (e == cudaSuccess) e = collapse_bvh4(b->out, ctx->ws, ctx->stream, &ctx->launches);
+    if (e != cudaSuccess) return fail(SBR_ECUDA, "SAH build: %s", cudaGetErrorString(e));
+    if (timing)
+        fprintf(stderr, "[sah] build+convert %.2f ms, pack+bvh4 %.2f ms, nodes %lld\n",
+                ms(t0, t1), ms(t1, now()), (long long)T.nnodes);
+    if (b->out.depth4 > kMaxDepth4)
+        return fail(SBR_EINVAL, "BVH4 depth %d exceeds the traversal stack limit (%d)",
+                    b->out.depth4, kMaxDepth4);
+    return SBR_OK;
+}
+
+static int ref_download(const sbr_bvh *bvh)
+{
+    sbr_bvh *b = const_cast<sbr_bvh *>(bvh);
+    if (!b->ref_first.empty() || b->ref_dev.nnodes == 0) return SBR_OK;
+    const size_t N = (size_t)b->ref_dev.nnodes;
+    const size_t T = (size_t)b->mesh->ntri;
     b->ref_nmin.resize(3 * N);
     b->ref_nmax.resize(3 * N);
     b->ref_first.resize(N);
     b->ref_count.resize(N);
-    b->ref_order.resize((size_t)mesh->ntri);
-    CUDA_TRY(cudaMemcpyAsync(b->ref_nmin.data(), T.nmin.p, 24 * N, cudaMemcpyDeviceToHost,
-                             ctx->stream));
-    CUDA_TRY(cudaMemcpyAsync(b->ref_nmax.data(), T.nmax.p, 24 * N, cudaMemcpyDeviceToHost,
-                             ctx->stream));
-    CUDA_TRY(cudaMemcpyAsync(b->ref_first.data(), T.first.p, 4 * N, cudaMemcpyDeviceToHost,
-                             ctx->stream));
-    CUDA_TRY(cudaMemcpyAsync(b->ref_count.data(), T.count.p, 4 * N, cudaMemcpyDeviceToHost,
-                             ctx->stream));
-    CUDA_TRY(cudaMemcpyAsync(b->ref_order.data(), T.order.p, 4 * (size_t)mesh->ntri,
-                             cudaMemcpyDeviceToHost, ctx->stream));
-    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    b->ref_depth = T.max_depth;
-    return upload_ref_tree(ctx, mesh, b->ref_nmin.data(), b->ref_nmax.data(),
-                           b->ref_first.data(), b->ref_count.data(), b->ref_order.data(),
-                           (int64_t)N, b);
+    b->ref_order.resize(T);
+    CUDA_TRY(cudaSetDevice(b->ctx->device));
+    CUDA_TRY(cudaMemcpy(b->ref_nmin.data(), b->ref_dev.nmin.p, 24 * N, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(b->ref_nmax.data(), b->ref_dev.nmax.p, 24 * N, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(b->ref_first.data(), b->ref_dev.first.p, 4 * N, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(b->ref_count.data(), b->ref_dev.count.p, 4 * N, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(b->ref_order.data(), b->ref_dev.order.p, 4 * T, cudaMemcpyDeviceToHost));
+    return SBR_OK;
 }
 
 // ---- export to the reference preorder layout -------------------------------
@@ -637,7 +681,8 @@ extern "C" int sbr_bvh_info(const sbr_bvh *bvh, int64_t *nnodes_export, int64_t 
     if (nnodes_device) *nnodes_device = bvh->out.nnodes;
     if (bvh->ref_depth >= 0) {
         if (max_depth) *max_depth = bvh->ref_depth;
-        if (nnodes_export) *nnodes_export = (int64_t)bvh->ref_first.size();
+        if (nnodes_export) *nnodes_export = bvh->ref_dev.nnodes ? bvh->ref_dev.nnodes
+                                                                : (int64_t)bvh->ref_first.size();
         return SBR_OK;
     }
     if (max_depth) *max_depth = bvh->out.max_depth + 1;
@@ -658,6 +703,7 @@ extern "C" int sbr_bvh_export(const sbr_bvh *bvh, double *nodes_min, double *nod
     REQUIRE(bvh && nodes_min && nodes_max && node_first && node_count && tri_order,
             "NULL argument");
     if (bvh->ref_depth >= 0) {
+        if (int rc = ref_download(bvh)) return rc;
         memcpy(nodes_min, bvh->ref_nmin.data(), sizeof(double) * bvh->ref_nmin.size());
         memcpy(nodes_max, bvh->ref_nmax.data(), sizeof(double) * bvh->ref_nmax.size());
         memcpy(node_first, bvh->ref_first.data(), sizeof(int32_t) * bvh->ref_first.size());

@@ -23,6 +23,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "sahbuild.h"
@@ -69,16 +71,12 @@ __global__ void k_tri_bounds(const double *__restrict__ verts, int64_t n,
     idx[t] = (int)t;
 }
 
-struct SegAcc {                      // per active segment (node)
-    unsigned long long box[6];       // lo xyz (min), hi xyz (max), ordered
-    unsigned long long cb[6];        // centroid lo xyz, hi xyz
-};
+
 
 __global__ void k_seg_init(SegAcc *__restrict__ acc, unsigned int *__restrict__ cnt,
-                           unsigned long long *__restrict__ bbox, int S, int nbins)
+                           unsigned long long *__restrict__ bbox, int S, int64_t nslots)
 {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const int64_t per = 3 * nbins;
     if (i < S) {
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
@@ -86,7 +84,7 @@ __global__ void k_seg_init(SegAcc *__restrict__ acc, unsigned int *__restrict__ 
             acc[i].cb[q] = kOrdPosInf; acc[i].cb[3 + q] = kOrdNegInf;
         }
     }
-    if (i < (int64_t)S * per) {
+    if (i < nslots) {
         cnt[i] = 0u;
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
@@ -172,7 +170,7 @@ __device__ __forceinline__ int bin_of(double c, double c_lo, double scale, int n
 
 __global__ void k_bin(const double *__restrict__ tb, const int *__restrict__ idx,
                       const int *__restrict__ eseg, int64_t n, const SegAcc *__restrict__ acc,
-                      int nbins, unsigned int *__restrict__ cnt,
+                      int nbins, int R, unsigned int *__restrict__ cnt,
                       unsigned long long *__restrict__ bbox)
 {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -187,7 +185,9 @@ __global__ void k_bin(const double *__restrict__ tb, const int *__restrict__ idx
         if (!(c_hi > c_lo)) continue;                       // bvh.py:177-178
         const double scale = __ddiv_rn((double)nbins, __dsub_rn(c_hi, c_lo));
         const int bi = bin_of(b[6 + axis], c_lo, scale, nbins);
-        const int64_t slot = ((int64_t)s * 3 + axis) * nbins + bi;
+        // near the root few segments share every bin: R replicas (chosen by
+        // block) spread the atomics; k_select merges them (min/max/sum: exact)
+        const int64_t slot = (((int64_t)s * R + blockIdx.x % R) * 3 + axis) * nbins + bi;
         atomicAdd(&cnt[slot], 1u);
         unsigned long long *bb = bbox + 6 * slot;
 #pragma unroll
@@ -207,19 +207,14 @@ __device__ __forceinline__ double sa_of(const double lo[3], const double hi[3])
                                     __dmul_rn(d2, d0)));
 }
 
-struct SegSplit {
-    int split;          // 1: internal (children at the next level)
-    int axis, boundary;
-    double c_lo, scale;
-    int64_t nl;
-};
+
 
 // one thread per segment: node box out, split decision (bvh.py:154-215 and
 // the leaf test of bvh.py:253-262)
 __global__ void k_select(const SegAcc *__restrict__ acc, const unsigned int *__restrict__ cnt,
                          const unsigned long long *__restrict__ bbox,
                          const int64_t *__restrict__ sc, const int *__restrict__ snode, int S,
-                         int depth, SahParams P, double *__restrict__ node_box,
+                         int R, int depth, SahParams P, double *__restrict__ node_box,
                          SegSplit *__restrict__ out, int *__restrict__ split_flag)
 {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
@@ -246,7 +241,28 @@ __global__ void k_select(const SegAcc *__restrict__ acc, const unsigned int *__r
         for (int axis = 0; axis < 3; ++axis) {
             const double c_lo = unordd(A.cb[axis]), c_hi = unordd(A.cb[3 + axis]);
             if (!(c_hi > c_lo)) continue;
-            const int64_t base = ((int64_t)s * 3 + axis) * B;
+            // merge the replicas of every bin (exact: min / max / sum)
+            double bmn[3][kSahMaxBins], bmx[3][kSahMaxBins];
+            int64_t bc[kSahMaxBins];
+            for (int b = 0; b < B; ++b) {
+                unsigned long long mn[3] = {kOrdPosInf, kOrdPosInf, kOrdPosInf};
+                unsigned long long mx[3] = {kOrdNegInf, kOrdNegInf, kOrdNegInf};
+                int64_t c = 0;
+                for (int rep = 0; rep < R; ++rep) {
+                    const int64_t slot = (((int64_t)s * R + rep) * 3 + axis) * B + b;
+                    const unsigned long long *bb = bbox + 6 * slot;
+                    c += cnt[slot];
+                    for (int q = 0; q < 3; ++q) {
+                        mn[q] = bb[q] < mn[q] ? bb[q] : mn[q];
+                        mx[q] = bb[3 + q] > mx[q] ? bb[3 + q] : mx[q];
+                    }
+                }
+                bc[b] = c;
+                for (int q = 0; q < 3; ++q) {
+                    bmn[q][b] = unordd(mn[q]);
+                    bmx[q][b] = unordd(mx[q]);
+                }
+            }
             // suffix sweep first (right side of boundary b is bins b+1..B-1)
             double rlo[3][kSahMaxBins], rhi[3][kSahMaxBins];
             int64_t rn[kSahMaxBins];
@@ -254,11 +270,10 @@ __global__ void k_select(const SegAcc *__restrict__ acc, const unsigned int *__r
                 double l3[3] = {INFINITY, INFINITY, INFINITY}, h3[3] = {-INFINITY, -INFINITY, -INFINITY};
                 int64_t acc_n = 0;
                 for (int b = B - 1; b >= 0; --b) {
-                    const unsigned long long *bb = bbox + 6 * (base + b);
-                    acc_n += cnt[base + b];
+                    acc_n += bc[b];
                     for (int q = 0; q < 3; ++q) {
-                        l3[q] = fmin(l3[q], unordd(bb[q]));
-                        h3[q] = fmax(h3[q], unordd(bb[3 + q]));
+                        l3[q] = fmin(l3[q], bmn[q][b]);
+                        h3[q] = fmax(h3[q], bmx[q][b]);
                         rlo[q][b] = l3[q];
                         rhi[q][b] = h3[q];
                     }
@@ -268,11 +283,10 @@ __global__ void k_select(const SegAcc *__restrict__ acc, const unsigned int *__r
             double l3[3] = {INFINITY, INFINITY, INFINITY}, h3[3] = {-INFINITY, -INFINITY, -INFINITY};
             int64_t ln = 0;
             for (int b = 0; b < B - 1; ++b) {
-                const unsigned long long *bb = bbox + 6 * (base + b);
-                ln += cnt[base + b];
+                ln += bc[b];
                 for (int q = 0; q < 3; ++q) {
-                    l3[q] = fmin(l3[q], unordd(bb[q]));
-                    h3[q] = fmax(h3[q], unordd(bb[3 + q]));
+                    l3[q] = fmin(l3[q], bmn[q][b]);
+                    h3[q] = fmax(h3[q], bmx[q][b]);
                 }
                 const int64_t nr = rn[b + 1];
                 if (ln == 0 || nr == 0) continue;
@@ -408,105 +422,196 @@ __global__ void k_emit_ref(int N, const int64_t *__restrict__ pre, const double 
     }
 }
 
+// reference-layout tree (device) -> child-pair BVH2 nodes for traversal:
+// one Node per internal reference node, numbered by an exclusive scan of the
+// internal flags (root stays 0); boxes relative to the frame, rounded
+// outward to float exactly as the host UploadBuilder does
+__global__ void k_ref_flags(int N, const int32_t *__restrict__ count, int *__restrict__ flag,
+                            int *__restrict__ big)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    flag[i] = count[i] == 0;
+    if (count[i] > kMaxLeafCount) atomicOr(big, 1);
+}
+
+__global__ void k_ref_nodes(int N, const double *__restrict__ nmin, const double *__restrict__ nmax,
+                            const int32_t *__restrict__ first, const int32_t *__restrict__ count,
+                            const int *__restrict__ rank, double3 frame, Node *__restrict__ out)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N || count[i] != 0) return;
+    const int kids[2] = {i + 1, first[i]};
+    float b[2][6];
+    int ref[2];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        const int k = kids[c];
+        const double f[3] = {frame.x, frame.y, frame.z};
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            b[c][a] = nextafterf(__double2float_rn(nmin[3 * (int64_t)k + a] - f[a]), -INFINITY);
+            b[c][3 + a] = nextafterf(__double2float_rn(nmax[3 * (int64_t)k + a] - f[a]), INFINITY);
+        }
+        ref[c] = count[k] > 0 ? leaf_ref(first[k], count[k]) : rank[k];
+    }
+    Node nd;
+    nd.a = make_float4(b[0][0], b[0][1], b[0][2], b[0][3]);
+    nd.b = make_float4(b[0][4], b[0][5], b[1][0], b[1][1]);
+    nd.c = make_float4(b[1][2], b[1][3], b[1][4], b[1][5]);
+    nd.d = make_int4(ref[0], ref[1], 0, 0);
+    out[rank[i]] = nd;
+}
+
+cudaError_t ref_to_bvh2(const SahTree &t, const double frame[3], SahWork &w, LbvhOutput &out,
+                        bool &host_needed, cudaStream_t st, int64_t *launches)
+{
+    const int N = (int)t.nnodes;
+    host_needed = false;
+    CK(w.flag.reserve(N + 1));
+    CK(w.rank.reserve(N + 1));
+    CK(w.big.reserve(1));
+    CK(cudaMemsetAsync(w.big.p, 0, sizeof(int), st));
+    CK(cudaMemsetAsync(w.flag.p + N, 0, sizeof(int), st));
+    k_ref_flags<<<nblk(N, 256), 256, 0, st>>>(N, t.count.p, w.flag.p, w.big.p);
+    size_t need = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, need, w.flag.p, w.rank.p, N + 1, st));
+    CK(w.scan_tmp.reserve(need));
+    CK(cub::DeviceScan::ExclusiveSum(w.scan_tmp.p, need, w.flag.p, w.rank.p, N + 1, st));
+    int big = 0, internal = 0, root_count = 0;
+    CK(cudaMemcpyAsync(&big, w.big.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&internal, w.rank.p + N, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&root_count, t.count.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (big || root_count > 0) {           // leaf > 63 triangles or a leaf root
+        host_needed = true;
+        return cudaSuccess;
+    }
+    CK(out.nodes.alloc(internal));
+    k_ref_nodes<<<nblk(N, 256), 256, 0, st>>>(N, t.nmin.p, t.nmax.p, t.first.p, t.count.p,
+                                              w.rank.p, make_double3(frame[0], frame[1], frame[2]),
+                                              out.nodes.p);
+    *launches += 3;
+    CK(cudaGetLastError());
+    out.nnodes = internal;
+    out.root = 0;
+    out.max_depth = t.max_depth;
+    return cudaSuccess;
+}
+
 cudaError_t sah_build(const double *d_verts, int64_t n, const SahParams &P, SahTree &out,
-                      cudaStream_t st, int64_t *launches)
+                      SahWork &w, cudaStream_t st, int64_t *launches)
 {
     if (n < 1 || P.bins < 2 || P.bins > kSahMaxBins) return cudaErrorInvalidValue;
     const int T = 256;
     const int B = P.bins;
-    DevBuf<double> tb(9 * (size_t)n);
-    DevBuf<int> idx(n), idx2(n), eseg(n), flag(n), rank(n + 1);
-    CK(tb.status()); CK(idx.status()); CK(idx2.status()); CK(eseg.status());
-    CK(flag.status()); CK(rank.status());
     const int64_t max_nodes = 2 * n;   // binary tree with >= 1 triangle per leaf
-    DevBuf<double> node_box(6 * (size_t)max_nodes);
-    DevBuf<int> left(max_nodes), right(max_nodes);
-    DevBuf<int64_t> lf(max_nodes), lc(max_nodes);
-    CK(node_box.status()); CK(left.status()); CK(right.status()); CK(lf.status());
-    CK(lc.status());
-    // segment buffers (double-buffered), accumulators, splits
-    DevBuf<int64_t> sb(n), sc(n), nsb(n), nsc(n);
-    DevBuf<int> snode(n), nsnode(n), crank(n + 1), sflag(n + 1);
-    CK(sb.status()); CK(sc.status()); CK(nsb.status()); CK(nsc.status());
-    CK(snode.status()); CK(nsnode.status()); CK(crank.status()); CK(sflag.status());
+    CK(w.tb.reserve(9 * (size_t)n));
+    CK(w.idx.reserve(n)); CK(w.idx2.reserve(n)); CK(w.eseg.reserve(n));
+    CK(w.flag.reserve(n + 1)); CK(w.rank.reserve(n + 1));
+    CK(w.node_box.reserve(6 * (size_t)max_nodes));
+    CK(w.left.reserve(max_nodes)); CK(w.right.reserve(max_nodes));
+    CK(w.lf.reserve(max_nodes)); CK(w.lc.reserve(max_nodes));
+    CK(w.size.reserve(max_nodes)); CK(w.pre.reserve(max_nodes));
+    CK(w.sb.reserve(n)); CK(w.sc.reserve(n)); CK(w.nsb.reserve(n)); CK(w.nsc.reserve(n));
+    CK(w.snode.reserve(n)); CK(w.nsnode.reserve(n));
+    CK(w.crank.reserve(n + 1)); CK(w.sflag.reserve(n + 1));
+    CK(w.acc.reserve(n)); CK(w.sp.reserve(n));
     size_t scan_bytes = 0;
     CK(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (int *)nullptr, (int *)nullptr,
                                      (int)(n + 1), st));
-    DevBuf<unsigned char> scan_tmp(scan_bytes);
-    CK(scan_tmp.status());
+    CK(w.scan_tmp.reserve(scan_bytes));
+    scan_bytes = w.scan_tmp.bytes();
+    int *idx = w.idx.p, *idx2 = w.idx2.p;
+    int64_t *sb = w.sb.p, *sc = w.sc.p, *nsb = w.nsb.p, *nsc = w.nsc.p;
+    int *snode = w.snode.p, *nsnode = w.nsnode.p;
 
-    k_tri_bounds<<<nblk(n, T), T, 0, st>>>(d_verts, n, tb.p, idx.p);
+    k_tri_bounds<<<nblk(n, T), T, 0, st>>>(d_verts, n, w.tb.p, idx);
     ++*launches;
-    // root segment
     const int64_t zero64 = 0;
     const int zero = 0;
-    CK(cudaMemcpyAsync(sb.p, &zero64, 8, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(sc.p, &n, 8, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(snode.p, &zero, 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(sb, &zero64, 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(sc, &n, 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(snode, &zero, 4, cudaMemcpyHostToDevice, st));
     int S = 1, node_count = 1, depth = 0;
     std::vector<int> level_start{0};
-    DevBuf<SegAcc> acc;
-    DevBuf<unsigned int> cnt;
-    DevBuf<unsigned long long> bbox;
-    DevBuf<SegSplit> sp;
+    const bool timing = getenv("SBR_SAH_TIMING") != nullptr;
     while (S > 0) {
-        CK(acc.reserve(S));
-        CK(cnt.reserve((size_t)S * 3 * B));
-        CK(bbox.reserve((size_t)S * 3 * B * 6));
-        CK(sp.reserve(S));
-        k_seg_init<<<nblk((int64_t)S * 3 * B, T), T, 0, st>>>(acc.p, cnt.p, bbox.p, S, B);
-        k_seg_of<<<nblk(n, T), T, 0, st>>>(sb.p, sc.p, S, n, eseg.p);
-        k_bounds<<<nblk(n, T), T, 0, st>>>(tb.p, idx.p, eseg.p, n, acc.p);
-        k_bin<<<nblk(n, T), T, 0, st>>>(tb.p, idx.p, eseg.p, n, acc.p, B, cnt.p, bbox.p);
-        CK(cudaMemsetAsync(sflag.p + S, 0, sizeof(int), st));
-        k_select<<<nblk(S, 128), 128, 0, st>>>(acc.p, cnt.p, bbox.p, sc.p, snode.p, S, depth, P,
-                                               node_box.p, sp.p, sflag.p);
-        k_flags<<<nblk(n, T), T, 0, st>>>(tb.p, idx.p, eseg.p, n, sp.p, B, flag.p);
-        CK(cub::DeviceScan::ExclusiveSum(scan_tmp.p, scan_bytes, flag.p, rank.p, (int)n, st));
-        k_partition<<<nblk(n, T), T, 0, st>>>(idx.p, eseg.p, n, sp.p, sb.p, flag.p, rank.p,
-                                              idx2.p);
-        std::swap(idx.p, idx2.p);
+        cudaEvent_t lv0 = nullptr, lv1 = nullptr;
+        if (timing) {
+            cudaEventCreate(&lv0); cudaEventCreate(&lv1);
+            cudaEventRecord(lv0, st);
+        }
+        const int R = S >= 4096 ? 1 : std::min(32, 4096 / S);
+        const int64_t nslots = (int64_t)S * R * 3 * B;
+        // grow geometrically so a build allocates O(log) times
+        if ((size_t)nslots > w.cnt.n) {
+            const size_t cap = std::max<size_t>((size_t)nslots, 2 * w.cnt.n);
+            CK(w.cnt.alloc(cap));
+            CK(w.bbox.alloc(6 * cap));
+        }
+        k_seg_init<<<nblk(std::max<int64_t>(nslots, S), T), T, 0, st>>>(w.acc.p, w.cnt.p,
+                                                                       w.bbox.p, S, nslots);
+        k_seg_of<<<nblk(n, T), T, 0, st>>>(sb, sc, S, n, w.eseg.p);
+        k_bounds<<<nblk(n, T), T, 0, st>>>(w.tb.p, idx, w.eseg.p, n, w.acc.p);
+        k_bin<<<nblk(n, T), T, 0, st>>>(w.tb.p, idx, w.eseg.p, n, w.acc.p, B, R, w.cnt.p,
+                                        w.bbox.p);
+        CK(cudaMemsetAsync(w.sflag.p + S, 0, sizeof(int), st));
+        k_select<<<nblk(S, 128), 128, 0, st>>>(w.acc.p, w.cnt.p, w.bbox.p, sc, snode, S, R, depth,
+                                               P, w.node_box.p, w.sp.p, w.sflag.p);
+        k_flags<<<nblk(n, T), T, 0, st>>>(w.tb.p, idx, w.eseg.p, n, w.sp.p, B, w.flag.p);
+        CK(cub::DeviceScan::ExclusiveSum(w.scan_tmp.p, scan_bytes, w.flag.p, w.rank.p, (int)n,
+                                         st));
+        k_partition<<<nblk(n, T), T, 0, st>>>(idx, w.eseg.p, n, w.sp.p, sb, w.flag.p, w.rank.p,
+                                              idx2);
+        std::swap(idx, idx2);
         // split flags of the segments -> child slots (exclusive scan; the
         // extra element S receives the total)
-        CK(cub::DeviceScan::ExclusiveSum(scan_tmp.p, scan_bytes, sflag.p, crank.p, S + 1, st));
-        k_children<<<nblk(S, 128), 128, 0, st>>>(S, sp.p, crank.p, sb.p, sc.p, snode.p,
-                                                 node_count, left.p, right.p, lf.p, lc.p, nsb.p,
-                                                 nsc.p, nsnode.p);
+        CK(cub::DeviceScan::ExclusiveSum(w.scan_tmp.p, scan_bytes, w.sflag.p, w.crank.p, S + 1,
+                                         st));
+        k_children<<<nblk(S, 128), 128, 0, st>>>(S, w.sp.p, w.crank.p, sb, sc, snode, node_count,
+                                                 w.left.p, w.right.p, w.lf.p, w.lc.p, nsb, nsc,
+                                                 nsnode);
         *launches += 9;
         CK(cudaGetLastError());
         int nsplit = 0;
-        CK(cudaMemcpyAsync(&nsplit, crank.p + S, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&nsplit, w.crank.p + S, sizeof(int), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-        std::swap(sb.p, nsb.p);
-        std::swap(sc.p, nsc.p);
-        std::swap(snode.p, nsnode.p);
+        if (timing) {
+            cudaEventRecord(lv1, st);
+            cudaEventSynchronize(lv1);
+            float m = 0.f;
+            cudaEventElapsedTime(&m, lv0, lv1);
+            fprintf(stderr, "[sah] level %d: %d segments, %d split, %.3f ms\n", depth, S, nsplit, m);
+            cudaEventDestroy(lv0); cudaEventDestroy(lv1);
+        }
+        std::swap(sb, nsb);
+        std::swap(sc, nsc);
+        std::swap(snode, nsnode);
         level_start.push_back(node_count);
         node_count += 2 * nsplit;
         S = 2 * nsplit;
         if (S > 0) ++depth;
     }
-    // level_start: first BFS id of each level, plus the end
     const int N = node_count;
-    DevBuf<int64_t> size(N), pre(N);
-    CK(size.status()); CK(pre.status());
     const int L = (int)level_start.size() - 1;
     for (int l = L - 1; l >= 0; --l) {
         const int a = level_start[l], b = level_start[l + 1];
-        if (b > a) k_sizes<<<nblk(b - a, T), T, 0, st>>>(a, b, left.p, right.p, size.p);
+        if (b > a) k_sizes<<<nblk(b - a, T), T, 0, st>>>(a, b, w.left.p, w.right.p, w.size.p);
     }
-    CK(cudaMemsetAsync(pre.p, 0, 8, st));
+    CK(cudaMemsetAsync(w.pre.p, 0, 8, st));
     for (int l = 0; l < L; ++l) {
         const int a = level_start[l], b = level_start[l + 1];
-        if (b > a) k_preorder<<<nblk(b - a, T), T, 0, st>>>(a, b, left.p, right.p, size.p, pre.p);
+        if (b > a)
+            k_preorder<<<nblk(b - a, T), T, 0, st>>>(a, b, w.left.p, w.right.p, w.size.p, w.pre.p);
     }
     CK(out.nmin.alloc(3 * (size_t)N)); CK(out.nmax.alloc(3 * (size_t)N));
     CK(out.first.alloc(N)); CK(out.count.alloc(N)); CK(out.order.alloc(n));
-    k_emit_ref<<<nblk(N, T), T, 0, st>>>(N, pre.p, node_box.p, right.p, lf.p, lc.p, out.nmin.p,
-                                         out.nmax.p, out.first.p, out.count.p);
-    CK(cudaMemcpyAsync(out.order.p, idx.p, sizeof(int) * n, cudaMemcpyDeviceToDevice, st));
+    k_emit_ref<<<nblk(N, T), T, 0, st>>>(N, w.pre.p, w.node_box.p, w.right.p, w.lf.p, w.lc.p,
+                                         out.nmin.p, out.nmax.p, out.first.p, out.count.p);
+    CK(cudaMemcpyAsync(out.order.p, idx, sizeof(int) * n, cudaMemcpyDeviceToDevice, st));
     *launches += 2 * L + 1;
     CK(cudaGetLastError());
-    CK(cudaStreamSynchronize(st));
     out.nnodes = N;
     out.max_depth = depth;
     return cudaSuccess;
