@@ -128,6 +128,9 @@ int sbr_ctx_kernel_stats(sbr_ctx *ctx, double *trace_ms, int64_t *trace_launches
 /* Accumulated time of the primary-visibility raster pass (memset + two
  * sweeps) that precedes each trace launch; trace_ms excludes it. */
 int sbr_ctx_raster_stats(sbr_ctx *ctx, double *raster_ms);
+/* Instrumentation: read bandwidth (GB/s) of a `bytes` buffer re-read `reps`
+ * times from L2 (16-byte ld.global.cg, 8 CTAs/SM, best of 5). */
+int sbr_probe_l2_bandwidth(sbr_ctx *ctx, int64_t bytes, int32_t reps, double *gbs);
 
 /* ---- mesh: geometry.py:130-180 mesh_from_soup output -> device --------- */
 int sbr_mesh_create(sbr_ctx *ctx, const double *v0, const double *v1,

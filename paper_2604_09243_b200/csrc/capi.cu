@@ -1435,6 +1435,15 @@ extern "C" int sbr_ctx_profile(sbr_ctx *ctx, int32_t enable)
     return SBR_OK;
 }
 
+extern "C" int sbr_probe_l2_bandwidth(sbr_ctx *ctx, int64_t bytes, int32_t reps, double *gbs)
+{
+    REQUIRE(ctx && gbs && bytes >= (1 << 20) && reps >= 1, "bad arguments");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (int rc = set_device(ctx)) return rc;
+    CUDA_TRY(probe_l2_read(bytes, reps, ctx->num_sms, ctx->stream, gbs));
+    return SBR_OK;
+}
+
 extern "C" int sbr_ctx_raster_stats(sbr_ctx *ctx, double *raster_ms)
 {
     REQUIRE(ctx && raster_ms, "NULL argument");

@@ -756,4 +756,51 @@ cudaError_t launch_box_pairs(const double *lo, const double *hi, const double *o
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// L2-resident read bandwidth probe (instrumentation for the roofline line)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_l2_read(const float4 *__restrict__ buf, int64_t n4,
+                                                 int reps, float *__restrict__ sink)
+{
+    float acc = 0.f;
+    for (int r = 0; r < reps; ++r)
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+             i += (int64_t)gridDim.x * blockDim.x) {
+            const float4 v = __ldcg(buf + i);     // L2, not L1
+            acc += v.x + v.y + v.z + v.w;
+        }
+    if (acc == 12345.678f) sink[blockIdx.x] = acc;   // keep the loads
+}
+
+cudaError_t probe_l2_read(int64_t bytes, int reps, int num_sms, cudaStream_t st, double *gbs)
+{
+    const int64_t n4 = bytes / 16;
+    float4 *buf = nullptr;
+    float *sink = nullptr;
+    cudaError_t e = cudaMalloc(&buf, n4 * 16);
+    if (e != cudaSuccess) return e;
+    e = cudaMalloc(&sink, sizeof(float) * num_sms * 8);
+    if (e == cudaSuccess) e = cudaMemsetAsync(buf, 0, n4 * 16, st);
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (e == cudaSuccess) e = cudaEventCreate(&a);
+    if (e == cudaSuccess) e = cudaEventCreate(&b);
+    double best = 0.0;
+    for (int t = 0; t < 5 && e == cudaSuccess; ++t) {
+        k_l2_read<<<num_sms * 8, 256, 0, st>>>(buf, n4, 1, sink);     // warm L2
+        cudaEventRecord(a, st);
+        k_l2_read<<<num_sms * 8, 256, 0, st>>>(buf, n4, reps, sink);
+        cudaEventRecord(b, st);
+        e = cudaEventSynchronize(b);
+        float ms = 0.f;
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, a, b);
+        if (e == cudaSuccess && ms > 0.f) best = fmax(best, (double)n4 * 16 * reps / (ms * 1e-3) / 1e9);
+    }
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+    cudaFree(buf);
+    cudaFree(sink);
+    *gbs = best;
+    return e;
+}
+
 }  // namespace sbr

@@ -169,4 +169,7 @@ cudaError_t launch_box_pairs(const double *lo, const double *hi, const double *o
                              const double *inv, int64_t n, double t_max, uint8_t *hit,
                              double *entry, cudaStream_t st, const LaunchStats &ls);
 
+// Best-of-5 read bandwidth of a `bytes` buffer re-read `reps` times through L2.
+cudaError_t probe_l2_read(int64_t bytes, int reps, int num_sms, cudaStream_t st, double *gbs);
+
 }  // namespace sbr
