@@ -163,6 +163,17 @@ static int check_depth(sbr_bvh *b)
                 kMaxDepth4);
 }
 
+// library stream per device for the stream-ordered allocator (lbvh.h)
+static std::mutex g_alloc_mu;
+static cudaStream_t g_alloc_stream[128];
+
+cudaStream_t sbr::alloc_stream(int device)
+{
+    if (device < 0 || device >= 128) return nullptr;
+    std::lock_guard<std::mutex> lk(g_alloc_mu);
+    return g_alloc_stream[device];
+}
+
 extern "C" int sbr_ctx_create(int device, sbr_ctx **out)
 {
     REQUIRE(out, "out is NULL");
@@ -174,6 +185,16 @@ extern "C" int sbr_ctx_create(int device, sbr_ctx **out)
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+    if (e == cudaSuccess) {
+        cudaMemPool_t pool;
+        e = cudaDeviceGetDefaultMemPool(&pool, device);
+        uint64_t keep = UINT64_MAX;
+        if (e == cudaSuccess) e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        if (e == cudaSuccess && device < 128) {
+            std::lock_guard<std::mutex> lk(g_alloc_mu);
+            if (!g_alloc_stream[device]) g_alloc_stream[device] = ctx->stream;
+        }
+    }
     if (e == cudaSuccess) e = ctx->counter.alloc(2);   // [0] trace, [1] raster
     if (e == cudaSuccess) e = ctx->err_flag.alloc(1);
     if (e == cudaSuccess) e = ctx->bad.alloc(1);
@@ -188,10 +209,19 @@ extern "C" int sbr_ctx_create(int device, sbr_ctx **out)
 extern "C" int sbr_ctx_destroy(sbr_ctx *ctx)
 {
     if (!ctx) return SBR_OK;
-    cudaSetDevice(ctx->device);
-    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-    if (ctx->stream) cudaStreamDestroy(ctx->stream);
-    delete ctx;
+    const int dev = ctx->device;
+    cudaStream_t s = ctx->stream;
+    cudaSetDevice(dev);
+    if (s) cudaStreamSynchronize(s);
+    delete ctx;               // its buffers are freed (stream-ordered) first
+    if (s) {
+        cudaStreamSynchronize(s);
+        {
+            std::lock_guard<std::mutex> lk(g_alloc_mu);
+            if (dev < 128 && g_alloc_stream[dev] == s) g_alloc_stream[dev] = nullptr;
+        }
+        cudaStreamDestroy(s);
+    }
     return SBR_OK;
 }
 
@@ -590,11 +620,13 @@ static int ref_download(const sbr_bvh *bvh)
     b->ref_count.resize(N);
     b->ref_order.resize(T);
     CUDA_TRY(cudaSetDevice(b->ctx->device));
-    CUDA_TRY(cudaMemcpy(b->ref_nmin.data(), b->ref_dev.nmin.p, 24 * N, cudaMemcpyDeviceToHost));
-    CUDA_TRY(cudaMemcpy(b->ref_nmax.data(), b->ref_dev.nmax.p, 24 * N, cudaMemcpyDeviceToHost));
-    CUDA_TRY(cudaMemcpy(b->ref_first.data(), b->ref_dev.first.p, 4 * N, cudaMemcpyDeviceToHost));
-    CUDA_TRY(cudaMemcpy(b->ref_count.data(), b->ref_dev.count.p, 4 * N, cudaMemcpyDeviceToHost));
-    CUDA_TRY(cudaMemcpy(b->ref_order.data(), b->ref_dev.order.p, 4 * T, cudaMemcpyDeviceToHost));
+    cudaStream_t st = b->ctx->stream;
+    CUDA_TRY(cudaMemcpyAsync(b->ref_nmin.data(), b->ref_dev.nmin.p, 24 * N, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(b->ref_nmax.data(), b->ref_dev.nmax.p, 24 * N, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(b->ref_first.data(), b->ref_dev.first.p, 4 * N, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(b->ref_count.data(), b->ref_dev.count.p, 4 * N, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(b->ref_order.data(), b->ref_dev.order.p, 4 * T, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
     return SBR_OK;
 }
 
@@ -650,8 +682,9 @@ struct Exporter {
 static int export_tree(const sbr_bvh *b, std::vector<Node> &nodes, Exporter **ex)
 {
     nodes.resize(b->out.nnodes);
-    CUDA_TRY(cudaMemcpy(nodes.data(), b->out.nodes.p, sizeof(Node) * nodes.size(),
-                        cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpyAsync(nodes.data(), b->out.nodes.p, sizeof(Node) * nodes.size(),
+                             cudaMemcpyDeviceToHost, b->ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(b->ctx->stream));
     Exporter *E = new Exporter{nodes, b->frame, {}, {}, {}, {}};
     const Node &r = nodes[0];
     float bl[6], br[6], root[6];
@@ -720,8 +753,9 @@ extern "C" int sbr_bvh_export(const sbr_bvh *bvh, double *nodes_min, double *nod
     memcpy(node_first, E->first.data(), sizeof(int32_t) * E->first.size());
     memcpy(node_count, E->count.data(), sizeof(int32_t) * E->count.size());
     delete E;
-    CUDA_TRY(cudaMemcpy(tri_order, bvh->out.leaf_ids.p, sizeof(int32_t) * bvh->mesh->ntri,
-                        cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpyAsync(tri_order, bvh->out.leaf_ids.p, sizeof(int32_t) * bvh->mesh->ntri,
+                             cudaMemcpyDeviceToHost, bvh->ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(bvh->ctx->stream));
     return SBR_OK;
 }
 

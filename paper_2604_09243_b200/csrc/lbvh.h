@@ -8,23 +8,48 @@
 
 namespace sbr {
 
+// Device allocations go through the device's stream-ordered memory pool on
+// the library stream of that device's context (registered by sbr_ctx_create,
+// release threshold = keep everything): allocating and freeing meshes, trees
+// and scratch never synchronises the device or returns pages to the driver
+// (plain cudaMalloc/cudaFree cost 10-300 ms spikes per sweep on 1M-triangle
+// scenes).  Without a context on the device, plain cudaMalloc/cudaFree.
+cudaStream_t alloc_stream(int device);   // capi.cu; nullptr if no context
+
+inline cudaError_t dev_alloc(void **p, size_t bytes, int &device)
+{
+    cudaGetDevice(&device);
+    cudaStream_t s = alloc_stream(device);
+    return s ? cudaMallocAsync(p, bytes, s) : cudaMalloc(p, bytes);
+}
+inline void dev_free(void *p, int device)
+{
+    cudaStream_t s = alloc_stream(device);
+    if (s) cudaFreeAsync(p, s);
+    else cudaFree(p);
+}
+
 // Owning device buffer (RAII, move-only).
 template <class T>
 struct DevBuf {
     T *p = nullptr;
     size_t n = 0;
     cudaError_t err = cudaSuccess;
+    int device = 0;
 
     DevBuf() = default;
     explicit DevBuf(size_t count) { alloc(count); }
     DevBuf(const DevBuf &) = delete;
     DevBuf &operator=(const DevBuf &) = delete;
-    DevBuf(DevBuf &&o) noexcept : p(o.p), n(o.n), err(o.err) { o.p = nullptr; o.n = 0; }
+    DevBuf(DevBuf &&o) noexcept : p(o.p), n(o.n), err(o.err), device(o.device)
+    {
+        o.p = nullptr; o.n = 0;
+    }
     DevBuf &operator=(DevBuf &&o) noexcept
     {
         if (this != &o) {
             release();
-            p = o.p; n = o.n; err = o.err;
+            p = o.p; n = o.n; err = o.err; device = o.device;
             o.p = nullptr; o.n = 0;
         }
         return *this;
@@ -36,7 +61,7 @@ struct DevBuf {
         release();
         err = cudaSuccess;
         if (count) {
-            err = cudaMalloc((void **)&p, sizeof(T) * count);
+            err = dev_alloc((void **)&p, sizeof(T) * count, device);
             if (err != cudaSuccess) p = nullptr;
         }
         n = p ? count : 0;
@@ -51,7 +76,7 @@ struct DevBuf {
     cudaError_t status() const { return err; }
     void release()
     {
-        if (p) cudaFree(p);
+        if (p) dev_free(p, device);
         p = nullptr;
         n = 0;
     }
