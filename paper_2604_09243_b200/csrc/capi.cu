@@ -89,6 +89,8 @@ struct sbr_ctx {
     DevBuf<int> bgrids;          // raster pass: grids of the current batch
     DevBuf<unsigned int> worklist;          // raster pass: slots whose query 0 hit
     DevBuf<unsigned long long> nwork;
+    DevBuf<int4> big;                       // raster pass: big-triangle chunk queue
+    DevBuf<unsigned long long> nbig;
     DevBuf<double> k2, gpow, scale;
     double dkturn = 0.0;         // uniform wavenumber step in turns (0: not uniform)
     DevBuf<double2> amp;
@@ -807,7 +809,24 @@ static RasterArgs raster_args(const sbr_bvh *bvh, const GridDev *grids, const in
     r.seg_slot = seg_slot;
     r.prim = prim;
     r.counter = nullptr;
+    r.sparse = 0;
+    r.big = nullptr;
+    r.nbig = nullptr;
+    r.big_cap = 0;
     return r;
+}
+
+// big-triangle chunk queue of the raster pass (grow-only, 4M items = 64 MB)
+static cudaError_t attach_big_queue(sbr_ctx *ctx, RasterArgs &ra)
+{
+    const size_t cap = (size_t)1 << 22;
+    cudaError_t e = ctx->big.reserve(cap);
+    if (e == cudaSuccess) e = ctx->nbig.reserve(1);
+    if (e != cudaSuccess) return e;
+    ra.big = ctx->big.p;
+    ra.nbig = ctx->nbig.p;
+    ra.big_cap = (int64_t)cap;
+    return cudaSuccess;
 }
 
 static TraceCfg make_cfg(const sbr_bvh *bvh, const sbr_trace_params *p, sbr_ctx *ctx)
@@ -919,6 +938,7 @@ static int trace_full_common(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *
         CUDA_TRY(cudaMemsetAsync(prim.p, 0xff, sizeof(PrimHit) * n, st));
         RasterArgs ra = raster_args(bvh, dg.p, dbg.p, 1, dsb.p, dss.p, prim.p);
         ra.counter = ctx->counter.p + 1;
+        CUDA_TRY(attach_big_queue(ctx, ra));
         CUDA_TRY(launch_raster(ra, st, ctx->stats()));
         CUDA_TRY(cudaStreamSynchronize(st));   // scratch tables die with this scope
     }
@@ -1080,6 +1100,10 @@ static int run_units(sbr_ctx *ctx, const sbr_bvh *bvh, const std::vector<UnitDev
                                         ctx->seg_base.p, ctx->seg_slot.p,
                                         reinterpret_cast<PrimHit *>(ctx->slots.p));
             ra.counter = ctx->counter.p + 1;
+            CUDA_TRY(attach_big_queue(ctx, ra));
+            for (int g : bgrids)       // a grid of the batch with a segment outside it
+                for (int64_t q = seg_base[g]; q < seg_base[g + 1] && !ra.sparse; ++q)
+                    ra.sparse = seg_slot[q] == kNoSlot;
             CUDA_TRY(launch_raster(ra, st, ctx->stats()));
         }
         if (raster) {

@@ -133,6 +133,10 @@ struct RasterArgs {
     const int64_t *seg_slot;   // per global segment row: slot - ray index, or kNoSlot
     PrimHit *prim;
     unsigned long long *counter;   // work counter (zeroed by launch_raster)
+    int sparse;                    // some segments of the batch's grids are not in it
+    int4 *big;                     // queue of big-triangle chunks (grid, tri, chunk, -)
+    unsigned long long *nbig;      // its fill counter
+    int64_t big_cap;               // its capacity (items beyond it stay in k_raster)
 };
 constexpr int64_t kNoSlot = INT64_MIN;   // segment not in this batch / shard
 cudaError_t launch_raster(const RasterArgs &a, cudaStream_t st, const LaunchStats &ls);

@@ -28,6 +28,8 @@ namespace sbr {
 constexpr double kMargin = 0.01;   // cells; >> every projection rounding error
 constexpr int kRasterThreads = 256;
 constexpr int kRasterWarps = kRasterThreads / 32;
+constexpr long long kBigTri = 2048;     // candidates above which a triangle is chunked
+constexpr long long kBigChunk = 1024;   // candidates per big-triangle work item
 
 struct __align__(16) RasterTri {
     double ax, ay, az, e1x, e1y, e1z, e2x, e2y, e2z, px, py, pz, det, inv;
@@ -57,8 +59,96 @@ __device__ __forceinline__ void prim_min(PrimHit *h, unsigned long long bits, un
     }
 }
 
+// Candidate rectangle of one (grid, triangle): the cells whose centre lies
+// in the triangle's projected bounding box widened by kMargin.  count == 0:
+// the triangle cannot be hit (det == 0, geometry.py:339) or lies outside.
+struct RasterSetup {
+    TriF64 T;
+    TriDir P;
+    double inv;
+    long long i0, j0, count;
+    int cols;
+};
+
+__device__ __forceinline__ RasterSetup raster_setup(const TriF64 &T, const GridDev &G)
+{
+    RasterSetup S;
+    S.T = T;
+    S.count = 0;
+    S.P = tri_dir(T, G.k[0], G.k[1], G.k[2]);
+    if (S.P.det == 0.0) return S;
+    const int64_t n_v = G.n_v, n_u = G.n_rays / n_v;
+    const double isp = 1.0 / G.spacing;
+    const double rx = T.ax - G.corner[0], ry = T.ay - G.corner[1], rz = T.az - G.corner[2];
+    const double a0 = (rx * G.u[0] + ry * G.u[1] + rz * G.u[2]) * isp - 0.5;
+    const double b0 = (rx * G.v[0] + ry * G.v[1] + rz * G.v[2]) * isp - 0.5;
+    const double a1 = a0 + (T.e1x * G.u[0] + T.e1y * G.u[1] + T.e1z * G.u[2]) * isp;
+    const double b1 = b0 + (T.e1x * G.v[0] + T.e1y * G.v[1] + T.e1z * G.v[2]) * isp;
+    const double a2 = a0 + (T.e2x * G.u[0] + T.e2y * G.u[1] + T.e2z * G.u[2]) * isp;
+    const double b2 = b0 + (T.e2x * G.v[0] + T.e2y * G.v[1] + T.e2z * G.v[2]) * isp;
+    const double alo = fmin(fmin(a0, a1), a2) - kMargin;
+    const double ahi = fmax(fmax(a0, a1), a2) + kMargin;
+    const double blo = fmin(fmin(b0, b1), b2) - kMargin;
+    const double bhi = fmax(fmax(b0, b1), b2) + kMargin;
+    if (!(ahi >= 0.0 && bhi >= 0.0 && alo <= (double)(n_u - 1) && blo <= (double)(n_v - 1)))
+        return S;                               // outside the aperture (or non-finite)
+    const int64_t i0 = alo <= 0.0 ? 0 : (int64_t)ceil(alo);
+    const int64_t i1 = ahi >= (double)(n_u - 1) ? n_u - 1 : (int64_t)floor(ahi);
+    const int64_t j0 = blo <= 0.0 ? 0 : (int64_t)ceil(blo);
+    const int64_t j1 = bhi >= (double)(n_v - 1) ? n_v - 1 : (int64_t)floor(bhi);
+    const int64_t rows = i1 - i0 + 1, cols = j1 - j0 + 1;
+    if (rows <= 0 || cols <= 0) return S;
+    S.i0 = i0;
+    S.j0 = j0;
+    S.cols = (int)cols;
+    S.count = rows * cols;
+    S.inv = __drcp_rn(S.P.det);                 // == IEEE 1.0 / det
+    return S;
+}
+
+__device__ __forceinline__ void split_cell(long long local, int cols, long long &li, long long &lj)
+{
+    if (local < 0x7fffffffLL) {
+        const unsigned l32 = (unsigned)local, c32 = (unsigned)cols;
+        li = l32 / c32;
+        lj = l32 - (unsigned)li * c32;
+    } else {
+        li = local / cols;
+        lj = local - li * cols;
+    }
+}
+
+// Exact test of ray (i, j) against one triangle; records the hit.
+__device__ __forceinline__ void raster_cell(const RasterArgs &a, const GridDev &G,
+                                            const int64_t *seg, const TriF64 &T,
+                                            const TriDir &P, double inv, int id, int64_t i,
+                                            int64_t j)
+{
+    const double inf = __longlong_as_double(0x7ff0000000000000LL);
+    const int64_t r = i * G.n_v + j;
+    // sharded / partial batches: skip cells of segments this launch does not
+    // own before doing any arithmetic
+    const int64_t off = __ldg(&seg[r / kSegRays]);
+    if (a.sparse && off == kNoSlot) return;
+    // origin exactly as the launcher builds it (pipeline.cu grid_origin)
+    const double sp = G.spacing;
+    const double si = DM(DA((double)i, 0.5), sp);
+    const double sj = DM(DA((double)j, 0.5), sp);
+    const double ox = DA(DA(G.corner[0], DM(si, G.u[0])), DM(sj, G.v[0]));
+    const double oy = DA(DA(G.corner[1], DM(si, G.u[1])), DM(sj, G.v[1]));
+    const double oz = DA(DA(G.corner[2], DM(si, G.u[2])), DM(sj, G.v[2]));
+    const double t = tri_hit_origin<true>(T, P, inv, ox, oy, oz, G.k[0], G.k[1], G.k[2], 0.0,
+                                          inf);
+    if (t > 0.0 && t < inf && off != kNoSlot)
+        prim_min(a.prim + (off + r), (unsigned long long)__double_as_longlong(t),
+                 (unsigned int)id);
+}
+
 // Persistent: each warp pulls its next 32-triangle item from a global
-// counter, so uneven candidate counts never leave warps idle.
+// counter, so uneven candidate counts never leave warps idle.  A triangle
+// with more than kBigTri candidates is not walked here: it is queued as
+// kBigChunk-candidate chunks for k_raster_big, so no warp ever holds a huge
+// triangle at the tail of the launch.
 template <int STORAGE>
 __global__ void __launch_bounds__(kRasterThreads, 4)
 k_raster(RasterArgs a, int64_t ntri_pad)
@@ -66,7 +156,6 @@ k_raster(RasterArgs a, int64_t ntri_pad)
     __shared__ RasterTri st[kRasterWarps][32];
     __shared__ int scan[kRasterWarps][32];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const double inf = __longlong_as_double(0x7ff0000000000000LL);
     const int64_t warps_total = (int64_t)a.nbg * (ntri_pad / 32);
     while (true) {
         unsigned long long got = 0;
@@ -78,46 +167,28 @@ k_raster(RasterArgs a, int64_t ntri_pad)
         const int64_t tri = item - (int64_t)gl * ntri_pad;
         const int g = __ldg(&a.bgrids[gl]);
         const GridDev &G = a.grids[g];
-        const double dx = G.k[0], dy = G.k[1], dz = G.k[2];
-        const double sp = G.spacing;
-        const int64_t n_v = G.n_v, n_u = G.n_rays / n_v;
         // ---- per-lane triangle set-up and candidate rectangle ----------
         long long count = 0;
         RasterTri &R = st[wib][lane];
         if (tri < a.ntri) {
-            const TriF64 T = load_tri<STORAGE>(a.B, (int)tri);
-            const TriDir P = tri_dir(T, dx, dy, dz);
-            if (P.det != 0.0) {                    // geometry.py:339: never accepted
-                const double isp = 1.0 / sp;
-                const double rx = T.ax - G.corner[0], ry = T.ay - G.corner[1],
-                             rz = T.az - G.corner[2];
-                const double a0 = (rx * G.u[0] + ry * G.u[1] + rz * G.u[2]) * isp - 0.5;
-                const double b0 = (rx * G.v[0] + ry * G.v[1] + rz * G.v[2]) * isp - 0.5;
-                const double a1 = a0 + (T.e1x * G.u[0] + T.e1y * G.u[1] + T.e1z * G.u[2]) * isp;
-                const double b1 = b0 + (T.e1x * G.v[0] + T.e1y * G.v[1] + T.e1z * G.v[2]) * isp;
-                const double a2 = a0 + (T.e2x * G.u[0] + T.e2y * G.u[1] + T.e2z * G.u[2]) * isp;
-                const double b2 = b0 + (T.e2x * G.v[0] + T.e2y * G.v[1] + T.e2z * G.v[2]) * isp;
-                const double alo = fmin(fmin(a0, a1), a2) - kMargin;
-                const double ahi = fmax(fmax(a0, a1), a2) + kMargin;
-                const double blo = fmin(fmin(b0, b1), b2) - kMargin;
-                const double bhi = fmax(fmax(b0, b1), b2) + kMargin;
-                if (ahi >= 0.0 && bhi >= 0.0 && alo <= (double)(n_u - 1) &&
-                    blo <= (double)(n_v - 1)) {
-                    const int64_t i0 = alo <= 0.0 ? 0 : (int64_t)ceil(alo);
-                    const int64_t i1 = ahi >= (double)(n_u - 1) ? n_u - 1 : (int64_t)floor(ahi);
-                    const int64_t j0 = blo <= 0.0 ? 0 : (int64_t)ceil(blo);
-                    const int64_t j1 = bhi >= (double)(n_v - 1) ? n_v - 1 : (int64_t)floor(bhi);
-                    const int64_t rows = i1 - i0 + 1, cols = j1 - j0 + 1;
-                    if (rows > 0 && cols > 0) {
-                        count = rows * cols;
-                        R.ax = T.ax; R.ay = T.ay; R.az = T.az;
-                        R.e1x = T.e1x; R.e1y = T.e1y; R.e1z = T.e1z;
-                        R.e2x = T.e2x; R.e2y = T.e2y; R.e2z = T.e2z;
-                        R.px = P.px; R.py = P.py; R.pz = P.pz; R.det = P.det;
-                        R.inv = __drcp_rn(P.det);    // == IEEE 1.0 / det
-                        R.i0 = i0; R.j0 = j0; R.cols = (int)cols; R.id = T.id;
-                    }
+            const RasterSetup S = raster_setup(load_tri<STORAGE>(a.B, (int)tri), G);
+            count = S.count;
+            if (count > kBigTri && a.big) {
+                const long long nch = (count + kBigChunk - 1) / kBigChunk;
+                const unsigned long long at = atomicAdd(a.nbig, (unsigned long long)nch);
+                if (at + nch <= (unsigned long long)a.big_cap) {
+                    for (long long c = 0; c < nch; ++c)
+                        a.big[at + c] = make_int4(gl, (int)tri, (int)c, 0);
+                    count = 0;                          // walked by k_raster_big
                 }
+            }
+            if (count) {
+                R.ax = S.T.ax; R.ay = S.T.ay; R.az = S.T.az;
+                R.e1x = S.T.e1x; R.e1y = S.T.e1y; R.e1z = S.T.e1z;
+                R.e2x = S.T.e2x; R.e2y = S.T.e2y; R.e2z = S.T.e2z;
+                R.px = S.P.px; R.py = S.P.py; R.pz = S.P.pz; R.det = S.P.det;
+                R.inv = S.inv;
+                R.i0 = S.i0; R.j0 = S.j0; R.cols = S.cols; R.id = S.T.id;
             }
         }
         // ---- warp scan of candidate counts --------------------------------
@@ -150,42 +221,61 @@ k_raster(RasterArgs a, int64_t ntri_pad)
                 for (int step = 16; step > 0; step >>= 1)
                     if (scan[wib][lo + step - 1] <= c) lo += step;
                 const RasterTri &Q = st[wib][lo];
-                const long long local = (long long)c + win - Q.excl;
                 long long li, lj;
-                if (local < 0x7fffffffLL) {
-                    const unsigned l32 = (unsigned)local, c32 = (unsigned)Q.cols;
-                    li = l32 / c32;
-                    lj = l32 - (unsigned)li * c32;
-                } else {
-                    li = local / Q.cols;
-                    lj = local - li * Q.cols;
-                }
-                const int64_t i = Q.i0 + li, j = Q.j0 + lj;
-                // origin exactly as the launcher builds it (pipeline.cu grid_origin)
-                const double si = DM(DA((double)i, 0.5), sp);
-                const double sj = DM(DA((double)j, 0.5), sp);
-                const double ox = DA(DA(G.corner[0], DM(si, G.u[0])), DM(sj, G.v[0]));
-                const double oy = DA(DA(G.corner[1], DM(si, G.u[1])), DM(sj, G.v[1]));
-                const double oz = DA(DA(G.corner[2], DM(si, G.u[2])), DM(sj, G.v[2]));
+                split_cell((long long)c + win - Q.excl, Q.cols, li, lj);
                 TriF64 T;
                 T.ax = Q.ax; T.ay = Q.ay; T.az = Q.az;
                 T.e1x = Q.e1x; T.e1y = Q.e1y; T.e1z = Q.e1z;
                 T.e2x = Q.e2x; T.e2y = Q.e2y; T.e2z = Q.e2z;
                 TriDir P;
                 P.px = Q.px; P.py = Q.py; P.pz = Q.pz; P.det = Q.det;
-                const double t = tri_hit_origin<true>(T, P, Q.inv, ox, oy, oz, dx, dy, dz,
-                                                      0.0, inf);
-                if (t > 0.0 && t < inf) {
-                    const int64_t r = i * n_v + j;
-                    const int64_t off = __ldg(&seg[r / kSegRays]);
-                    if (off != kNoSlot)
-                        prim_min(a.prim + (off + r), (unsigned long long)__double_as_longlong(t),
-                                 (unsigned int)Q.id);
-                }
+                raster_cell(a, G, seg, T, P, Q.inv, Q.id, Q.i0 + li, Q.j0 + lj);
             }
         }
         __syncwarp();
     }
+}
+
+// Chunks of big triangles: a warp takes one chunk (kBigChunk candidates of
+// one triangle), recomputes the (identical) set-up and walks 32 cells at a
+// time.
+template <int STORAGE>
+__global__ void __launch_bounds__(kRasterThreads, 4)
+k_raster_big(RasterArgs a)
+{
+    const int lane = threadIdx.x & 31;
+    const unsigned long long nbig = *a.nbig;
+    const unsigned long long n = nbig < (unsigned long long)a.big_cap ? nbig : a.big_cap;
+    while (true) {
+        unsigned long long got = 0;
+        if (lane == 0) got = atomicAdd(a.counter, 1ULL);
+        const unsigned long long w = __shfl_sync(0xffffffffu, got, 0);
+        if (w >= n) break;
+        const int4 it = a.big[w];
+        const int g = __ldg(&a.bgrids[it.x]);
+        const GridDev &G = a.grids[g];
+        const RasterSetup S = raster_setup(load_tri<STORAGE>(a.B, it.y), G);
+        const int64_t *seg = a.seg_slot + __ldg(&a.seg_base[g]);
+        const long long c0 = (long long)it.z * kBigChunk;
+        const long long c1 = c0 + kBigChunk < S.count ? c0 + kBigChunk : S.count;
+        for (long long c = c0 + lane; c < c1; c += 32) {
+            long long li, lj;
+            split_cell(c, S.cols, li, lj);
+            raster_cell(a, G, seg, S.T, S.P, S.inv, S.T.id, S.i0 + li, S.j0 + lj);
+        }
+    }
+}
+
+template <int S>
+static int persistent_raster_blocks(int num_sms, bool big)
+{
+    int per_sm = 0;
+    const cudaError_t e =
+        big ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_raster_big<S>,
+                                                            kRasterThreads, 0)
+            : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_raster<S>,
+                                                            kRasterThreads, 0);
+    return (e != cudaSuccess || per_sm < 1 ? 1 : per_sm) * num_sms;
 }
 
 template <int S>
@@ -193,25 +283,28 @@ static void raster_dispatch(const RasterArgs &a, cudaStream_t st, int num_sms)
 {
     const int64_t ntri_pad = (a.ntri + 31) / 32 * 32;
     const int64_t warps = (int64_t)a.nbg * (ntri_pad / 32);
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_raster<S>, kRasterThreads, 0) !=
-            cudaSuccess || per_sm < 1)
-        per_sm = 1;
     int64_t blocks = (warps + kRasterWarps - 1) / kRasterWarps;
-    if (blocks > (int64_t)per_sm * num_sms) blocks = (int64_t)per_sm * num_sms;
+    const int64_t cap = persistent_raster_blocks<S>(num_sms, false);
+    if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     k_raster<S><<<(unsigned)blocks, kRasterThreads, 0, st>>>(a, ntri_pad);
+    if (a.big) {
+        cudaMemsetAsync(a.counter, 0, sizeof(unsigned long long), st);
+        k_raster_big<S><<<persistent_raster_blocks<S>(num_sms, true), kRasterThreads, 0, st>>>(a);
+    }
 }
 
 cudaError_t launch_raster(const RasterArgs &a, cudaStream_t st, const LaunchStats &ls)
 {
     if (a.nbg == 0 || a.ntri == 0) return cudaSuccess;
     cudaError_t e = cudaMemsetAsync(a.counter, 0, sizeof(unsigned long long), st);
+    if (e == cudaSuccess && a.big)
+        e = cudaMemsetAsync(a.nbig, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
     if (a.storage == kF64) raster_dispatch<kF64>(a, st, ls.num_sms);
     else if (a.storage == kSingle) raster_dispatch<kSingle>(a, st, ls.num_sms);
     else raster_dispatch<kF32Exact>(a, st, ls.num_sms);
-    *ls.launches += 1;
+    *ls.launches += a.big ? 2 : 1;
     return cudaGetLastError();
 }
 
