@@ -209,16 +209,27 @@ __device__ __forceinline__ double sa_of(const double lo[3], const double hi[3])
 
 
 
-// one thread per segment: node box out, split decision (bvh.py:154-215 and
-// the leaf test of bvh.py:253-262)
-__global__ void k_select(const SegAcc *__restrict__ acc, const unsigned int *__restrict__ cnt,
-                         const unsigned long long *__restrict__ bbox,
-                         const int64_t *__restrict__ sc, const int *__restrict__ snode, int S,
-                         int R, int depth, SahParams P, double *__restrict__ node_box,
-                         SegSplit *__restrict__ out, int *__restrict__ split_flag)
+// one warp per segment: node box out, split decision (bvh.py:154-215 and
+// the leaf test of bvh.py:253-262).  Lanes merge the bin replicas, lanes
+// 0..2 sweep one axis each, lane 0 picks the first minimum in (axis,
+// boundary) order -- the reference's strict-< scan order.
+constexpr int kSelWarps = 4;
+
+__global__ void __launch_bounds__(kSelWarps * 32)
+k_select(const SegAcc *__restrict__ acc, const unsigned int *__restrict__ cnt,
+         const unsigned long long *__restrict__ bbox, const int64_t *__restrict__ sc,
+         const int *__restrict__ snode, int S, int R, int depth, SahParams P,
+         double *__restrict__ node_box, SegSplit *__restrict__ out,
+         int *__restrict__ split_flag)
 {
-    const int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= S) return;
+    __shared__ int64_t sbc[kSelWarps][3][kSahMaxBins];
+    __shared__ double smn[kSelWarps][3][3][kSahMaxBins], smx[kSelWarps][3][3][kSahMaxBins];
+    __shared__ double abest[kSelWarps][3];
+    __shared__ int ab[kSelWarps][3], ahave[kSelWarps][3];
+    __shared__ int64_t anl[kSelWarps][3];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int s = blockIdx.x * kSelWarps + w;
+    if (s >= S) return;                               // warp-uniform
     const SegAcc &A = acc[s];
     double lo[3], hi[3];
 #pragma unroll
@@ -226,94 +237,123 @@ __global__ void k_select(const SegAcc *__restrict__ acc, const unsigned int *__r
         lo[q] = unordd(A.box[q]);
         hi[q] = unordd(A.box[3 + q]);
     }
-    double *nb = node_box + 6 * (int64_t)snode[s];
+    if (lane == 0) {
+        double *nb = node_box + 6 * (int64_t)snode[s];
 #pragma unroll
-    for (int q = 0; q < 3; ++q) { nb[q] = lo[q]; nb[3 + q] = hi[q]; }
+        for (int q = 0; q < 3; ++q) { nb[q] = lo[q]; nb[3 + q] = hi[q]; }
+    }
     SegSplit r;
     r.split = 0; r.axis = -1; r.boundary = -1; r.c_lo = 0.0; r.scale = 0.0; r.nl = 0;
     const int64_t n = sc[s];
+    const int B = P.bins;
     if (n > P.n_leaf && depth < P.max_depth) {
-        double sa_p = sa_of(lo, hi);
-        if (!(sa_p >= 1e-300)) sa_p = 1e-300;          // max(sa, 1e-300)
-        bool have = false;
-        double best = 0.0;
-        const int B = P.bins;
-        for (int axis = 0; axis < 3; ++axis) {
-            const double c_lo = unordd(A.cb[axis]), c_hi = unordd(A.cb[3 + axis]);
-            if (!(c_hi > c_lo)) continue;
-            // merge the replicas of every bin (exact: min / max / sum)
-            double bmn[3][kSahMaxBins], bmx[3][kSahMaxBins];
-            int64_t bc[kSahMaxBins];
-            for (int b = 0; b < B; ++b) {
-                unsigned long long mn[3] = {kOrdPosInf, kOrdPosInf, kOrdPosInf};
-                unsigned long long mx[3] = {kOrdNegInf, kOrdNegInf, kOrdNegInf};
-                int64_t c = 0;
-                for (int rep = 0; rep < R; ++rep) {
-                    const int64_t slot = (((int64_t)s * R + rep) * 3 + axis) * B + b;
-                    const unsigned long long *bb = bbox + 6 * slot;
-                    c += cnt[slot];
-                    for (int q = 0; q < 3; ++q) {
-                        mn[q] = bb[q] < mn[q] ? bb[q] : mn[q];
-                        mx[q] = bb[3 + q] > mx[q] ? bb[3 + q] : mx[q];
-                    }
-                }
-                bc[b] = c;
+        // merge the replicas of every (axis, bin) (exact: min / max / sum)
+        for (int idx = lane; idx < 3 * B; idx += 32) {
+            const int axis = idx / B, b = idx - axis * B;
+            unsigned long long mn[3] = {kOrdPosInf, kOrdPosInf, kOrdPosInf};
+            unsigned long long mx[3] = {kOrdNegInf, kOrdNegInf, kOrdNegInf};
+            int64_t c = 0;
+            for (int rep = 0; rep < R; ++rep) {
+                const int64_t slot = (((int64_t)s * R + rep) * 3 + axis) * B + b;
+                const unsigned long long *bb = bbox + 6 * slot;
+                c += cnt[slot];
+#pragma unroll
                 for (int q = 0; q < 3; ++q) {
-                    bmn[q][b] = unordd(mn[q]);
-                    bmx[q][b] = unordd(mx[q]);
+                    mn[q] = bb[q] < mn[q] ? bb[q] : mn[q];
+                    mx[q] = bb[3 + q] > mx[q] ? bb[3 + q] : mx[q];
                 }
             }
-            // suffix sweep first (right side of boundary b is bins b+1..B-1)
-            double rlo[3][kSahMaxBins], rhi[3][kSahMaxBins];
-            int64_t rn[kSahMaxBins];
-            {
+            sbc[w][axis][b] = c;
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                smn[w][q][axis][b] = unordd(mn[q]);
+                smx[w][q][axis][b] = unordd(mx[q]);
+            }
+        }
+        __syncwarp();
+        double sa_p = sa_of(lo, hi);
+        if (!(sa_p >= 1e-300)) sa_p = 1e-300;          // max(sa, 1e-300)
+        if (lane < 3) {
+            const int axis = lane;
+            bool have = false;
+            double best = 0.0;
+            int bb_best = -1;
+            int64_t nl_best = 0;
+            const double c_lo = unordd(A.cb[axis]), c_hi = unordd(A.cb[3 + axis]);
+            if (c_hi > c_lo) {
+                // suffix sweep (right side of boundary b is bins b+1..B-1)
+                double rlo[3][kSahMaxBins], rhi[3][kSahMaxBins];
+                int64_t rn[kSahMaxBins];
                 double l3[3] = {INFINITY, INFINITY, INFINITY}, h3[3] = {-INFINITY, -INFINITY, -INFINITY};
                 int64_t acc_n = 0;
                 for (int b = B - 1; b >= 0; --b) {
-                    acc_n += bc[b];
+                    acc_n += sbc[w][axis][b];
                     for (int q = 0; q < 3; ++q) {
-                        l3[q] = fmin(l3[q], bmn[q][b]);
-                        h3[q] = fmax(h3[q], bmx[q][b]);
+                        l3[q] = fmin(l3[q], smn[w][q][axis][b]);
+                        h3[q] = fmax(h3[q], smx[w][q][axis][b]);
                         rlo[q][b] = l3[q];
                         rhi[q][b] = h3[q];
                     }
                     rn[b] = acc_n;
                 }
-            }
-            double l3[3] = {INFINITY, INFINITY, INFINITY}, h3[3] = {-INFINITY, -INFINITY, -INFINITY};
-            int64_t ln = 0;
-            for (int b = 0; b < B - 1; ++b) {
-                ln += bc[b];
-                for (int q = 0; q < 3; ++q) {
-                    l3[q] = fmin(l3[q], bmn[q][b]);
-                    h3[q] = fmax(h3[q], bmx[q][b]);
-                }
-                const int64_t nr = rn[b + 1];
-                if (ln == 0 || nr == 0) continue;
-                double rl[3] = {rlo[0][b + 1], rlo[1][b + 1], rlo[2][b + 1]};
-                double rh[3] = {rhi[0][b + 1], rhi[1][b + 1], rhi[2][b + 1]};
-                const double sal = sa_of(l3, h3), sar = sa_of(rl, rh);
-                // sah_cost (bvh.py:124-127): c_t + (sal/sa_p) n_l c_i + (sar/sa_p) n_r c_i
-                const double cost = __dadd_rn(
-                    __dadd_rn(P.c_t, __dmul_rn(__dmul_rn(__ddiv_rn(sal, sa_p), (double)ln), P.c_i)),
-                    __dmul_rn(__dmul_rn(__ddiv_rn(sar, sa_p), (double)nr), P.c_i));
-                if (!have || cost < best) {
-                    have = true;
-                    best = cost;
-                    r.axis = axis;
-                    r.boundary = b;
-                    r.c_lo = c_lo;
-                    r.scale = __ddiv_rn((double)B, __dsub_rn(c_hi, c_lo));
-                    r.nl = ln;
+                for (int q = 0; q < 3; ++q) { l3[q] = INFINITY; h3[q] = -INFINITY; }
+                int64_t ln = 0;
+                for (int b = 0; b < B - 1; ++b) {
+                    ln += sbc[w][axis][b];
+                    for (int q = 0; q < 3; ++q) {
+                        l3[q] = fmin(l3[q], smn[w][q][axis][b]);
+                        h3[q] = fmax(h3[q], smx[w][q][axis][b]);
+                    }
+                    const int64_t nr = rn[b + 1];
+                    if (ln == 0 || nr == 0) continue;
+                    double rl[3] = {rlo[0][b + 1], rlo[1][b + 1], rlo[2][b + 1]};
+                    double rh[3] = {rhi[0][b + 1], rhi[1][b + 1], rhi[2][b + 1]};
+                    const double sal = sa_of(l3, h3), sar = sa_of(rl, rh);
+                    // sah_cost (bvh.py:124-127): c_t + (sal/sa_p) n_l c_i + (sar/sa_p) n_r c_i
+                    const double cost = __dadd_rn(
+                        __dadd_rn(P.c_t, __dmul_rn(__dmul_rn(__ddiv_rn(sal, sa_p), (double)ln), P.c_i)),
+                        __dmul_rn(__dmul_rn(__ddiv_rn(sar, sa_p), (double)nr), P.c_i));
+                    if (!have || cost < best) {
+                        have = true;
+                        best = cost;
+                        bb_best = b;
+                        nl_best = ln;
+                    }
                 }
             }
+            ahave[w][axis] = have;
+            abest[w][axis] = best;
+            ab[w][axis] = bb_best;
+            anl[w][axis] = nl_best;
         }
-        // bvh.py:210-211: no admissible split, or not worth it for a small node
-        if (have && !(best >= __dmul_rn((double)n, P.c_i) && n <= 4 * (int64_t)P.n_leaf))
-            r.split = 1;
+        __syncwarp();
+        if (lane == 0) {
+            bool have = false;
+            double best = 0.0;
+            for (int axis = 0; axis < 3; ++axis) {
+                if (!ahave[w][axis]) continue;
+                if (!have || abest[w][axis] < best) {
+                    have = true;
+                    best = abest[w][axis];
+                    r.axis = axis;
+                    r.boundary = ab[w][axis];
+                    r.nl = anl[w][axis];
+                }
+            }
+            if (have) {
+                const double c_lo = unordd(A.cb[r.axis]), c_hi = unordd(A.cb[3 + r.axis]);
+                r.c_lo = c_lo;
+                r.scale = __ddiv_rn((double)B, __dsub_rn(c_hi, c_lo));
+            }
+            // bvh.py:210-211: no admissible split, or not worth it for a small node
+            if (have && !(best >= __dmul_rn((double)n, P.c_i) && n <= 4 * (int64_t)P.n_leaf))
+                r.split = 1;
+        }
     }
-    out[s] = r;
-    split_flag[s] = r.split;
+    if (lane == 0) {
+        out[s] = r;
+        split_flag[s] = r.split;
+    }
 }
 
 __global__ void k_flags(const double *__restrict__ tb, const int *__restrict__ idx,
@@ -557,8 +597,8 @@ cudaError_t sah_build(const double *d_verts, int64_t n, const SahParams &P, SahT
         k_bin<<<nblk(n, T), T, 0, st>>>(w.tb.p, idx, w.eseg.p, n, w.acc.p, B, R, w.cnt.p,
                                         w.bbox.p);
         CK(cudaMemsetAsync(w.sflag.p + S, 0, sizeof(int), st));
-        k_select<<<nblk(S, 128), 128, 0, st>>>(w.acc.p, w.cnt.p, w.bbox.p, sc, snode, S, R, depth,
-                                               P, w.node_box.p, w.sp.p, w.sflag.p);
+        k_select<<<nblk(S, kSelWarps), kSelWarps * 32, 0, st>>>(
+            w.acc.p, w.cnt.p, w.bbox.p, sc, snode, S, R, depth, P, w.node_box.p, w.sp.p, w.sflag.p);
         k_flags<<<nblk(n, T), T, 0, st>>>(w.tb.p, idx, w.eseg.p, n, w.sp.p, B, w.flag.p);
         CK(cub::DeviceScan::ExclusiveSum(w.scan_tmp.p, scan_bytes, w.flag.p, w.rank.p, (int)n,
                                          st));

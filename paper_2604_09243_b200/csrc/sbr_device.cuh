@@ -279,12 +279,20 @@ __device__ __forceinline__ int node4_visit(const Node4 *np, const RayBox &r, flo
 #undef SBR_SLAB
     const int n = (tn[0] != inf) + (tn[1] != inf) + (tn[2] != inf) + (tn[3] != inf);
     ref[0] = rf.x; ref[1] = rf.y; ref[2] = rf.z; ref[3] = rf.w;
+#ifdef SBR_SORT3
+    // nearest first only (3 compare-exchanges); the others stay partially
+    // ordered and misses may sit anywhere in 1..3 (callers test tn != inf)
+    cswap(tn[0], ref[0], tn[1], ref[1]);
+    cswap(tn[2], ref[2], tn[3], ref[3]);
+    cswap(tn[0], ref[0], tn[2], ref[2]);
+#else
     // 4-element sorting network, misses (+inf) sink to the end
     cswap(tn[0], ref[0], tn[1], ref[1]);
     cswap(tn[2], ref[2], tn[3], ref[3]);
     cswap(tn[0], ref[0], tn[2], ref[2]);
     cswap(tn[1], ref[1], tn[3], ref[3]);
     cswap(tn[1], ref[1], tn[2], ref[2]);
+#endif
     return n;
 }
 

@@ -243,7 +243,11 @@ k_trace_persistent(TraceArgs a)
                 if (n > 0) {
 #pragma unroll
                     for (int c = 3; c >= 1; --c)   // farther hits first: nearest pops first
+#ifdef SBR_SORT3
+                        if (tt[c] != __int_as_float(0x7f800000)) {
+#else
                         if (c < n) {
+#endif
                             stack[L.sp].ref = rr[c];
                             stack[L.sp].tn = tt[c];
                             ++L.sp;
