@@ -51,13 +51,15 @@ def parse():
     p.add_argument("--angles", type=int, default=N_ANGLES)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
-    p.add_argument("--n-leaf", type=int, default=4, help="BVH leaf size (BuildParams.n_leaf)")
+    p.add_argument("--n-leaf", type=int, default=2,
+                   help="BVH leaf size (BuildParams.n_leaf; 2 measured fastest, "
+                        "profiles/experiments/r01_scheduler_experiments.json)")
     p.add_argument("--bounces", type=int, default=MAX_BOUNCES,
                    help="max bounces (experiments only; the C4 workload is 5)")
     return p.parse_args()
 
 
-def workload(density, n_angles, bounces=MAX_BOUNCES):
+def workload(density, n_angles, bounces=MAX_BOUNCES, n_leaf=2):
     import paper_2604_09243_b200 as sbr
     from paper_2604_09243_b200 import meshgen
     mesh = meshgen.generate_aircraft(density=density)
@@ -65,7 +67,7 @@ def workload(density, n_angles, bounces=MAX_BOUNCES):
     cfg = sbr.SweepConfig(mesh_path="<procedural aircraft>", frequency_hz=FREQ_HZ,
                           theta=sbr.AngleRange(math.pi / 2, math.pi / 2, 1),
                           phi=sbr.AngleRange(0.0, math.radians(n_angles - 1), n_angles),
-                          max_bounces=bounces)
+                          max_bounces=bounces, split_rule="sah", n_leaf=n_leaf)
     return mesh, lam, cfg
 
 
@@ -76,6 +78,7 @@ def config_dict(mesh, n_angles, world, bounces=MAX_BOUNCES):
             "theta_deg": 90, "phi_deg": [0, n_angles - 1], "frequency_hz": FREQ_HZ,
             "max_bounces": bounces, "spacing": "lambda/5 (5.996 mm)",
             "parallelism": f"angle-sharded x{world}, one NCCL reduce" if world > 1 else "1 GPU",
+            "bvh": "reference binned-SAH tree (16 bins, n_leaf=2) built on the GPU, BVH4 traversal",
             "l2": "flushed (512 MB write) between timed steps"}
 
 
@@ -230,8 +233,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ctx = nat.context(local)
 
-    mesh, lam, cfg = workload(args.density, args.angles, args.bounces)
-    tree = sbr.build(mesh, sbr.BuildParams(n_leaf=args.n_leaf))
+    mesh, lam, cfg = workload(args.density, args.angles, args.bounces, args.n_leaf)
+    tree = sbr.build(mesh, cfg.build_params())
     th, ph, cells, grids = sweep_grids(cfg, mesh)
     tp = cfg.trace_params()
     k = [2 * math.pi / lam]
