@@ -131,6 +131,9 @@ int sbr_ctx_raster_stats(sbr_ctx *ctx, double *raster_ms);
 /* Instrumentation: read bandwidth (GB/s) of a `bytes` buffer re-read `reps`
  * times from L2 (16-byte ld.global.cg, 8 CTAs/SM, best of 5). */
 int sbr_probe_l2_bandwidth(sbr_ctx *ctx, int64_t bytes, int32_t reps, double *gbs);
+/* Instrumented builds only (-DSBR_TRACE_STATS): read and clear n <= 24
+ * lane-state counters of the trace kernel (zeros otherwise). */
+int sbr_ctx_debug_counters(sbr_ctx *ctx, int64_t *out, int32_t n);
 
 /* ---- mesh: geometry.py:130-180 mesh_from_soup output -> device --------- */
 int sbr_mesh_create(sbr_ctx *ctx, const double *v0, const double *v1,

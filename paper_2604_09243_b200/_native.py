@@ -74,6 +74,7 @@ _SIGS = {
                                             ctypes.POINTER(c_dbl), ctypes.POINTER(c_i64)]),
     "sbr_ctx_raster_stats": (ctypes.c_int, [c_vp, ctypes.POINTER(c_dbl)]),
     "sbr_probe_l2_bandwidth": (ctypes.c_int, [c_vp, c_i64, c_i32, ctypes.POINTER(c_dbl)]),
+    "sbr_ctx_debug_counters": (ctypes.c_int, [c_vp, c_vp, c_i32]),
     "sbr_mesh_create": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i32,
                                        ctypes.POINTER(c_vp)]),
     "sbr_mesh_destroy": (ctypes.c_int, [c_vp]),

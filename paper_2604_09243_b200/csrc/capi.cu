@@ -197,7 +197,7 @@ extern "C" int sbr_ctx_create(int device, sbr_ctx **out)
             if (!g_alloc_stream[device]) g_alloc_stream[device] = ctx->stream;
         }
     }
-    if (e == cudaSuccess) e = ctx->counter.alloc(2);   // [0] trace, [1] raster
+    if (e == cudaSuccess) e = ctx->counter.alloc(32);  // [0] trace, [1] raster, [8..] stats builds
     if (e == cudaSuccess) e = ctx->err_flag.alloc(1);
     if (e == cudaSuccess) e = ctx->bad.alloc(1);
     if (e != cudaSuccess) {
@@ -1499,6 +1499,20 @@ extern "C" int sbr_probe_l2_bandwidth(sbr_ctx *ctx, int64_t bytes, int32_t reps,
     std::lock_guard<std::mutex> lk(ctx->mu);
     if (int rc = set_device(ctx)) return rc;
     CUDA_TRY(probe_l2_read(bytes, reps, ctx->num_sms, ctx->stream, gbs));
+    return SBR_OK;
+}
+
+// Instrumented builds (-DSBR_TRACE_STATS) accumulate lane-state counters in
+// counter[8..31]; this reads and clears them (all zero in normal builds).
+extern "C" int sbr_ctx_debug_counters(sbr_ctx *ctx, int64_t *out, int32_t n)
+{
+    REQUIRE(ctx && out && n >= 0 && n <= 24, "bad arguments");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (int rc = set_device(ctx)) return rc;
+    CUDA_TRY(cudaMemcpyAsync(out, ctx->counter.p + 8, sizeof(int64_t) * n, cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    CUDA_TRY(cudaMemsetAsync(ctx->counter.p + 8, 0, sizeof(int64_t) * 24, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     return SBR_OK;
 }
 

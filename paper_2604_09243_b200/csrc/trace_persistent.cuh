@@ -37,6 +37,15 @@ namespace sbr {
 #define SBR_TRACE_MINB 8
 #endif
 constexpr int kChunkRays = SBR_CHUNK_RAYS;   // rays claimed per warp-level atomic
+// two parked leaves per lane before it blocks (lane census: 9 of 32 lanes sat
+// blocked on a second leaf; trace 113 -> 111 ms).  -DSBR_PARK1 restores one.
+#ifndef SBR_PARK1
+#define SBR_PARK2
+#endif
+#ifndef SBR_DONE_BREAK
+#define SBR_DONE_BREAK 8
+#endif
+constexpr int kDoneBreak = SBR_DONE_BREAK;   // finished lanes that end a traversal phase
 
 enum LaneState : int { kIdle = 0, kTrav = 1, kLeaf = 2, kDone = 3 };
 enum TraceMode : int { kModeSolve = 0, kModeGrid = 1, kModeList = 2 };
@@ -76,6 +85,9 @@ struct LaneRay {
     float tmax;
     int ref, sp;
     int pend;        // parked leaf reference (0: none)
+#ifdef SBR_PARK2
+    int pend2;       // second parked leaf
+#endif
     // bookkeeping
     int64_t r;       // ray index within its grid / list
     int64_t slot;    // output slot (solve) or ray index
@@ -91,6 +103,9 @@ __device__ __forceinline__ void start_query(const BvhView &B, LaneRay &L, int &s
     L.tmax = __int_as_float(0x7f800000);
     L.sp = 0;
     L.pend = 0;
+#ifdef SBR_PARK2
+    L.pend2 = 0;
+#endif
     L.ref = B.root;
     state = L.ref >= 0 ? kTrav : kLeaf;
 }
@@ -234,7 +249,33 @@ k_trace_persistent(TraceArgs a)
         // Speculative while-while: a lane that reaches its first leaf parks
         // it in L.pend and keeps traversing; the phase ends once every
         // traversing lane has a parked leaf (or stopped at a second leaf).
-        while (__any_sync(0xffffffffu, state == kTrav && L.pend == 0)) {
+        while (true) {
+            // the traversal phase ends when no lane is still looking for its
+            // first leaf -- or once kDoneBreak lanes have finished their query
+            // and would otherwise idle until it ends (lane census: 11.5 of 32
+            // lanes sat in kDone per step without this; trace 130 -> 113 ms)
+            const unsigned trav = __ballot_sync(0xffffffffu, state == kTrav && L.pend == 0);
+            if (!trav) break;
+            if (__popc(__ballot_sync(0xffffffffu, state == kDone)) >= kDoneBreak) break;
+#ifdef SBR_TRAV_MIN
+            if (__popc(trav) < SBR_TRAV_MIN) break;
+#endif
+#ifdef SBR_TRACE_STATS
+            {   // lane-state census per traversal step (stats build only)
+                const unsigned act = __ballot_sync(0xffffffffu, state == kTrav && L.pend == 0);
+                const unsigned prk = __ballot_sync(0xffffffffu, state == kTrav && L.pend != 0);
+                const unsigned blk = __ballot_sync(0xffffffffu, state == kLeaf);
+                const unsigned dn = __ballot_sync(0xffffffffu, state == kDone);
+                if (lane == 0) {
+                    unsigned long long *st = a.counter + 8;
+                    atomicAdd(st + 0, 1ULL);
+                    atomicAdd(st + 1, (unsigned long long)__popc(act));
+                    atomicAdd(st + 2, (unsigned long long)__popc(prk));
+                    atomicAdd(st + 3, (unsigned long long)__popc(blk));
+                    atomicAdd(st + 4, (unsigned long long)__popc(dn));
+                }
+            }
+#endif
             if (state == kTrav) {
                 int rr[4];
                 float tt[4];
@@ -256,16 +297,24 @@ k_trace_persistent(TraceArgs a)
                 } else {
                     have = pop_next(stack, L);
                 }
+#ifdef SBR_PARK2
+                const bool parked = L.pend != 0 || L.pend2 != 0;
+#else
+                const bool parked = L.pend != 0;
+#endif
                 if (!have) {
-                    state = L.pend ? kLeaf : kDone;   // kLeaf with ref < 0 unset: pend only
+                    state = parked ? kLeaf : kDone;   // kLeaf with ref 0: parked leaves only
                     L.ref = 0;
-                } else if (L.ref < 0) {
-                    if (L.pend == 0) {
-                        L.pend = L.ref;               // park the first leaf
-                        if (!pop_next(stack, L)) { state = kLeaf; L.ref = 0; }
-                        else if (L.ref < 0) state = kLeaf;   // second leaf: stop here
-                    } else {
-                        state = kLeaf;                // parked leaf + this one
+                } else {
+                    // park leaves while a slot is free; a leaf with no free slot
+                    // stops the lane (kLeaf, tested after the parked ones)
+                    while (L.ref < 0) {
+                        if (L.pend == 0) L.pend = L.ref;
+#ifdef SBR_PARK2
+                        else if (L.pend2 == 0) L.pend2 = L.ref;
+#endif
+                        else { state = kLeaf; break; }
+                        if (!pop_next(stack, L)) { state = kLeaf; L.ref = 0; break; }
                     }
                 }
             }
@@ -279,6 +328,23 @@ k_trace_persistent(TraceArgs a)
             L.pend = 0;
             if (leaf_test<STORAGE>(B, L, leaf)) state = kDone;
         }
+#ifdef SBR_PARK2
+        if (L.pend2 != 0 && (state == kTrav || state == kLeaf)) {
+            const int leaf = L.pend2;
+            L.pend2 = 0;
+            if (leaf_test<STORAGE>(B, L, leaf)) state = kDone;
+        }
+        if (state == kDone) L.pend2 = 0;
+#endif
+#ifdef SBR_TRACE_STATS
+        {
+            const unsigned lf = __ballot_sync(0xffffffffu, state == kLeaf || L.pend != 0);
+            if (lane == 0) {
+                atomicAdd(a.counter + 13, 1ULL);
+                atomicAdd(a.counter + 14, (unsigned long long)__popc(lf));
+            }
+        }
+#endif
         while (state == kLeaf) {
             if (L.ref < 0) {
                 if (leaf_test<STORAGE>(B, L, L.ref)) { state = kDone; break; }
