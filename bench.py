@@ -181,14 +181,14 @@ def run_reference(args):
     scene, eps, build_s, phis = cpu_sample(mesh, lam, cfg)
     cores = os.cpu_count() or 1
     for _ in range(max(args.warmup, 0)):
-        cpu_run(scene, eps, lam, phis[:1], 4, 8)
+        cpu_run(scene, eps, lam, phis[:1], 4, 32)
     q = r = 0
     t = 0.0
     for s in range(args.steps):
-        qq, rr, tt = cpu_run(scene, eps, lam, [phis[s % len(phis)]], 8, 8)
+        qq, rr, tt = cpu_run(scene, eps, lam, [phis[s % len(phis)]], 8, 32)
         q += qq; r += rr; t += tt
     value = q / t
-    sample = (f"{args.steps} steps x 1 azimuth x 8 row bands of 8 rows ({r} rays, {q} queries) "
+    sample = (f"{args.steps} steps x 1 azimuth x 8 row bands of 32 rows ({r} rays, {q} queries) "
               f"of the C4 sweep; reference SAH tree built in {build_s:.2f} s (not timed)")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
@@ -376,10 +376,10 @@ def main():
         line["e2e"] = e2e
     if world == 1 and not args.no_cpu:
         scene, eps, build_s, phis = cpu_sample(mesh, lam, cfg)
-        q, r, t = cpu_run(scene, eps, lam, phis, 8, 16)
+        q, r, t = cpu_run(scene, eps, lam, phis, 8, 32)
         line["cpu_baseline"] = {
             "value": q / t, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port",
-            "sample": f"{len(phis)} azimuths x 8 row bands of 16 rows ({r} rays, {q} queries) "
+            "sample": f"{len(phis)} azimuths x 8 row bands of 32 rows ({r} rays, {q} queries) "
                       f"of the same sweep, reference SAH tree (built in {build_s:.2f} s, not "
                       "timed), oracle/ C port of the numba kernels, OpenMP all cores"}
     print(json.dumps(line), flush=True)
