@@ -464,3 +464,40 @@ def test_gpu_sah_build_matches_oracle_large(orc, case):
                        with_ids=True)
     for k in ("valid", "path", "bounces", "tri_ids", "out_dir"):
         assert np.array_equal(getattr(a, k), getattr(b, k)), (case, k)
+
+
+def test_l2_probe_and_debug_counters():
+    import ctypes
+    from paper_2604_09243_b200 import _native as nat
+    ctx = nat.context()
+    g = nat.c_dbl()
+    nat.check(ctx.lib.sbr_probe_l2_bandwidth(ctx.handle, 8 << 20, 2, ctypes.byref(g)))
+    assert g.value > 100.0          # GB/s; the measured peak lives in profiles/l2_peak.json
+    buf = np.ones(24, np.int64)
+    nat.check(ctx.lib.sbr_ctx_debug_counters(ctx.handle, nat.ptr(buf), 24))
+    assert (buf >= 0).all()         # zeros unless built with -DSBR_TRACE_STATS
+
+
+def test_sah_build_handles_leaf_roots_and_coincident_centroids():
+    """A 1-triangle mesh (leaf root) and a stack of coincident triangles (no
+    admissible split: one big leaf) take the host conversion path; the tree
+    is still the reference's and traversal still matches the LBVH."""
+    tri = np.array([[[0.0, 0, 0], [1, 0, 0], [0, 1, 0]]])
+    m1 = sbr.mesh_from_soup(tri)
+    t1 = sbr.build(m1, sbr.BuildParams(split_rule="sah"))
+    assert t1.node_count.tolist() == [1] and t1.max_depth_seen == 0
+    # 200 copies of one triangle at slightly different heights along z: all
+    # centroids share x, y -> splits along z only; plus 100 exact duplicates
+    base = np.array([[0.0, 0, 0], [1, 0, 0], [0, 1, 0]])
+    stack = [base + [0, 0, 0.001 * k] for k in range(200)] + [base + [0, 0, 5.0]] * 100
+    m2 = sbr.mesh_from_soup(np.array(stack))
+    t2 = sbr.build(m2, sbr.BuildParams(split_rule="sah"))
+    t2.validate(m2)
+    assert int(t2.node_count.max()) >= 100      # the duplicates end in one leaf
+    grid = sbr.build_aperture(m2.aabb, sbr.IncidentDirection(0.3, 0.2), 0.02, wavelength=0.1)
+    tp = sbr.TraceParams(max_bounces=3)
+    a = sbr.trace_grid(t2, m2, grid, tp, with_ids=True)
+    b = sbr.trace_grid(sbr.build(m2, sbr.BuildParams(split_rule="lbvh")), m2, grid, tp,
+                       with_ids=True)
+    for k in ("valid", "path", "bounces", "tri_ids"):
+        assert np.array_equal(getattr(a, k), getattr(b, k)), k
