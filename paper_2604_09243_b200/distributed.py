@@ -58,12 +58,19 @@ def reduce_partials(seg, diag, root: int = 0, group=None):
     import torch
     import torch.distributed as dist
     stride = diag.shape[1]
-    maxb = diag[:, 2].clone()
-    dist.reduce(seg, dst=root, op=dist.ReduceOp.SUM, group=group)
-    dist.reduce(diag, dst=root, op=dist.ReduceOp.SUM, group=group)
+    # gloo reduces host tensors only: stage device buffers through the host
+    # (a CPU process group driving GPUs, e.g. several ranks sharing one GPU)
+    staged = dist.get_backend(group) == "gloo" and seg.is_cuda
+    s, d = (seg.cpu(), diag.cpu()) if staged else (seg, diag)
+    maxb = d[:, 2].clone()
+    dist.reduce(s, dst=root, op=dist.ReduceOp.SUM, group=group)
+    dist.reduce(d, dst=root, op=dist.ReduceOp.SUM, group=group)
     dist.reduce(maxb, dst=root, op=dist.ReduceOp.MAX, group=group)
     if dist.get_rank(group) == root:
-        diag[:, 2] = maxb
+        d[:, 2] = maxb
+        if staged:
+            seg.copy_(s)
+            diag.copy_(d)
     assert stride == diag.shape[1]
     return seg, diag
 

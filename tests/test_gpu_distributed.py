@@ -1,0 +1,81 @@
+"""The multi-GPU driver end to end on the GPU box: two ranks (processes)
+share cuda:0 over a gloo group, each traces its shard with sbr_solve_shard,
+one disjoint-support reduce combines them; the result must equal the
+single-process solve bit for bit, for both shard modes and run_sweep."""
+
+import math
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _case():
+    import paper_2604_09243_b200 as sbr
+    from paper_2604_09243_b200 import meshgen
+    mesh = meshgen.generate_aircraft(density=0.03)
+    lam = 0.05
+    grids = [sbr.build_aperture(mesh.aabb, sbr.IncidentDirection(math.pi / 2, ph), lam / 5,
+                                wavelength=lam) for ph in np.linspace(0.0, 3.0, 5)]
+    return sbr, mesh, grids, sbr.TraceParams(max_bounces=4), 2 * np.pi / (lam * np.linspace(0.98, 1.02, 3))
+
+
+def _worker(rank, world, port, mode, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2604_09243_b200 import distributed as D
+    sbr, mesh, grids, tp, ks = _case()
+    tree = sbr.build(mesh)
+    res = D.solve_grids_distributed(tree, mesh, grids, tp, ks, shard_mode=mode)
+    cfg = sbr.SweepConfig(mesh_path="x", frequency_hz=6e9,
+                          theta=sbr.AngleRange(math.pi / 2, math.pi / 2, 1),
+                          phi=sbr.AngleRange(0.0, 1.0, 3), max_bounces=3)
+    sw = D.run_sweep_distributed(cfg, mesh, shard_mode=mode)
+    if rank == 0:
+        q.put((res.amplitude, res.valid_rays, res.bounce_counts, res.queries, sw.amplitude,
+               sw.valid_rays, sw.bounce_histogram))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode", ["angles", "rays"])
+def test_two_ranks_equal_one(mode):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, mode, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    sbr, mesh, grids, tp, ks = _case()
+    tree = sbr.build(mesh)
+    ref = sbr.solve_grids(tree, mesh, grids, tp, ks)
+    assert np.array_equal(got[0], ref.amplitude)          # bit-identical
+    assert np.array_equal(got[1], ref.valid_rays)
+    assert np.array_equal(got[2], ref.bounce_counts)
+    assert np.array_equal(got[3], ref.queries)
+    cfg = sbr.SweepConfig(mesh_path="x", frequency_hz=6e9,
+                          theta=sbr.AngleRange(math.pi / 2, math.pi / 2, 1),
+                          phi=sbr.AngleRange(0.0, 1.0, 3), max_bounces=3)
+    sw = sbr.run_sweep(cfg, mesh)
+    assert np.array_equal(got[4], sw.amplitude)
+    assert np.array_equal(got[5], sw.valid_rays)
+    assert np.array_equal(got[6], sw.bounce_histogram)
