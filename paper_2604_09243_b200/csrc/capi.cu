@@ -138,6 +138,8 @@ struct sbr_bvh {
         BvhView v;
         v.nodes = out.nodes.p;
         v.nodes4 = out.nodes4.p;
+        v.nodes8 = out.nodes8.p;
+        v.width = out.width;
         v.tri32 = out.tri32.p;
         v.tri64 = out.tri64.p;
         v.normals = mesh->normals.p;
@@ -158,6 +160,7 @@ static int set_device(sbr_ctx *ctx)
 // per-thread stack (kStack); deletes the handle on failure
 static int check_depth(sbr_bvh *b)
 {
+    if (b->out.width == 8 && 7 * b->out.depth8 + 1 >= kStack) b->out.width = 4;  // stack bound
     if (b->out.depth4 <= kMaxDepth4) return SBR_OK;
     const int d = b->out.depth4;
     delete b;
@@ -514,6 +517,7 @@ static int upload_ref_tree(sbr_ctx *ctx, const sbr_mesh *mesh, const double *nod
     b->out.storage = mesh->storage;
     e = collapse_bvh4(b->out, ctx->ws, ctx->stream, &ctx->launches);
     if (e != cudaSuccess) return fail(SBR_ECUDA, "BVH upload: %s", cudaGetErrorString(e));
+    if (b->out.width == 8 && 7 * b->out.depth8 + 1 >= kStack) b->out.width = 4;  // stack bound
     if (b->out.depth4 > kMaxDepth4)
         return fail(SBR_EINVAL, "BVH4 depth %d exceeds the traversal stack limit (%d)",
                     b->out.depth4, kMaxDepth4);
@@ -604,6 +608,7 @@ static int build_sah(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_build_params 
     if (timing)
         fprintf(stderr, "[sah] build+convert %.2f ms, pack+bvh4 %.2f ms, nodes %lld\n",
                 ms(t0, t1), ms(t1, now()), (long long)T.nnodes);
+    if (b->out.width == 8 && 7 * b->out.depth8 + 1 >= kStack) b->out.width = 4;  // stack bound
     if (b->out.depth4 > kMaxDepth4)
         return fail(SBR_EINVAL, "BVH4 depth %d exceeds the traversal stack limit (%d)",
                     b->out.depth4, kMaxDepth4);

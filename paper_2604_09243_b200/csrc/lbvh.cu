@@ -22,6 +22,7 @@
 #include <cstring>
 
 #include <cub/cub.cuh>
+#include <cstdlib>
 
 #include "lbvh.h"
 
@@ -493,7 +494,9 @@ __device__ __forceinline__ float half_area(const float b[6])
     return dx * dy + dy * dz + dz * dx;
 }
 
-// pass A: open up to four descendants of each item, count internal ones
+// pass A: open up to W descendants of each item (greedily the child with the
+// largest surface area), count internal ones
+template <int W>
 __global__ void k_collapse_open(const Node *__restrict__ bvh2, const int *__restrict__ items,
                                 int n_items, int *__restrict__ cref, float *__restrict__ cbox,
                                 int *__restrict__ cnt)
@@ -501,14 +504,14 @@ __global__ void k_collapse_open(const Node *__restrict__ bvh2, const int *__rest
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_items) return;
     const Node x = bvh2[items[i]];
-    int ref[4];
-    float box[4][6];
+    int ref[W];
+    float box[W][6];
     ref[0] = x.d.x;
     ref[1] = x.d.y;
     child_box(x, 0, box[0]);
     child_box(x, 1, box[1]);
     int n = 2;
-    while (n < 4) {
+    while (n < W) {
         int pick = -1;
         float best = -1.f;
         for (int k = 0; k < n; ++k)
@@ -525,34 +528,32 @@ __global__ void k_collapse_open(const Node *__restrict__ bvh2, const int *__rest
         ++n;
     }
     int internal = 0;
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < W; ++k) {
         const bool have = k < n;
-        cref[4 * i + k] = have ? ref[k] : kEmptyRef;
-        for (int q = 0; q < 6; ++q) cbox[24 * i + 6 * k + q] = have ? box[k][q] : 0.f;
+        cref[W * i + k] = have ? ref[k] : kEmptyRef;
+        for (int q = 0; q < 6; ++q) cbox[6 * W * i + 6 * k + q] = have ? box[k][q] : 0.f;
         internal += (have && ref[k] >= 0) ? 1 : 0;
     }
     cnt[i] = internal;
 }
 
-// pass B: write the BVH4 nodes, allocate (by prefix offset) and enqueue the
+// pass B: write the wide nodes, allocate (by prefix offset) and enqueue the
 // internal children as the next level
+template <int W>
 __global__ void k_collapse_emit(const int *__restrict__ cref, const float *__restrict__ cbox,
                                 const int *__restrict__ off, const int *__restrict__ out_idx,
-                                int n_items, int next_base, Node4 *__restrict__ out,
+                                int n_items, int next_base,
+                                typename WideNode<W>::T *__restrict__ out,
                                 int *__restrict__ next_items, int *__restrict__ next_out)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_items) return;
-    Node4 nd;
-    int r[4];
-    float lo[3][4], hi[3][4];
+    float pl[6][W];     // lox loy loz hix hiy hiz planes
+    int r[W];
     int j = off[i];
-    for (int k = 0; k < 4; ++k) {
-        int c = cref[4 * i + k];
-        for (int a = 0; a < 3; ++a) {
-            lo[a][k] = cbox[24 * i + 6 * k + a];
-            hi[a][k] = cbox[24 * i + 6 * k + 3 + a];
-        }
+    for (int k = 0; k < W; ++k) {
+        int c = cref[W * i + k];
+        for (int q = 0; q < 6; ++q) pl[q][k] = cbox[6 * W * i + 6 * k + q];
         if (c >= 0 && c != kEmptyRef) {
             next_items[j] = c;
             next_out[j] = next_base + j;
@@ -561,44 +562,49 @@ __global__ void k_collapse_emit(const int *__restrict__ cref, const float *__res
         }
         r[k] = c;
     }
-    nd.lox = make_float4(lo[0][0], lo[0][1], lo[0][2], lo[0][3]);
-    nd.loy = make_float4(lo[1][0], lo[1][1], lo[1][2], lo[1][3]);
-    nd.loz = make_float4(lo[2][0], lo[2][1], lo[2][2], lo[2][3]);
-    nd.hix = make_float4(hi[0][0], hi[0][1], hi[0][2], hi[0][3]);
-    nd.hiy = make_float4(hi[1][0], hi[1][1], hi[1][2], hi[1][3]);
-    nd.hiz = make_float4(hi[2][0], hi[2][1], hi[2][2], hi[2][3]);
-    nd.ref = make_int4(r[0], r[1], r[2], r[3]);
-    nd.pad = make_int4(0, 0, 0, 0);
+    // SoA planes: W/4 float4 per plane, then W/4 int4 refs, then padding
+    typename WideNode<W>::T nd;
+    float4 *f = reinterpret_cast<float4 *>(&nd);
+    for (int q = 0; q < 6; ++q)
+        for (int h = 0; h < W / 4; ++h)
+            f[q * (W / 4) + h] = make_float4(pl[q][4 * h], pl[q][4 * h + 1], pl[q][4 * h + 2],
+                                             pl[q][4 * h + 3]);
+    int4 *ri = reinterpret_cast<int4 *>(f + 6 * (W / 4));
+    for (int h = 0; h < W / 4; ++h) {
+        ri[h] = make_int4(r[4 * h], r[4 * h + 1], r[4 * h + 2], r[4 * h + 3]);
+        ri[W / 4 + h] = make_int4(0, 0, 0, 0);
+    }
     out[out_idx[i]] = nd;
 }
 
-cudaError_t collapse_bvh4(LbvhOutput &out, Arena &ws, cudaStream_t st, int64_t *launches)
+template <int W>
+static cudaError_t collapse_wide(LbvhOutput &out, typename WideNode<W>::T **dst, int64_t &nn,
+                                 int &depth, Arena &ws, cudaStream_t st, int64_t *launches)
 {
     const int n2 = (int)out.nnodes;
     size_t scan_bytes = 0;
     CK(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (int *)nullptr, (int *)nullptr, n2,
                                      st));
-    CK(ws.reserve(256 * 12 + (size_t)n2 * (4 * 4 + 4 * 4 + 24 * 4 + 4 * 2) + scan_bytes + 64));
+    CK(ws.reserve(256 * 12 + (size_t)n2 * (4 * 4 + W * 4 + 6 * W * 4 + 4 * 2) + scan_bytes + 64));
     int *items[2] = {ws.take<int>(n2), ws.take<int>(n2)};
     int *outs[2] = {ws.take<int>(n2), ws.take<int>(n2)};
-    int *cref = ws.take<int>(4 * (size_t)n2);
-    float *cbox = ws.take<float>(24 * (size_t)n2);
+    int *cref = ws.take<int>((size_t)W * n2);
+    float *cbox = ws.take<float>((size_t)6 * W * n2);
     int *cnt = ws.take<int>(n2), *off = ws.take<int>(n2);
     unsigned char *scan_tmp = ws.take<unsigned char>(scan_bytes);
-    CK(out.nodes4.alloc(n2));
     const int zero = 0;
     CK(cudaMemcpyAsync(items[0], &out.root, sizeof(int), cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(outs[0], &zero, sizeof(int), cudaMemcpyHostToDevice, st));
     int n_items = 1, next_base = 1, level = 0, cur = 0;
     while (n_items > 0) {
         const unsigned nb = (unsigned)((n_items + 127) / 128);
-        k_collapse_open<<<nb, 128, 0, st>>>(out.nodes.p, items[cur], n_items, cref, cbox, cnt);
+        k_collapse_open<W><<<nb, 128, 0, st>>>(out.nodes.p, items[cur], n_items, cref, cbox, cnt);
         ++*launches;
         CK(cudaGetLastError());
         CK(cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, cnt, off, n_items, st));
         ++*launches;
-        k_collapse_emit<<<nb, 128, 0, st>>>(cref, cbox, off, outs[cur], n_items, next_base,
-                                            out.nodes4.p, items[cur ^ 1], outs[cur ^ 1]);
+        k_collapse_emit<W><<<nb, 128, 0, st>>>(cref, cbox, off, outs[cur], n_items, next_base,
+                                               *dst, items[cur ^ 1], outs[cur ^ 1]);
         ++*launches;
         CK(cudaGetLastError());
         int last_off = 0, last_cnt = 0;
@@ -611,8 +617,32 @@ cudaError_t collapse_bvh4(LbvhOutput &out, Arena &ws, cudaStream_t st, int64_t *
         cur ^= 1;
         ++level;
     }
-    out.nnodes4 = next_base;
-    out.depth4 = level - 1;
+    nn = next_base;
+    depth = level - 1;
+    return cudaSuccess;
+}
+
+// the traversal tree width: 4 unless SBR_WIDTH=8
+int traversal_width()
+{
+    const char *s = getenv("SBR_WIDTH");
+    return (s && atoi(s) == 8) ? 8 : 4;
+}
+
+cudaError_t collapse_bvh4(LbvhOutput &out, Arena &ws, cudaStream_t st, int64_t *launches)
+{
+    const int n2 = (int)out.nnodes;
+    CK(out.nodes4.alloc(n2));
+    Node4 *p4 = out.nodes4.p;
+    CK(collapse_wide<4>(out, &p4, out.nnodes4, out.depth4, ws, st, launches));
+    out.width = traversal_width();
+    if (out.width == 8) {
+        CK(out.nodes8.alloc(n2));
+        Node8 *p8 = out.nodes8.p;
+        int d8 = 0;
+        CK(collapse_wide<8>(out, &p8, out.nnodes8, d8, ws, st, launches));
+        out.depth8 = d8;
+    }
     return cudaSuccess;
 }
 

@@ -125,6 +125,11 @@ struct LbvhOutput {
     DevBuf<Node4> nodes4;
     int64_t nnodes4 = 0;
     int depth4 = 0;
+    // optional 8-wide traversal tree (SBR_WIDTH=8)
+    DevBuf<Node8> nodes8;
+    int64_t nnodes8 = 0;
+    int depth8 = 0;
+    int width = 4;
 };
 
 // Collapse the binary tree in out.nodes into out.nodes4: every BVH4 node

@@ -528,8 +528,13 @@ static int persistent_blocks(K kernel, int threads, int num_sms)
 template <int S, int M>
 static void trace_dispatch(const TraceArgs &a, cudaStream_t st, int num_sms)
 {
-    int nb = persistent_blocks(k_trace_persistent<S, M>, kTraceThreads, num_sms);
-    k_trace_persistent<S, M><<<nb, kTraceThreads, 0, st>>>(a);
+    if (a.cfg.B.width == 8 && a.cfg.B.nodes8) {
+        int nb = persistent_blocks(k_trace_persistent<S, M, 8>, kTraceThreads, num_sms);
+        k_trace_persistent<S, M, 8><<<nb, kTraceThreads, 0, st>>>(a);
+    } else {
+        int nb = persistent_blocks(k_trace_persistent<S, M, 4>, kTraceThreads, num_sms);
+        k_trace_persistent<S, M, 4><<<nb, kTraceThreads, 0, st>>>(a);
+    }
 }
 
 template <int M>

@@ -47,6 +47,15 @@ struct __align__(128) Node4 {
 };
 constexpr int kEmptyRef = 0x7fffffff;
 
+// 8-wide node, 256 B = two cache lines: the same SoA planes with eight
+// children each (two float4 per plane), eight refs, padding.
+struct __align__(128) Node8 {
+    float4 lox[2], loy[2], loz[2], hix[2], hiy[2], hiz[2];
+    int4 ref[2];
+    int4 pad[2];
+};
+static_assert(sizeof(Node8) == 256, "Node8 is two lines");
+
 constexpr int kLeafCountShift = 25;
 constexpr int kLeafFirstMask = (1 << kLeafCountShift) - 1;
 constexpr int kMaxLeafCount = 63;
@@ -70,6 +79,8 @@ enum Storage : int { kF32Exact = 1, kF64 = 2, kSingle = 3 };
 struct BvhView {
     const Node *nodes;       // binary tree (build / export)
     const Node4 *nodes4;     // 4-wide tree (traversal)
+    const Node8 *nodes8;     // 8-wide tree (traversal when width == 8)
+    int width;               // 4 or 8: which wide tree the trace kernel walks
     const float4 *tri32;
     const double2 *tri64;
     const double *normals;   // (T,3), original triangle order
@@ -295,5 +306,75 @@ __device__ __forceinline__ int node4_visit(const Node4 *np, const RayBox &r, flo
 #endif
     return n;
 }
+
+// Visit one BVH8 node: eight padded slab tests (two float4 per plane), hit
+// children sorted near -> far by an optimal 19-comparator network; misses
+// (+inf) sink to the end.  Returns the hit count.
+__device__ __forceinline__ int node8_visit(const Node8 *np, const RayBox &r, float tmax,
+                                           int ref[8], float tn[8])
+{
+    const float4 *q = reinterpret_cast<const float4 *>(np);
+    const int nxi = r.sel & 7, nyi = (r.sel >> 3) & 7, nzi = (r.sel >> 6) & 7;
+    const float inf = __int_as_float(0x7f800000);
+    int n = 0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const float4 nxv = __ldg(q + 2 * nxi + h), fxv = __ldg(q + 2 * (3 - nxi) + h);
+        const float4 nyv = __ldg(q + 2 * nyi + h), fyv = __ldg(q + 2 * (5 - nyi) + h);
+        const float4 nzv = __ldg(q + 2 * nzi + h), fzv = __ldg(q + 2 * (7 - nzi) + h);
+        const int4 rf = __ldg(&np->ref[h]);
+#define SBR_SLAB8(c, k)                                                                    \
+        {                                                                                  \
+            const float a = fmaxf(fmaxf(fmaf(nxv.c, r.ix, r.nx), fmaf(nyv.c, r.iy, r.ny)), \
+                                  fmaxf(fmaf(nzv.c, r.iz, r.nz), 0.0f));                   \
+            const float b = fminf(fminf(fmaf(fxv.c, r.ix, r.fx), fmaf(fyv.c, r.iy, r.fy)), \
+                                  fminf(fmaf(fzv.c, r.iz, r.fz), tmax));                   \
+            tn[4 * h + k] = (a <= b && rf.c != kEmptyRef) ? a : inf;                       \
+            ref[4 * h + k] = rf.c;                                                         \
+            n += tn[4 * h + k] != inf;                                                     \
+        }
+        SBR_SLAB8(x, 0)
+        SBR_SLAB8(y, 1)
+        SBR_SLAB8(z, 2)
+        SBR_SLAB8(w, 3)
+#undef SBR_SLAB8
+    }
+#define SBR_CS(i, j) cswap(tn[i], ref[i], tn[j], ref[j]);
+#ifdef SBR_W8_NEAREST
+    // nearest child to slot 0 (7 compare-exchanges); the rest unordered,
+    // misses anywhere in 1..7 (callers test tn != inf)
+    SBR_CS(0, 1) SBR_CS(2, 3) SBR_CS(4, 5) SBR_CS(6, 7)
+    SBR_CS(0, 2) SBR_CS(4, 6)
+    SBR_CS(0, 4)
+#else
+    SBR_CS(0, 2) SBR_CS(1, 3) SBR_CS(4, 6) SBR_CS(5, 7)
+    SBR_CS(0, 4) SBR_CS(1, 5) SBR_CS(2, 6) SBR_CS(3, 7)
+    SBR_CS(0, 1) SBR_CS(2, 3) SBR_CS(4, 5) SBR_CS(6, 7)
+    SBR_CS(2, 4) SBR_CS(3, 5)
+    SBR_CS(1, 4) SBR_CS(3, 6)
+    SBR_CS(1, 2) SBR_CS(3, 4) SBR_CS(5, 6)
+#endif
+#undef SBR_CS
+    return n;
+}
+
+// width-generic visit used by the traversal loops
+template <int W> struct WideNode;
+template <> struct WideNode<4> {
+    using T = Node4;
+    static __device__ __forceinline__ int visit(const Node4 *p, const RayBox &r, float tmax,
+                                                int *ref, float *tn)
+    {
+        return node4_visit(p, r, tmax, ref, tn);
+    }
+};
+template <> struct WideNode<8> {
+    using T = Node8;
+    static __device__ __forceinline__ int visit(const Node8 *p, const RayBox &r, float tmax,
+                                                int *ref, float *tn)
+    {
+        return node8_visit(p, r, tmax, ref, tn);
+    }
+};
 
 }  // namespace sbr

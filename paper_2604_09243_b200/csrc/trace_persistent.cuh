@@ -144,7 +144,11 @@ __device__ __forceinline__ bool pop_next(StackEntry *stack, LaneRay &L)
 // MINB = 8 caps registers at 64 (32 resident warps per SM): measured
 // faster than unconstrained 80-92 registers despite a few spills, since the
 // traversal is latency-bound.
-template <int STORAGE, int MODE, int MINB = SBR_TRACE_MINB>
+template <int W> __device__ __forceinline__ const typename WideNode<W>::T *wide_nodes(const BvhView &B);
+template <> __device__ __forceinline__ const Node4 *wide_nodes<4>(const BvhView &B) { return B.nodes4; }
+template <> __device__ __forceinline__ const Node8 *wide_nodes<8>(const BvhView &B) { return B.nodes8; }
+
+template <int STORAGE, int MODE, int W = 4, int MINB = SBR_TRACE_MINB>
 __global__ void __launch_bounds__(128, MINB)
 k_trace_persistent(TraceArgs a)
 {
@@ -277,14 +281,14 @@ k_trace_persistent(TraceArgs a)
             }
 #endif
             if (state == kTrav) {
-                int rr[4];
-                float tt[4];
-                const int n = node4_visit(B.nodes4 + L.ref, L.rb, L.tmax, rr, tt);
+                int rr[W];
+                float tt[W];
+                const int n = WideNode<W>::visit(wide_nodes<W>(B) + L.ref, L.rb, L.tmax, rr, tt);
                 bool have = true;
                 if (n > 0) {
 #pragma unroll
-                    for (int c = 3; c >= 1; --c)   // farther hits first: nearest pops first
-#ifdef SBR_SORT3
+                    for (int c = W - 1; c >= 1; --c)   // farther hits first: nearest pops first
+#if defined(SBR_SORT3) || defined(SBR_W8_NEAREST)
                         if (tt[c] != __int_as_float(0x7f800000)) {
 #else
                         if (c < n) {
