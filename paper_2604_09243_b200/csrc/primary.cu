@@ -175,10 +175,26 @@ k_raster(RasterArgs a, int64_t ntri_pad)
             count = S.count;
             if (count > kBigTri && a.big) {
                 const long long nch = (count + kBigChunk - 1) / kBigChunk;
-                const unsigned long long at = atomicAdd(a.nbig, (unsigned long long)nch);
-                if (at + nch <= (unsigned long long)a.big_cap) {
+                // sharded / partial batches: queue only chunks whose rows touch
+                // a segment of this launch (ray-tile shards skip 7/8 of them)
+                const int64_t *segs = a.seg_slot + __ldg(&a.seg_base[g]);
+                auto owned = [&](long long c) {
+                    if (!a.sparse) return true;
+                    const long long c1 = (c + 1) * kBigChunk < count ? (c + 1) * kBigChunk : count;
+                    const int64_t r0 = (S.i0 + c * kBigChunk / S.cols) * G.n_v + S.j0;
+                    const int64_t r1 = (S.i0 + (c1 - 1) / S.cols) * G.n_v + S.j0 + S.cols - 1;
+                    for (int64_t q = r0 / kSegRays; q <= r1 / kSegRays; ++q)
+                        if (__ldg(&segs[q]) != kNoSlot) return true;
+                    return false;
+                };
+                long long nown = 0;
+                for (long long c = 0; c < nch; ++c) nown += owned(c);
+                const unsigned long long at =
+                    nown ? atomicAdd(a.nbig, (unsigned long long)nown) : 0ULL;
+                if (at + nown <= (unsigned long long)a.big_cap) {
+                    long long w = 0;
                     for (long long c = 0; c < nch; ++c)
-                        a.big[at + c] = make_int4(gl, (int)tri, (int)c, 0);
+                        if (owned(c)) a.big[at + w++] = make_int4(gl, (int)tri, (int)c, 0);
                     count = 0;                          // walked by k_raster_big
                 }
             }
