@@ -6,7 +6,9 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <algorithm>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/sbr200.h"
@@ -95,6 +97,9 @@ struct sbr_ctx {
     double dkturn = 0.0;         // uniform wavenumber step in turns (0: not uniform)
     DevBuf<double2> amp;
     DevBuf<double> stage;        // host->device staging (mesh ingest, records)
+    // pinned double buffer for large host->device uploads (upload_host)
+    unsigned char *pin[2] = {nullptr, nullptr};
+    cudaEvent_t pin_ev[2] = {nullptr, nullptr};
     Arena ws;                    // LBVH build workspace
     SahWork sah;                 // SAH build workspace
     // optional per-kernel CUDA-event timing of the solve pipeline
@@ -107,6 +112,10 @@ struct sbr_ctx {
     {
         for (auto &e : ev)
             if (e) cudaEventDestroy(e);
+        for (int b = 0; b < 2; ++b) {
+            if (pin[b]) cudaFreeHost(pin[b]);
+            if (pin_ev[b]) cudaEventDestroy(pin_ev[b]);
+        }
     }
 };
 
@@ -255,6 +264,53 @@ extern "C" int sbr_ctx_launch_count(sbr_ctx *ctx, int64_t *count_out)
 // ---------------------------------------------------------------------------
 // mesh
 // ---------------------------------------------------------------------------
+// Host (pageable) -> device upload through two pinned 16 MB chunks: host
+// threads copy chunk k+1 into one pinned buffer while the DMA engine moves
+// chunk k from the other (pageable cudaMemcpy runs at ~10 GB/s and
+// serialises the staging copy with the transfer).
+static constexpr size_t kPinChunk = (size_t)16 << 20;
+
+static cudaError_t upload_host(sbr_ctx *ctx, void *dst, const void *src, size_t bytes)
+{
+    if (bytes < ((size_t)4 << 20))
+        return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream);
+    for (int b = 0; b < 2; ++b) {
+        if (!ctx->pin[b]) {
+            cudaError_t e = cudaHostAlloc((void **)&ctx->pin[b], kPinChunk, cudaHostAllocDefault);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->pin_ev[b], cudaEventDisableTiming);
+            if (e != cudaSuccess) {
+                if (ctx->pin[b]) cudaFreeHost(ctx->pin[b]);
+                ctx->pin[b] = nullptr;
+                cudaGetLastError();
+                return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream);
+            }
+            cudaEventRecord(ctx->pin_ev[b], ctx->stream);
+        }
+    }
+    const unsigned hw = std::thread::hardware_concurrency();
+    const int nth = (int)std::max(1u, std::min(8u, hw ? hw : 1u));
+    const unsigned char *s = static_cast<const unsigned char *>(src);
+    unsigned char *d = static_cast<unsigned char *>(dst);
+    int b = 0;
+    for (size_t off = 0; off < bytes; off += kPinChunk, b ^= 1) {
+        const size_t n = std::min(kPinChunk, bytes - off);
+        cudaError_t e = cudaEventSynchronize(ctx->pin_ev[b]);   // buffer b free again
+        if (e != cudaSuccess) return e;
+        std::vector<std::thread> pool;
+        const size_t part = (n + nth - 1) / nth;
+        for (int t = 1; t < nth; ++t) {
+            const size_t a = std::min(n, t * part), z = std::min(n, a + part);
+            if (z > a) pool.emplace_back([=] { memcpy(ctx->pin[b] + a, s + off + a, z - a); });
+        }
+        memcpy(ctx->pin[b], s + off, std::min(n, part));
+        for (auto &th : pool) th.join();
+        e = cudaMemcpyAsync(d + off, ctx->pin[b], n, cudaMemcpyHostToDevice, ctx->stream);
+        if (e == cudaSuccess) e = cudaEventRecord(ctx->pin_ev[b], ctx->stream);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
 extern "C" int sbr_mesh_create(sbr_ctx *ctx, const double *v0, const double *v1,
                                const double *v2, const double *normals, int64_t ntri,
                                int32_t storage, sbr_mesh **out)
@@ -277,17 +333,10 @@ extern "C" int sbr_mesh_create(sbr_ctx *ctx, const double *v0, const double *v1,
     cudaError_t e = m->verts.alloc((size_t)ntri * 9);
     if (e == cudaSuccess) e = m->normals.alloc((size_t)ntri * 3);
     if (e == cudaSuccess) e = ctx->stage.reserve((size_t)ntri * 9);
-    if (e == cudaSuccess)
-        e = cudaMemcpyAsync(ctx->stage.p, v0, 24 * ntri, cudaMemcpyHostToDevice, ctx->stream);
-    if (e == cudaSuccess)
-        e = cudaMemcpyAsync(ctx->stage.p + 3 * ntri, v1, 24 * ntri, cudaMemcpyHostToDevice,
-                            ctx->stream);
-    if (e == cudaSuccess)
-        e = cudaMemcpyAsync(ctx->stage.p + 6 * ntri, v2, 24 * ntri, cudaMemcpyHostToDevice,
-                            ctx->stream);
-    if (e == cudaSuccess)
-        e = cudaMemcpyAsync(m->normals.p, normals, sizeof(double) * 3 * ntri,
-                            cudaMemcpyHostToDevice, ctx->stream);
+    if (e == cudaSuccess) e = upload_host(ctx, ctx->stage.p, v0, 24 * ntri);
+    if (e == cudaSuccess) e = upload_host(ctx, ctx->stage.p + 3 * ntri, v1, 24 * ntri);
+    if (e == cudaSuccess) e = upload_host(ctx, ctx->stage.p + 6 * ntri, v2, 24 * ntri);
+    if (e == cudaSuccess) e = upload_host(ctx, m->normals.p, normals, sizeof(double) * 3 * ntri);
     if (e == cudaSuccess)
         e = mesh_ingest(ctx->stage.p, ntri, m->verts.p, ing, ctx->stream, &ctx->launches);
     if (e != cudaSuccess) {
@@ -1001,24 +1050,15 @@ extern "C" int sbr_segment_layout(const sbr_grid *grids, int32_t ngrids, int64_t
 }
 
 // slots (16 B each) staged per batch: up to 2^30 (16 GB, a whole C4 sweep in
-// one persistent launch, so the kernel drains once per solve), capped at an
-// eighth of the free device memory.  SBR_SLOT_BUDGET overrides (tests use
-// tiny budgets to prove results do not depend on batching).
+// one persistent launch, so the kernels drain once per solve); run_units
+// halves the budget when the device cannot hold a batch.  (Sizing it from
+// cudaMemGetInfo made the batching depend on what the allocator pools
+// happened to hold.)  SBR_SLOT_BUDGET overrides (tests use tiny budgets to
+// prove results do not depend on batching).
 static int64_t slot_budget()
 {
     const char *s = getenv("SBR_SLOT_BUDGET");
-    int64_t v;
-    if (s) {
-        v = atoll(s);
-    } else {
-        size_t free_b = 0, total_b = 0;
-        v = (int64_t)1 << 30;
-        if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
-            const int64_t cap = (int64_t)(free_b / 8 / sizeof(SlotRec));
-            if (cap < v) v = cap;
-        }
-        if (v < ((int64_t)1 << 22)) v = (int64_t)1 << 22;
-    }
+    int64_t v = s ? atoll(s) : ((int64_t)1 << 30);
     if (v < kChunk) v = kChunk;
     return round_chunk(v);
 }
@@ -1056,7 +1096,7 @@ static int run_units(sbr_ctx *ctx, const sbr_bvh *bvh, const std::vector<UnitDev
                      double2 *seg_dev, int64_t *diag_dev)
 {
     cudaStream_t st = ctx->stream;
-    const int64_t budget = slot_budget();
+    int64_t budget = slot_budget();
     const int ngrids = (int)seg_base.size() - 1;
     const bool raster = raster_primary(bvh->mesh->ntri, ngrids);
     std::vector<int64_t> seg_slot;
@@ -1083,9 +1123,21 @@ static int run_units(sbr_ctx *ctx, const sbr_bvh *bvh, const std::vector<UnitDev
             batch.push_back(u);
             ++u1;
         }
-        CUDA_TRY(ctx->slots.reserve(slots));
+        {   // device memory for the batch; on exhaustion retry with half the slots
+            cudaError_t e = ctx->slots.reserve(slots);
+            if (e == cudaSuccess && raster) e = ctx->worklist.reserve(slots);
+            if (e == cudaSuccess) e = ctx->chunk_part.reserve((size_t)(slots / kChunk) * nk);
+            if (e == cudaErrorMemoryAllocation && budget > ((int64_t)1 << 22)) {
+                cudaGetLastError();
+                ctx->slots.release();
+                ctx->worklist.release();
+                ctx->chunk_part.release();
+                budget = round_chunk(budget / 2);
+                continue;
+            }
+            CUDA_TRY(e);
+        }
         CUDA_TRY(ctx->units.reserve(batch.size()));
-        CUDA_TRY(ctx->chunk_part.reserve((size_t)(slots / kChunk) * nk));
         CUDA_TRY(cudaMemcpyAsync(ctx->units.p, batch.data(), sizeof(UnitDev) * batch.size(),
                                  cudaMemcpyHostToDevice, st));
         if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev[0], st));
