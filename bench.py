@@ -138,7 +138,7 @@ class Clocks:
 # ---------------------------------------------------------------------------
 # CPU baseline: the reference algorithm (oracle port) on the host cores
 # ---------------------------------------------------------------------------
-def cpu_sample(mesh, lam, cfg, n_angles_sample=4, bands=8, band_rows=8):
+def cpu_sample(mesh, lam, cfg, n_angles_sample=8, bands=8, band_rows=8):
     """Bounded sample of the same workload through the CPU port of the
     reference kernels (oracle/, test infrastructure): reference SAH tree,
     then trace + PO on row bands of a few azimuths; returns a dict."""
@@ -185,10 +185,11 @@ def run_reference(args):
     q = r = 0
     t = 0.0
     for s in range(args.steps):
-        qq, rr, tt = cpu_run(scene, eps, lam, [phis[s % len(phis)]], 8, 32)
+        qq, rr, tt = cpu_run(scene, eps, lam, phis, 16, 64)
         q += qq; r += rr; t += tt
     value = q / t
-    sample = (f"{args.steps} steps x 1 azimuth x 8 row bands of 32 rows ({r} rays, {q} queries) "
+    sample = (f"{args.steps} steps x {len(phis)} azimuths x 16 row bands of 64 rows ({r} rays, "
+              f"{q} queries) "
               f"of the C4 sweep; reference SAH tree built in {build_s:.2f} s (not timed)")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
@@ -376,10 +377,10 @@ def main():
         line["e2e"] = e2e
     if world == 1 and not args.no_cpu:
         scene, eps, build_s, phis = cpu_sample(mesh, lam, cfg)
-        q, r, t = cpu_run(scene, eps, lam, phis, 8, 32)
+        q, r, t = cpu_run(scene, eps, lam, phis, 16, 64)
         line["cpu_baseline"] = {
             "value": q / t, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port",
-            "sample": f"{len(phis)} azimuths x 8 row bands of 32 rows ({r} rays, {q} queries) "
+            "sample": f"{len(phis)} azimuths x 16 row bands of 64 rows ({r} rays, {q} queries) "
                       f"of the same sweep, reference SAH tree (built in {build_s:.2f} s, not "
                       "timed), oracle/ C port of the numba kernels, OpenMP all cores"}
     print(json.dumps(line), flush=True)
