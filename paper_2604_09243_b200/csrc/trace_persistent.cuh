@@ -165,6 +165,9 @@ k_trace_persistent(TraceArgs a)
     int64_t chunk_next = 0, chunk_end = 0;   // warp-uniform private work range
 
     while (true) {
+#ifdef SBR_TRACE_STATS
+        long long clk0 = clock64();
+#endif
         // ---------------- refill idle lanes -------------------------------
         const unsigned want = __ballot_sync(0xffffffffu, state == kIdle && !exhausted);
         if (want) {
@@ -249,6 +252,9 @@ k_trace_persistent(TraceArgs a)
         }
         if (!__any_sync(0xffffffffu, state != kIdle || !exhausted)) break;
 
+#ifdef SBR_TRACE_STATS
+        long long clk1 = clock64();
+#endif
         // ---------------- traversal phase ---------------------------------
         // Speculative while-while: a lane that reaches its first leaf parks
         // it in L.pend and keeps traversing; the phase ends once every
@@ -324,6 +330,9 @@ k_trace_persistent(TraceArgs a)
             }
         }
 
+#ifdef SBR_TRACE_STATS
+        long long clk2 = clock64();
+#endif
         // ---------------- leaf phase --------------------------------------
         // parked leaf first, then (kLeaf lanes) the leaf in L.ref and any
         // further leaves popped straight off the stack
@@ -357,6 +366,9 @@ k_trace_persistent(TraceArgs a)
             else if (L.ref >= 0) state = kTrav;
         }
 
+#ifdef SBR_TRACE_STATS
+        long long clk3 = clock64();
+#endif
         // ---------------- query completion (transport.py:293-326) ---------
         if (state == kDone) {
             bool finish = false, escaped = false;
@@ -436,6 +448,18 @@ k_trace_persistent(TraceArgs a)
                 state = kIdle;
             }
         }
+#ifdef SBR_TRACE_STATS
+        {   // cycles per phase (warp-uniform points; lane 0 records)
+            __syncwarp();
+            const long long clk4 = clock64();
+            if (lane == 0) {
+                atomicAdd(a.counter + 16, (unsigned long long)(clk1 - clk0));   // refill
+                atomicAdd(a.counter + 17, (unsigned long long)(clk2 - clk1));   // traversal
+                atomicAdd(a.counter + 18, (unsigned long long)(clk3 - clk2));   // leaf
+                atomicAdd(a.counter + 19, (unsigned long long)(clk4 - clk3));   // completion
+            }
+        }
+#endif
     }
 }
 

@@ -26,4 +26,7 @@ out = {"trav_steps": int(buf[0]), "lanes_traversing": buf[1] / it, "lanes_parked
        "leaf_phases": int(buf[5]), "lanes_in_leaf_phase": buf[6] / max(buf[5], 1),
        "trav_steps_per_leaf_phase": buf[0] / max(buf[5], 1),
        "queries": int(res.queries.sum())}
+cyc = buf[8:12].astype(float)
+out["cycle_share"] = dict(zip(("refill", "traversal", "leaf", "completion"),
+                              (cyc / max(cyc.sum(), 1)).round(3).tolist()))
 print(json.dumps(out, indent=1))
