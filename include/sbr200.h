@@ -62,11 +62,11 @@ typedef struct sbr_mesh sbr_mesh;
 typedef struct sbr_bvh sbr_bvh;
 
 /* Replaces bvh.py:22-49 BuildParams.
- *  SBR_SPLIT_SAH:  the reference's binned-SAH tree (bvh.py:154-299), built on
- *                  the GPU level by level and identical node for node
- *                  (sbr_bvh_export returns it verbatim);
- *  SBR_SPLIT_LBVH: a GPU LBVH (Morton order; fastest build);
- *  SBR_SPLIT_MEDIAN: accepted for API parity, built as an LBVH.
+ *  SBR_SPLIT_SAH / SBR_SPLIT_MEDIAN: the reference's binned-SAH
+ *                  (bvh.py:154-215) or median-split (bvh.py:135-151) tree,
+ *                  built on the GPU level by level and identical node for
+ *                  node (sbr_bvh_export returns it verbatim);
+ *  SBR_SPLIT_LBVH: a GPU LBVH (Morton order; fastest build).
  * Closest-hit results do not depend on the tree. */
 enum { SBR_SPLIT_MEDIAN = 0, SBR_SPLIT_SAH = 1, SBR_SPLIT_LBVH = 2 };
 typedef struct {

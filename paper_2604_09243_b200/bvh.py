@@ -287,12 +287,11 @@ def binned_sah_split(tri_min: np.ndarray, tri_max: np.ndarray, centroids: np.nda
 def build(mesh: Mesh, params: BuildParams = BuildParams()) -> Bvh:
     """BVH over the mesh triangles on the GPU (replaces bvh.py:218-299).
 
-    ``split_rule="sah"`` (the reference default) builds the reference's
-    binned-SAH tree on the GPU, node for node identical to bvh.build;
-    ``"lbvh"`` builds a Morton-order LBVH (fastest build); ``"median"`` is
-    accepted for parity and built as an LBVH.  Closest hits are identical
-    for every tree."""
-    if params.split_rule != "sah" and params.n_leaf > 63:
+    ``split_rule="sah"`` (the reference default) and ``"median"`` build the
+    reference's binned-SAH / median-split tree on the GPU, node for node
+    identical to bvh.build; ``"lbvh"`` builds a Morton-order LBVH (fastest
+    build).  Closest hits are identical for every tree."""
+    if params.split_rule == "lbvh" and params.n_leaf > 63:
         raise ValidationError("the LBVH builder supports n_leaf <= 63")
     ctx = nat.context()
     dm = mesh.device(ctx)

@@ -411,7 +411,7 @@ extern "C" int sbr_bvh_build(sbr_ctx *ctx, const sbr_mesh *mesh,
     sbr_bvh *b = new sbr_bvh();
     b->ctx = ctx;
     b->mesh = mesh;
-    if (rule == SBR_SPLIT_SAH) {
+    if (rule == SBR_SPLIT_SAH || rule == SBR_SPLIT_MEDIAN) {
         sbr_build_params p = *params;
         if (int rc = build_sah(ctx, mesh, &p, b)) {
             delete b;
@@ -616,8 +616,9 @@ static int build_sah(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_build_params 
     P.bins = params->bins_per_axis > 0 ? params->bins_per_axis : 16;
     P.c_t = params->c_t > 0.0 ? params->c_t : 1.0;
     P.c_i = params->c_i > 0.0 ? params->c_i : 1.0;
-    REQUIRE(P.bins >= 2 && P.bins <= kSahMaxBins, "bins_per_axis must be in [2, %d]",
-            kSahMaxBins);
+    P.median = params->split_rule == SBR_SPLIT_MEDIAN;
+    REQUIRE(P.median || (P.bins >= 2 && P.bins <= kSahMaxBins),
+            "bins_per_axis must be in [2, %d]", kSahMaxBins);
     const bool timing = getenv("SBR_SAH_TIMING") != nullptr;
     auto now = [] { return std::chrono::steady_clock::now(); };
     auto ms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point z) {

@@ -356,6 +356,69 @@ k_select(const SegAcc *__restrict__ acc, const unsigned int *__restrict__ cnt,
     }
 }
 
+// median split (bvh.py:135-151): split along the longest axis of the node box
+// (np.argmax: first maximum) unless every centroid coincides; the left child
+// takes the n // 2 first elements of the stable (centroid, position) order
+__global__ void k_select_median(const SegAcc *__restrict__ acc, const int64_t *__restrict__ sc,
+                                const int *__restrict__ snode, int S, int depth, SahParams P,
+                                double *__restrict__ node_box, SegSplit *__restrict__ out,
+                                int *__restrict__ split_flag)
+{
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= S) return;
+    const SegAcc &A = acc[s];
+    double lo[3], hi[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        lo[q] = unordd(A.box[q]);
+        hi[q] = unordd(A.box[3 + q]);
+    }
+    double *nb = node_box + 6 * (int64_t)snode[s];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) { nb[q] = lo[q]; nb[3 + q] = hi[q]; }
+    SegSplit r;
+    r.split = 0; r.axis = -1; r.boundary = -1; r.c_lo = 0.0; r.scale = 0.0; r.nl = 0;
+    const int64_t n = sc[s];
+    bool same = true;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) same = same && A.cb[q] == A.cb[3 + q];
+    if (n > P.n_leaf && depth < P.max_depth && !same) {
+        const double e0 = __dsub_rn(hi[0], lo[0]), e1 = __dsub_rn(hi[1], lo[1]),
+                     e2 = __dsub_rn(hi[2], lo[2]);
+        int axis = 0;
+        double best = e0;
+        if (e1 > best) { best = e1; axis = 1; }
+        if (e2 > best) axis = 2;
+        r.split = 1;
+        r.axis = axis;
+        r.nl = n / 2;
+    }
+    out[s] = r;
+    split_flag[s] = r.split;
+}
+
+// sort keys (centroid on the split axis; -0.0 folded onto +0.0 as np.lexsort
+// compares them equal) for elements of split segments
+__global__ void k_median_keys(const double *__restrict__ tb, const int *__restrict__ idx,
+                              const int *__restrict__ eseg, int64_t n,
+                              const SegSplit *__restrict__ sp, double *__restrict__ key)
+{
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int s = eseg[i];
+    key[i] = (s >= 0 && sp[s].split) ? tb[9 * (int64_t)idx[i] + 6 + sp[s].axis] + 0.0 : 0.0;
+}
+
+__global__ void k_split_offsets(int S, const int *__restrict__ sflag, const int *__restrict__ crank,
+                                const int64_t *__restrict__ sb, const int64_t *__restrict__ sc,
+                                int64_t *__restrict__ beg, int64_t *__restrict__ end)
+{
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= S || !sflag[s]) return;
+    beg[crank[s]] = sb[s];
+    end[crank[s]] = sb[s] + sc[s];
+}
+
 __global__ void k_flags(const double *__restrict__ tb, const int *__restrict__ idx,
                         const int *__restrict__ eseg, int64_t n,
                         const SegSplit *__restrict__ sp, int nbins, int *__restrict__ flag)
@@ -594,21 +657,52 @@ cudaError_t sah_build(const double *d_verts, int64_t n, const SahParams &P, SahT
                                                                        w.bbox.p, S, nslots);
         k_seg_of<<<nblk(n, T), T, 0, st>>>(sb, sc, S, n, w.eseg.p);
         k_bounds<<<nblk(n, T), T, 0, st>>>(w.tb.p, idx, w.eseg.p, n, w.acc.p);
-        k_bin<<<nblk(n, T), T, 0, st>>>(w.tb.p, idx, w.eseg.p, n, w.acc.p, B, R, w.cnt.p,
-                                        w.bbox.p);
         CK(cudaMemsetAsync(w.sflag.p + S, 0, sizeof(int), st));
-        k_select<<<nblk(S, kSelWarps), kSelWarps * 32, 0, st>>>(
-            w.acc.p, w.cnt.p, w.bbox.p, sc, snode, S, R, depth, P, w.node_box.p, w.sp.p, w.sflag.p);
-        k_flags<<<nblk(n, T), T, 0, st>>>(w.tb.p, idx, w.eseg.p, n, w.sp.p, B, w.flag.p);
-        CK(cub::DeviceScan::ExclusiveSum(w.scan_tmp.p, scan_bytes, w.flag.p, w.rank.p, (int)n,
-                                         st));
-        k_partition<<<nblk(n, T), T, 0, st>>>(idx, w.eseg.p, n, w.sp.p, sb, w.flag.p, w.rank.p,
-                                              idx2);
-        std::swap(idx, idx2);
+        if (!P.median) {
+            k_bin<<<nblk(n, T), T, 0, st>>>(w.tb.p, idx, w.eseg.p, n, w.acc.p, B, R, w.cnt.p,
+                                            w.bbox.p);
+            k_select<<<nblk(S, kSelWarps), kSelWarps * 32, 0, st>>>(
+                w.acc.p, w.cnt.p, w.bbox.p, sc, snode, S, R, depth, P, w.node_box.p, w.sp.p,
+                w.sflag.p);
+        } else {
+            k_select_median<<<nblk(S, 128), 128, 0, st>>>(w.acc.p, sc, snode, S, depth, P,
+                                                          w.node_box.p, w.sp.p, w.sflag.p);
+        }
         // split flags of the segments -> child slots (exclusive scan; the
         // extra element S receives the total)
         CK(cub::DeviceScan::ExclusiveSum(w.scan_tmp.p, scan_bytes, w.sflag.p, w.crank.p, S + 1,
                                          st));
+        if (!P.median) {
+            k_flags<<<nblk(n, T), T, 0, st>>>(w.tb.p, idx, w.eseg.p, n, w.sp.p, B, w.flag.p);
+            CK(cub::DeviceScan::ExclusiveSum(w.scan_tmp.p, scan_bytes, w.flag.p, w.rank.p,
+                                             (int)n, st));
+            k_partition<<<nblk(n, T), T, 0, st>>>(idx, w.eseg.p, n, w.sp.p, sb, w.flag.p,
+                                                  w.rank.p, idx2);
+        } else {
+            // stable sort of each split segment by its centroid key; the
+            // other positions keep their order
+            int nsp = 0;
+            CK(cudaMemcpyAsync(&nsp, w.crank.p + S, sizeof(int), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            CK(cudaMemcpyAsync(idx2, idx, sizeof(int) * n, cudaMemcpyDeviceToDevice, st));
+            if (nsp > 0) {
+                CK(w.key.reserve(n)); CK(w.key2.reserve(n));
+                CK(w.sbeg.reserve(nsp)); CK(w.send.reserve(nsp));
+                k_median_keys<<<nblk(n, T), T, 0, st>>>(w.tb.p, idx, w.eseg.p, n, w.sp.p,
+                                                        w.key.p);
+                k_split_offsets<<<nblk(S, 128), 128, 0, st>>>(S, w.sflag.p, w.crank.p, sb, sc,
+                                                              w.sbeg.p, w.send.p);
+                size_t need = 0;
+                CK(cub::DeviceSegmentedSort::StableSortPairs(
+                    nullptr, need, w.key.p, w.key2.p, idx, idx2, (int)n, nsp, w.sbeg.p, w.send.p,
+                    st));
+                CK(w.sort_tmp.reserve(need));
+                CK(cub::DeviceSegmentedSort::StableSortPairs(
+                    w.sort_tmp.p, need, w.key.p, w.key2.p, idx, idx2, (int)n, nsp, w.sbeg.p,
+                    w.send.p, st));
+            }
+        }
+        std::swap(idx, idx2);
         k_children<<<nblk(S, 128), 128, 0, st>>>(S, w.sp.p, w.crank.p, sb, sc, snode, node_count,
                                                  w.left.p, w.right.p, w.lf.p, w.lc.p, nsb, nsc,
                                                  nsnode);

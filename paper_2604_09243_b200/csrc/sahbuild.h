@@ -12,6 +12,7 @@ struct SahParams {          // bvh.py:22-49 BuildParams
     int max_depth;
     int bins;               // bins_per_axis, 2..kSahMaxBins
     double c_t, c_i;
+    int median = 0;         // 1: the reference median split (bvh.py:135-151) instead of SAH
 };
 
 // The tree in the reference's preorder layout (bvh.py:58-88), on device:
@@ -46,6 +47,10 @@ struct SahWork {
     DevBuf<SegAcc> acc;
     DevBuf<SegSplit> sp;
     DevBuf<unsigned char> scan_tmp;
+    // median split: per-element keys / values and split-segment offsets
+    DevBuf<double> key, key2;
+    DevBuf<int64_t> sbeg, send;
+    DevBuf<unsigned char> sort_tmp;
 };
 
 // d_verts: (T,9) FP64 vertices in original triangle order.  Leaves the tree

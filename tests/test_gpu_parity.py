@@ -423,33 +423,34 @@ _TREE_KEYS = ("nodes_min", "nodes_max", "node_first", "node_count", "tri_order")
 
 
 @pytest.mark.parametrize("name", golden_names("bvh_"))
-def test_gpu_sah_build_is_the_reference_tree(name):
+@pytest.mark.parametrize("rule", ["sah", "median"])
+def test_gpu_build_is_the_reference_tree(name, rule):
     g = load_golden(name)
     mesh = _mesh(g)
-    tree = sbr.build(mesh, sbr.BuildParams(split_rule="sah"))
+    tree = sbr.build(mesh, sbr.BuildParams(split_rule=rule))
     for k in _TREE_KEYS:
-        ref = g[f"sah_{k}"]
+        ref = g[f"{rule}_{k}"]
         got = getattr(tree, k)
         assert got.dtype == ref.dtype or k in ("node_first", "node_count", "tri_order"), k
         assert np.array_equal(got, ref), k
-    assert tree.max_depth_seen == int(g["sah_max_depth_seen"])
+    assert tree.max_depth_seen == int(g[f"{rule}_max_depth_seen"])
     tree.validate(mesh)
 
 
-@pytest.mark.parametrize("case", ["aircraft", "sphere_s6", "rough", "bins8_leaf2"])
+@pytest.mark.parametrize("case", ["aircraft", "sphere_s6", "rough", "bins8_leaf2", "median"])
 def test_gpu_sah_build_matches_oracle_large(orc, case):
-    params = sbr.BuildParams(split_rule="sah")
+    params = sbr.BuildParams(split_rule="median" if case == "median" else "sah")
     if case == "aircraft":
         mesh = meshgen.generate_aircraft(density=0.08)
     elif case == "sphere_s6":
         mesh = meshgen.quantized_icosphere(1.0, 6)
-    elif case == "rough":
+    elif case in ("rough", "median"):
         mesh = meshgen.perturbed_grid_mesh(cells=150, extent=4.0, amplitude=0.08, seed=3)
     else:
         mesh = meshgen.generate_aircraft(density=0.03)
         params = sbr.BuildParams(split_rule="sah", bins_per_axis=8, n_leaf=2, c_t=0.5, c_i=2.0)
     tree = sbr.build(mesh, params)
-    ref = orc.build(mesh.v0, mesh.v1, mesh.v2, split_rule="sah", n_leaf=params.n_leaf,
+    ref = orc.build(mesh.v0, mesh.v1, mesh.v2, split_rule=params.split_rule, n_leaf=params.n_leaf,
                     bins_per_axis=params.bins_per_axis, c_t=params.c_t, c_i=params.c_i)
     for k in _TREE_KEYS:
         assert np.array_equal(getattr(tree, k), getattr(ref, k)), (case, k)
