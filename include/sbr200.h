@@ -265,6 +265,10 @@ int sbr_obj_free(sbr_obj *obj);
  * (first-seen order, "%.17g"), then one "f a b c" per triangle. */
 int sbr_obj_write(const char *path, const double *v0, const double *v1, const double *v2,
                   int64_t ntri);
+/* transport.py:425-436 dump_hits_csv: one "i,j,valid,nx,ny,nz,R,N" row per
+ * ray of an n_u x n_v grid's HitRecords (record r = i*n_v + j), "%.9g". */
+int sbr_dump_hits_csv(const char *path, int64_t n_u, int64_t n_v, const uint8_t *valid,
+                      const double *normal0, const double *path_len, const int32_t *bounces);
 
 #ifdef __cplusplus
 }

@@ -110,6 +110,7 @@ _SIGS = {
     "sbr_obj_copy": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
     "sbr_obj_free": (ctypes.c_int, [c_vp]),
     "sbr_obj_write": (ctypes.c_int, [ctypes.c_char_p, c_vp, c_vp, c_vp, c_i64]),
+    "sbr_dump_hits_csv": (ctypes.c_int, [ctypes.c_char_p, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "sbr_solve_shard": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_i32,
                                        ctypes.POINTER(TraceParams), c_vp, c_i32, c_dbl, c_i32,
                                        c_i32, c_i32, c_i32, c_vp, c_vp]),

@@ -433,3 +433,58 @@ extern "C" int sbr_obj_write(const char *path, const double *v0, const double *v
     if (fclose(fh) != 0 || !ok) return sbr_fail(SBR_EIO, "%s: write error", path);
     return SBR_OK;
 }
+
+// transport.py:425-436 dump_hits_csv: "i,j,valid,nx,ny,nz,R,N" per ray in
+// record order, Python's "{:.9g}" for the doubles (C "%.9g"; NaN as "nan").
+// Rows are formatted in parallel blocks and written in order.
+extern "C" int sbr_dump_hits_csv(const char *path, int64_t n_u, int64_t n_v,
+                                 const uint8_t *valid, const double *normal0,
+                                 const double *rpath, const int32_t *bounces)
+{
+    if (!path || n_u < 0 || n_v < 0 || (n_u * n_v > 0 && !(valid && normal0 && rpath && bounces)))
+        return sbr_fail(SBR_EINVAL, "NULL argument");
+    FILE *fh = fopen(path, "wb");
+    if (!fh) return sbr_fail(SBR_EIO, "%s: %s", path, strerror(errno));
+    const int64_t n = n_u * n_v;
+    auto g9 = [](double d, char *p) {
+        if (std::isnan(d)) return sprintf(p, "nan");
+        return sprintf(p, "%.9g", d);
+    };
+    unsigned hw = std::thread::hardware_concurrency();
+    const int64_t nblk = std::max<int64_t>(1, std::min<int64_t>((hw ? hw : 1) * 4, n / 8192 + 1));
+    std::vector<std::string> blk((size_t)nblk);
+    std::atomic<int64_t> next(0);
+    auto work = [&]() {
+        char line[256];
+        for (int64_t bi; (bi = next.fetch_add(1)) < nblk;) {
+            const int64_t r0 = n * bi / nblk, r1 = n * (bi + 1) / nblk;
+            std::string &o = blk[(size_t)bi];
+            o.reserve((size_t)(r1 - r0) * 64);
+            for (int64_t r = r0; r < r1; ++r) {
+                char *p = line;
+                p += sprintf(p, "%lld,%lld,%d,", (long long)(r / n_v), (long long)(r % n_v),
+                             valid[r] ? 1 : 0);
+                p += g9(normal0[3 * r], p);
+                *p++ = ',';
+                p += g9(normal0[3 * r + 1], p);
+                *p++ = ',';
+                p += g9(normal0[3 * r + 2], p);
+                *p++ = ',';
+                p += g9(rpath[r], p);
+                p += sprintf(p, ",%d\n", (int)bounces[r]);
+                o.append(line, p - line);
+            }
+        }
+    };
+    {
+        std::vector<std::thread> pool;
+        for (int64_t t = 1; t < std::min<int64_t>(hw ? hw : 1, nblk); ++t) pool.emplace_back(work);
+        work();
+        for (auto &t : pool) t.join();
+    }
+    static const char head[] = "i,j,valid,nx,ny,nz,R,N\n";
+    bool ok = fwrite(head, 1, sizeof(head) - 1, fh) == sizeof(head) - 1;
+    for (const std::string &o : blk) ok = ok && fwrite(o.data(), 1, o.size(), fh) == o.size();
+    if (fclose(fh) != 0 || !ok) return sbr_fail(SBR_EIO, "%s: write error", path);
+    return SBR_OK;
+}

@@ -270,7 +270,21 @@ def trace_grid(bvh: Bvh, mesh: Mesh, grid: ApertureGrid, params: TraceParams = T
 
 
 def dump_hits_csv(records: HitRecords, grid: ApertureGrid, path) -> None:
-    """Per-ray diagnostic dump: i, j, valid, n0, R, N (transport.py:425-436)."""
+    """Per-ray diagnostic dump: i, j, valid, n0, R, N (transport.py:425-436),
+    formatted by the native multi-threaded writer (sbr_dump_hits_csv)."""
+    import os
+    lib = nat.load_library()
+    n = grid.n_u * grid.n_v
+    valid = np.ascontiguousarray(records.valid[:n], dtype=np.uint8)
+    n0 = nat.f64(records.normal0[:n], (-1, 3))
+    rp = nat.f64(records.path[:n])
+    nb = np.ascontiguousarray(records.bounces[:n], dtype=np.int32)
+    nat.check(lib.sbr_dump_hits_csv(os.fsencode(path), grid.n_u, grid.n_v, nat.ptr(valid),
+                                    nat.ptr(n0), nat.ptr(rp), nat.ptr(nb)), "sbr_dump_hits_csv")
+
+
+def _dump_hits_csv_py(records: HitRecords, grid: ApertureGrid, path) -> None:
+    """The reference writer loop (transport.py:425-436), kept as the test oracle."""
     with open(path, "w", encoding="utf-8") as fh:
         fh.write("i,j,valid,nx,ny,nz,R,N\n")
         for r in range(grid.n_u * grid.n_v):

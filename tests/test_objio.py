@@ -152,3 +152,26 @@ def test_number_parsing_is_correctly_rounded(tmp_path):
     assert got is not None
     ref = np.array([[float(t) for t in ln.split()[1:4]] for ln in lines])
     assert np.array_equal(got[0], ref)
+
+
+def test_dump_hits_csv_matches_python_loop(tmp_path):
+    from paper_2604_09243_b200 import transport as TR
+    rng = np.random.default_rng(5)
+    n_u, n_v = 37, 53
+    n = n_u * n_v
+    rec = sbr.HitRecords(valid=rng.random(n) < 0.4,
+                         normal0=np.where(rng.random((n, 1)) < 0.5, 0.0,
+                                          rng.standard_normal((n, 3))) * np.array([1, -1, 1e-7]),
+                         path=rng.random(n) * 1e3, bounces=rng.integers(0, 6, n).astype(np.int32),
+                         escaped=rng.random(n) < 0.5, out_dir=rng.standard_normal((n, 3)))
+    rec.normal0[3] = [-0.0, np.inf, -np.inf]
+    rec.path[4] = np.nan
+
+    class G:
+        pass
+    g = G()
+    g.n_u, g.n_v = n_u, n_v
+    a, b = tmp_path / "nat.csv", tmp_path / "py.csv"
+    TR.dump_hits_csv(rec, g, a)
+    TR._dump_hits_csv_py(rec, g, b)
+    assert a.read_bytes() == b.read_bytes()
