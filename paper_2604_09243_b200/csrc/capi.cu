@@ -838,7 +838,7 @@ static int check_pair(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *bvh)
 // Query 0 of aperture rays: rasterised per triangle or traced through the
 // BVH like every other query.  Both give the same bits.  The raster pass
 // hands each warp 32 triangles of one grid, so it needs many (grid,
-// triangle) pairs to fill the GPU: below ~16k warps of work (a handful of
+// triangle) pairs to fill the GPU: below ~512 warps of work (a handful of
 // large triangles, e.g. corner reflectors) the BVH path is faster.
 // SBR_PRIMARY=raster|bvh forces a path (A/B measurement, parity tests).
 static bool raster_primary(int64_t ntri, int64_t ngrids)
@@ -846,7 +846,7 @@ static bool raster_primary(int64_t ntri, int64_t ngrids)
     const char *s = getenv("SBR_PRIMARY");
     if (s && std::strcmp(s, "bvh") == 0) return false;
     if (s && std::strcmp(s, "raster") == 0) return true;
-    return ngrids * ((ntri + 31) / 32) >= 16384;
+    return ngrids * ((ntri + 31) / 32) >= 512;
 }
 
 static RasterArgs raster_args(const sbr_bvh *bvh, const GridDev *grids, const int *bgrids,
