@@ -290,20 +290,12 @@ __device__ __forceinline__ int node4_visit(const Node4 *np, const RayBox &r, flo
 #undef SBR_SLAB
     const int n = (tn[0] != inf) + (tn[1] != inf) + (tn[2] != inf) + (tn[3] != inf);
     ref[0] = rf.x; ref[1] = rf.y; ref[2] = rf.z; ref[3] = rf.w;
-#ifdef SBR_SORT3
-    // nearest first only (3 compare-exchanges); the others stay partially
-    // ordered and misses may sit anywhere in 1..3 (callers test tn != inf)
-    cswap(tn[0], ref[0], tn[1], ref[1]);
-    cswap(tn[2], ref[2], tn[3], ref[3]);
-    cswap(tn[0], ref[0], tn[2], ref[2]);
-#else
     // 4-element sorting network, misses (+inf) sink to the end
     cswap(tn[0], ref[0], tn[1], ref[1]);
     cswap(tn[2], ref[2], tn[3], ref[3]);
     cswap(tn[0], ref[0], tn[2], ref[2]);
     cswap(tn[1], ref[1], tn[3], ref[3]);
     cswap(tn[1], ref[1], tn[2], ref[2]);
-#endif
     return n;
 }
 
@@ -340,20 +332,12 @@ __device__ __forceinline__ int node8_visit(const Node8 *np, const RayBox &r, flo
 #undef SBR_SLAB8
     }
 #define SBR_CS(i, j) cswap(tn[i], ref[i], tn[j], ref[j]);
-#ifdef SBR_W8_NEAREST
-    // nearest child to slot 0 (7 compare-exchanges); the rest unordered,
-    // misses anywhere in 1..7 (callers test tn != inf)
-    SBR_CS(0, 1) SBR_CS(2, 3) SBR_CS(4, 5) SBR_CS(6, 7)
-    SBR_CS(0, 2) SBR_CS(4, 6)
-    SBR_CS(0, 4)
-#else
     SBR_CS(0, 2) SBR_CS(1, 3) SBR_CS(4, 6) SBR_CS(5, 7)
     SBR_CS(0, 4) SBR_CS(1, 5) SBR_CS(2, 6) SBR_CS(3, 7)
     SBR_CS(0, 1) SBR_CS(2, 3) SBR_CS(4, 5) SBR_CS(6, 7)
     SBR_CS(2, 4) SBR_CS(3, 5)
     SBR_CS(1, 4) SBR_CS(3, 6)
     SBR_CS(1, 2) SBR_CS(3, 4) SBR_CS(5, 6)
-#endif
 #undef SBR_CS
     return n;
 }

@@ -294,11 +294,7 @@ k_trace_persistent(TraceArgs a)
                 if (n > 0) {
 #pragma unroll
                     for (int c = W - 1; c >= 1; --c)   // farther hits first: nearest pops first
-#if defined(SBR_SORT3) || defined(SBR_W8_NEAREST)
-                        if (tt[c] != __int_as_float(0x7f800000)) {
-#else
                         if (c < n) {
-#endif
                             stack[L.sp].ref = rr[c];
                             stack[L.sp].tn = tt[c];
                             ++L.sp;

@@ -40,11 +40,7 @@ __device__ __forceinline__ int closest_hit(const BvhView &B, double ox, double o
             if (n > 0) {
 #pragma unroll
                 for (int c = 3; c >= 1; --c)
-#ifdef SBR_SORT3
-                    if (tt[c] != __int_as_float(0x7f800000)) {
-#else
                     if (c < n) {
-#endif
                         stack[sp].ref = rr[c];
                         stack[sp].tn = tt[c];
                         ++sp;
