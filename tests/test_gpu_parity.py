@@ -502,3 +502,32 @@ def test_sah_build_handles_leaf_roots_and_coincident_centroids():
                        with_ids=True)
     for k in ("valid", "path", "bounces", "tri_ids"):
         assert np.array_equal(getattr(a, k), getattr(b, k)), k
+
+
+@pytest.mark.parametrize("mesh_name", ["aircraft", "sphere", "rough"])
+def test_raster_vs_bvh_random_directions(monkeypatch, mesh_name):
+    """Query 0 by rasterisation == query 0 by traversal, ray for ray (all
+    HitRecords fields and per-bounce ids), over random incidence directions
+    including grazing ones, on meshes with slivers, big and tiny triangles."""
+    if mesh_name == "aircraft":
+        mesh, lam = meshgen.generate_aircraft(density=0.05), 0.08
+    elif mesh_name == "sphere":
+        mesh, lam = meshgen.quantized_icosphere(1.0, 5), 0.05
+    else:
+        mesh, lam = meshgen.perturbed_grid_mesh(cells=90, extent=4.0, amplitude=0.3, seed=11), 0.1
+    tree = sbr.build(mesh)
+    rng = np.random.default_rng(2024)
+    tp = sbr.TraceParams(max_bounces=4)
+    for _ in range(6):
+        th = float(np.arccos(rng.uniform(-1, 1)))
+        ph = float(rng.uniform(0, 2 * np.pi))
+        if _ == 0:
+            th = np.pi / 2 - 1e-9          # grazing a plane of the aircraft / plate
+        grid = sbr.build_aperture(mesh.aabb, sbr.IncidentDirection(th, ph), lam / 5,
+                                  wavelength=lam)
+        out = {}
+        for mode in ("bvh", "raster"):
+            monkeypatch.setenv("SBR_PRIMARY", mode)
+            out[mode] = sbr.trace_grid(tree, mesh, grid, tp, with_ids=True)
+        for k in ("valid", "normal0", "path", "bounces", "escaped", "out_dir", "tri_ids"):
+            assert np.array_equal(getattr(out["raster"], k), getattr(out["bvh"], k)), (th, ph, k)
