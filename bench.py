@@ -326,7 +326,7 @@ def main():
                    "calls_ms": [round(1e3 * t, 1) for t in times],
                    "mean_value": sum(qs) / sum(times),
                    "path": "paper_2604_09243_b200.run_sweep(config, mesh) from host arrays: "
-                           "mesh upload + GPU LBVH + 360 apertures + fused solve + readback; "
+                           "mesh upload + GPU SAH build + 360 apertures + fused solve + readback; "
                            "median of the timed calls after one untimed call"}
 
     if rank != 0:
