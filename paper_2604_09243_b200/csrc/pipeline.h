@@ -43,7 +43,7 @@ constexpr uint32_t kMetaActive = 1u << 19;
 constexpr uint32_t kMetaBounceMask = 0xffffu;
 
 // Primary-visibility result of one ray (query 0), written by the raster
-// pass with two atomicMin sweeps and read by the trace kernel.  Aliases the
+// pass (128-bit compare-and-swap minimum) and read by the trace kernel.  Aliases the
 // SlotRec of the same slot in the fused solve: tbits <-> R, id <-> meta.
 // All-ones = no hit (the buffer is memset to 0xff before the pass).
 struct __align__(16) PrimHit {
@@ -119,9 +119,8 @@ cudaError_t launch_closest(const BvhView &B, int storage, const double *d_orig,
 // ray: each (grid, triangle) pair enumerates the grid cells inside the
 // triangle's projected bounding box (plus a margin) and runs the same exact
 // FP64 Moller-Trumbore test on each (origin built exactly as the launcher
-// builds it).  Pass 0 atomicMin's the t bits, pass 1 atomicMin's the id
-// among triangles that reached that t: the lexicographic (t, id) minimum of
-// bvh.py:340, independent of execution order.
+// builds it).  A 128-bit compare-and-swap keeps the lexicographic (t, id)
+// minimum of bvh.py:340 per ray, independent of execution order.
 struct RasterArgs {
     BvhView B;
     int storage;
