@@ -11,9 +11,13 @@
 //     k_bounds       node box + centroid bounds per segment (ordered-int
 //                    atomicMin/Max on doubles: exact)
 //     k_bin          per (segment, axis, bin) counts + child-box bounds
-//     k_select       one thread per segment: the reference's SAH sweep,
+//     k_select       one warp per segment: the reference's SAH sweep,
 //                    cost formula with the reference's association, tie to
 //                    the lowest (axis, boundary), leaf rule (bvh.py:154-215)
+//     k_small        segments of <= kSmallSeg triangles skip the three
+//                    kernels above: one warp loads the triangles, reduces
+//                    the bounds and evaluates every (axis, boundary) in a
+//                    lane of its own, with no bins in memory
 //     scan           stable partition ranks (CUB exclusive sum over flags)
 //     k_partition    left block first, both order-preserving (bvh.py:213-214)
 //     k_children     BFS node ids of the children, next level's segments
@@ -73,8 +77,11 @@ __global__ void k_tri_bounds(const double *__restrict__ verts, int64_t n,
 
 
 
+constexpr int kSmallSeg = 32;   // segments this small are handled by k_small
+
 __global__ void k_seg_init(SegAcc *__restrict__ acc, unsigned int *__restrict__ cnt,
-                           unsigned long long *__restrict__ bbox, int S, int64_t nslots)
+                           unsigned long long *__restrict__ bbox, int S, int64_t nslots,
+                           const int64_t *__restrict__ sc, int64_t slots_per_seg)
 {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < S) {
@@ -84,7 +91,7 @@ __global__ void k_seg_init(SegAcc *__restrict__ acc, unsigned int *__restrict__ 
             acc[i].cb[q] = kOrdPosInf; acc[i].cb[3 + q] = kOrdNegInf;
         }
     }
-    if (i < nslots) {
+    if (i < nslots && sc[i / slots_per_seg] > kSmallSeg) {   // small segments: no bins
         cnt[i] = 0u;
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
@@ -110,12 +117,14 @@ __global__ void k_seg_of(const int64_t *__restrict__ sb, const int64_t *__restri
 // node box + centroid bounds, one warp-segmented pre-reduction per run of
 // equal segment ids (segments are contiguous in element order)
 __global__ void k_bounds(const double *__restrict__ tb, const int *__restrict__ idx,
-                         const int *__restrict__ eseg, int64_t n, SegAcc *__restrict__ acc)
+                         const int *__restrict__ eseg, int64_t n, SegAcc *__restrict__ acc,
+                         const int64_t *__restrict__ sc, int skip_small)
 {
     const int lane = threadIdx.x & 31;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i - lane < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        const int s = i < n ? eseg[i] : -1;
+        int s = i < n ? eseg[i] : -1;
+        if (skip_small && s >= 0 && sc[s] <= kSmallSeg) s = -1;   // k_small's
         unsigned long long v[12];
         if (s >= 0) {
             const double *b = tb + 9 * (int64_t)idx[i];
@@ -171,12 +180,12 @@ __device__ __forceinline__ int bin_of(double c, double c_lo, double scale, int n
 __global__ void k_bin(const double *__restrict__ tb, const int *__restrict__ idx,
                       const int *__restrict__ eseg, int64_t n, const SegAcc *__restrict__ acc,
                       int nbins, int R, unsigned int *__restrict__ cnt,
-                      unsigned long long *__restrict__ bbox)
+                      unsigned long long *__restrict__ bbox, const int64_t *__restrict__ sc)
 {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int s = eseg[i];
-    if (s < 0) return;
+    if (s < 0 || sc[s] <= kSmallSeg) return;
     const double *b = tb + 9 * (int64_t)idx[i];
     const SegAcc &A = acc[s];
 #pragma unroll
@@ -229,7 +238,7 @@ k_select(const SegAcc *__restrict__ acc, const unsigned int *__restrict__ cnt,
     __shared__ int64_t anl[kSelWarps][3];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int s = blockIdx.x * kSelWarps + w;
-    if (s >= S) return;                               // warp-uniform
+    if (s >= S || sc[s] <= kSmallSeg) return;         // warp-uniform; small: k_small
     const SegAcc &A = acc[s];
     double lo[3], hi[3];
 #pragma unroll
@@ -349,6 +358,154 @@ k_select(const SegAcc *__restrict__ acc, const unsigned int *__restrict__ cnt,
             if (have && !(best >= __dmul_rn((double)n, P.c_i) && n <= 4 * (int64_t)P.n_leaf))
                 r.split = 1;
         }
+    }
+    if (lane == 0) {
+        out[s] = r;
+        split_flag[s] = r.split;
+    }
+}
+
+// Segments of at most kSmallSeg triangles (most of the deep levels): one
+// warp per segment, no bins in memory.  Lane l holds triangle l; the node
+// box and centroid bounds are butterfly reductions on the same ordered
+// integers k_bounds uses (bit-identical boxes, -0.0 < +0.0 included).  Each
+// (axis, boundary) candidate then gets a lane that unions the triangles on
+// either side: the same counts and the same child boxes as the bin sweep of
+// k_select (a union over bins is a union over their triangles; signed zeros
+// cannot change a surface area), hence the same costs, and the warp picks
+// the first minimum in (axis, boundary) order as the reference scan does.
+constexpr int kSmallWarps = 4;
+
+__global__ void __launch_bounds__(kSmallWarps * 32)
+k_small(const double *__restrict__ tb, const int *__restrict__ idx,
+        const int64_t *__restrict__ sb, const int64_t *__restrict__ sc,
+        const int *__restrict__ snode, int S, int depth, SahParams P,
+        double *__restrict__ node_box, SegSplit *__restrict__ out, int *__restrict__ split_flag)
+{
+    __shared__ double sbox[kSmallWarps][6][kSmallSeg];
+    __shared__ unsigned char sbin[kSmallWarps][3][kSmallSeg];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int s = blockIdx.x * kSmallWarps + w;
+    if (s >= S) return;
+    const int64_t n64 = sc[s];
+    if (n64 > kSmallSeg) return;                      // warp-uniform
+    const int n = (int)n64;
+    unsigned long long v[12];
+    double c[3] = {0.0, 0.0, 0.0};
+    if (lane < n) {
+        const double *b = tb + 9 * (int64_t)idx[sb[s] + lane];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            sbox[w][q][lane] = b[q];
+            sbox[w][3 + q][lane] = b[3 + q];
+            c[q] = b[6 + q];
+            v[q] = ordd(b[q]);
+            v[3 + q] = ordd(b[3 + q]);
+            v[6 + q] = ordd(c[q]);
+            v[9 + q] = v[6 + q];
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            v[q] = kOrdPosInf; v[3 + q] = kOrdNegInf;
+            v[6 + q] = kOrdPosInf; v[9 + q] = kOrdNegInf;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+#pragma unroll
+        for (int q = 0; q < 12; ++q) {
+            const unsigned long long x = __shfl_xor_sync(0xffffffffu, v[q], o);
+            const bool is_min = (q < 3) || (q >= 6 && q < 9);
+            v[q] = is_min ? (x < v[q] ? x : v[q]) : (x > v[q] ? x : v[q]);
+        }
+    }
+    double lo[3], hi[3], clo[3], chi[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        lo[q] = unordd(v[q]); hi[q] = unordd(v[3 + q]);
+        clo[q] = unordd(v[6 + q]); chi[q] = unordd(v[9 + q]);
+    }
+    if (lane == 0) {
+        double *nb = node_box + 6 * (int64_t)snode[s];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) { nb[q] = lo[q]; nb[3 + q] = hi[q]; }
+    }
+    SegSplit r;
+    r.split = 0; r.axis = -1; r.boundary = -1; r.c_lo = 0.0; r.scale = 0.0; r.nl = 0;
+    const int B = P.bins;
+    if (n > P.n_leaf && depth < P.max_depth) {
+        double scale[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            scale[q] = chi[q] > clo[q] ? __ddiv_rn((double)B, __dsub_rn(chi[q], clo[q])) : 0.0;
+            if (lane < n) sbin[w][q][lane] = (unsigned char)bin_of(c[q], clo[q], scale[q], B);
+        }
+        __syncwarp();
+        double sa_p = sa_of(lo, hi);
+        if (!(sa_p >= 1e-300)) sa_p = 1e-300;          // max(sa, 1e-300)
+        // best candidate of this lane over the rounds: (have, cost, index)
+        bool have = false;
+        double best = 0.0;
+        int best_c = 0x7fffffff, best_nl = 0;
+        const int ncand = 3 * (B - 1);
+        for (int cand = lane; cand < ncand; cand += 32) {
+            const int axis = cand / (B - 1), b = cand - axis * (B - 1);
+            if (!(chi[axis] > clo[axis])) continue;     // bvh.py:177-178
+            double l3[3] = {INFINITY, INFINITY, INFINITY}, h3[3] = {-INFINITY, -INFINITY, -INFINITY};
+            double r3[3] = {INFINITY, INFINITY, INFINITY}, g3[3] = {-INFINITY, -INFINITY, -INFINITY};
+            int ln = 0;
+            for (int t = 0; t < n; ++t) {
+                if (sbin[w][axis][t] <= b) {
+                    ++ln;
+#pragma unroll
+                    for (int q = 0; q < 3; ++q) {
+                        l3[q] = fmin(l3[q], sbox[w][q][t]);
+                        h3[q] = fmax(h3[q], sbox[w][3 + q][t]);
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 3; ++q) {
+                        r3[q] = fmin(r3[q], sbox[w][q][t]);
+                        g3[q] = fmax(g3[q], sbox[w][3 + q][t]);
+                    }
+                }
+            }
+            const int nr = n - ln;
+            if (ln == 0 || nr == 0) continue;
+            const double sal = sa_of(l3, h3), sar = sa_of(r3, g3);
+            // sah_cost (bvh.py:124-127), same association as k_select
+            const double cost = __dadd_rn(
+                __dadd_rn(P.c_t, __dmul_rn(__dmul_rn(__ddiv_rn(sal, sa_p), (double)ln), P.c_i)),
+                __dmul_rn(__dmul_rn(__ddiv_rn(sar, sa_p), (double)nr), P.c_i));
+            if (!have || cost < best) {   // candidates ascend per lane: keeps the first
+                have = true;
+                best = cost;
+                best_c = cand;
+                best_nl = ln;
+            }
+        }
+        // warp argmin: lowest cost, then lowest candidate index
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+            const int oh = __shfl_xor_sync(0xffffffffu, (int)have, o);
+            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int oc = __shfl_xor_sync(0xffffffffu, best_c, o);
+            const int on = __shfl_xor_sync(0xffffffffu, best_nl, o);
+            if (oh && (!have || ob < best || (ob == best && oc < best_c))) {
+                have = true; best = ob; best_c = oc; best_nl = on;
+            }
+        }
+        if (have) {
+            r.axis = best_c / (B - 1);
+            r.boundary = best_c - r.axis * (B - 1);
+            r.nl = best_nl;
+            r.c_lo = clo[r.axis];
+            r.scale = scale[r.axis];
+        }
+        // bvh.py:210-211: no admissible split, or not worth it for a small node
+        if (have && !(best >= __dmul_rn((double)n, P.c_i) && n <= 4 * (int64_t)P.n_leaf))
+            r.split = 1;
     }
     if (lane == 0) {
         out[s] = r;
@@ -653,17 +810,20 @@ cudaError_t sah_build(const double *d_verts, int64_t n, const SahParams &P, SahT
             CK(w.cnt.alloc(cap));
             CK(w.bbox.alloc(6 * cap));
         }
-        k_seg_init<<<nblk(std::max<int64_t>(nslots, S), T), T, 0, st>>>(w.acc.p, w.cnt.p,
-                                                                       w.bbox.p, S, nslots);
+        k_seg_init<<<nblk(std::max<int64_t>(nslots, S), T), T, 0, st>>>(
+            w.acc.p, w.cnt.p, w.bbox.p, S, nslots, sc, (int64_t)R * 3 * B);
         k_seg_of<<<nblk(n, T), T, 0, st>>>(sb, sc, S, n, w.eseg.p);
-        k_bounds<<<nblk(n, T), T, 0, st>>>(w.tb.p, idx, w.eseg.p, n, w.acc.p);
+        k_bounds<<<nblk(n, T), T, 0, st>>>(w.tb.p, idx, w.eseg.p, n, w.acc.p, sc, !P.median);
         CK(cudaMemsetAsync(w.sflag.p + S, 0, sizeof(int), st));
         if (!P.median) {
             k_bin<<<nblk(n, T), T, 0, st>>>(w.tb.p, idx, w.eseg.p, n, w.acc.p, B, R, w.cnt.p,
-                                            w.bbox.p);
+                                            w.bbox.p, sc);
             k_select<<<nblk(S, kSelWarps), kSelWarps * 32, 0, st>>>(
                 w.acc.p, w.cnt.p, w.bbox.p, sc, snode, S, R, depth, P, w.node_box.p, w.sp.p,
                 w.sflag.p);
+            k_small<<<nblk(S, kSmallWarps), kSmallWarps * 32, 0, st>>>(
+                w.tb.p, idx, sb, sc, snode, S, depth, P, w.node_box.p, w.sp.p, w.sflag.p);
+            ++*launches;
         } else {
             k_select_median<<<nblk(S, 128), 128, 0, st>>>(w.acc.p, sc, snode, S, depth, P,
                                                           w.node_box.p, w.sp.p, w.sflag.p);
