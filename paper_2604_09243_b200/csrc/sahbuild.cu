@@ -114,16 +114,65 @@ __global__ void k_seg_of(const int64_t *__restrict__ sb, const int64_t *__restri
     eseg[i] = (S > 0 && sb[lo] <= i && i < sb[lo] + sc[lo]) ? lo : -1;
 }
 
-// node box + centroid bounds, one warp-segmented pre-reduction per run of
-// equal segment ids (segments are contiguous in element order)
-__global__ void k_bounds(const double *__restrict__ tb, const int *__restrict__ idx,
-                         const int *__restrict__ eseg, int64_t n, SegAcc *__restrict__ acc,
-                         const int64_t *__restrict__ sc, int skip_small)
+// Work tiles of the per-element kernels: a block takes kTile consecutive
+// elements.  Active segments are contiguous and ordered in element order, so
+// a tile spans segments [s_lo, s_hi]; when that is at most kLocalSegs (all
+// levels near the root, where every element hits the same few addresses)
+// the block reduces into shared memory first and flushes once per value.
+constexpr int kTile = 1024;
+constexpr int kTileThreads = 256;
+constexpr int kLocalSegs = 4;
+
+// [s_lo, s_hi] of the tile's elements that belong to a segment handled by
+// the bin kernels (s_hi < 0: none); block-uniform result
+__device__ __forceinline__ void tile_range(const int *__restrict__ eseg,
+                                           const int64_t *__restrict__ sc, int64_t t0,
+                                           int64_t t1, int skip_small, int *srange, int &s_lo,
+                                           int &s_hi)
 {
-    const int lane = threadIdx.x & 31;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i - lane < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        int s = i < n ? eseg[i] : -1;
+    const int tid = threadIdx.x, lane = tid & 31;
+    if (tid == 0) { srange[0] = 0x7fffffff; srange[1] = -1; }
+    __syncthreads();
+    int mn = 0x7fffffff, mx = -1;
+    for (int64_t i = t0 + tid; i < t1; i += blockDim.x) {
+        const int s = eseg[i];
+        if (s >= 0 && !(skip_small && sc[s] <= kSmallSeg)) { mn = min(mn, s); mx = max(mx, s); }
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (lane == 0 && mx >= 0) { atomicMin(&srange[0], mn); atomicMax(&srange[1], mx); }
+    __syncthreads();
+    s_lo = srange[0];
+    s_hi = srange[1];
+}
+
+// node box + centroid bounds: a warp-segmented pre-reduction per run of
+// equal segment ids, then shared (few segments per tile) or global
+// ordered-integer atomics -- min/max, exact in any order
+__global__ void __launch_bounds__(kTileThreads)
+k_bounds(const double *__restrict__ tb, const int *__restrict__ idx,
+         const int *__restrict__ eseg, int64_t n, SegAcc *__restrict__ acc,
+         const int64_t *__restrict__ sc, int skip_small)
+{
+    __shared__ unsigned long long sacc[kLocalSegs][12];
+    __shared__ int srange[2];
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int64_t t0 = (int64_t)blockIdx.x * kTile;
+    const int64_t t1 = t0 + kTile < n ? t0 + kTile : n;
+    int s_lo, s_hi;
+    tile_range(eseg, sc, t0, t1, skip_small, srange, s_lo, s_hi);
+    if (s_hi < 0) return;                               // block-uniform
+    const bool local = s_hi - s_lo < kLocalSegs;
+    if (local && tid < kLocalSegs * 12) {
+        const int q = tid % 12;
+        sacc[tid / 12][q] = (q < 3 || (q >= 6 && q < 9)) ? kOrdPosInf : kOrdNegInf;
+    }
+    __syncthreads();
+    for (int64_t i = t0 + tid; i - lane < t1; i += blockDim.x) {
+        int s = i < t1 ? eseg[i] : -1;
         if (skip_small && s >= 0 && sc[s] <= kSmallSeg) s = -1;   // k_small's
         unsigned long long v[12];
         if (s >= 0) {
@@ -157,13 +206,39 @@ __global__ void k_bounds(const double *__restrict__ tb, const int *__restrict__ 
         }
         const int sp = __shfl_up_sync(0xffffffffu, s, 1);
         if (s >= 0 && (lane == 0 || sp != s)) {      // head of its run
-            SegAcc &A = acc[s];
+            if (local) {
+                unsigned long long *L = sacc[s - s_lo];
 #pragma unroll
-            for (int q = 0; q < 3; ++q) {
-                atomicMin(&A.box[q], v[q]);
-                atomicMax(&A.box[3 + q], v[3 + q]);
-                atomicMin(&A.cb[q], v[6 + q]);
-                atomicMax(&A.cb[3 + q], v[9 + q]);
+                for (int q = 0; q < 3; ++q) {
+                    atomicMin(&L[q], v[q]);
+                    atomicMax(&L[3 + q], v[3 + q]);
+                    atomicMin(&L[6 + q], v[6 + q]);
+                    atomicMax(&L[9 + q], v[9 + q]);
+                }
+            } else {
+                SegAcc &A = acc[s];
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    atomicMin(&A.box[q], v[q]);
+                    atomicMax(&A.box[3 + q], v[3 + q]);
+                    atomicMin(&A.cb[q], v[6 + q]);
+                    atomicMax(&A.cb[3 + q], v[9 + q]);
+                }
+            }
+        }
+    }
+    if (local) {
+        __syncthreads();
+        if (tid < (s_hi - s_lo + 1) * 12) {
+            const int ls = tid / 12, q = tid % 12;
+            const int s = s_lo + ls;
+            if (!(skip_small && sc[s] <= kSmallSeg)) {
+                const unsigned long long x = sacc[ls][q];
+                SegAcc &A = acc[s];
+                if (q < 3) atomicMin(&A.box[q], x);
+                else if (q < 6) atomicMax(&A.box[q], x);
+                else if (q < 9) atomicMin(&A.cb[q - 6], x);
+                else atomicMax(&A.cb[q - 6], x);
             }
         }
     }
@@ -177,32 +252,77 @@ __device__ __forceinline__ int bin_of(double c, double c_lo, double scale, int n
     return b > nbins - 1 ? nbins - 1 : (int)b;
 }
 
-__global__ void k_bin(const double *__restrict__ tb, const int *__restrict__ idx,
-                      const int *__restrict__ eseg, int64_t n, const SegAcc *__restrict__ acc,
-                      int nbins, int R, unsigned int *__restrict__ cnt,
-                      unsigned long long *__restrict__ bbox, const int64_t *__restrict__ sc)
+__global__ void __launch_bounds__(kTileThreads)
+k_bin(const double *__restrict__ tb, const int *__restrict__ idx,
+      const int *__restrict__ eseg, int64_t n, const SegAcc *__restrict__ acc, int nbins,
+      int R, unsigned int *__restrict__ cnt, unsigned long long *__restrict__ bbox,
+      const int64_t *__restrict__ sc)
 {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const int s = eseg[i];
-    if (s < 0 || sc[s] <= kSmallSeg) return;
-    const double *b = tb + 9 * (int64_t)idx[i];
-    const SegAcc &A = acc[s];
+    __shared__ unsigned int scnt[kLocalSegs * 3 * kSahMaxBins];
+    __shared__ unsigned long long sbb[kLocalSegs * 3 * kSahMaxBins * 6];
+    __shared__ int srange[2];
+    const int tid = threadIdx.x;
+    const int64_t t0 = (int64_t)blockIdx.x * kTile;
+    const int64_t t1 = t0 + kTile < n ? t0 + kTile : n;
+    int s_lo, s_hi;
+    tile_range(eseg, sc, t0, t1, 1, srange, s_lo, s_hi);
+    if (s_hi < 0) return;                               // block-uniform
+    const bool local = s_hi - s_lo < kLocalSegs;
+    const int nloc = (s_hi - s_lo + 1) * 3 * nbins;
+    if (local) {
+        for (int k = tid; k < nloc; k += blockDim.x) {
+            scnt[k] = 0u;
 #pragma unroll
-    for (int axis = 0; axis < 3; ++axis) {
-        const double c_lo = unordd(A.cb[axis]), c_hi = unordd(A.cb[3 + axis]);
-        if (!(c_hi > c_lo)) continue;                       // bvh.py:177-178
-        const double scale = __ddiv_rn((double)nbins, __dsub_rn(c_hi, c_lo));
-        const int bi = bin_of(b[6 + axis], c_lo, scale, nbins);
-        // near the root few segments share every bin: R replicas (chosen by
-        // block) spread the atomics; k_select merges them (min/max/sum: exact)
-        const int64_t slot = (((int64_t)s * R + blockIdx.x % R) * 3 + axis) * nbins + bi;
-        atomicAdd(&cnt[slot], 1u);
-        unsigned long long *bb = bbox + 6 * slot;
+            for (int q = 0; q < 3; ++q) { sbb[6 * k + q] = kOrdPosInf; sbb[6 * k + 3 + q] = kOrdNegInf; }
+        }
+        __syncthreads();
+    }
+    // near the root few segments share every bin: R replicas (chosen by
+    // block) spread the global atomics; k_select merges them (exact)
+    const int rep = blockIdx.x % R;
+    for (int64_t i = t0 + tid; i < t1; i += blockDim.x) {
+        const int s = eseg[i];
+        if (s < 0 || sc[s] <= kSmallSeg) continue;
+        const double *b = tb + 9 * (int64_t)idx[i];
+        const SegAcc &A = acc[s];
 #pragma unroll
-        for (int q = 0; q < 3; ++q) {
-            atomicMin(&bb[q], ordd(b[q]));
-            atomicMax(&bb[3 + q], ordd(b[3 + q]));
+        for (int axis = 0; axis < 3; ++axis) {
+            const double c_lo = unordd(A.cb[axis]), c_hi = unordd(A.cb[3 + axis]);
+            if (!(c_hi > c_lo)) continue;                   // bvh.py:177-178
+            const double scale = __ddiv_rn((double)nbins, __dsub_rn(c_hi, c_lo));
+            const int bi = bin_of(b[6 + axis], c_lo, scale, nbins);
+            unsigned int *cp;
+            unsigned long long *bb;
+            if (local) {
+                const int k = ((s - s_lo) * 3 + axis) * nbins + bi;
+                cp = scnt + k;
+                bb = sbb + 6 * k;
+            } else {
+                const int64_t slot = (((int64_t)s * R + rep) * 3 + axis) * nbins + bi;
+                cp = cnt + slot;
+                bb = bbox + 6 * slot;
+            }
+            atomicAdd(cp, 1u);
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                atomicMin(&bb[q], ordd(b[q]));
+                atomicMax(&bb[3 + q], ordd(b[3 + q]));
+            }
+        }
+    }
+    if (local) {
+        __syncthreads();
+        for (int k = tid; k < nloc; k += blockDim.x) {
+            const unsigned int c = scnt[k];
+            if (c == 0u) continue;
+            const int ls = k / (3 * nbins), rest = k - ls * 3 * nbins;
+            const int64_t slot = ((int64_t)(s_lo + ls) * R + rep) * 3 * nbins + rest;
+            atomicAdd(&cnt[slot], c);
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                atomicMin(&bbox[6 * slot + q], sbb[6 * k + q]);
+                atomicMax(&bbox[6 * slot + 3 + q], sbb[6 * k + 3 + q]);
+            }
         }
     }
 }
@@ -813,11 +933,12 @@ cudaError_t sah_build(const double *d_verts, int64_t n, const SahParams &P, SahT
         k_seg_init<<<nblk(std::max<int64_t>(nslots, S), T), T, 0, st>>>(
             w.acc.p, w.cnt.p, w.bbox.p, S, nslots, sc, (int64_t)R * 3 * B);
         k_seg_of<<<nblk(n, T), T, 0, st>>>(sb, sc, S, n, w.eseg.p);
-        k_bounds<<<nblk(n, T), T, 0, st>>>(w.tb.p, idx, w.eseg.p, n, w.acc.p, sc, !P.median);
+        k_bounds<<<nblk(n, kTile), kTileThreads, 0, st>>>(w.tb.p, idx, w.eseg.p, n, w.acc.p, sc,
+                                                          !P.median);
         CK(cudaMemsetAsync(w.sflag.p + S, 0, sizeof(int), st));
         if (!P.median) {
-            k_bin<<<nblk(n, T), T, 0, st>>>(w.tb.p, idx, w.eseg.p, n, w.acc.p, B, R, w.cnt.p,
-                                            w.bbox.p, sc);
+            k_bin<<<nblk(n, kTile), kTileThreads, 0, st>>>(w.tb.p, idx, w.eseg.p, n, w.acc.p, B,
+                                                           R, w.cnt.p, w.bbox.p, sc);
             k_select<<<nblk(S, kSelWarps), kSelWarps * 32, 0, st>>>(
                 w.acc.p, w.cnt.p, w.bbox.p, sc, snode, S, R, depth, P, w.node_box.p, w.sp.p,
                 w.sflag.p);
