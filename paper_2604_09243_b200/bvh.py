@@ -28,9 +28,10 @@ from .geometry import Aabb, Mesh
 
 @dataclass(frozen=True)
 class BuildParams:
-    """Construction knobs (bvh.py:22-49).  The GPU builder honours
-    ``n_leaf`` (<= 63); ``split_rule``/``bins_per_axis``/``c_t``/``c_i``
-    select the host split helpers below and are validated for parity."""
+    """Construction knobs (bvh.py:22-49), all honoured by the GPU builders:
+    ``split_rule`` "sah" / "median" (the reference trees, node for node) or
+    "lbvh" (Morton LBVH, ``n_leaf`` <= 63); ``bins_per_axis`` (<= 64),
+    ``c_t``, ``c_i``, ``max_depth`` as in the reference."""
 
     split_rule: str = "sah"
     n_leaf: int = 4
