@@ -106,6 +106,33 @@ __device__ __forceinline__ RasterSetup raster_setup(const TriF64 &T, const GridD
     return S;
 }
 
+// Sharded launches (a.sparse): shrink the candidate rectangle to the rows
+// between the first and the last owned segment it touches (count 0: none
+// owned).  Only cells raster_cell would skip anyway are dropped; k_raster and
+// k_raster_big apply it identically, so chunk indices agree.
+__device__ __forceinline__ void trim_owned(RasterSetup &S, const GridDev &G, const int64_t *segs)
+{
+    if (S.count == 0) return;
+    const int64_t rows = S.count / S.cols;
+    const int64_t r0 = S.i0 * G.n_v + S.j0;
+    const int64_t r1 = (S.i0 + rows - 1) * G.n_v + S.j0 + S.cols - 1;
+    int64_t qf = -1, ql = -1;
+    for (int64_t q = r0 / kSegRays; q <= r1 / kSegRays; ++q)
+        if (__ldg(&segs[q]) != kNoSlot) {
+            if (qf < 0) qf = q;
+            ql = q;
+        }
+    if (qf < 0) {
+        S.count = 0;
+        return;
+    }
+    const int64_t fa = (qf * kSegRays) / G.n_v, fb = ((ql + 1) * kSegRays - 1) / G.n_v;
+    const int64_t a = fa > S.i0 ? fa : S.i0;
+    const int64_t b = fb < S.i0 + rows - 1 ? fb : S.i0 + rows - 1;
+    S.i0 = a;
+    S.count = (b - a + 1) * S.cols;
+}
+
 __device__ __forceinline__ void split_cell(long long local, int cols, long long &li, long long &lj)
 {
     if (local < 0x7fffffffLL) {
@@ -171,7 +198,8 @@ k_raster(RasterArgs a, int64_t ntri_pad)
         long long count = 0;
         RasterTri &R = st[wib][lane];
         if (tri < a.ntri) {
-            const RasterSetup S = raster_setup(load_tri<STORAGE>(a.B, (int)tri), G);
+            RasterSetup S = raster_setup(load_tri<STORAGE>(a.B, (int)tri), G);
+            if (a.sparse) trim_owned(S, G, a.seg_slot + __ldg(&a.seg_base[g]));
             count = S.count;
             if (count > kBigTri && a.big) {
                 const long long nch = (count + kBigChunk - 1) / kBigChunk;
@@ -270,8 +298,9 @@ k_raster_big(RasterArgs a)
         const int4 it = a.big[w];
         const int g = __ldg(&a.bgrids[it.x]);
         const GridDev &G = a.grids[g];
-        const RasterSetup S = raster_setup(load_tri<STORAGE>(a.B, it.y), G);
+        RasterSetup S = raster_setup(load_tri<STORAGE>(a.B, it.y), G);
         const int64_t *seg = a.seg_slot + __ldg(&a.seg_base[g]);
+        if (a.sparse) trim_owned(S, G, seg);
         const long long c0 = (long long)it.z * kBigChunk;
         const long long c1 = c0 + kBigChunk < S.count ? c0 + kBigChunk : S.count;
         for (long long c = c0 + lane; c < c1; c += 32) {
