@@ -147,7 +147,9 @@ struct sbr_bvh {
         BvhView v;
         v.nodes = out.nodes.p;
         v.nodes4 = out.nodes4.p;
+        v.nodes4q = out.nodes4q.p;
         v.nodes8 = out.nodes8.p;
+        v.nodes8q = out.nodes8q.p;
         v.width = out.width;
         v.tri32 = out.tri32.p;
         v.tri64 = out.tri64.p;

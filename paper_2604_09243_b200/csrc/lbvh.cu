@@ -479,6 +479,11 @@ cudaError_t pack_tris(const double *d_verts, const int *d_order, int64_t n, int 
 // ---------------------------------------------------------------------------
 // BVH2 -> BVH4 collapse (level by level, deterministic)
 // ---------------------------------------------------------------------------
+template <int W> struct PlainNode;
+template <> struct PlainNode<4> { using T = Node4; };
+template <> struct PlainNode<8> { using T = Node8; };
+// ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
 __device__ __forceinline__ void child_box(const Node &n, int which, float b[6])
 {
     if (which == 0) {
@@ -543,7 +548,7 @@ template <int W>
 __global__ void k_collapse_emit(const int *__restrict__ cref, const float *__restrict__ cbox,
                                 const int *__restrict__ off, const int *__restrict__ out_idx,
                                 int n_items, int next_base,
-                                typename WideNode<W>::T *__restrict__ out,
+                                typename PlainNode<W>::T *__restrict__ out,
                                 int *__restrict__ next_items, int *__restrict__ next_out)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -563,7 +568,7 @@ __global__ void k_collapse_emit(const int *__restrict__ cref, const float *__res
         r[k] = c;
     }
     // SoA planes: W/4 float4 per plane, then W/4 int4 refs, then padding
-    typename WideNode<W>::T nd;
+    typename PlainNode<W>::T nd;
     float4 *f = reinterpret_cast<float4 *>(&nd);
     for (int q = 0; q < 6; ++q)
         for (int h = 0; h < W / 4; ++h)
@@ -578,7 +583,7 @@ __global__ void k_collapse_emit(const int *__restrict__ cref, const float *__res
 }
 
 template <int W>
-static cudaError_t collapse_wide(LbvhOutput &out, typename WideNode<W>::T **dst, int64_t &nn,
+static cudaError_t collapse_wide(LbvhOutput &out, typename PlainNode<W>::T **dst, int64_t &nn,
                                  int &depth, Arena &ws, cudaStream_t st, int64_t *launches)
 {
     const int n2 = (int)out.nnodes;
@@ -622,6 +627,58 @@ static cudaError_t collapse_wide(LbvhOutput &out, typename WideNode<W>::T **dst,
     return cudaSuccess;
 }
 
+// Node4 / Node8 -> quantised node: per axis the origin p = min child lo (a
+// float) and the smallest power-of-two step 2^e with 255 * 2^e >= max child
+// hi - p; child planes are rounded outward (floor / ceil, exact in FP64).
+template <int W> struct QNode;
+template <> struct QNode<4> { using T = Node4Q; };
+template <> struct QNode<8> { using T = Node8Q; };
+
+template <int W>
+__global__ void k_quantize(const typename PlainNode<W>::T *__restrict__ in, int64_t n,
+                           typename QNode<W>::T *__restrict__ out)
+{
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    // plain layout: 6 planes of W floats, then W refs
+    const float *pl = reinterpret_cast<const float *>(in + i);
+    const int *rf = reinterpret_cast<const int *>(pl + 6 * W);
+    typename QNode<W>::T Q;
+    float p[3];
+    unsigned int exps = 0;
+    unsigned int qw[6][W / 4];
+    for (int a = 0; a < 3; ++a) {
+        float mn = INFINITY, mx = -INFINITY;
+        for (int k = 0; k < W; ++k)
+            if (rf[k] != kEmptyRef) { mn = fminf(mn, pl[a * W + k]); mx = fmaxf(mx, pl[(3 + a) * W + k]); }
+        if (!(mn <= mx)) { mn = 0.f; mx = 0.f; }
+        p[a] = mn;
+        const double ext = (double)mx - (double)mn;    // exact
+        int e = -100;
+        while ((double)255 * ldexp(1.0, e) < ext) ++e;
+        exps |= (unsigned int)(e + 127) << (8 * a);
+        for (int h = 0; h < W / 4; ++h) { qw[a][h] = 0u; qw[3 + a][h] = 0u; }
+        for (int k = 0; k < W; ++k) {
+            unsigned int ql = 0u, qh = 0u;
+            if (rf[k] != kEmptyRef) {
+                ql = (unsigned int)floor(ldexp((double)pl[a * W + k] - (double)mn, -e));
+                qh = (unsigned int)ceil(ldexp((double)pl[(3 + a) * W + k] - (double)mn, -e));
+                qh = qh > 255u ? 255u : qh;
+            }
+            qw[a][k >> 2] |= ql << (8 * (k & 3));
+            qw[3 + a][k >> 2] |= qh << (8 * (k & 3));
+        }
+    }
+    Q.px = p[0]; Q.py = p[1]; Q.pz = p[2];
+    Q.exps = exps;
+    int *qr = reinterpret_cast<int *>(&Q.ref);
+    for (int k = 0; k < W; ++k) qr[k] = rf[k];
+    for (int j = 0; j < 6; ++j)
+        for (int h = 0; h < W / 4; ++h) Q.q[j * (W / 4) + h] = qw[j][h];
+    if (W == 4) reinterpret_cast<unsigned int *>(&Q)[14] = reinterpret_cast<unsigned int *>(&Q)[15] = 0u;
+    out[i] = Q;
+}
+
 // the traversal tree width: 4 unless SBR_WIDTH=8
 int traversal_width()
 {
@@ -635,12 +692,28 @@ cudaError_t collapse_bvh4(LbvhOutput &out, Arena &ws, cudaStream_t st, int64_t *
     CK(out.nodes4.alloc(n2));
     Node4 *p4 = out.nodes4.p;
     CK(collapse_wide<4>(out, &p4, out.nnodes4, out.depth4, ws, st, launches));
+#ifdef SBR_NODE_Q
+    // quantised boxes (-DSBR_NODE_Q): measured neutral at width 4, 9% faster
+    // than the 256 B nodes at width 8 (profiles/experiments)
+    CK(out.nodes4q.alloc((size_t)out.nnodes4));
+    k_quantize<4><<<(unsigned)((out.nnodes4 + 127) / 128), 128, 0, st>>>(p4, out.nnodes4,
+                                                                      out.nodes4q.p);
+    ++*launches;
+    CK(cudaGetLastError());
+#endif
     out.width = traversal_width();
     if (out.width == 8) {
         CK(out.nodes8.alloc(n2));
         Node8 *p8 = out.nodes8.p;
         int d8 = 0;
         CK(collapse_wide<8>(out, &p8, out.nnodes8, d8, ws, st, launches));
+#ifdef SBR_NODE_Q
+        CK(out.nodes8q.alloc((size_t)out.nnodes8));
+        k_quantize<8><<<(unsigned)((out.nnodes8 + 127) / 128), 128, 0, st>>>(p8, out.nnodes8,
+                                                                          out.nodes8q.p);
+        ++*launches;
+        CK(cudaGetLastError());
+#endif
         out.depth8 = d8;
     }
     return cudaSuccess;

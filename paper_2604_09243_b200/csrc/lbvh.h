@@ -123,10 +123,12 @@ struct LbvhOutput {
     int storage = 0;
     // 4-wide traversal tree collapsed from `nodes` (level order, root 0)
     DevBuf<Node4> nodes4;
+    DevBuf<Node4Q> nodes4q;  // nodes4 with quantised boxes (same indices)
     int64_t nnodes4 = 0;
     int depth4 = 0;
     // optional 8-wide traversal tree (SBR_WIDTH=8)
     DevBuf<Node8> nodes8;
+    DevBuf<Node8Q> nodes8q;
     int64_t nnodes8 = 0;
     int depth8 = 0;
     int width = 4;

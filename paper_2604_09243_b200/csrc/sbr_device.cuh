@@ -47,6 +47,29 @@ struct __align__(128) Node4 {
 };
 constexpr int kEmptyRef = 0x7fffffff;
 
+// 4-wide node with 8-bit quantised child boxes, 64 B (half a line, four
+// loads instead of eight).  Per axis a: plane = p_a + q * 2^e_a with the
+// child box rounded OUTWARD onto that grid at build time (k_quantize4);
+// the slab test folds the decode into its fma (node4q_visit).
+struct __align__(64) Node4Q {
+    float px, py, pz;     // quantisation origin (box frame)
+    unsigned int exps;    // biased float exponents of the scales: ex | ey << 8 | ez << 16
+    int4 ref;
+    unsigned int q[6];    // planes lox loy loz hix hiy hiz; child k in byte k
+    unsigned int pad[2];
+};
+static_assert(sizeof(Node4Q) == 64, "Node4Q is half a line");
+
+// 8-wide node with quantised child boxes, 96 B (three sectors): header,
+// eight refs, six planes of eight bytes (plane j in q[2j], q[2j+1]).
+struct __align__(32) Node8Q {
+    float px, py, pz;
+    unsigned int exps;
+    int4 ref[2];
+    unsigned int q[12];
+};
+static_assert(sizeof(Node8Q) == 96, "Node8Q is three sectors");
+
 // 8-wide node, 256 B = two cache lines: the same SoA planes with eight
 // children each (two float4 per plane), eight refs, padding.
 struct __align__(128) Node8 {
@@ -79,7 +102,9 @@ enum Storage : int { kF32Exact = 1, kF64 = 2, kSingle = 3 };
 struct BvhView {
     const Node *nodes;       // binary tree (build / export)
     const Node4 *nodes4;     // 4-wide tree (traversal)
+    const Node4Q *nodes4q;   // the same tree with quantised child boxes
     const Node8 *nodes8;     // 8-wide tree (traversal when width == 8)
+    const Node8Q *nodes8q;   // the same with quantised child boxes
     int width;               // 4 or 8: which wide tree the trace kernel walks
     const float4 *tri32;
     const double2 *tri64;
@@ -342,23 +367,141 @@ __device__ __forceinline__ int node8_visit(const Node8 *np, const RayBox &r, flo
     return n;
 }
 
+// byte k of w as an exact float (0x4B0000kk = 2^23 + k)
+__device__ __forceinline__ float qbyte(unsigned int w, int k)
+{
+    return __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7540 | k)) - 8388608.0f;
+}
+
+// Visit one quantised BVH4 node.  t = fma(q, 2^e inv, fma(p, inv, off)):
+// the exact plane p + q 2^e (outward-rounded, so it contains the child box)
+// times inv plus the padded offset, with two roundings where node4_visit has
+// one -- a few ulp of (|o'| + scale), still far inside the 2^-17 padding.
+__device__ __forceinline__ int node4q_visit(const Node4Q *np, const RayBox &r, float tmax,
+                                            int ref[4], float tn[4])
+{
+    const uint4 h = __ldg(reinterpret_cast<const uint4 *>(np));
+    const int4 rf = __ldg(&np->ref);
+    const uint4 qa = __ldg(reinterpret_cast<const uint4 *>(np->q));
+    const uint2 qb = __ldg(reinterpret_cast<const uint2 *>(np->q + 4));
+    const float px = __uint_as_float(h.x), py = __uint_as_float(h.y), pz = __uint_as_float(h.z);
+    const float ax = __uint_as_float((h.w & 0xffu) << 23) * r.ix;
+    const float ay = __uint_as_float(((h.w >> 8) & 0xffu) << 23) * r.iy;
+    const float az = __uint_as_float(((h.w >> 16) & 0xffu) << 23) * r.iz;
+    const float bnx = fmaf(px, r.ix, r.nx), bfx = fmaf(px, r.ix, r.fx);
+    const float bny = fmaf(py, r.iy, r.ny), bfy = fmaf(py, r.iy, r.fy);
+    const float bnz = fmaf(pz, r.iz, r.nz), bfz = fmaf(pz, r.iz, r.fz);
+    // near plane per axis: lo when the float4 index in sel is the lo one
+    const bool lx = (r.sel & 7) == 0, ly = ((r.sel >> 3) & 7) == 1, lz = ((r.sel >> 6) & 7) == 2;
+    const unsigned int wnx = lx ? qa.x : qa.w, wfx = lx ? qa.w : qa.x;
+    const unsigned int wny = ly ? qa.y : qb.x, wfy = ly ? qb.x : qa.y;
+    const unsigned int wnz = lz ? qa.z : qb.y, wfz = lz ? qb.y : qa.z;
+    const float inf = __int_as_float(0x7f800000);
+    const int rr[4] = {rf.x, rf.y, rf.z, rf.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const float a = fmaxf(fmaxf(fmaf(qbyte(wnx, k), ax, bnx), fmaf(qbyte(wny, k), ay, bny)),
+                              fmaxf(fmaf(qbyte(wnz, k), az, bnz), 0.0f));
+        const float b = fminf(fminf(fmaf(qbyte(wfx, k), ax, bfx), fmaf(qbyte(wfy, k), ay, bfy)),
+                              fminf(fmaf(qbyte(wfz, k), az, bfz), tmax));
+        tn[k] = (a <= b && rr[k] != kEmptyRef) ? a : inf;
+        ref[k] = rr[k];
+    }
+    const int n = (tn[0] != inf) + (tn[1] != inf) + (tn[2] != inf) + (tn[3] != inf);
+    cswap(tn[0], ref[0], tn[1], ref[1]);
+    cswap(tn[2], ref[2], tn[3], ref[3]);
+    cswap(tn[0], ref[0], tn[2], ref[2]);
+    cswap(tn[1], ref[1], tn[3], ref[3]);
+    cswap(tn[1], ref[1], tn[2], ref[2]);
+    return n;
+}
+
+// Visit one quantised BVH8 node (decode as node4q_visit), hit children
+// sorted near -> far by the 19-comparator network of node8_visit.
+__device__ __forceinline__ int node8q_visit(const Node8Q *np, const RayBox &r, float tmax,
+                                            int ref[8], float tn[8])
+{
+    const uint4 h = __ldg(reinterpret_cast<const uint4 *>(np));
+    const int4 r0 = __ldg(&np->ref[0]), r1 = __ldg(&np->ref[1]);
+    const uint4 qa = __ldg(reinterpret_cast<const uint4 *>(np->q));
+    const uint4 qb = __ldg(reinterpret_cast<const uint4 *>(np->q + 4));
+    const uint4 qc = __ldg(reinterpret_cast<const uint4 *>(np->q + 8));
+    // planes: lox = (qa.x, qa.y), loy = (qa.z, qa.w), loz = (qb.x, qb.y),
+    //         hix = (qb.z, qb.w), hiy = (qc.x, qc.y), hiz = (qc.z, qc.w)
+    const float px = __uint_as_float(h.x), py = __uint_as_float(h.y), pz = __uint_as_float(h.z);
+    const float ax = __uint_as_float((h.w & 0xffu) << 23) * r.ix;
+    const float ay = __uint_as_float(((h.w >> 8) & 0xffu) << 23) * r.iy;
+    const float az = __uint_as_float(((h.w >> 16) & 0xffu) << 23) * r.iz;
+    const float bnx = fmaf(px, r.ix, r.nx), bfx = fmaf(px, r.ix, r.fx);
+    const float bny = fmaf(py, r.iy, r.ny), bfy = fmaf(py, r.iy, r.fy);
+    const float bnz = fmaf(pz, r.iz, r.nz), bfz = fmaf(pz, r.iz, r.fz);
+    const bool lx = (r.sel & 7) == 0, ly = ((r.sel >> 3) & 7) == 1, lz = ((r.sel >> 6) & 7) == 2;
+    const unsigned int wnx[2] = {lx ? qa.x : qb.z, lx ? qa.y : qb.w};
+    const unsigned int wfx[2] = {lx ? qb.z : qa.x, lx ? qb.w : qa.y};
+    const unsigned int wny[2] = {ly ? qa.z : qc.x, ly ? qa.w : qc.y};
+    const unsigned int wfy[2] = {ly ? qc.x : qa.z, ly ? qc.y : qa.w};
+    const unsigned int wnz[2] = {lz ? qb.x : qc.z, lz ? qb.y : qc.w};
+    const unsigned int wfz[2] = {lz ? qc.z : qb.x, lz ? qc.w : qb.y};
+    const float inf = __int_as_float(0x7f800000);
+    const int rr[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+    int n = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int hh = k >> 2, kk = k & 3;
+        const float a = fmaxf(fmaxf(fmaf(qbyte(wnx[hh], kk), ax, bnx), fmaf(qbyte(wny[hh], kk), ay, bny)),
+                              fmaxf(fmaf(qbyte(wnz[hh], kk), az, bnz), 0.0f));
+        const float b = fminf(fminf(fmaf(qbyte(wfx[hh], kk), ax, bfx), fmaf(qbyte(wfy[hh], kk), ay, bfy)),
+                              fminf(fmaf(qbyte(wfz[hh], kk), az, bfz), tmax));
+        tn[k] = (a <= b && rr[k] != kEmptyRef) ? a : inf;
+        ref[k] = rr[k];
+        n += tn[k] != inf;
+    }
+#define SBR_CS(i, j) cswap(tn[i], ref[i], tn[j], ref[j]);
+    SBR_CS(0, 2) SBR_CS(1, 3) SBR_CS(4, 6) SBR_CS(5, 7)
+    SBR_CS(0, 4) SBR_CS(1, 5) SBR_CS(2, 6) SBR_CS(3, 7)
+    SBR_CS(0, 1) SBR_CS(2, 3) SBR_CS(4, 5) SBR_CS(6, 7)
+    SBR_CS(2, 4) SBR_CS(3, 5)
+    SBR_CS(1, 4) SBR_CS(3, 6)
+    SBR_CS(1, 2) SBR_CS(3, 4) SBR_CS(5, 6)
+#undef SBR_CS
+    return n;
+}
+
 // width-generic visit used by the traversal loops
 template <int W> struct WideNode;
 template <> struct WideNode<4> {
+#ifdef SBR_NODE_Q
+    using T = Node4Q;
+    static __device__ __forceinline__ int visit(const Node4Q *p, const RayBox &r, float tmax,
+                                                int *ref, float *tn)
+    {
+        return node4q_visit(p, r, tmax, ref, tn);
+    }
+#else
     using T = Node4;
     static __device__ __forceinline__ int visit(const Node4 *p, const RayBox &r, float tmax,
                                                 int *ref, float *tn)
     {
         return node4_visit(p, r, tmax, ref, tn);
     }
+#endif
 };
 template <> struct WideNode<8> {
+#ifdef SBR_NODE_Q
+    using T = Node8Q;
+    static __device__ __forceinline__ int visit(const Node8Q *p, const RayBox &r, float tmax,
+                                                int *ref, float *tn)
+    {
+        return node8q_visit(p, r, tmax, ref, tn);
+    }
+#else
     using T = Node8;
     static __device__ __forceinline__ int visit(const Node8 *p, const RayBox &r, float tmax,
                                                 int *ref, float *tn)
     {
         return node8_visit(p, r, tmax, ref, tn);
     }
+#endif
 };
 
 }  // namespace sbr

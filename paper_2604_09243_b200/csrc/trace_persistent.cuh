@@ -145,8 +145,16 @@ __device__ __forceinline__ bool pop_next(StackEntry *stack, LaneRay &L)
 // faster than unconstrained 80-92 registers despite a few spills, since the
 // traversal is latency-bound.
 template <int W> __device__ __forceinline__ const typename WideNode<W>::T *wide_nodes(const BvhView &B);
+#ifdef SBR_NODE_Q
+template <> __device__ __forceinline__ const Node4Q *wide_nodes<4>(const BvhView &B) { return B.nodes4q; }
+#else
 template <> __device__ __forceinline__ const Node4 *wide_nodes<4>(const BvhView &B) { return B.nodes4; }
+#endif
+#ifdef SBR_NODE_Q
+template <> __device__ __forceinline__ const Node8Q *wide_nodes<8>(const BvhView &B) { return B.nodes8q; }
+#else
 template <> __device__ __forceinline__ const Node8 *wide_nodes<8>(const BvhView &B) { return B.nodes8; }
+#endif
 
 template <int STORAGE, int MODE, int W = 4, int MINB = SBR_TRACE_MINB>
 __global__ void __launch_bounds__(128, MINB)
