@@ -160,7 +160,12 @@ k_po(const SlotRec *__restrict__ slots, const UnitDev *__restrict__ units, int n
     int my_valid = 0;
 #pragma unroll
     for (int q = 0; q < kPerThread; ++q) {
-        const SlotRec r = slots[slot0 + q * kPoThreads + tid];
+        SlotRec r = slots[slot0 + q * kPoThreads + tid];
+        if (r.meta == kMissMeta) {   // primary miss left by k_prim_compact
+            r.R = 0.0;
+            r.cosv = 0.f;
+            r.meta = kMetaActive | kMetaEscaped;
+        }
         rec[q] = r;
         const bool sel = (r.meta & kMetaSel) != 0;
         const unsigned bal = __ballot_sync(0xffffffffu, sel);
@@ -342,8 +347,9 @@ k_po(const SlotRec *__restrict__ slots, const UnitDev *__restrict__ units, int n
 // hit-list compaction after the raster pass
 // ---------------------------------------------------------------------------
 // A slot whose primary ray missed is finished (transport.py:294-296: miss on
-// query 0 -> escaped, invalid, N = 0); write its record here so the trace
-// kernel only ever receives rays with work left.  Hits are appended to the
+// query 0 -> escaped, invalid, N = 0); its all-ones PrimHit stays in place as
+// that record (k_po decodes kMissMeta), so the trace kernel only ever
+// receives rays with work left and misses cost no write.  Hits are appended to the
 // work list 32 slots (one warp ballot) at a time, so consecutive list entries
 // are neighbouring rays of one aperture: coherent first bounces.
 constexpr int kCompactThreads = 256;
@@ -378,11 +384,14 @@ k_prim_compact(TraceCfg cfg, const GridDev *__restrict__ grids,
                 const bool real = r < U.ray_end && alias_ok;
                 const PrimHit h = reinterpret_cast<const PrimHit *>(slots)[slot];
                 hit = real && h.tbits != kNoHitBits;
-                if (!hit) {
+                // a real miss keeps the all-ones PrimHit: k_po reads it as the
+                // finished miss record (kMissMeta); only padding / refused
+                // slots are rewritten
+                if (!real) {
                     SlotRec z;
                     z.R = 0.0;
                     z.cosv = 0.f;
-                    z.meta = real ? (kMetaActive | kMetaEscaped) : 0u;
+                    z.meta = 0u;
                     slots[slot] = z;
                 }
             }

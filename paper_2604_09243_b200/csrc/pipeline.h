@@ -41,6 +41,9 @@ constexpr uint32_t kMetaEscaped = 1u << 17;
 constexpr uint32_t kMetaSel = 1u << 18;
 constexpr uint32_t kMetaActive = 1u << 19;
 constexpr uint32_t kMetaBounceMask = 0xffffu;
+// meta of an all-ones slot (a PrimHit that no triangle reached): a finished
+// primary miss -- no real record has bits 20..31 set
+constexpr uint32_t kMissMeta = 0xffffffffu;
 
 // Primary-visibility result of one ray (query 0), written by the raster
 // pass (128-bit compare-and-swap minimum) and read by the trace kernel.  Aliases the
