@@ -79,3 +79,70 @@ def test_two_ranks_equal_one(mode):
     assert np.array_equal(got[4], sw.amplitude)
     assert np.array_equal(got[5], sw.valid_rays)
     assert np.array_equal(got[6], sw.bounce_histogram)
+
+
+def _emulated_ranks(sbr, mesh, tree, grids, tp, ks, world, mode):
+    """Every rank's sbr_solve_shard run in turn in this process, partials
+    combined as reduce_partials does (SUM; MAX for the max-bounce column)."""
+    import ctypes
+    import torch
+    from paper_2604_09243_b200 import _native as nat, distributed as D
+    from paper_2604_09243_b200.sweep import grid_array
+    ctx = nat.context()
+    d = tree.device(mesh, ctx)
+    k = nat.f64(ks)
+    base = D.segment_layout(grids)
+    garr = grid_array(grids)
+    cp = nat.make_trace_params(tp.max_bounces, tp.resolve_epsilon(mesh), False, True, 0.0, 5.0)
+    seg_sum = diag_sum = None
+    for r in range(world):
+        seg = torch.zeros(int(base[-1]) * k.size * 2, dtype=torch.float64, device="cuda")
+        diag = torch.zeros((len(grids), D.diag_stride(tp.max_bounces)), dtype=torch.int64,
+                           device="cuda")
+        nat.check(ctx.lib.sbr_solve_shard(ctx.handle, d.mesh_dev.handle, d.handle, garr,
+                                          len(grids), ctypes.byref(cp), nat.ptr(k), k.size, -1.0,
+                                          0, r, world, D.MODES[mode], nat.c_vp(seg.data_ptr()),
+                                          nat.c_vp(diag.data_ptr())), "sbr_solve_shard")
+        ctx.synchronize()
+        if seg_sum is None:
+            seg_sum, diag_sum = seg.clone(), diag.clone()
+        else:
+            # disjoint support: at most one rank wrote each element
+            assert not bool(((seg_sum != 0) & (seg != 0)).any())
+            seg_sum += seg
+            mx = torch.maximum(diag_sum[:, 2], diag[:, 2])
+            diag_sum += diag
+            diag_sum[:, 2] = mx
+    ng, B = len(grids), tp.max_bounces
+    amp = np.zeros((ng, k.size, 2))
+    valid = np.zeros(ng, np.int64)
+    maxb = np.zeros(ng, np.int32)
+    hist = np.zeros((ng, B + 1), np.int64)
+    queries = np.zeros(ng, np.int64)
+    dg = nat.Diag(valid.ctypes.data, maxb.ctypes.data, hist.ctypes.data, queries.ctypes.data)
+    nat.check(ctx.lib.sbr_finalize(ctx.handle, garr, ng, nat.ptr(k), k.size, B,
+                                   nat.c_vp(seg_sum.data_ptr()), nat.c_vp(diag_sum.data_ptr()),
+                                   nat.ptr(amp), ctypes.byref(dg)), "sbr_finalize")
+    return amp.view(np.complex128)[..., 0], valid, maxb, hist, queries
+
+
+@pytest.mark.parametrize("world,mode", [(3, "rays"), (5, "rays"), (8, "rays"), (7, "angles")])
+def test_emulated_ranks_equal_one(world, mode):
+    """N-rank shards (ray tiles cut through triangles' candidate rows, big
+    triangles' chunk queues and grid boundaries) recombine bit for bit."""
+    import paper_2604_09243_b200 as sbr
+    from paper_2604_09243_b200 import meshgen
+    mesh = meshgen.generate_aircraft(density=0.05)
+    lam = 0.04
+    grids = [sbr.build_aperture(mesh.aabb, sbr.IncidentDirection(th, ph), lam / 5, wavelength=lam)
+             for th, ph in ((math.pi / 2, 0.3), (1.1, 2.0), (math.pi / 2, 4.4))]
+    tp = sbr.TraceParams(max_bounces=3)
+    ks = 2 * np.pi / (lam * np.array([0.99, 1.0]))
+    tree = sbr.build(mesh)
+    got = _emulated_ranks(sbr, mesh, tree, grids, tp, ks, world, mode)
+    ref = sbr.solve_grids(tree, mesh, grids, tp, ks)
+    assert np.array_equal(got[0], ref.amplitude)
+    assert np.array_equal(got[1], ref.valid_rays)
+    assert np.array_equal(got[2], ref.max_bounce)
+    assert np.array_equal(got[3], ref.bounce_counts)
+    assert np.array_equal(got[4], ref.queries)
