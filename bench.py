@@ -173,13 +173,19 @@ def cpu_run(scene, eps, lam, phis, bands, band_rows):
     return queries, rays, time.perf_counter() - t0
 
 
+def host_cores():
+    # the threads the oracle runs with (oracle._threads(0)): every core this
+    # process may use, whatever OMP_NUM_THREADS a launcher exported
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     mesh, lam, cfg = workload(args.density, args.angles)
     scene, eps, build_s, phis = cpu_sample(mesh, lam, cfg)
-    cores = os.cpu_count() or 1
+    cores = host_cores()
     for _ in range(max(args.warmup, 0)):
         cpu_run(scene, eps, lam, phis[:1], 4, 32)
     q = r = 0
@@ -229,9 +235,17 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # SBR_BENCH_SHARE_GPU=1 (testing the N-rank path on a 1-GPU box): every
+    # rank on cuda:0 over gloo -- NCCL refuses two ranks on one device
+    share = os.environ.get("SBR_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ctx = nat.context(local)
 
     mesh, lam, cfg = workload(args.density, args.angles, args.bounces, args.n_leaf)
@@ -284,7 +298,7 @@ def main():
     clk = clocks.stop()
     kst = ctx.kernel_stats()
     if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cpu" if share else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
 
@@ -310,7 +324,7 @@ def main():
             torch.cuda.synchronize()
             dt = time.perf_counter() - t0
             if world > 1:
-                tt = torch.tensor([dt], dtype=torch.float64, device="cuda")
+                tt = torch.tensor([dt], dtype=torch.float64, device="cpu" if share else "cuda")
                 dist.all_reduce(tt, op=dist.ReduceOp.MAX)
                 dt = float(tt.item())
             if rep == 0:
@@ -379,7 +393,7 @@ def main():
         scene, eps, build_s, phis = cpu_sample(mesh, lam, cfg)
         q, r, t = cpu_run(scene, eps, lam, phis, 16, 64)
         line["cpu_baseline"] = {
-            "value": q / t, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port",
+            "value": q / t, "unit": UNIT, "cores": host_cores(), "kind": "port",
             "sample": f"{len(phis)} azimuths x 16 row bands of 64 rows ({r} rays, {q} queries) "
                       f"of the same sweep, reference SAH tree (built in {build_s:.2f} s, not "
                       "timed), oracle/ C port of the numba kernels, OpenMP all cores"}

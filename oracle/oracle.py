@@ -79,7 +79,11 @@ def _f64(a, shape=None):
 
 
 def _threads(n):
-    return int(n) if n else 0
+    # 0 = every host core.  Resolved here rather than by omp_get_max_threads():
+    # launchers such as torchrun export OMP_NUM_THREADS=1, which would time
+    # the reference CPU path on one core.
+    return int(n) if n else (len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity")
+                             else (os.cpu_count() or 1))
 
 
 # ---------------------------------------------------------------------------
