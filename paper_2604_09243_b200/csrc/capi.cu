@@ -89,7 +89,7 @@ struct sbr_ctx {
     DevBuf<int64_t> seg_base;
     DevBuf<int64_t> seg_slot;    // raster pass: global segment row -> slot offset
     DevBuf<int> bgrids;          // raster pass: grids of the current batch
-    DevBuf<unsigned int> worklist;          // raster pass: slots whose query 0 hit
+    DevBuf<uint2> worklist;                 // raster pass: (slot, unit) whose query 0 hit
     DevBuf<unsigned long long> nwork;
     DevBuf<int4> big;                       // raster pass: big-triangle chunk queue
     DevBuf<unsigned long long> nbig;

@@ -359,7 +359,7 @@ constexpr int kCompactTile = kCompactThreads * kCompactPer;   // == kChunk
 __global__ void __launch_bounds__(kCompactThreads)
 k_prim_compact(TraceCfg cfg, const GridDev *__restrict__ grids,
                const UnitDev *__restrict__ units, int n_units, int64_t n_slots,
-               SlotRec *__restrict__ slots, unsigned int *__restrict__ list,
+               SlotRec *__restrict__ slots, uint2 *__restrict__ list,
                unsigned long long *__restrict__ nlist)
 {
     constexpr int W = kCompactThreads / 32;
@@ -370,7 +370,8 @@ k_prim_compact(TraceCfg cfg, const GridDev *__restrict__ grids,
     for (int64_t tile = (int64_t)blockIdx.x * kCompactTile; tile < n_slots;
          tile += (int64_t)gridDim.x * kCompactTile) {
         // slots are chunk-aligned per unit and kCompactTile == kChunk: one unit
-        const UnitDev U = units[find_unit(units, n_units, tile)];
+        const int ui = find_unit(units, n_units, tile);
+        const UnitDev U = units[ui];
         const bool alias_ok =
             cfg.allow_aliasing || !(grids[U.grid].spacing > cfg.spacing_limit);
         if (!alias_ok && tid == 0) atomicOr(cfg.error_flag, 1u);
@@ -417,7 +418,7 @@ k_prim_compact(TraceCfg cfg, const GridDev *__restrict__ grids,
             const unsigned bal = __ballot_sync(0xffffffffu, hit);
             if (hit)
                 list[at + pos[q][warp] + __popc(bal & ((1u << lane) - 1u))] =
-                    (unsigned int)(tile + q * kCompactThreads + tid);
+                    make_uint2((unsigned int)(tile + q * kCompactThreads + tid), (unsigned int)ui);
         }
         __syncthreads();
     }
@@ -425,7 +426,7 @@ k_prim_compact(TraceCfg cfg, const GridDev *__restrict__ grids,
 
 cudaError_t launch_prim_compact(const TraceCfg &cfg, const GridDev *d_grids,
                                 const UnitDev *d_units, int n_units, int64_t n_slots,
-                                SlotRec *d_slots, unsigned int *d_worklist,
+                                SlotRec *d_slots, uint2 *d_worklist,
                                 unsigned long long *d_nwork, cudaStream_t st,
                                 const LaunchStats &ls)
 {
@@ -557,7 +558,7 @@ static void trace_storage_dispatch(const TraceArgs &a, cudaStream_t st, int num_
 cudaError_t launch_trace_solve(const TraceCfg &cfg, const GridDev *d_grids,
                                const UnitDev *d_units, int n_units, int64_t n_slots,
                                SlotRec *d_slots, unsigned long long *d_counter,
-                               bool prim_from_slots, const unsigned int *d_worklist,
+                               bool prim_from_slots, const uint2 *d_worklist,
                                const unsigned long long *d_nwork, cudaStream_t st,
                                const LaunchStats &ls)
 {

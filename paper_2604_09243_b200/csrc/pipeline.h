@@ -81,7 +81,7 @@ struct LaunchStats {
 cudaError_t launch_trace_solve(const TraceCfg &cfg, const GridDev *d_grids,
                                const UnitDev *d_units, int n_units, int64_t n_slots,
                                SlotRec *d_slots, unsigned long long *d_counter,
-                               bool prim_from_slots, const unsigned int *d_worklist,
+                               bool prim_from_slots, const uint2 *d_worklist,
                                const unsigned long long *d_nwork, cudaStream_t st,
                                const LaunchStats &ls);
 
@@ -89,7 +89,7 @@ cudaError_t launch_trace_solve(const TraceCfg &cfg, const GridDev *d_grids,
 // missed slots, and the list of slots whose query 0 hit (warp-ordered).
 cudaError_t launch_prim_compact(const TraceCfg &cfg, const GridDev *d_grids,
                                 const UnitDev *d_units, int n_units, int64_t n_slots,
-                                SlotRec *d_slots, unsigned int *d_worklist,
+                                SlotRec *d_slots, uint2 *d_worklist,
                                 unsigned long long *d_nwork, cudaStream_t st,
                                 const LaunchStats &ls);
 

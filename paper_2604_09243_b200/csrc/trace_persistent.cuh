@@ -64,7 +64,7 @@ struct TraceArgs {
     const PrimHit *prim;
     // solve + raster: the slots whose query 0 hit (k_prim_compact); the other
     // slots already hold their final records.  n_work is read from n_work_dev.
-    const unsigned int *worklist;
+    const uint2 *worklist;    // (slot, unit index)
     const unsigned long long *n_work_dev;
     // outputs
     SlotRec *slots;           // solve
@@ -189,11 +189,21 @@ k_trace_persistent(TraceArgs a)
                 if (lane == 0) base = atomicAdd(a.counter, (unsigned long long)kChunkRays);
                 fresh = (int64_t)__shfl_sync(0xffffffffu, base, 0);
             }
+            int wl_unit = -1;
             if (want & (1u << lane)) {
                 const int rank = __popc(want & lt_mask);
                 const int64_t w = rank < avail ? chunk_next + rank : fresh + (rank - avail);
-                if (w < n_work) L.slot = a.worklist ? (int64_t)__ldg(&a.worklist[w]) : w;
-                else exhausted = true;
+                if (w < n_work) {
+                    if (a.worklist) {
+                        const uint2 e = __ldg(&a.worklist[w]);
+                        L.slot = (int64_t)e.x;
+                        wl_unit = (int)e.y;
+                    } else {
+                        L.slot = w;
+                    }
+                } else {
+                    exhausted = true;
+                }
             }
             if (avail >= need) {
                 chunk_next += need;
@@ -206,7 +216,7 @@ k_trace_persistent(TraceArgs a)
                 bool real = true;
                 const GridDev *G = nullptr;
                 if (MODE == kModeSolve) {
-                    const int ui = find_unit(a.units, a.n_units, L.slot);
+                    const int ui = wl_unit >= 0 ? wl_unit : find_unit(a.units, a.n_units, L.slot);
                     const UnitDev U = a.units[ui];
                     L.r = U.ray_begin + (L.slot - U.slot_base);
                     L.grid = U.grid;
