@@ -198,6 +198,11 @@ k_trace_persistent(TraceArgs a)
                         const uint2 e = __ldg(&a.worklist[w]);
                         L.slot = (int64_t)e.x;
                         wl_unit = (int)e.y;
+                        // listed slots are raster hits: their query-0 result is
+                        // loaded now, beside the unit / grid loads below
+                        const PrimHit h = a.prim[L.slot];
+                        L.best_t = __longlong_as_double((long long)h.tbits);
+                        L.best = (int)h.id;
                     } else {
                         L.slot = w;
                     }
@@ -254,7 +259,9 @@ k_trace_persistent(TraceArgs a)
                     }
                     L.path = 0.0; L.n0x = L.n0y = L.n0z = 0.0; L.cosd = 0.0;
                     L.bounces = 0; L.valid = false; L.probe = false;
-                    if (MODE != kModeList && a.prim) {
+                    if (MODE == kModeSolve && wl_unit >= 0) {
+                        state = kDone;   // query 0 answered by the raster pass (loaded above)
+                    } else if (MODE != kModeList && a.prim) {
                         // query 0 already answered by the raster pass
                         const PrimHit h = a.prim[MODE == kModeSolve ? L.slot : L.r];
                         const bool hit = h.tbits != kNoHitBits;
