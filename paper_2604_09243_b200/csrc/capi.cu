@@ -1063,6 +1063,8 @@ static int64_t slot_budget()
     const char *s = getenv("SBR_SLOT_BUDGET");
     int64_t v = s ? atoll(s) : ((int64_t)1 << 30);
     if (v < kChunk) v = kChunk;
+    // work-list entries and the raster's slot arithmetic hold 32-bit slots
+    if (v > ((int64_t)1 << 31)) v = (int64_t)1 << 31;
     return round_chunk(v);
 }
 
