@@ -166,3 +166,39 @@ def test_aircraft_generator_deterministic():
     assert a.triangle_count > 5000
     soup = np.concatenate([a.v0, a.v1, a.v2])
     assert np.array_equal(soup.astype(np.float32).astype(np.float64), soup)
+
+
+# ---- "never traces" contract (reference test_sweep.py:88-98, 163-170) -----
+def _plate_config(tmp_path, **extra):
+    p = tmp_path / "plate.obj"
+    sbr.save_obj(meshgen.plate_mesh(1.0), p)
+    doc = {"mesh": str(p), "frequency_hz": sbr.SPEED_OF_LIGHT / 0.2,
+           "theta_deg": {"start_deg": 0, "stop_deg": 40, "samples": 2},
+           "phi_deg": {"start_deg": 0, "stop_deg": 90, "samples": 2}, "max_bounces": 3}
+    doc.update(extra)
+    return sbr.SweepConfig.from_dict(doc)
+
+
+def _forbid_tracing(monkeypatch):
+    import paper_2604_09243_b200.sweep as sweep_mod
+
+    def boom(*a, **k):
+        raise AssertionError("trace path invoked")
+
+    # the per-angle tracer (reference symbol) and the fused GPU solver
+    monkeypatch.setattr(sweep_mod, "trace_grid", boom)
+    monkeypatch.setattr(sweep_mod, "solve_grids", boom)
+
+
+def test_dry_run_never_traces(tmp_path, monkeypatch):
+    _forbid_tracing(monkeypatch)
+    from paper_2604_09243_b200.sweep import dry_run_summary
+    summary = dry_run_summary(_plate_config(tmp_path))
+    assert summary["angles"] == 4
+    assert summary["triangles"] == 2
+
+
+def test_sampling_violation_aborts_before_trace(tmp_path, monkeypatch):
+    _forbid_tracing(monkeypatch)
+    with pytest.raises(sbr.ValidationError):
+        sbr.run_sweep(_plate_config(tmp_path, spacing_m=0.15))
