@@ -226,6 +226,9 @@ def _area(lo, hi) -> float:
     return float(2.0 * (e[0] * e[1] + e[1] * e[2] + e[2] * e[0]))
 
 
+_box_surface_area = _area   # the reference's private name (bvh.py:130-132)
+
+
 def median_split(centroids: np.ndarray, node_box: Aabb):
     """Median partition on the longest box axis (bvh.py:135-151):
     ``(axis, left_positions, right_positions)`` or None if all coincide."""
