@@ -115,6 +115,10 @@ int sbr_abi_version(void);
 int sbr_ctx_create(int device, sbr_ctx **out);
 int sbr_ctx_destroy(sbr_ctx *ctx);
 int sbr_ctx_synchronize(sbr_ctx *ctx);
+/* Release the context's grow-only scratch (solve slots and work list, build
+ * workspaces, staging and pinned upload buffers) back to the device pool;
+ * the next call re-grows what it needs.  Meshes and trees are untouched. */
+int sbr_ctx_trim(sbr_ctx *ctx);
 /* Stream the library launches on (cudaStream_t as void*). */
 int sbr_ctx_stream(sbr_ctx *ctx, void **stream_out);
 /* Number of kernels this context has launched (instrumentation). */

@@ -67,6 +67,7 @@ _SIGS = {
     "sbr_ctx_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(c_vp)]),
     "sbr_ctx_destroy": (ctypes.c_int, [c_vp]),
     "sbr_ctx_synchronize": (ctypes.c_int, [c_vp]),
+    "sbr_ctx_trim": (ctypes.c_int, [c_vp]),
     "sbr_ctx_stream": (ctypes.c_int, [c_vp, ctypes.POINTER(c_vp)]),
     "sbr_ctx_launch_count": (ctypes.c_int, [c_vp, ctypes.POINTER(c_i64)]),
     "sbr_ctx_profile": (ctypes.c_int, [c_vp, c_i32]),
@@ -220,6 +221,11 @@ class Context:
 
     def synchronize(self):
         check(self.lib.sbr_ctx_synchronize(self.handle))
+
+    def trim(self):
+        """Return the grow-only solve/build scratch to the device (the next
+        call re-grows it); meshes and trees stay resident."""
+        check(self.lib.sbr_ctx_trim(self.handle), "sbr_ctx_trim")
 
     @property
     def launches(self) -> int:

@@ -249,6 +249,33 @@ extern "C" int sbr_ctx_synchronize(sbr_ctx *ctx)
     return SBR_OK;
 }
 
+extern "C" int sbr_ctx_trim(sbr_ctx *ctx)
+{
+    REQUIRE(ctx, "ctx is NULL");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (int rc = set_device(ctx)) return rc;
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    ctx->slots.release(); ctx->units.release(); ctx->grids.release();
+    ctx->chunk_part.release(); ctx->seg_part.release(); ctx->diag.release();
+    ctx->seg_base.release(); ctx->seg_slot.release(); ctx->bgrids.release();
+    ctx->worklist.release(); ctx->big.release(); ctx->amp.release(); ctx->stage.release();
+    ctx->ws.buf.release();
+    ctx->ws.off = 0;
+    ctx->sah = SahWork();
+    for (int b = 0; b < 2; ++b) {
+        if (ctx->pin[b]) cudaFreeHost(ctx->pin[b]);
+        if (ctx->pin_ev[b]) cudaEventDestroy(ctx->pin_ev[b]);
+        ctx->pin[b] = nullptr;
+        ctx->pin_ev[b] = nullptr;
+    }
+    // hand the freed blocks back to the device (release threshold is "keep")
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, ctx->device) == cudaSuccess)
+        cudaMemPoolTrimTo(pool, 0);
+    return SBR_OK;
+}
+
 extern "C" int sbr_ctx_stream(sbr_ctx *ctx, void **stream_out)
 {
     REQUIRE(ctx && stream_out, "NULL argument");
