@@ -68,6 +68,7 @@ struct RasterSetup {
     double inv;
     long long i0, j0, count;
     int cols;
+    double pa[3], pb[3];   // projected vertices in cell units (row a, column b)
 };
 
 __device__ __forceinline__ RasterSetup raster_setup(const TriF64 &T, const GridDev &G)
@@ -86,6 +87,8 @@ __device__ __forceinline__ RasterSetup raster_setup(const TriF64 &T, const GridD
     const double b1 = b0 + (T.e1x * G.v[0] + T.e1y * G.v[1] + T.e1z * G.v[2]) * isp;
     const double a2 = a0 + (T.e2x * G.u[0] + T.e2y * G.u[1] + T.e2z * G.u[2]) * isp;
     const double b2 = b0 + (T.e2x * G.v[0] + T.e2y * G.v[1] + T.e2z * G.v[2]) * isp;
+    S.pa[0] = a0; S.pa[1] = a1; S.pa[2] = a2;
+    S.pb[0] = b0; S.pb[1] = b1; S.pb[2] = b2;
     const double alo = fmin(fmin(a0, a1), a2) - kMargin;
     const double ahi = fmax(fmax(a0, a1), a2) + kMargin;
     const double blo = fmin(fmin(b0, b1), b2) - kMargin;
@@ -169,6 +172,35 @@ __device__ __forceinline__ void raster_cell(const RasterArgs &a, const GridDev &
     if (t > 0.0 && t < inf && off != kNoSlot)
         prim_min(a.prim + (off + r), (unsigned long long)__double_as_longlong(t),
                  (unsigned int)id);
+}
+
+// Column extent of the cells of row a within kMargin (L-inf) of the
+// projected triangle: the b-range of the triangle clipped to the band
+// |a' - a| <= kMargin (its extreme points are vertices inside the band or
+// edge / band-boundary crossings), widened by kMargin.  The exact test can
+// only accept cells within rounding (<< kMargin) of the triangle, so this
+// span holds every cell the bounding box would have offered that can hit.
+__device__ __forceinline__ void row_span(const RasterSetup &S, double a, double &blo, double &bhi)
+{
+    double lo = __longlong_as_double(0x7ff0000000000000LL), hi = -lo;
+    const double c[2] = {a - kMargin, a + kMargin};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const int k1 = k == 2 ? 0 : k + 1;
+        if (S.pa[k] >= c[0] && S.pa[k] <= c[1]) { lo = fmin(lo, S.pb[k]); hi = fmax(hi, S.pb[k]); }
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const double d0 = S.pa[k] - c[e], d1 = S.pa[k1] - c[e];
+            if ((d0 < 0.0 && d1 > 0.0) || (d0 > 0.0 && d1 < 0.0)) {
+                const double t = d0 / (d0 - d1);   // in (0, 1)
+                const double b = S.pb[k] + t * (S.pb[k1] - S.pb[k]);
+                lo = fmin(lo, b);
+                hi = fmax(hi, b);
+            }
+        }
+    }
+    blo = lo - kMargin;
+    bhi = hi + kMargin;
 }
 
 // Persistent: each warp pulls its next 32-triangle item from a global
@@ -303,10 +335,46 @@ k_raster_big(RasterArgs a)
         if (a.sparse) trim_owned(S, G, seg);
         const long long c0 = (long long)it.z * kBigChunk;
         const long long c1 = c0 + kBigChunk < S.count ? c0 + kBigChunk : S.count;
-        for (long long c = c0 + lane; c < c1; c += 32) {
-            long long li, lj;
-            split_cell(c, S.cols, li, lj);
-            raster_cell(a, G, seg, S.T, S.P, S.inv, S.T.id, S.i0 + li, S.j0 + lj);
+        if (c0 >= c1) continue;
+        // the chunk's rows, 32 at a time: lane r takes row r's cells that
+        // lie within kMargin of the triangle (not the whole box row), then
+        // the warp walks the concatenated spans 32 cells at a time
+        const long long row_a = c0 / S.cols, row_b = (c1 - 1) / S.cols;
+        for (long long rbase = row_a; rbase <= row_b; rbase += 32) {
+            const long long li = rbase + lane;
+            long long jl = 0, jr = -1;
+            if (li <= row_b) {
+                const long long wl = li == row_a ? c0 % S.cols : 0;
+                const long long wr = li == row_b ? (c1 - 1) % S.cols : S.cols - 1;
+                double blo, bhi;
+                row_span(S, (double)(S.i0 + li), blo, bhi);
+                const long long sl = blo > (double)(S.j0 + wl) ? (long long)ceil(blo) - S.j0 : wl;
+                const long long sr = bhi < (double)(S.j0 + wr) ? (long long)floor(bhi) - S.j0 : wr;
+                jl = sl;
+                jr = sr;
+            }
+            const int cnt = jr >= jl ? (int)(jr - jl + 1) : 0;
+            int incl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const int total = __shfl_sync(0xffffffffu, incl, 31);
+            const int excl = incl - cnt;
+            const int jl32 = (int)jl;
+            for (int base = 0; base < total; base += 32) {
+                const int c = base + lane;
+                int owner = 0;   // first lane whose inclusive count exceeds c
+#pragma unroll
+                for (int st = 16; st >= 1; st >>= 1)
+                    if (__shfl_sync(0xffffffffu, incl, owner + st - 1) <= c) owner += st;
+                const int oex = __shfl_sync(0xffffffffu, excl, owner);
+                const int ojl = __shfl_sync(0xffffffffu, jl32, owner);
+                if (c < total)
+                    raster_cell(a, G, seg, S.T, S.P, S.inv, S.T.id, S.i0 + rbase + owner,
+                                S.j0 + ojl + (c - oex));
+            }
         }
     }
 }
