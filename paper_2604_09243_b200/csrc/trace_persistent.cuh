@@ -292,9 +292,6 @@ k_trace_persistent(TraceArgs a)
             const unsigned trav = __ballot_sync(0xffffffffu, state == kTrav && L.pend == 0);
             if (!trav) break;
             if (__popc(__ballot_sync(0xffffffffu, state == kDone)) >= kDoneBreak) break;
-#ifdef SBR_TRAV_MIN
-            if (__popc(trav) < SBR_TRAV_MIN) break;
-#endif
 #ifdef SBR_TRACE_STATS
             {   // lane-state census per traversal step (stats build only)
                 const unsigned act = __ballot_sync(0xffffffffu, state == kTrav && L.pend == 0);
