@@ -123,7 +123,8 @@ constexpr int kPoWarps = kPoThreads / 32;
 constexpr int kPerThread = kChunk / kPoThreads;   // 4
 constexpr int kMaxHist = 64;                      // bounce histogram bins in smem
 
-template <int FPT>
+// ROT: equally spaced wavenumbers, phases by rotation recurrence (FPT > 1)
+template <int FPT, bool ROT>
 __global__ void __launch_bounds__(kPoThreads)
 k_po(const SlotRec *__restrict__ slots, const UnitDev *__restrict__ units, int n_units,
      const double *__restrict__ kturn, int nk, double dkturn, const double *__restrict__ gpow,
@@ -261,17 +262,21 @@ k_po(const SlotRec *__restrict__ slots, const UnitDev *__restrict__ units, int n
         const bool active = grp < G && (G >= kPoWarps || warp < G * wpg);
         // phase 2 k R in turns: tau = (k / pi) R, reduced exactly in FP64
         // (tau - rint(tau) has no rounding error), then one float conversion
-        // and __sincosf on the SFU; a lane's <= 32 terms per chunk accumulate
-        // in FP32 (error comparable to the SFU's), cross-lane sums in FP64
-        float sacc[FPT], cacc[FPT];
         double kk[FPT];
+        double sred[FPT], cred[FPT];   // this lane's sums (FP64)
 #pragma unroll
         for (int f = 0; f < FPT; ++f) {
-            sacc[f] = 0.f; cacc[f] = 0.f;
             const int fi = grp * FPT + f;
             kk[f] = (active && fi < nk) ? kturn[fi] : 0.0;
+            sred[f] = 0.0;
+            cred[f] = 0.0;
         }
-        if (active && FPT > 1 && dkturn != 0.0) {
+        if (ROT && active) {
+            // __sincosf on the SFU; a lane's <= 32 terms per chunk accumulate
+            // in FP32 (error comparable to the SFU's)
+            float sacc[FPT], cacc[FPT];
+#pragma unroll
+            for (int f = 0; f < FPT; ++f) { sacc[f] = 0.f; cacc[f] = 0.f; }
             // equally spaced wavenumbers: one SFU sincos for the group's first
             // phase and one for the step, then FPT-1 exact-phase rotations
             // (FP32 complex products, error <= FPT ulps), re-anchored per group
@@ -291,26 +296,30 @@ k_po(const SlotRec *__restrict__ slots, const UnitDev *__restrict__ units, int n
                     sn = s2;
                 }
             }
-        } else if (active) {
+#pragma unroll
+            for (int f = 0; f < FPT; ++f) { sred[f] = (double)sacc[f]; cred[f] = (double)cacc[f]; }
+        } else if (!ROT && active) {
+            // per-frequency phases: sincospif of the FP32 fraction (~1 ulp; the
+            // factor 2 pi is folded into the function, not rounded into the
+            // argument) and FP32 x FP32 products (exact in FP64) accumulated
+            // in FP64 -- within 1e-4 relative field even at the near-nulls
+            // of a 2M-ray aperture (scripts/parity_c4_full.py)
             for (int m = sub * 32 + lane; m < M; m += wpg * 32) {
                 const double2 rw = srec[m];
-                const float wf = (float)rw.y;
+                const double wd = (double)(float)rw.y;
 #pragma unroll
                 for (int f = 0; f < FPT; ++f) {
                     const double tau = kk[f] * rw.x;
                     const float fr = (float)(tau - rint(tau));
                     float sn, cs;
-                    __sincosf(fr * 6.28318530717958648f, &sn, &cs);
-                    sacc[f] = fmaf(wf, sn, sacc[f]);
-                    cacc[f] = fmaf(wf, cs, cacc[f]);
+                    sincospif(2.0f * fr, &sn, &cs);
+                    sred[f] = fma(wd, (double)sn, sred[f]);
+                    cred[f] = fma(wd, (double)cs, cred[f]);
                 }
             }
         }
-        double sred[FPT], cred[FPT];
 #pragma unroll
         for (int f = 0; f < FPT; ++f) {
-            sred[f] = (double)sacc[f];
-            cred[f] = (double)cacc[f];
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
                 sred[f] += __shfl_xor_sync(0xffffffffu, sred[f], o);
@@ -646,18 +655,15 @@ cudaError_t launch_po(const SlotRec *d_slots, const UnitDev *d_units, int n_unit
 {
     if (n_chunks <= 0) return cudaSuccess;
     dim3 grid((unsigned)n_chunks);
-    if (nk >= 8)
-        k_po<8><<<grid, kPoThreads, 0, st>>>(d_slots, d_units, n_units, d_k2, nk, dkturn, d_gpow,
-                                             max_bounces, d_chunk_part, d_diag, d_bad);
-    else if (nk >= 4)
-        k_po<4><<<grid, kPoThreads, 0, st>>>(d_slots, d_units, n_units, d_k2, nk, dkturn, d_gpow,
-                                             max_bounces, d_chunk_part, d_diag, d_bad);
-    else if (nk >= 2)
-        k_po<2><<<grid, kPoThreads, 0, st>>>(d_slots, d_units, n_units, d_k2, nk, dkturn, d_gpow,
-                                             max_bounces, d_chunk_part, d_diag, d_bad);
-    else
-        k_po<1><<<grid, kPoThreads, 0, st>>>(d_slots, d_units, n_units, d_k2, nk, dkturn, d_gpow,
-                                             max_bounces, d_chunk_part, d_diag, d_bad);
+    const bool rot = nk > 1 && dkturn != 0.0;
+#define SBR_PO(F, R)                                                                       \
+    k_po<F, R><<<grid, kPoThreads, 0, st>>>(d_slots, d_units, n_units, d_k2, nk, dkturn,    \
+                                            d_gpow, max_bounces, d_chunk_part, d_diag, d_bad)
+    if (nk >= 8) { if (rot) SBR_PO(8, true); else SBR_PO(8, false); }
+    else if (nk >= 4) { if (rot) SBR_PO(4, true); else SBR_PO(4, false); }
+    else if (nk >= 2) { if (rot) SBR_PO(2, true); else SBR_PO(2, false); }
+    else SBR_PO(1, false);
+#undef SBR_PO
     ++*ls.launches;
     return cudaGetLastError();
 }
