@@ -6,14 +6,15 @@
 //                  from the grid scalars (transport.py:339-345, no launch
 //                  record is materialised), walks up to B bounces
 //                  (transport.py:276-327) and stores a 16-byte SlotRec.
-//   k_po           one block per 2048-slot chunk: coalesced SlotRec loads,
+//   k_po           one block per 1024-slot chunk: coalesced SlotRec loads,
 //                  warp __ballot_sync + popc + block scan compact the
 //                  selected records (po.py:96-101) into shared memory in
 //                  slot order, then evaluates (po.py:105-108)
 //                    term_f = j k_f dA/4pi * 2 cos Gamma^N exp(-2j k_f R)
 //                  for nk wavenumbers: phase in turns reduced exactly in
-//                  FP64, FP32 __sincosf on the SFU, per-lane FP32 then FP64
-//                  accumulation, warp shuffle tree, fixed cross-warp order.
+//                  FP64; sincospif + FP64 lane sums per wavenumber, or (a
+//                  uniform sweep) SFU __sincosf anchors + FP32 rotations and
+//                  lane sums; warp shuffle tree, fixed cross-warp order.
 //   k_seg_reduce / k_finalize  fixed pairwise trees (po.py:59-80 shape)
 //                  over chunk -> segment -> grid partials: results are
 //                  bit-stable and independent of GPU count.
