@@ -12,7 +12,7 @@
 //                  slot order, then evaluates (po.py:105-108)
 //                    term_f = j k_f dA/4pi * 2 cos Gamma^N exp(-2j k_f R)
 //                  for nk wavenumbers: phase in turns reduced exactly in
-//                  FP64; sincospif + FP64 lane sums per wavenumber, or (a
+//                  FP64; FP64 sincospi + lane sums per wavenumber, or (a
 //                  uniform sweep) SFU __sincosf anchors + FP32 rotations and
 //                  lane sums; warp shuffle tree, fixed cross-warp order.
 //   k_seg_reduce / k_finalize  fixed pairwise trees (po.py:59-80 shape)
@@ -300,22 +300,20 @@ k_po(const SlotRec *__restrict__ slots, const UnitDev *__restrict__ units, int n
 #pragma unroll
             for (int f = 0; f < FPT; ++f) { sred[f] = (double)sacc[f]; cred[f] = (double)cacc[f]; }
         } else if (!ROT && active) {
-            // per-frequency phases: sincospif of the FP32 fraction (~1 ulp; the
-            // factor 2 pi is folded into the function, not rounded into the
-            // argument) and FP32 x FP32 products (exact in FP64) accumulated
-            // in FP64 -- within 1e-4 relative field even at the near-nulls
-            // of a 2M-ray aperture (scripts/parity_c4_full.py)
+            // per-frequency phases in FP64: sincospi of twice the exactly
+            // reduced fraction (2 pi folded into the function), FP64 lane
+            // sums -- the field follows the reference's complex128 sum to
+            // ~1e-12 even at deep nulls, where any FP32 phase (1e-7 per term)
+            // breaks a 1e-4 relative tolerance (scripts/parity_full_configs.py)
             for (int m = sub * 32 + lane; m < M; m += wpg * 32) {
                 const double2 rw = srec[m];
-                const double wd = (double)(float)rw.y;
 #pragma unroll
                 for (int f = 0; f < FPT; ++f) {
                     const double tau = kk[f] * rw.x;
-                    const float fr = (float)(tau - rint(tau));
-                    float sn, cs;
-                    sincospif(2.0f * fr, &sn, &cs);
-                    sred[f] = fma(wd, (double)sn, sred[f]);
-                    cred[f] = fma(wd, (double)cs, cred[f]);
+                    double sn, cs;
+                    sincospi(2.0 * (tau - rint(tau)), &sn, &cs);
+                    sred[f] = fma(rw.y, sn, sred[f]);
+                    cred[f] = fma(rw.y, cs, cred[f]);
                 }
             }
         }
