@@ -654,7 +654,10 @@ cudaError_t launch_po(const SlotRec *d_slots, const UnitDev *d_units, int n_unit
 {
     if (n_chunks <= 0) return cudaSuccess;
     dim3 grid((unsigned)n_chunks);
-    const bool rot = nk > 1 && dkturn != 0.0;
+    // uniform sweeps take the SFU rotation path (~1e-5 relative field);
+    // SBR_PO_FP64=1 forces the FP64 per-wavenumber path for them too
+    static const bool force64 = getenv("SBR_PO_FP64") && atoi(getenv("SBR_PO_FP64")) != 0;
+    const bool rot = nk > 1 && dkturn != 0.0 && !force64;
 #define SBR_PO(F, R)                                                                       \
     k_po<F, R><<<grid, kPoThreads, 0, st>>>(d_slots, d_units, n_units, d_k2, nk, dkturn,    \
                                             d_gpow, max_bounces, d_chunk_part, d_diag, d_bad)
