@@ -546,9 +546,15 @@ static int persistent_blocks(K kernel, int threads, int num_sms)
 template <int S, int M>
 static void trace_dispatch(const TraceArgs &a, cudaStream_t st, int num_sms)
 {
+    // query 0 from the raster pass and a one-bounce budget: every traced
+    // query is an escape probe (probe-only stack, see pop_next)
+    const bool probes = M != kModeList && a.prim && a.cfg.max_bounces == 1;
     if (a.cfg.B.width == 8 && a.cfg.B.nodes8) {
         int nb = persistent_blocks(k_trace_persistent<S, M, 8>, kTraceThreads, num_sms);
         k_trace_persistent<S, M, 8><<<nb, kTraceThreads, 0, st>>>(a);
+    } else if (probes) {
+        int nb = persistent_blocks(k_trace_persistent<S, M, 4, true>, kTraceThreads, num_sms);
+        k_trace_persistent<S, M, 4, true><<<nb, kTraceThreads, 0, st>>>(a);
     } else {
         int nb = persistent_blocks(k_trace_persistent<S, M, 4>, kTraceThreads, num_sms);
         k_trace_persistent<S, M, 4><<<nb, kTraceThreads, 0, st>>>(a);

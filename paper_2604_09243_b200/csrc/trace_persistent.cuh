@@ -25,6 +25,8 @@
 // triangles, and the per-bounce FP64 arithmetic is unchanged.
 #pragma once
 
+#include <type_traits>
+
 #include "pipeline.h"
 #include "traverse.cuh"
 
@@ -140,6 +142,31 @@ __device__ __forceinline__ bool pop_next(StackEntry *stack, LaneRay &L)
     }
     return false;
 }
+__device__ __forceinline__ void push_entry(StackEntry *stack, LaneRay &L, int ref, float tn)
+{
+    stack[L.sp].ref = ref;
+    stack[L.sp].tn = tn;
+    ++L.sp;
+}
+
+// Probe-only launches (every traced query is an escape probe: max_bounces
+// == 1 with query 0 answered by the raster pass): a probe stops at its first
+// hit, so entry distances never cull a pop -- 4-byte entries (refs only)
+// halve the stack's local-memory lines (C5 trace 137 -> 133 ms).
+__device__ __forceinline__ bool pop_next(int *stack, LaneRay &L)
+{
+    if (L.sp > 0) {
+        --L.sp;
+        L.ref = stack[L.sp];
+        return true;
+    }
+    return false;
+}
+__device__ __forceinline__ void push_entry(int *stack, LaneRay &L, int ref, float)
+{
+    stack[L.sp] = ref;
+    ++L.sp;
+}
 
 // MINB = 8 caps registers at 64 (32 resident warps per SM): measured
 // faster than unconstrained 80-92 registers despite a few spills, since the
@@ -156,7 +183,7 @@ template <> __device__ __forceinline__ const Node8Q *wide_nodes<8>(const BvhView
 template <> __device__ __forceinline__ const Node8 *wide_nodes<8>(const BvhView &B) { return B.nodes8; }
 #endif
 
-template <int STORAGE, int MODE, int W = 4, int MINB = SBR_TRACE_MINB>
+template <int STORAGE, int MODE, int W = 4, bool PROBES = false, int MINB = SBR_TRACE_MINB>
 __global__ void __launch_bounds__(128, MINB)
 k_trace_persistent(TraceArgs a)
 {
@@ -165,7 +192,7 @@ k_trace_persistent(TraceArgs a)
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
 
-    StackEntry stack[kStack];
+    typename std::conditional<PROBES, int, StackEntry>::type stack[kStack];
     LaneRay L;
     int state = kIdle;
     const int64_t n_work = a.worklist ? (int64_t)*a.n_work_dev : a.n_work;
@@ -316,11 +343,7 @@ k_trace_persistent(TraceArgs a)
                 if (n > 0) {
 #pragma unroll
                     for (int c = W - 1; c >= 1; --c)   // farther hits first: nearest pops first
-                        if (c < n) {
-                            stack[L.sp].ref = rr[c];
-                            stack[L.sp].tn = tt[c];
-                            ++L.sp;
-                        }
+                        if (c < n) push_entry(stack, L, rr[c], tt[c]);
                     L.ref = rr[0];
                 } else {
                     have = pop_next(stack, L);
