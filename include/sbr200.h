@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SBR200_ABI_VERSION 2
+#define SBR200_ABI_VERSION 3
 
 typedef enum {
     SBR_OK = 0,
@@ -124,6 +124,22 @@ int sbr_ctx_stream(sbr_ctx *ctx, void **stream_out);
 /* Number of kernels this context has launched (instrumentation). */
 int sbr_ctx_launch_count(sbr_ctx *ctx, int64_t *count_out);
 
+/* Traversal order of every query entry point (closest hit, trace_grid*,
+ * trace_rays, solve*):
+ *  SBR_TRAVERSAL_FAST (default): query 0 of aperture rays by the raster
+ *    pass (the exact linear-scan answer), later queries by the persistent
+ *    BVH4 kernel.  Bit-identical to the reference on every query whose
+ *    winning triangle's hit point lies robustly inside its box with no
+ *    accepting triangle tied within rounding.
+ *  SBR_TRAVERSAL_REFERENCE: every query replays bvh.py:306-362 _traverse on
+ *    the reference tree (FP64 slabs, far-first pushes, best_t culling) --
+ *    bit-identical to the reference on every ray, including near-edge-on
+ *    and edge/vertex tie rays; needs a SAH/median build or an uploaded
+ *    tree (SBR_EINVAL otherwise).  Visit counts equal the reference's. */
+enum { SBR_TRAVERSAL_FAST = 0, SBR_TRAVERSAL_REFERENCE = 1 };
+int sbr_ctx_set_traversal(sbr_ctx *ctx, int32_t mode);
+int sbr_ctx_get_traversal(sbr_ctx *ctx, int32_t *mode);
+
 /* Per-kernel CUDA-event timing of the solve pipeline (trace kernel and
  * compaction+PO kernel), accumulated over calls; enabling resets it. */
 int sbr_ctx_profile(sbr_ctx *ctx, int32_t enable);
@@ -197,6 +213,27 @@ int sbr_trace_grid(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *bvh,
                    uint8_t *valid, double *normal0, double *path,
                    int32_t *bounces, uint8_t *escaped, double *out_dir,
                    int32_t *tri_ids);
+
+/* transport.py:330-356 _trace_rows(i_start, i_end): rows [i_begin, i_end)
+ * of the grid only; outputs hold (i_end - i_begin) * n_v records starting at
+ * ray i_begin * n_v (the reference's per-worker row split). */
+int sbr_trace_grid_rows(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *bvh,
+                        const sbr_grid *grid, const sbr_trace_params *params,
+                        int64_t i_begin, int64_t i_end, uint8_t *valid,
+                        double *normal0, double *path, int32_t *bounces,
+                        uint8_t *escaped, double *out_dir, int32_t *tri_ids);
+
+/* Record checksums of rows [i_begin, i_end) without materialising records
+ * (parity at 1e9-ray scale): seg_hash[s] = wrapping sum over rays r of
+ * segment s (r / seg_rays == s, r over the whole grid, ceil(n_u*n_v /
+ * seg_rays) entries) of a splitmix64 chain over r, the per-bounce triangle
+ * ids (-1 padded to max_bounces), valid | escaped << 8 | bounces << 16,
+ * normal0 xyz, path, out_dir xyz (bit patterns).  oracle/sbr_oracle.c
+ * orc_trace_grid_hash computes the same function on the CPU. */
+int sbr_trace_grid_hash(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *bvh,
+                        const sbr_grid *grid, const sbr_trace_params *params,
+                        int64_t i_begin, int64_t i_end, int64_t seg_rays,
+                        uint64_t *seg_hash);
 
 /* transport.py:359-372 trace_ray over an explicit ray list. */
 int sbr_trace_rays(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *bvh,

@@ -256,6 +256,74 @@ def trace_rays(scene: Scene, origins, dirs, max_bounces=10, eps=1e-6,
     return rec
 
 
+def trace_grid_hash(scene: Scene, grid, max_bounces=10, eps=None, strict=False,
+                    rows=None, seg_rays=1 << 19, threads=0) -> np.ndarray:
+    """Per-segment record hashes of trace_grid (+ per-bounce ids): the CPU
+    twin of paper_2604_09243_b200.trace_grid_hash (same hash function)."""
+    if eps is None:
+        eps = scene.default_eps
+    i0, i1 = (0, grid.n_u) if rows is None else rows
+    out = np.zeros(-(-grid.n_u * grid.n_v // int(seg_rays)), np.uint64)
+    corner = _f64(grid.corner); u = _f64(grid.u); v = _f64(grid.v)
+    k = _f64(grid.k_inc)
+    rc = lib().orc_trace_grid_hash(
+        scene.ref, _p(corner), _p(u), _p(v), _p(k), ctypes.c_double(grid.spacing),
+        ctypes.c_int64(grid.n_u), ctypes.c_int64(grid.n_v), ctypes.c_int64(i0),
+        ctypes.c_int64(i1), ctypes.c_int32(max_bounces), ctypes.c_double(eps),
+        ctypes.c_int32(int(strict)), ctypes.c_int64(int(seg_rays)), _p(out),
+        ctypes.c_int(_threads(threads)))
+    if rc != 0:
+        raise RuntimeError(f"orc_trace_grid_hash rc={rc}")
+    return out
+
+
+def records_hash(rec: Records, max_bounces, r_base=0, seg_rays=1 << 19, n_total=None):
+    """Per-segment hashes of materialised records (with tri_ids), same
+    function as trace_grid_hash; rays r_base + [0, len(rec))."""
+    n = len(rec)
+    n_total = n_total if n_total is not None else r_base + n
+    out = np.zeros(-(-n_total // int(seg_rays)), np.uint64)
+    ids = np.ascontiguousarray(rec.tri_ids, np.int32)
+    valid = np.ascontiguousarray(rec.valid, np.uint8)
+    esc = np.ascontiguousarray(rec.escaped, np.uint8)
+    b = np.ascontiguousarray(rec.bounces, np.int32)
+    n0 = _f64(rec.normal0, (-1, 3)); pth = _f64(rec.path); od = _f64(rec.out_dir, (-1, 3))
+    lib().orc_records_hash(ctypes.c_int64(n), ctypes.c_int64(r_base), ctypes.c_int32(max_bounces),
+                           _p(valid), _p(n0), _p(pth), _p(b), _p(esc), _p(od), _p(ids),
+                           ctypes.c_int64(int(seg_rays)), _p(out))
+    return out
+
+
+def classify_grid(scene: Scene, grid, max_bounces=10, eps=None, strict=False, rows=None,
+                  threads=0):
+    """(robust u8 per ray, linear-scan query-0 tri, t) -- see
+    orc_classify_grid: robust rays have a tree-independent reference answer."""
+    if eps is None:
+        eps = scene.default_eps
+    i0, i1 = (0, grid.n_u) if rows is None else rows
+    n = (i1 - i0) * grid.n_v
+    robust = np.empty(n, np.uint8)
+    tri = np.empty(n, np.int64)
+    t = np.empty(n)
+    corner = _f64(grid.corner); u = _f64(grid.u); v = _f64(grid.v)
+    k = _f64(grid.k_inc)
+    lib().orc_classify_grid(scene.ref, _p(corner), _p(u), _p(v), _p(k),
+                            ctypes.c_double(grid.spacing), ctypes.c_int64(grid.n_v),
+                            ctypes.c_int64(i0), ctypes.c_int64(i1), ctypes.c_int32(max_bounces),
+                            ctypes.c_double(eps), ctypes.c_int32(int(strict)), _p(robust),
+                            _p(tri), _p(t), ctypes.c_int(_threads(threads)))
+    return robust.astype(bool), tri, t
+
+
+def classify_rays(scene: Scene, origins, dirs, threads=0):
+    o = _f64(origins, (-1, 3)); d = _f64(dirs, (-1, 3))
+    n = o.shape[0]
+    robust = np.empty(n, np.uint8)
+    lib().orc_classify_rays(scene.ref, _p(o), _p(d), ctypes.c_int64(n), _p(robust),
+                            ctypes.c_int(_threads(threads)))
+    return robust.astype(bool)
+
+
 def pairwise_sum(values) -> complex:
     w = np.ascontiguousarray(np.asarray(values, np.complex128)).view(np.float64).copy()
     out = np.zeros(2)

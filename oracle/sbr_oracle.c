@@ -392,6 +392,232 @@ int orc_trace_rays(const orc_scene *s, const double *origins, const double *dirs
 }
 
 /* ---------------------------------------------------------------------- */
+/* Record hash (parity at 1e9-ray scale): the same function as the device's */
+/* record_hash (paper_2604_09243_b200/csrc/pipeline.h) -- a splitmix64 chain */
+/* over r, ids[0..B) (-1 padded), valid|escaped<<8|N<<16, n0, R, out_dir.   */
+/* Segment hash = wrapping sum over the segment's rays.                     */
+/* ---------------------------------------------------------------------- */
+static inline uint64_t orc_mix(uint64_t z)
+{
+    z += 0x9e3779b97f4a7c15ULL;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+static inline uint64_t orc_dbits(double x)
+{
+    uint64_t u;
+    memcpy(&u, &x, 8);
+    return u;
+}
+
+uint64_t orc_record_hash(int64_t r, const int32_t *ids, int32_t max_bounces,
+                         const orc_record *rec)
+{
+    uint64_t h = orc_mix((uint64_t)r);
+    for (int32_t b = 0; b < max_bounces; ++b) h = orc_mix(h ^ (uint64_t)(uint32_t)ids[b]);
+    h = orc_mix(h ^ ((uint64_t)rec->valid | ((uint64_t)rec->escaped << 8) |
+                     ((uint64_t)(uint32_t)rec->bounces << 16)));
+    h = orc_mix(h ^ orc_dbits(rec->n0[0]));
+    h = orc_mix(h ^ orc_dbits(rec->n0[1]));
+    h = orc_mix(h ^ orc_dbits(rec->n0[2]));
+    h = orc_mix(h ^ orc_dbits(rec->path));
+    h = orc_mix(h ^ orc_dbits(rec->out_dir[0]));
+    h = orc_mix(h ^ orc_dbits(rec->out_dir[1]));
+    h = orc_mix(h ^ orc_dbits(rec->out_dir[2]));
+    return h;
+}
+
+/* trace_grid rows [i_begin, i_end) reduced to per-segment record hashes
+ * (seg_hash: ceil(n_u*n_v/seg_rays) entries, zeroed here) */
+int orc_trace_grid_hash(const orc_scene *s, const double corner[3], const double u[3],
+                        const double v[3], const double k[3], double spacing,
+                        int64_t n_u, int64_t n_v, int64_t i_begin, int64_t i_end,
+                        int32_t max_bounces, double eps, int32_t strict,
+                        int64_t seg_rays, uint64_t *seg_hash, int nthreads)
+{
+    int nt = orc_threads(nthreads);
+    const int64_t nseg = (n_u * n_v + seg_rays - 1) / seg_rays;
+    memset(seg_hash, 0, sizeof(uint64_t) * (size_t)nseg);
+    int failed = 0;
+#pragma omp parallel num_threads(nt)
+    {
+        int32_t *stack = (int32_t *)malloc(sizeof(int32_t) * (size_t)s->stack_depth);
+        int32_t *ids = (int32_t *)malloc(sizeof(int32_t) * (size_t)max_bounces);
+        uint64_t *loc = (uint64_t *)calloc((size_t)nseg, sizeof(uint64_t));
+        if (!stack || !ids || !loc) {
+#pragma omp atomic write
+            failed = 1;
+        } else {
+#pragma omp for schedule(dynamic, 1)
+            for (int64_t i = i_begin; i < i_end; ++i) {
+                double bx = corner[0] + (i + 0.5) * spacing * u[0];
+                double by = corner[1] + (i + 0.5) * spacing * u[1];
+                double bz = corner[2] + (i + 0.5) * spacing * u[2];
+                for (int64_t j = 0; j < n_v; ++j) {
+                    double o[3], d[3];
+                    o[0] = bx + (j + 0.5) * spacing * v[0];
+                    o[1] = by + (j + 0.5) * spacing * v[1];
+                    o[2] = bz + (j + 0.5) * spacing * v[2];
+                    d[0] = k[0]; d[1] = k[1]; d[2] = k[2];
+                    for (int32_t z = 0; z < max_bounces; ++z) ids[z] = -1;
+                    orc_record rec;
+                    orc_trace_one(s, o, d, max_bounces, eps, strict, stack, &rec, ids, NULL);
+                    const int64_t r = i * n_v + j;
+                    loc[r / seg_rays] += orc_record_hash(r, ids, max_bounces, &rec);
+                }
+            }
+#pragma omp critical
+            for (int64_t q = 0; q < nseg; ++q) seg_hash[q] += loc[q];
+        }
+        free(stack);
+        free(ids);
+        free(loc);
+    }
+    return failed ? ORC_ENOMEM : ORC_OK;
+}
+
+/* hashes of materialised records (rays r_base + [0, n)) */
+void orc_records_hash(int64_t n, int64_t r_base, int32_t max_bounces, const uint8_t *valid,
+                      const double *n0, const double *path, const int32_t *bounces,
+                      const uint8_t *escaped, const double *out_dir, const int32_t *ids,
+                      int64_t seg_rays, uint64_t *seg_hash)
+{
+    for (int64_t w = 0; w < n; ++w) {
+        orc_record rec;
+        rec.valid = valid[w]; rec.escaped = escaped[w]; rec.bounces = bounces[w];
+        rec.path = path[w];
+        for (int a = 0; a < 3; ++a) { rec.n0[a] = n0[3 * w + a]; rec.out_dir[a] = out_dir[3 * w + a]; }
+        const int64_t r = r_base + w;
+        seg_hash[r / seg_rays] += orc_record_hash(r, ids + w * max_bounces, max_bounces, &rec);
+    }
+}
+
+/* ---------------------------------------------------------------------- */
+/* Tree-independence classifier.  A query is ROBUST when the */
+/* linear-scan winner W (lexicographic (t, id) minimum over every accepting */
+/* triangle, tests/meshes.py:51-86 brute force) has its hit point o + t d   */
+/* inside W's own AABB by a relative margin of 1e-9 on every axis where the */
+/* box has extent (on flat axes the ray must cross the plane, |d_k| >= 1e-9)*/
+/* and no other accepting triangle has t <= t_W (1 + 1e-9).  Then every     */
+/* traversal whose culling is conservative -- the reference's _traverse on  */
+/* any tree (bvh.py:306-362), the GPU BVH4 kernel, the raster pass --       */
+/* returns W.  A ray is robust when every query of its walk is.             */
+/* ---------------------------------------------------------------------- */
+static int orc_query_robust(const orc_scene *s, const double o[3], const double d[3],
+                            int64_t *w_out, double *t_out)
+{
+    double best_t = INFINITY;
+    int64_t best = -1;
+    for (int64_t ti = 0; ti < s->ntri; ++ti) {
+        double h = orc_tri_hit(s, ti, o[0], o[1], o[2], d[0], d[1], d[2], 0.0, best_t);
+        if (h > 0.0 && (h < best_t || (h == best_t && ti < best))) {
+            best_t = h;
+            best = ti;
+        }
+    }
+    *w_out = best;
+    *t_out = best_t;
+    if (best < 0) return 1;
+    const double lim = best_t * (1.0 + 1e-9) + 1e-300;
+    for (int64_t ti = 0; ti < s->ntri; ++ti) {
+        if (ti == best) continue;
+        double h = orc_tri_hit(s, ti, o[0], o[1], o[2], d[0], d[1], d[2], 0.0, lim);
+        if (h > 0.0) return 0;     /* near-tie (edge / vertex / coplanar) */
+    }
+    const double *a = s->v0 + 3 * best, *b = s->v1 + 3 * best, *c = s->v2 + 3 * best;
+    const double dn = fabs(d[0]) + fabs(d[1]) + fabs(d[2]);
+    for (int ax = 0; ax < 3; ++ax) {
+        double lo = fmin(fmin(a[ax], b[ax]), c[ax]), hi = fmax(fmax(a[ax], b[ax]), c[ax]);
+        if (s->single) {   /* bvh.py:286-290 boxes of float32 meshes */
+            lo = (double)nextafterf((float)lo, -INFINITY);
+            hi = (double)nextafterf((float)hi, INFINITY);
+        }
+        const double hp = o[ax] + best_t * d[ax];
+        const double mu = 1e-9 * (fabs(lo) + fabs(hi) + fabs(o[ax]) + fabs(best_t * d[ax])) + 1e-300;
+        if (hi - lo > 2.0 * mu) {
+            if (!(hp >= lo + mu && hp <= hi - mu)) return 0;
+        } else {
+            if (!(fabs(d[ax]) >= 1e-9 * dn)) return 0;
+            if (!(fabs(hp - 0.5 * (lo + hi)) <= mu + 0.5 * (hi - lo))) return 0;
+        }
+    }
+    return 1;
+}
+
+/* per ray of rows [i_begin, i_end): robust[r] = 1 if every query of the
+ * walk (transport.py:276-327, driven by the linear-scan winners) is robust;
+ * prim_tri / prim_t (optional): the linear-scan answer of query 0 */
+int orc_classify_grid(const orc_scene *s, const double corner[3], const double u[3],
+                      const double v[3], const double k[3], double spacing,
+                      int64_t n_v, int64_t i_begin, int64_t i_end, int32_t max_bounces,
+                      double eps, int32_t strict, uint8_t *robust, int64_t *prim_tri,
+                      double *prim_t, int nthreads)
+{
+    int nt = orc_threads(nthreads);
+#pragma omp parallel for num_threads(nt) schedule(dynamic, 16)
+    for (int64_t r = i_begin * n_v; r < i_end * n_v; ++r) {
+        const int64_t i = r / n_v, j = r - i * n_v, slot = r - i_begin * n_v;
+        double o[3], d[3];
+        for (int a = 0; a < 3; ++a) {
+            double bx = corner[a] + (i + 0.5) * spacing * u[a];
+            o[a] = bx + (j + 0.5) * spacing * v[a];
+            d[a] = k[a];
+        }
+        int ok = 1, bounces = 0, valid = 0, escaped = 0;
+        for (int32_t it = 0; it < max_bounces && ok; ++it) {
+            int64_t tri;
+            double t;
+            ok = orc_query_robust(s, o, d, &tri, &t);
+            if (it == 0) {
+                if (prim_tri) prim_tri[slot] = tri;
+                if (prim_t) prim_t[slot] = t;
+            }
+            if (!ok) break;
+            if (tri < 0) { escaped = 1; break; }
+            const double *nn = s->normals + 3 * tri;
+            double nx = nn[0], ny = nn[1], nz = nn[2];
+            double nd = nx * d[0] + ny * d[1] + nz * d[2];
+            if (nd > 0.0) {
+                if (strict && bounces == 0) { escaped = 1; valid = 0; break; }
+                nx = -nx; ny = -ny; nz = -nz; nd = -nd;
+            }
+            double hx = o[0] + t * d[0], hy = o[1] + t * d[1], hz = o[2] + t * d[2];
+            bounces += 1;
+            valid = 1;
+            d[0] -= 2.0 * nd * nx;
+            d[1] -= 2.0 * nd * ny;
+            d[2] -= 2.0 * nd * nz;
+            o[0] = hx + eps * nx;
+            o[1] = hy + eps * ny;
+            o[2] = hz + eps * nz;
+        }
+        if (ok && valid && !escaped) {
+            int64_t tri;
+            double t;
+            ok = orc_query_robust(s, o, d, &tri, &t);
+        }
+        robust[slot] = (uint8_t)ok;
+    }
+    return ORC_OK;
+}
+
+/* single queries (closest_hit_batch rays) */
+int orc_classify_rays(const orc_scene *s, const double *o, const double *d, int64_t n,
+                      uint8_t *robust, int nthreads)
+{
+    int nt = orc_threads(nthreads);
+#pragma omp parallel for num_threads(nt) schedule(dynamic, 16)
+    for (int64_t r = 0; r < n; ++r) {
+        int64_t tri;
+        double t;
+        robust[r] = (uint8_t)orc_query_robust(s, o + 3 * r, d + 3 * r, &tri, &t);
+    }
+    return ORC_OK;
+}
+
+/* ---------------------------------------------------------------------- */
 /* po.py:59-80  pairwise_sum : adjacent-pair tree, odd tail carried          */
 /* ---------------------------------------------------------------------- */
 void orc_pairwise_sum(double *work /* (n,2) in/out scratch */, int64_t n,

@@ -18,7 +18,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(CSRC, "build")
 LIB = os.path.join(PKG, "libsbr200.so")
-SOURCES = ["capi.cu", "lbvh.cu", "pipeline.cu", "primary.cu", "sahbuild.cu", "objio.cpp"]
+SOURCES = ["capi.cu", "lbvh.cu", "pipeline.cu", "primary.cu", "reforder.cu", "sahbuild.cu",
+           "objio.cpp"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",

@@ -23,6 +23,7 @@ SBR_OK, SBR_EINVAL, SBR_EIO, SBR_ENUMERIC, SBR_ENOTSUP, SBR_ECUDA, SBR_ENOMEM = 
     0, 2, 3, 4, 5, 10, 12
 STORAGE_AUTO, STORAGE_F32_EXACT, STORAGE_F64, STORAGE_SINGLE = 0, 1, 2, 3
 SEGMENT_RAYS = 1 << 19
+TRAVERSAL_FAST, TRAVERSAL_REFERENCE = 0, 1
 
 
 class NativeUnavailable(SbrError, RuntimeError):
@@ -97,6 +98,14 @@ _SIGS = {
     "sbr_trace_grid": (ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.POINTER(Grid),
                                       ctypes.POINTER(TraceParams), c_vp, c_vp, c_vp, c_vp,
                                       c_vp, c_vp, c_vp]),
+    "sbr_trace_grid_rows": (ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.POINTER(Grid),
+                                           ctypes.POINTER(TraceParams), c_i64, c_i64, c_vp,
+                                           c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "sbr_trace_grid_hash": (ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.POINTER(Grid),
+                                           ctypes.POINTER(TraceParams), c_i64, c_i64, c_i64,
+                                           c_vp]),
+    "sbr_ctx_set_traversal": (ctypes.c_int, [c_vp, c_i32]),
+    "sbr_ctx_get_traversal": (ctypes.c_int, [c_vp, ctypes.POINTER(c_i32)]),
     "sbr_trace_rays": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64,
                                       ctypes.POINTER(TraceParams), c_vp, c_vp, c_vp, c_vp,
                                       c_vp, c_vp, c_vp]),
@@ -244,6 +253,16 @@ class Context:
         check(self.lib.sbr_ctx_raster_stats(self.handle, ctypes.byref(rm)))
         return {"trace_ms": tm.value, "trace_launches": int(tn.value), "po_ms": pm.value,
                 "po_launches": int(pn.value), "raster_ms": rm.value}
+
+    @property
+    def traversal(self) -> int:
+        m = c_i32()
+        check(self.lib.sbr_ctx_get_traversal(self.handle, ctypes.byref(m)))
+        return int(m.value)
+
+    @traversal.setter
+    def traversal(self, mode: int):
+        check(self.lib.sbr_ctx_set_traversal(self.handle, int(mode)), "sbr_ctx_set_traversal")
 
     @property
     def stream(self) -> int:

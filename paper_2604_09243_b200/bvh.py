@@ -15,6 +15,7 @@ device tree's node fetches.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 from dataclasses import dataclass
 from typing import NamedTuple, Optional
@@ -314,6 +315,44 @@ def build(mesh: Mesh, params: BuildParams = BuildParams()) -> Bvh:
     tree._dev[(ctx.device, id(mesh))] = _DeviceBvh(ctx, handle, dm)
     tree._origin = (ctx.device, mesh)
     return tree
+
+
+# ---------------------------------------------------------------------------
+# traversal order (sbr_ctx_set_traversal)
+# ---------------------------------------------------------------------------
+_ORDERS = {"fast": nat.TRAVERSAL_FAST, "reference": nat.TRAVERSAL_REFERENCE}
+
+
+def set_traversal_order(order: str, device: Optional[int] = None) -> None:
+    """Select how every query of this device's context is answered.
+
+    ``"fast"`` (default): raster pass for query 0 of aperture rays (the exact
+    linear-scan answer, bvh.py:394-395) and the persistent BVH4 kernel for
+    the rest; bit-identical to the reference on every query whose winning
+    triangle's hit point lies robustly inside its box with no accepting
+    triangle tied within rounding.  ``"reference"``: every query replays
+    bvh.py:306-362 ``_traverse`` on the reference tree, so edge/vertex ties
+    and near-edge-on acceptances resolve exactly as the reference resolves
+    them (needs a ``"sah"``/``"median"`` build or an uploaded tree)."""
+    if order not in _ORDERS:
+        raise ValidationError(f"unknown traversal order {order!r}")
+    nat.context(device).traversal = _ORDERS[order]
+
+
+def get_traversal_order(device: Optional[int] = None) -> str:
+    m = nat.context(device).traversal
+    return next(k for k, v in _ORDERS.items() if v == m)
+
+
+@contextlib.contextmanager
+def traversal_order(order: str, device: Optional[int] = None):
+    """``with traversal_order("reference"): ...`` -- scoped set_traversal_order."""
+    prev = get_traversal_order(device)
+    set_traversal_order(order, device)
+    try:
+        yield
+    finally:
+        set_traversal_order(prev, device)
 
 
 def closest_hit(bvh: Bvh, mesh: Mesh, origin, direction, t_min: float = 0.0,

@@ -76,6 +76,7 @@ struct sbr_ctx {
     int num_sms = 148;
     int64_t launches = 0;
     std::mutex mu;
+    int traversal = SBR_TRAVERSAL_FAST;   // sbr_ctx_set_traversal
     DevBuf<unsigned long long> counter;
     DevBuf<unsigned int> err_flag;
     DevBuf<unsigned long long> bad;
@@ -140,6 +141,8 @@ struct sbr_bvh {
     std::vector<double> ref_nmin, ref_nmax;
     std::vector<int32_t> ref_first, ref_count, ref_order;
     int ref_depth = -1;
+    int ref_round_f32 = 0;     // GPU-built tree of a float32 mesh: replica rounds boxes
+    int ref_tree_depth = -1;   // depth of ref_dev (reference-order traversal stack bound)
     double frame[3];
     float scale = 0.f;
     BvhView view() const
@@ -627,6 +630,42 @@ extern "C" int sbr_bvh_upload(sbr_ctx *ctx, const sbr_mesh *mesh, const double *
         delete b;
         return rc;
     }
+    // device copy of the layout itself for reference-order traversal
+    // (bvh.py:306-362 replayed as given: no further box rounding)
+    {
+        SahTree &T = b->ref_dev;
+        const size_t N = (size_t)nnodes, Tn = (size_t)mesh->ntri;
+        cudaError_t e = T.nmin.alloc(3 * N);
+        if (e == cudaSuccess) e = T.nmax.alloc(3 * N);
+        if (e == cudaSuccess) e = T.first.alloc(N);
+        if (e == cudaSuccess) e = T.count.alloc(N);
+        if (e == cudaSuccess) e = T.order.alloc(Tn);
+        cudaStream_t st = ctx->stream;
+        if (e == cudaSuccess) e = cudaMemcpyAsync(T.nmin.p, nodes_min, 24 * N, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(T.nmax.p, nodes_max, 24 * N, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(T.first.p, node_first, 4 * N, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(T.count.p, node_count, 4 * N, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(T.order.p, tri_order, 4 * Tn, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) {
+            delete b;
+            return fail(SBR_ECUDA, "BVH upload: %s", cudaGetErrorString(e));
+        }
+        T.nnodes = (int64_t)nnodes;
+        // depth by walking the preorder layout (children of i: i+1, first[i])
+        std::vector<int> depth(N, 0);
+        int md = 0;
+        for (size_t i = 0; i < N; ++i) {
+            md = depth[i] > md ? depth[i] : md;
+            if (node_count[i] == 0) {
+                const int32_t l = (int32_t)i + 1, r = node_first[i];
+                if (l > 0 && (size_t)l < N) depth[l] = depth[i] + 1;
+                if (r > 0 && (size_t)r < N) depth[r] = depth[i] + 1;
+            }
+        }
+        T.max_depth = md;
+        b->ref_tree_depth = md;
+    }
     *out = b;
     return SBR_OK;
 }
@@ -661,6 +700,8 @@ static int build_sah(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_build_params 
         return fail(e == cudaErrorMemoryAllocation ? SBR_ENOMEM : SBR_ECUDA, "SAH build: %s",
                     cudaGetErrorString(e));
     b->ref_depth = T.max_depth;
+    b->ref_tree_depth = T.max_depth;
+    b->ref_round_f32 = mesh->storage == kSingle;
     set_frame(b, mesh);
     bool host = false;
     e = ref_to_bvh2(T, b->frame, ctx->sah, b->out, host, ctx->stream, &ctx->launches);
@@ -864,6 +905,50 @@ static int check_pair(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *bvh)
     return SBR_OK;
 }
 
+static RefView ref_view(const sbr_bvh *b)
+{
+    RefView v;
+    v.nmin = b->ref_dev.nmin.p;
+    v.nmax = b->ref_dev.nmax.p;
+    v.first = b->ref_dev.first.p;
+    v.count = b->ref_dev.count.p;
+    v.order = b->ref_dev.order.p;
+    v.round_f32 = b->ref_round_f32;
+    v.verts = b->mesh->verts.p;
+    v.single = b->mesh->storage == kSingle;
+    return v;
+}
+
+// reference-order traversal needs the reference-layout tree on the device
+static int check_ref_mode(const sbr_ctx *ctx, const sbr_bvh *bvh)
+{
+    if (ctx->traversal != SBR_TRAVERSAL_REFERENCE) return SBR_OK;
+    REQUIRE(bvh->ref_dev.nnodes > 0,
+            "reference-order traversal needs the reference tree (split_rule 'sah' or 'median', "
+            "or an uploaded tree)");
+    REQUIRE(bvh->ref_tree_depth >= 0 && bvh->ref_tree_depth + 1 < 256,
+            "tree depth %d exceeds the reference-order traversal stack (255)",
+            bvh->ref_tree_depth);
+    return SBR_OK;
+}
+
+extern "C" int sbr_ctx_set_traversal(sbr_ctx *ctx, int32_t mode)
+{
+    REQUIRE(ctx, "ctx is NULL");
+    REQUIRE(mode == SBR_TRAVERSAL_FAST || mode == SBR_TRAVERSAL_REFERENCE,
+            "unknown traversal mode %d", (int)mode);
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    ctx->traversal = mode;
+    return SBR_OK;
+}
+
+extern "C" int sbr_ctx_get_traversal(sbr_ctx *ctx, int32_t *mode)
+{
+    REQUIRE(ctx && mode, "NULL argument");
+    *mode = ctx->traversal;
+    return SBR_OK;
+}
+
 // Query 0 of aperture rays: rasterised per triangle or traced through the
 // BVH like every other query.  Both give the same bits.  The raster pass
 // hands each warp 32 triangles of one grid, so it needs many (grid,
@@ -897,13 +982,20 @@ static RasterArgs raster_args(const sbr_bvh *bvh, const GridDev *grids, const in
     r.big = nullptr;
     r.nbig = nullptr;
     r.big_cap = 0;
+    r.row_lo = 0;
+    r.row_hi = INT64_MAX;
     return r;
 }
 
-// big-triangle chunk queue of the raster pass (grow-only, 4M items = 64 MB)
+// big-triangle chunk queue of the raster pass (grow-only, 4M items = 64 MB);
+// SBR_BIG_CAP (tests) shrinks it to force the overflow path
 static cudaError_t attach_big_queue(sbr_ctx *ctx, RasterArgs &ra)
 {
-    const size_t cap = (size_t)1 << 22;
+    size_t cap = (size_t)1 << 22;
+    if (const char *s = getenv("SBR_BIG_CAP")) {
+        const long long v = atoll(s);
+        if (v >= 1 && v < (long long)cap) cap = (size_t)v;
+    }
     cudaError_t e = ctx->big.reserve(cap);
     if (e == cudaSuccess) e = ctx->nbig.reserve(1);
     if (e != cudaSuccess) return e;
@@ -957,8 +1049,13 @@ extern "C" int sbr_closest_hit(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh
     cudaStream_t st = ctx->stream;
     CUDA_TRY(cudaMemcpyAsync(o.p, origins, 24 * n, cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaMemcpyAsync(d.p, dirs, 24 * n, cudaMemcpyHostToDevice, st));
-    CUDA_TRY(launch_closest(bvh->view(), mesh->storage, o.p, d.p, n, t_min, t_max, ti.p, tt.p,
-                            vi.p, st, ctx->stats()));
+    if (int rc = check_ref_mode(ctx, bvh)) return rc;
+    if (ctx->traversal == SBR_TRAVERSAL_REFERENCE)
+        CUDA_TRY(launch_closest_ref(ref_view(bvh), o.p, d.p, n, t_min, t_max, ti.p, tt.p, vi.p,
+                                    st, ctx->stats()));
+    else
+        CUDA_TRY(launch_closest(bvh->view(), mesh->storage, o.p, d.p, n, t_min, t_max, ti.p,
+                                tt.p, vi.p, st, ctx->stats()));
     CUDA_TRY(cudaMemcpyAsync(tri, ti.p, 8 * n, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaMemcpyAsync(t, tt.p, 8 * n, cudaMemcpyDeviceToHost, st));
     if (visits) CUDA_TRY(cudaMemcpyAsync(visits, vi.p, 8 * n, cudaMemcpyDeviceToHost, st));
@@ -966,27 +1063,47 @@ extern "C" int sbr_closest_hit(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh
     return SBR_OK;
 }
 
+// Shared body of sbr_trace_grid[_rows|_hash] and sbr_trace_rays.  Grid mode
+// traces rows [i_begin, i_end) of the grid (records indexed from
+// i_begin * n_v); seg_hash != NULL selects hash mode (no per-ray outputs:
+// per-segment record hashes, segment = seg_rays consecutive ray indices of
+// the whole grid).
 static int trace_full_common(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *bvh,
                              const sbr_grid *grid, const double *origins, const double *dirs,
-                             int64_t n, const sbr_trace_params *params, uint8_t *valid,
+                             int64_t n_list, int64_t i_begin, int64_t i_end,
+                             const sbr_trace_params *params, uint8_t *valid,
                              double *normal0, double *path, int32_t *bounces, uint8_t *escaped,
-                             double *out_dir, int32_t *tri_ids)
+                             double *out_dir, int32_t *tri_ids, uint64_t *seg_hash,
+                             int64_t seg_rays)
 {
     if (int rc = check_pair(ctx, mesh, bvh)) return rc;
     if (int rc = check_params(params)) return rc;
-    REQUIRE(valid && normal0 && path && bounces && escaped && out_dir, "NULL output");
+    const bool hash = seg_hash != nullptr;
+    REQUIRE(hash || (valid && normal0 && path && bounces && escaped && out_dir), "NULL output");
+    const int64_t n = grid ? (i_end - i_begin) * grid->n_v : n_list;
+    const int64_t r_base = grid ? i_begin * grid->n_v : 0;
+    const int64_t n_grid = grid ? grid->n_u * grid->n_v : 0;
+    const int64_t nhash = hash ? (n_grid + seg_rays - 1) / seg_rays : 0;
+    if (hash) std::memset(seg_hash, 0, sizeof(uint64_t) * nhash);
     if (n == 0) return SBR_OK;
     std::lock_guard<std::mutex> lk(ctx->mu);
     if (int rc = set_device(ctx)) return rc;
+    if (int rc = check_ref_mode(ctx, bvh)) return rc;
     cudaStream_t st = ctx->stream;
     const int B = params->max_bounces;
-    DevBuf<uint8_t> dv(n), de(n);
-    DevBuf<double> dn(3 * n), dp(n), dd(3 * n), o, d;
-    DevBuf<int32_t> db(n), di;
+    const int64_t m = hash ? 0 : n;
+    DevBuf<uint8_t> dv(m), de(m);
+    DevBuf<double> dn(3 * m), dp(m), dd(3 * m), o, d;
+    DevBuf<int32_t> db(m), di;
+    DevBuf<unsigned long long> dh;
     DevBuf<GridDev> dg;
     CUDA_TRY(dv.status()); CUDA_TRY(de.status()); CUDA_TRY(dn.status()); CUDA_TRY(dp.status());
     CUDA_TRY(dd.status()); CUDA_TRY(db.status());
-    if (tri_ids) CUDA_TRY(di.alloc((size_t)n * B));
+    if (tri_ids && !hash) CUDA_TRY(di.alloc((size_t)n * B));
+    if (hash) {
+        CUDA_TRY(dh.alloc(nhash));
+        CUDA_TRY(cudaMemsetAsync(dh.p, 0, 8 * nhash, st));
+    }
     if (grid) {
         GridDev g;
         for (int a = 0; a < 3; ++a) {
@@ -995,7 +1112,7 @@ static int trace_full_common(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *
         }
         g.spacing = grid->spacing;
         g.n_v = grid->n_v;
-        g.n_rays = n;
+        g.n_rays = n_grid;
         CUDA_TRY(dg.alloc(1));
         CUDA_TRY(cudaMemcpyAsync(dg.p, &g, sizeof(g), cudaMemcpyHostToDevice, st));
     } else {
@@ -1005,39 +1122,59 @@ static int trace_full_common(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *
         CUDA_TRY(cudaMemcpyAsync(d.p, dirs, 24 * n, cudaMemcpyHostToDevice, st));
     }
     TraceCfg cfg = make_cfg(bvh, params, ctx);
-    FullOut fo{dv.p, dn.p, dp.p, db.p, de.p, dd.p, tri_ids ? di.p : nullptr};
-    DevBuf<PrimHit> prim;
-    if (grid && raster_primary(mesh->ntri, 1)) {
-        // one grid, slot == ray index: every segment maps with offset 0
-        const int64_t nseg = (n + kSegRays - 1) / kSegRays;
-        std::vector<int64_t> sb{0, nseg}, ss(nseg, 0);
-        const int bg = 0;
-        DevBuf<int64_t> dsb(2), dss(nseg);
+    FullOut fo{dv.p, dn.p, dp.p, db.p, de.p, dd.p, (tri_ids && !hash) ? di.p : nullptr,
+               hash ? dh.p : nullptr, seg_rays};
+    if (ctx->traversal == SBR_TRAVERSAL_REFERENCE) {
+        CUDA_TRY(launch_trace_ref(ref_view(bvh), cfg, dg.p, o.p, d.p, n, r_base, fo, nullptr,
+                                  nullptr, 0, st, ctx->stats()));
+    } else {
+        DevBuf<PrimHit> prim;
+        DevBuf<int64_t> dsb(2), dss;
         DevBuf<int> dbg(1);
-        CUDA_TRY(prim.alloc(n));
-        CUDA_TRY(dsb.status()); CUDA_TRY(dss.status()); CUDA_TRY(dbg.status());
-        CUDA_TRY(cudaMemcpyAsync(dsb.p, sb.data(), 16, cudaMemcpyHostToDevice, st));
-        CUDA_TRY(cudaMemcpyAsync(dss.p, ss.data(), 8 * nseg, cudaMemcpyHostToDevice, st));
-        CUDA_TRY(cudaMemcpyAsync(dbg.p, &bg, 4, cudaMemcpyHostToDevice, st));
-        CUDA_TRY(cudaMemsetAsync(prim.p, 0xff, sizeof(PrimHit) * n, st));
-        RasterArgs ra = raster_args(bvh, dg.p, dbg.p, 1, dsb.p, dss.p, prim.p);
-        ra.counter = ctx->counter.p + 1;
-        CUDA_TRY(attach_big_queue(ctx, ra));
-        CUDA_TRY(launch_raster(ra, st, ctx->stats()));
+        if (grid && raster_primary(mesh->ntri, 1)) {
+            // one grid, prim index = ray index - r_base for every segment
+            const int64_t nseg = (n_grid + kSegRays - 1) / kSegRays;
+            std::vector<int64_t> sb{0, nseg}, ss(nseg, -r_base);
+            const int bg = 0;
+            CUDA_TRY(prim.alloc(n));
+            CUDA_TRY(dss.alloc(nseg));
+            CUDA_TRY(dsb.status()); CUDA_TRY(dbg.status());
+            CUDA_TRY(cudaMemcpyAsync(dsb.p, sb.data(), 16, cudaMemcpyHostToDevice, st));
+            CUDA_TRY(cudaMemcpyAsync(dss.p, ss.data(), 8 * nseg, cudaMemcpyHostToDevice, st));
+            CUDA_TRY(cudaMemcpyAsync(dbg.p, &bg, 4, cudaMemcpyHostToDevice, st));
+            CUDA_TRY(cudaMemsetAsync(prim.p, 0xff, sizeof(PrimHit) * n, st));
+            RasterArgs ra = raster_args(bvh, dg.p, dbg.p, 1, dsb.p, dss.p, prim.p);
+            ra.counter = ctx->counter.p + 1;
+            ra.row_lo = i_begin;
+            ra.row_hi = i_end;
+            CUDA_TRY(attach_big_queue(ctx, ra));
+            CUDA_TRY(launch_raster(ra, st, ctx->stats()));
+        }
+        CUDA_TRY(launch_trace_full(cfg, dg.p, o.p, d.p, n, r_base, fo, prim.p, ctx->counter.p,
+                                   st, ctx->stats()));
         CUDA_TRY(cudaStreamSynchronize(st));   // scratch tables die with this scope
     }
-    CUDA_TRY(launch_trace_full(cfg, dg.p, o.p, d.p, n, fo, prim.p, ctx->counter.p, st,
-                               ctx->stats()));
-    CUDA_TRY(cudaMemcpyAsync(valid, dv.p, n, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaMemcpyAsync(escaped, de.p, n, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaMemcpyAsync(normal0, dn.p, 24 * n, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaMemcpyAsync(path, dp.p, 8 * n, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaMemcpyAsync(out_dir, dd.p, 24 * n, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaMemcpyAsync(bounces, db.p, 4 * n, cudaMemcpyDeviceToHost, st));
-    if (tri_ids)
-        CUDA_TRY(cudaMemcpyAsync(tri_ids, di.p, sizeof(int32_t) * n * B, cudaMemcpyDeviceToHost,
-                                 st));
+    if (hash) {
+        CUDA_TRY(cudaMemcpyAsync(seg_hash, dh.p, 8 * nhash, cudaMemcpyDeviceToHost, st));
+    } else {
+        CUDA_TRY(cudaMemcpyAsync(valid, dv.p, n, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(escaped, de.p, n, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(normal0, dn.p, 24 * n, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(path, dp.p, 8 * n, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(out_dir, dd.p, 24 * n, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(bounces, db.p, 4 * n, cudaMemcpyDeviceToHost, st));
+        if (tri_ids)
+            CUDA_TRY(cudaMemcpyAsync(tri_ids, di.p, sizeof(int32_t) * n * B,
+                                     cudaMemcpyDeviceToHost, st));
+    }
     CUDA_TRY(cudaStreamSynchronize(st));
+    return SBR_OK;
+}
+
+static int check_grid(const sbr_grid *grid)
+{
+    REQUIRE(grid, "grid is NULL");
+    REQUIRE(grid->n_u >= 1 && grid->n_v >= 1 && grid->spacing > 0.0, "invalid grid");
     return SBR_OK;
 }
 
@@ -1046,10 +1183,36 @@ extern "C" int sbr_trace_grid(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh 
                               uint8_t *valid, double *normal0, double *path, int32_t *bounces,
                               uint8_t *escaped, double *out_dir, int32_t *tri_ids)
 {
-    REQUIRE(grid, "grid is NULL");
-    REQUIRE(grid->n_u >= 1 && grid->n_v >= 1 && grid->spacing > 0.0, "invalid grid");
-    return trace_full_common(ctx, mesh, bvh, grid, nullptr, nullptr, grid->n_u * grid->n_v,
-                             params, valid, normal0, path, bounces, escaped, out_dir, tri_ids);
+    if (int rc = check_grid(grid)) return rc;
+    return trace_full_common(ctx, mesh, bvh, grid, nullptr, nullptr, 0, 0, grid->n_u, params,
+                             valid, normal0, path, bounces, escaped, out_dir, tri_ids, nullptr,
+                             0);
+}
+
+extern "C" int sbr_trace_grid_rows(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *bvh,
+                                   const sbr_grid *grid, const sbr_trace_params *params,
+                                   int64_t i_begin, int64_t i_end, uint8_t *valid,
+                                   double *normal0, double *path, int32_t *bounces,
+                                   uint8_t *escaped, double *out_dir, int32_t *tri_ids)
+{
+    if (int rc = check_grid(grid)) return rc;
+    REQUIRE(0 <= i_begin && i_begin <= i_end && i_end <= grid->n_u, "row range out of bounds");
+    return trace_full_common(ctx, mesh, bvh, grid, nullptr, nullptr, 0, i_begin, i_end, params,
+                             valid, normal0, path, bounces, escaped, out_dir, tri_ids, nullptr,
+                             0);
+}
+
+extern "C" int sbr_trace_grid_hash(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *bvh,
+                                   const sbr_grid *grid, const sbr_trace_params *params,
+                                   int64_t i_begin, int64_t i_end, int64_t seg_rays,
+                                   uint64_t *seg_hash)
+{
+    if (int rc = check_grid(grid)) return rc;
+    REQUIRE(0 <= i_begin && i_begin <= i_end && i_end <= grid->n_u, "row range out of bounds");
+    REQUIRE(seg_rays >= 1 && seg_hash, "bad hash output");
+    return trace_full_common(ctx, mesh, bvh, grid, nullptr, nullptr, 0, i_begin, i_end, params,
+                             nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                             seg_hash, seg_rays);
 }
 
 extern "C" int sbr_trace_rays(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *bvh,
@@ -1060,8 +1223,8 @@ extern "C" int sbr_trace_rays(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh 
 {
     REQUIRE(n >= 0, "negative ray count");
     REQUIRE(n == 0 || (origins && dirs), "NULL rays");
-    return trace_full_common(ctx, mesh, bvh, nullptr, origins, dirs, n, params, valid, normal0,
-                             path, bounces, escaped, out_dir, tri_ids);
+    return trace_full_common(ctx, mesh, bvh, nullptr, origins, dirs, n, 0, 0, params, valid,
+                             normal0, path, bounces, escaped, out_dir, tri_ids, nullptr, 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -1130,7 +1293,8 @@ static int run_units(sbr_ctx *ctx, const sbr_bvh *bvh, const std::vector<UnitDev
     cudaStream_t st = ctx->stream;
     int64_t budget = slot_budget();
     const int ngrids = (int)seg_base.size() - 1;
-    const bool raster = raster_primary(bvh->mesh->ntri, ngrids);
+    const bool refmode = ctx->traversal == SBR_TRAVERSAL_REFERENCE;
+    const bool raster = !refmode && raster_primary(bvh->mesh->ntri, ngrids);
     std::vector<int64_t> seg_slot;
     std::vector<int> bgrids;
     if (raster) {
@@ -1203,10 +1367,17 @@ static int run_units(sbr_ctx *ctx, const sbr_bvh *bvh, const std::vector<UnitDev
                                          ctx->stats()));
         }
         if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev[3], st));
-        CUDA_TRY(launch_trace_solve(cfg, ctx->grids.p, ctx->units.p, (int)batch.size(), slots,
-                                    ctx->slots.p, ctx->counter.p, raster,
-                                    raster ? ctx->worklist.p : nullptr,
-                                    raster ? ctx->nwork.p : nullptr, st, ctx->stats()));
+        if (refmode) {
+            const FullOut none{};
+            CUDA_TRY(launch_trace_ref(ref_view(bvh), cfg, ctx->grids.p, nullptr, nullptr, slots,
+                                      0, none, ctx->units.p, ctx->slots.p, (int)batch.size(), st,
+                                      ctx->stats()));
+        } else {
+            CUDA_TRY(launch_trace_solve(cfg, ctx->grids.p, ctx->units.p, (int)batch.size(),
+                                        slots, ctx->slots.p, ctx->counter.p, raster,
+                                        raster ? ctx->worklist.p : nullptr,
+                                        raster ? ctx->nwork.p : nullptr, st, ctx->stats()));
+        }
         if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev[1], st));
         CUDA_TRY(launch_po(ctx->slots.p, ctx->units.p, (int)batch.size(), slots / kChunk,
                            ctx->k2.p, nk, ctx->dkturn, ctx->gpow.p, cfg.max_bounces, ctx->chunk_part.p,
@@ -1332,6 +1503,7 @@ static int validate_solve(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *bvh
     REQUIRE(k && nk >= 1 && nk <= 65535, "need 1..65535 wavenumbers");
     for (int f = 0; f < nk; ++f) REQUIRE(k[f] > 0.0 && std::isfinite(k[f]), "bad wavenumber");
     REQUIRE(std::fabs(gamma) <= 1.0, "|gamma| must be <= 1");
+    if (int rc = check_ref_mode(ctx, bvh)) return rc;
     return check_sampling(grids, ngrids, params);
 }
 

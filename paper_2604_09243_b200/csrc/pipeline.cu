@@ -28,29 +28,7 @@ namespace sbr {
 // ---------------------------------------------------------------------------
 // helpers
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ int find_unit(const UnitDev *u, int n, int64_t slot)
-{
-    int lo = 0, hi = n - 1;
-    while (lo < hi) {
-        int mid = (lo + hi + 1) >> 1;
-        if (__ldg(&u[mid].slot_base) <= slot) lo = mid; else hi = mid - 1;
-    }
-    return lo;
-}
 
-__device__ __forceinline__ void grid_origin(const GridDev &g, int64_t r, double &ox,
-                                            double &oy, double &oz)
-{
-    int64_t i = r / g.n_v, j = r - i * g.n_v;
-    double si = DM(DA((double)i, 0.5), g.spacing);
-    double sj = DM(DA((double)j, 0.5), g.spacing);
-    double bx = DA(g.corner[0], DM(si, g.u[0]));
-    double by = DA(g.corner[1], DM(si, g.u[1]));
-    double bz = DA(g.corner[2], DM(si, g.u[2]));
-    ox = DA(bx, DM(sj, g.v[0]));
-    oy = DA(by, DM(sj, g.v[1]));
-    oz = DA(bz, DM(sj, g.v[2]));
-}
 
 __device__ __forceinline__ int64_t warp_fetch(unsigned long long *counter)
 {
@@ -596,7 +574,7 @@ cudaError_t launch_trace_solve(const TraceCfg &cfg, const GridDev *d_grids,
 
 cudaError_t launch_trace_full(const TraceCfg &cfg, const GridDev *d_grid,
                               const double *d_orig, const double *d_dirs, int64_t n,
-                              const FullOut &out, const PrimHit *d_prim,
+                              int64_t r_base, const FullOut &out, const PrimHit *d_prim,
                               unsigned long long *d_counter, cudaStream_t st,
                               const LaunchStats &ls)
 {
@@ -610,6 +588,7 @@ cudaError_t launch_trace_full(const TraceCfg &cfg, const GridDev *d_grid,
     a.n_work = n;
     a.counter = d_counter;
     a.full = out;
+    a.r_base = d_grid ? r_base : 0;
     a.prim = d_grid ? d_prim : nullptr;
     if (d_grid) trace_storage_dispatch<kModeGrid>(a, st, ls.num_sms);
     else trace_storage_dispatch<kModeList>(a, st, ls.num_sms);

@@ -57,6 +57,35 @@ struct __align__(16) PrimHit {
 static_assert(sizeof(PrimHit) == sizeof(SlotRec), "PrimHit aliases SlotRec");
 constexpr unsigned long long kNoHitBits = ~0ULL;
 
+enum TraceMode : int { kModeSolve = 0, kModeGrid = 1, kModeList = 2 };
+
+// unit owning a slot (units sorted by slot_base)
+__device__ inline int find_unit(const UnitDev *u, int n, int64_t slot)
+{
+    int lo = 0, hi = n - 1;
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (__ldg(&u[mid].slot_base) <= slot) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+// origin of ray r = i * n_v + j exactly as transport.py:339-345 builds it:
+// bx = corner + ((i+.5) ds) u, ox = bx + ((j+.5) ds) v (no FMA contraction)
+__device__ inline void grid_origin(const GridDev &g, int64_t r, double &ox,
+                                            double &oy, double &oz)
+{
+    int64_t i = r / g.n_v, j = r - i * g.n_v;
+    double si = DM(DA((double)i, 0.5), g.spacing);
+    double sj = DM(DA((double)j, 0.5), g.spacing);
+    double bx = DA(g.corner[0], DM(si, g.u[0]));
+    double by = DA(g.corner[1], DM(si, g.u[1]));
+    double bz = DA(g.corner[2], DM(si, g.u[2]));
+    ox = DA(bx, DM(sj, g.v[0]));
+    oy = DA(by, DM(sj, g.v[1]));
+    oz = DA(bz, DM(sj, g.v[2]));
+}
+
 struct TraceCfg {
     BvhView B;
     int storage;
@@ -101,15 +130,80 @@ struct FullOut {
     uint8_t *escaped;
     double *out_dir;
     int32_t *ids;      // may be null
+    // hash mode (grid only): no per-ray stores; record_hash() of every ray is
+    // added into seg_hash[r / seg_rays] (r = ray index in the grid)
+    unsigned long long *seg_hash;
+    int64_t seg_rays;
 };
+
+// Per-ray record hash (a checksum of every HitRecords field plus the
+// per-bounce ids, -1 padded to max_bounces), shared with the oracle
+// (oracle/sbr_oracle.c orc_record_hash): splitmix64 finaliser chained over
+//   r, ids[0..B), flags (valid | escaped << 8 | N << 16), n0 xyz, R, out_dir xyz.
+// A segment's hash is the wrapping sum over its rays, so it is independent
+// of execution order.
+__host__ __device__ inline unsigned long long hash_mix(unsigned long long z)
+{
+    z += 0x9e3779b97f4a7c15ULL;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+__device__ __forceinline__ unsigned long long dbits(double x)
+{
+    return (unsigned long long)__double_as_longlong(x);
+}
+// hid = ids folded so far (hash_mix(r) then hash_mix(h ^ id) per recorded
+// bounce); n_ids = bounces recorded
+__device__ __forceinline__ unsigned long long record_hash(unsigned long long hid, int n_ids,
+                                                          int max_bounces, bool valid,
+                                                          bool escaped, double n0x, double n0y,
+                                                          double n0z, double path, double ox,
+                                                          double oy, double oz)
+{
+    for (int b = n_ids; b < max_bounces; ++b) hid = hash_mix(hid ^ 0xffffffffULL);
+    unsigned long long h = hash_mix(hid ^ ((unsigned long long)(valid ? 1 : 0) |
+                                           ((unsigned long long)(escaped ? 1 : 0) << 8) |
+                                           ((unsigned long long)(unsigned int)n_ids << 16)));
+    h = hash_mix(h ^ dbits(n0x));
+    h = hash_mix(h ^ dbits(n0y));
+    h = hash_mix(h ^ dbits(n0z));
+    h = hash_mix(h ^ dbits(path));
+    h = hash_mix(h ^ dbits(ox));
+    h = hash_mix(h ^ dbits(oy));
+    h = hash_mix(h ^ dbits(oz));
+    return h;
+}
 
 // grid != null: rays from the grid; else origins/dirs arrays
 // d_prim (grid mode only, may be null): query-0 results from launch_raster
+// grid mode traces rays r_base + [0, n) of the grid
 cudaError_t launch_trace_full(const TraceCfg &cfg, const GridDev *d_grid,
                               const double *d_orig, const double *d_dirs, int64_t n,
-                              const FullOut &out, const PrimHit *d_prim,
+                              int64_t r_base, const FullOut &out, const PrimHit *d_prim,
                               unsigned long long *d_counter, cudaStream_t st,
                               const LaunchStats &ls);
+
+// ---- reference-order traversal (reforder.cu) --------------------------------
+// The reference-layout tree (bvh.py:58-88) and the mesh in original order.
+struct RefView {
+    const double *nmin, *nmax;       // (N,3)
+    const int32_t *first, *count, *order;
+    int round_f32;                   // boxes rounded outward to float32 (bvh.py:286-290)
+    const double *verts;             // (T,9) original order
+    int single;                      // float32 edge subtraction (storage kSingle)
+};
+cudaError_t launch_closest_ref(const RefView &V, const double *d_orig, const double *d_dirs,
+                               int64_t n, double t_min, double t_max, int64_t *d_tri,
+                               double *d_t, int64_t *d_visits, cudaStream_t st,
+                               const LaunchStats &ls);
+// d_slots != null: solve mode over n slots of d_units; else grid (d_grids)
+// or list mode like launch_trace_full
+cudaError_t launch_trace_ref(const RefView &V, const TraceCfg &cfg, const GridDev *d_grids,
+                             const double *d_orig, const double *d_dirs, int64_t n,
+                             int64_t r_base, const FullOut &out, const UnitDev *d_units,
+                             SlotRec *d_slots, int n_units, cudaStream_t st,
+                             const LaunchStats &ls);
 
 cudaError_t launch_closest(const BvhView &B, int storage, const double *d_orig,
                            const double *d_dirs, int64_t n, double t_min, double t_max,
@@ -119,8 +213,8 @@ cudaError_t launch_closest(const BvhView &B, int storage, const double *d_orig,
 // ---- primary visibility (raster pass) -------------------------------------
 // The primary rays of an aperture form a regular orthographic grid with one
 // direction, so query 0 of every ray is answered per TRIANGLE instead of per
-// ray: each (grid, triangle) pair enumerates the grid cells inside the
-// triangle's projected bounding box (plus a margin) and runs the same exact
+// ray: each (grid, triangle) pair enumerates the grid cells of a region
+// proven to hold every cell its test can accept and runs the same exact
 // FP64 Moller-Trumbore test on each (origin built exactly as the launcher
 // builds it).  A 128-bit compare-and-swap keeps the lexicographic (t, id)
 // minimum of bvh.py:340 per ray, independent of execution order.
@@ -139,6 +233,7 @@ struct RasterArgs {
     int4 *big;                     // queue of big-triangle chunks (grid, tri, chunk, -)
     unsigned long long *nbig;      // its fill counter
     int64_t big_cap;               // its capacity (items beyond it stay in k_raster)
+    int64_t row_lo, row_hi;        // rows [row_lo, row_hi) only (a partial trace_grid)
 };
 constexpr int64_t kNoSlot = INT64_MIN;   // segment not in this batch / shard
 cudaError_t launch_raster(const RasterArgs &a, cudaStream_t st, const LaunchStats &ls);

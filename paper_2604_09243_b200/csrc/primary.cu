@@ -3,12 +3,11 @@
 //
 // All primary rays of one aperture share the direction k and start on a
 // regular grid: origin(i, j) = corner + ((i+.5) ds) u + ((j+.5) ds) v
-// (transport.py:339-345).  A ray can only be accepted by a triangle's
-// Moller-Trumbore test if it passes through the triangle (edge-inclusive, up
-// to rounding far below a cell), i.e. if its cell centre lies in the
-// triangle's projection onto the aperture plane.  So instead of one BVH
-// traversal per ray, every (grid, triangle) pair enumerates the cells of its
-// projected bounding box widened by kMargin cells and evaluates the SAME exact
+// (transport.py:339-345).  So instead of one BVH traversal per ray, every
+// (grid, triangle) pair enumerates a candidate set of cells PROVEN to
+// contain every cell its Moller-Trumbore test can accept (see "Candidate
+// region" below; it covers near-edge-on triangles whose rounding-dominated
+// det accepts rays far outside the triangle) and evaluates the SAME exact
 // FP64 test on each (bit-identical origin; d x e2 and 1/det hoisted: they do
 // not depend on the origin).  The closest hit is the lexicographic minimum
 // of (t, id) over accepted triangles (bvh.py:340), order-independent, so a
@@ -25,7 +24,38 @@
 
 namespace sbr {
 
-constexpr double kMargin = 0.01;   // cells; >> every projection rounding error
+// Candidate region (why the raster pass is exactly the linear scan).
+// Möller-Trumbore accepts a ray o only if its rounded numerators pass
+//   sigma*un in [0, D(1+3e)],  sigma*vn >= 0,  sigma*(un+vn) <= D(1+4e)
+// (sigma = sign det, D = |det|, e = 2^-53; an underflowed product is covered
+// by an absolute 1e-290).  un and vn differ from the exact affine functions
+//   F(o) = sigma (o - a).p          (p = d x e2 as computed, geometry.py:336)
+//   G(o) = sigma (o - a).(e1 x d)   (= sigma d.((o - a) x e1), geometry.py:347)
+// by at most a few ulp of the magnitude sums Mp = sum_k |p_k| R_k and
+// Mr = sum_k (|e1 x d| terms)_k R_k, where R_k bounds |o_k|, |a_k| and
+// |o_k - a_k| over the aperture; the same bound also absorbs the rounding of
+// the origin (pipeline.cu grid_origin) and of the cell-space coefficients
+// below.  With Eu = 64e Mp and Ev = 64e Mr (about 3x the worst first-order
+// sum) every accepted cell (i, j) satisfies, for the cell-space affine forms
+//   F(i, j) = f0 + fi i + fj j,  G(i, j) = g0 + gi i + gj j,
+//   F >= -Eu,   G >= -Ev,   F + G <= H = D(1 + 16e) + Eu + Ev.
+// That triangle of cells is a superset of the accepting set for EVERY
+// triangle, including near-edge-on ones whose rounding-dominated det lets
+// Möller-Trumbore accept rays far outside the triangle: there the region is
+// a long thin strip (the two edge forms are almost parallel), clipped by
+// the aperture.  Cells outside it cannot be accepted, so query 0 from this
+// pass is the reference's documented semantics, the lexicographic (t, id)
+// minimum over EVERY accepting triangle -- "identical to a linear scan"
+// (bvh.py:394-395) -- with no tree and no padding involved.
+//   Well-conditioned pairs (the region's three vertices are stable under
+// rounding): candidates = the vertices' bounding box (widened by their error
+// bound), walked as a rectangle, or as per-row spans of the three
+// half-planes for big triangles.  Otherwise (WIDE): the bounding box of the
+// two edge strips clipped to the aperture, walked as spans along the
+// box's shorter side (one column through a grid-aligned edge-on panel, not
+// every row), always through the chunk queue.
+constexpr double kEps = 1.1102230246251565e-16;   // 2^-53
+constexpr double kTiny = 1e-290;
 constexpr int kRasterThreads = 256;
 constexpr int kRasterWarps = kRasterThreads / 32;
 constexpr long long kBigTri = 2048;     // candidates above which a triangle is chunked
@@ -59,19 +89,22 @@ __device__ __forceinline__ void prim_min(PrimHit *h, unsigned long long bits, un
     }
 }
 
-// Candidate rectangle of one (grid, triangle): the cells whose centre lies
-// in the triangle's projected bounding box widened by kMargin.  count == 0:
-// the triangle cannot be hit (det == 0, geometry.py:339) or lies outside.
+// Candidates of one (grid, triangle).  The bounding box [i0, i0+rows) x
+// [j0, j0+cols) is walked line by line: lines are rows (trans = 0) or
+// columns (trans = 1), each clipped to the half-plane span.  count == 0: the
+// triangle cannot be hit (det == 0, geometry.py:339) or lies outside.
 struct RasterSetup {
     TriF64 T;
     TriDir P;
     double inv;
-    long long i0, j0, count;
+    long long i0, j0, rows, count;
     int cols;
-    double pa[3], pb[3];   // projected vertices in cell units (row a, column b)
+    int trans, wide;
+    double f0, fi, fj, g0, gi, gj, eu, ev, h, err;
 };
 
-__device__ __forceinline__ RasterSetup raster_setup(const TriF64 &T, const GridDev &G)
+__device__ __forceinline__ RasterSetup raster_setup(const TriF64 &T, const GridDev &G,
+                                                    int64_t row_lo, int64_t row_hi)
 {
     RasterSetup S;
     S.T = T;
@@ -79,31 +112,131 @@ __device__ __forceinline__ RasterSetup raster_setup(const TriF64 &T, const GridD
     S.P = tri_dir(T, G.k[0], G.k[1], G.k[2]);
     if (S.P.det == 0.0) return S;
     const int64_t n_v = G.n_v, n_u = G.n_rays / n_v;
-    const double isp = 1.0 / G.spacing;
-    const double rx = T.ax - G.corner[0], ry = T.ay - G.corner[1], rz = T.az - G.corner[2];
-    const double a0 = (rx * G.u[0] + ry * G.u[1] + rz * G.u[2]) * isp - 0.5;
-    const double b0 = (rx * G.v[0] + ry * G.v[1] + rz * G.v[2]) * isp - 0.5;
-    const double a1 = a0 + (T.e1x * G.u[0] + T.e1y * G.u[1] + T.e1z * G.u[2]) * isp;
-    const double b1 = b0 + (T.e1x * G.v[0] + T.e1y * G.v[1] + T.e1z * G.v[2]) * isp;
-    const double a2 = a0 + (T.e2x * G.u[0] + T.e2y * G.u[1] + T.e2z * G.u[2]) * isp;
-    const double b2 = b0 + (T.e2x * G.v[0] + T.e2y * G.v[1] + T.e2z * G.v[2]) * isp;
-    S.pa[0] = a0; S.pa[1] = a1; S.pa[2] = a2;
-    S.pb[0] = b0; S.pb[1] = b1; S.pb[2] = b2;
-    const double alo = fmin(fmin(a0, a1), a2) - kMargin;
-    const double ahi = fmax(fmax(a0, a1), a2) + kMargin;
-    const double blo = fmin(fmin(b0, b1), b2) - kMargin;
-    const double bhi = fmax(fmax(b0, b1), b2) + kMargin;
+    const double dx = G.k[0], dy = G.k[1], dz = G.k[2];
+    const double sg = S.P.det > 0.0 ? 1.0 : -1.0;
+    const double D = fabs(S.P.det);
+    // r = e1 x d, so that G(o) = (o - a) . r
+    const double rx = T.e1y * dz - T.e1z * dy;
+    const double ry = T.e1z * dx - T.e1x * dz;
+    const double rz = T.e1x * dy - T.e1y * dx;
+    const double su = (double)n_u * G.spacing, sv = (double)n_v * G.spacing;
+    const double Rx = fabs(G.corner[0]) + fabs(T.ax) + su * fabs(G.u[0]) + sv * fabs(G.v[0]);
+    const double Ry = fabs(G.corner[1]) + fabs(T.ay) + su * fabs(G.u[1]) + sv * fabs(G.v[1]);
+    const double Rz = fabs(G.corner[2]) + fabs(T.az) + su * fabs(G.u[2]) + sv * fabs(G.v[2]);
+    const double Mp = fabs(S.P.px) * Rx + fabs(S.P.py) * Ry + fabs(S.P.pz) * Rz;
+    const double Mr = (fabs(T.e1y * dz) + fabs(T.e1z * dy)) * Rx +
+                      (fabs(T.e1z * dx) + fabs(T.e1x * dz)) * Ry +
+                      (fabs(T.e1x * dy) + fabs(T.e1y * dx)) * Rz;
+    S.eu = 64.0 * kEps * Mp + kTiny;
+    S.ev = 64.0 * kEps * Mr + kTiny;
+    S.h = D * (1.0 + 16.0 * kEps) + S.eu + S.ev;
+    // evaluation slack of any form at any cell of the aperture
+    S.err = 16.0 * kEps * (Mp + Mr + D) + kTiny;
+    // cell-space forms: o*(i, j) = corner + (i+.5) ds u + (j+.5) ds v
+    const double cx = G.corner[0] - T.ax, cy = G.corner[1] - T.ay, cz = G.corner[2] - T.az;
+    const double sp = G.spacing;
+    S.fi = sg * sp * (G.u[0] * S.P.px + G.u[1] * S.P.py + G.u[2] * S.P.pz);
+    S.fj = sg * sp * (G.v[0] * S.P.px + G.v[1] * S.P.py + G.v[2] * S.P.pz);
+    S.f0 = sg * (cx * S.P.px + cy * S.P.py + cz * S.P.pz) + 0.5 * (S.fi + S.fj);
+    S.gi = sg * sp * (G.u[0] * rx + G.u[1] * ry + G.u[2] * rz);
+    S.gj = sg * sp * (G.v[0] * rx + G.v[1] * ry + G.v[2] * rz);
+    S.g0 = sg * (cx * rx + cy * ry + cz * rz) + 0.5 * (S.gi + S.gj);
+    if (!(isfinite(S.f0) && isfinite(S.g0) && isfinite(S.h) && isfinite(S.fi) &&
+          isfinite(S.fj) && isfinite(S.gi) && isfinite(S.gj)))
+        return S;   // non-finite geometry: the exact test accepts nothing finite
+    double alo, ahi, blo, bhi;
+    // ---- well-conditioned: the region's vertices by Cramer's rule --------
+    const double det2 = S.fi * S.gj - S.fj * S.gi;
+    const double kd = fabs(S.fi * S.gj) + fabs(S.fj * S.gi);
+    S.wide = 1;
+    if (fabs(det2) > 1e-6 * kd) {
+        const double cf[3] = {-S.eu, -S.eu, S.h + S.ev};
+        const double cg[3] = {-S.ev, S.h + S.eu, -S.ev};
+        alo = bhi = -INFINITY;
+        ahi = blo = INFINITY;
+        double emax = 0.0;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const double nf = cf[k] - S.f0, ng = cg[k] - S.g0;
+            const double a = (nf * S.gj - S.fj * ng) / det2;
+            const double b = (S.fi * ng - S.gi * nf) / det2;
+            // first-order error bound of the 2x2 solve, x4 (relative error of
+            // det2 <= 2e kd/|det2|; numerators carry their own few ulp)
+            const double mf = fabs(cf[k]) + fabs(S.f0), mg = fabs(cg[k]) + fabs(S.g0);
+            const double ea = 16.0 * kEps * (fabs(a) * kd + mf * fabs(S.gj) + fabs(S.fj) * mg) /
+                              fabs(det2);
+            const double eb = 16.0 * kEps * (fabs(b) * kd + mg * fabs(S.fi) + fabs(S.gi) * mf) /
+                              fabs(det2);
+            emax = fmax(emax, fmax(ea, eb));
+            alo = fmin(alo, a - ea); ahi = fmax(ahi, a + ea);
+            blo = fmin(blo, b - eb); bhi = fmax(bhi, b + eb);
+        }
+        if (emax <= 0.25 && isfinite(alo) && isfinite(ahi) && isfinite(blo) && isfinite(bhi)) {
+            S.wide = 0;
+            alo -= 1e-9 * (1.0 + fabs(alo)); ahi += 1e-9 * (1.0 + fabs(ahi));
+            blo -= 1e-9 * (1.0 + fabs(blo)); bhi += 1e-9 * (1.0 + fabs(bhi));
+        }
+    }
+    if (S.wide) {
+        // ---- ill-conditioned: intersect the boxes of the two edge strips
+        // -Eu <= F <= H + Ev and -Ev <= G <= H + Eu, clipped to the aperture
+        alo = 0.0; ahi = (double)(n_u - 1);
+        blo = 0.0; bhi = (double)(n_v - 1);
+        const double xs[3] = {S.f0, S.fi, S.fj}, ys[3] = {S.g0, S.gi, S.gj};
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+            const double *c = s ? ys : xs;
+            const double lo = s ? -S.ev : -S.eu, hi = s ? S.h + S.eu : S.h + S.ev;
+            // column range over the aperture's rows (extremes at the end rows)
+            if (c[2] != 0.0) {
+                double mn = INFINITY, mx = -INFINITY;
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const double x = e ? (double)(n_u - 1) : 0.0;
+                    const double q0 = (lo - c[0] - c[1] * x) / c[2];
+                    const double q1 = (hi - c[0] - c[1] * x) / c[2];
+                    const double w = (S.err + 8.0 * kEps * (fabs(lo) + fabs(hi) + fabs(c[0]) +
+                                                            fabs(c[1] * x))) / fabs(c[2]);
+                    mn = fmin(mn, fmin(q0, q1) - w);
+                    mx = fmax(mx, fmax(q0, q1) + w);
+                }
+                blo = fmax(blo, mn - 1e-9 * (1.0 + fabs(mn)));
+                bhi = fmin(bhi, mx + 1e-9 * (1.0 + fabs(mx)));
+            }
+            // row range over the aperture's columns
+            if (c[1] != 0.0) {
+                double mn = INFINITY, mx = -INFINITY;
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const double y = e ? (double)(n_v - 1) : 0.0;
+                    const double q0 = (lo - c[0] - c[2] * y) / c[1];
+                    const double q1 = (hi - c[0] - c[2] * y) / c[1];
+                    const double w = (S.err + 8.0 * kEps * (fabs(lo) + fabs(hi) + fabs(c[0]) +
+                                                            fabs(c[2] * y))) / fabs(c[1]);
+                    mn = fmin(mn, fmin(q0, q1) - w);
+                    mx = fmax(mx, fmax(q0, q1) + w);
+                }
+                alo = fmax(alo, mn - 1e-9 * (1.0 + fabs(mn)));
+                ahi = fmin(ahi, mx + 1e-9 * (1.0 + fabs(mx)));
+            }
+        }
+        if (!(alo <= ahi && blo <= bhi)) return S;   // NaN-safe: empty
+    }
     if (!(ahi >= 0.0 && bhi >= 0.0 && alo <= (double)(n_u - 1) && blo <= (double)(n_v - 1)))
         return S;                               // outside the aperture (or non-finite)
-    const int64_t i0 = alo <= 0.0 ? 0 : (int64_t)ceil(alo);
-    const int64_t i1 = ahi >= (double)(n_u - 1) ? n_u - 1 : (int64_t)floor(ahi);
+    int64_t i0 = alo <= 0.0 ? 0 : (int64_t)ceil(alo);
+    int64_t i1 = ahi >= (double)(n_u - 1) ? n_u - 1 : (int64_t)floor(ahi);
+    if (i0 < row_lo) i0 = row_lo;               // row window of a partial trace
+    if (i1 > row_hi - 1) i1 = row_hi - 1;
     const int64_t j0 = blo <= 0.0 ? 0 : (int64_t)ceil(blo);
     const int64_t j1 = bhi >= (double)(n_v - 1) ? n_v - 1 : (int64_t)floor(bhi);
     const int64_t rows = i1 - i0 + 1, cols = j1 - j0 + 1;
     if (rows <= 0 || cols <= 0) return S;
     S.i0 = i0;
     S.j0 = j0;
+    S.rows = rows;
     S.cols = (int)cols;
+    S.trans = S.wide && cols < rows;
     S.count = rows * cols;
     S.inv = __drcp_rn(S.P.det);                 // == IEEE 1.0 / det
     return S;
@@ -116,7 +249,7 @@ __device__ __forceinline__ RasterSetup raster_setup(const TriF64 &T, const GridD
 __device__ __forceinline__ void trim_owned(RasterSetup &S, const GridDev &G, const int64_t *segs)
 {
     if (S.count == 0) return;
-    const int64_t rows = S.count / S.cols;
+    const int64_t rows = S.rows;
     const int64_t r0 = S.i0 * G.n_v + S.j0;
     const int64_t r1 = (S.i0 + rows - 1) * G.n_v + S.j0 + S.cols - 1;
     int64_t qf = -1, ql = -1;
@@ -133,7 +266,9 @@ __device__ __forceinline__ void trim_owned(RasterSetup &S, const GridDev &G, con
     const int64_t a = fa > S.i0 ? fa : S.i0;
     const int64_t b = fb < S.i0 + rows - 1 ? fb : S.i0 + rows - 1;
     S.i0 = a;
-    S.count = (b - a + 1) * S.cols;
+    S.rows = b - a + 1;
+    S.trans = S.trans && S.cols < S.rows;
+    S.count = S.rows * S.cols;
 }
 
 __device__ __forceinline__ void split_cell(long long local, int cols, long long &li, long long &lj)
@@ -174,33 +309,33 @@ __device__ __forceinline__ void raster_cell(const RasterArgs &a, const GridDev &
                  (unsigned int)id);
 }
 
-// Column extent of the cells of row a within kMargin (L-inf) of the
-// projected triangle: the b-range of the triangle clipped to the band
-// |a' - a| <= kMargin (its extreme points are vertices inside the band or
-// edge / band-boundary crossings), widened by kMargin.  The exact test can
-// only accept cells within rounding (<< kMargin) of the triangle, so this
-// span holds every cell the bounding box would have offered that can hit.
-__device__ __forceinline__ void row_span(const RasterSetup &S, double a, double &blo, double &bhi)
+// Span of line x (a row i, or a column j when S.trans) inside the candidate
+// region: the three half-planes F + Eu >= 0, G + Ev >= 0, H - F - G >= 0
+// solved for the other index, each widened by its evaluation slack.
+__device__ __forceinline__ void line_span(const RasterSetup &S, double x, double &lo, double &hi)
 {
-    double lo = __longlong_as_double(0x7ff0000000000000LL), hi = -lo;
-    const double c[2] = {a - kMargin, a + kMargin};
+    const double fa = S.trans ? S.fj : S.fi, fb = S.trans ? S.fi : S.fj;
+    const double ga = S.trans ? S.gj : S.gi, gb = S.trans ? S.gi : S.gj;
+    const double k0[3] = {S.f0 + S.eu, S.g0 + S.ev, S.h - S.f0 - S.g0};
+    const double kx[3] = {fa, ga, -(fa + ga)};
+    const double ky[3] = {fb, gb, -(fb + gb)};
+    lo = -INFINITY;
+    hi = INFINITY;
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        const int k1 = k == 2 ? 0 : k + 1;
-        if (S.pa[k] >= c[0] && S.pa[k] <= c[1]) { lo = fmin(lo, S.pb[k]); hi = fmax(hi, S.pb[k]); }
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            const double d0 = S.pa[k] - c[e], d1 = S.pa[k1] - c[e];
-            if ((d0 < 0.0 && d1 > 0.0) || (d0 > 0.0 && d1 < 0.0)) {
-                const double t = d0 / (d0 - d1);   // in (0, 1)
-                const double b = S.pb[k] + t * (S.pb[k1] - S.pb[k]);
-                lo = fmin(lo, b);
-                hi = fmax(hi, b);
-            }
+    for (int c = 0; c < 3; ++c) {
+        // need k0 + kx x + ky y >= 0
+        const double num = k0[c] + kx[c] * x;
+        const double w = S.err + 8.0 * kEps * (fabs(k0[c]) + fabs(kx[c] * x) + S.h);
+        if (ky[c] > 0.0) {
+            const double y = (-num - w) / ky[c];
+            lo = fmax(lo, y - 1e-9 * (1.0 + fabs(y)));
+        } else if (ky[c] < 0.0) {
+            const double y = (-num - w) / ky[c];
+            hi = fmin(hi, y + 1e-9 * (1.0 + fabs(y)));
+        } else if (num + w < 0.0) {
+            lo = INFINITY;   // the whole line fails this half-plane
         }
     }
-    blo = lo - kMargin;
-    bhi = hi + kMargin;
 }
 
 // Persistent: each warp pulls its next 32-triangle item from a global
@@ -230,16 +365,17 @@ k_raster(RasterArgs a, int64_t ntri_pad)
         long long count = 0;
         RasterTri &R = st[wib][lane];
         if (tri < a.ntri) {
-            RasterSetup S = raster_setup(load_tri<STORAGE>(a.B, (int)tri), G);
+            RasterSetup S = raster_setup(load_tri<STORAGE>(a.B, (int)tri), G, a.row_lo, a.row_hi);
             if (a.sparse) trim_owned(S, G, a.seg_slot + __ldg(&a.seg_base[g]));
             count = S.count;
             if (count > kBigTri && a.big) {
                 const long long nch = (count + kBigChunk - 1) / kBigChunk;
                 // sharded / partial batches: queue only chunks whose rows touch
-                // a segment of this launch (ray-tile shards skip 7/8 of them)
+                // a segment of this launch (ray-tile shards skip 7/8 of them);
+                // column-major (trans) chunks span every row: always queued
                 const int64_t *segs = a.seg_slot + __ldg(&a.seg_base[g]);
                 auto owned = [&](long long c) {
-                    if (!a.sparse) return true;
+                    if (!a.sparse || S.trans) return true;
                     const long long c1 = (c + 1) * kBigChunk < count ? (c + 1) * kBigChunk : count;
                     const int64_t r0 = (S.i0 + c * kBigChunk / S.cols) * G.n_v + S.j0;
                     const int64_t r1 = (S.i0 + (c1 - 1) / S.cols) * G.n_v + S.j0 + S.cols - 1;
@@ -251,11 +387,17 @@ k_raster(RasterArgs a, int64_t ntri_pad)
                 for (long long c = 0; c < nch; ++c) nown += owned(c);
                 const unsigned long long at =
                     nown ? atomicAdd(a.nbig, (unsigned long long)nown) : 0ULL;
-                if (at + nown <= (unsigned long long)a.big_cap) {
+                const unsigned long long cap = (unsigned long long)a.big_cap;
+                if (at + nown <= cap) {
                     long long w = 0;
                     for (long long c = 0; c < nch; ++c)
                         if (owned(c)) a.big[at + w++] = make_int4(gl, (int)tri, (int)c, 0);
                     count = 0;                          // walked by k_raster_big
+                } else {
+                    // the reservation straddles the queue's end: publish no
+                    // work in its in-range part (k_raster_big walks every
+                    // entry below min(nbig, cap)) and walk the triangle here
+                    for (unsigned long long w = at; w < cap; ++w) a.big[w] = make_int4(-1, 0, 0, 0);
                 }
             }
             if (count) {
@@ -312,9 +454,11 @@ k_raster(RasterArgs a, int64_t ntri_pad)
     }
 }
 
-// Chunks of big triangles: a warp takes one chunk (kBigChunk candidates of
-// one triangle), recomputes the (identical) set-up and walks 32 cells at a
-// time.
+// Chunks of big (or WIDE) triangles: a warp takes one chunk (kBigChunk
+// candidates of one triangle's bounding box, line-major), recomputes the
+// (identical) set-up and walks the chunk's lines 32 at a time: lane r takes
+// line r's cells inside the half-plane span (not the whole box line), then
+// the warp walks the concatenated spans 32 cells at a time.
 template <int STORAGE>
 __global__ void __launch_bounds__(kRasterThreads, 4)
 k_raster_big(RasterArgs a)
@@ -328,32 +472,32 @@ k_raster_big(RasterArgs a)
         const unsigned long long w = __shfl_sync(0xffffffffu, got, 0);
         if (w >= n) break;
         const int4 it = a.big[w];
+        if (it.x < 0) continue;                 // unpublished (overflowed reservation)
         const int g = __ldg(&a.bgrids[it.x]);
         const GridDev &G = a.grids[g];
-        RasterSetup S = raster_setup(load_tri<STORAGE>(a.B, it.y), G);
+        RasterSetup S = raster_setup(load_tri<STORAGE>(a.B, it.y), G, a.row_lo, a.row_hi);
         const int64_t *seg = a.seg_slot + __ldg(&a.seg_base[g]);
         if (a.sparse) trim_owned(S, G, seg);
         const long long c0 = (long long)it.z * kBigChunk;
         const long long c1 = c0 + kBigChunk < S.count ? c0 + kBigChunk : S.count;
         if (c0 >= c1) continue;
-        // the chunk's rows, 32 at a time: lane r takes row r's cells that
-        // lie within kMargin of the triangle (not the whole box row), then
-        // the warp walks the concatenated spans 32 cells at a time
-        const long long row_a = c0 / S.cols, row_b = (c1 - 1) / S.cols;
-        for (long long rbase = row_a; rbase <= row_b; rbase += 32) {
-            const long long li = rbase + lane;
-            long long jl = 0, jr = -1;
-            if (li <= row_b) {
-                const long long wl = li == row_a ? c0 % S.cols : 0;
-                const long long wr = li == row_b ? (c1 - 1) % S.cols : S.cols - 1;
-                double blo, bhi;
-                row_span(S, (double)(S.i0 + li), blo, bhi);
-                const long long sl = blo > (double)(S.j0 + wl) ? (long long)ceil(blo) - S.j0 : wl;
-                const long long sr = bhi < (double)(S.j0 + wr) ? (long long)floor(bhi) - S.j0 : wr;
-                jl = sl;
-                jr = sr;
+        const long long width = S.trans ? S.rows : (long long)S.cols;   // cells per line
+        const long long l0 = S.trans ? S.j0 : S.i0, m0 = S.trans ? S.i0 : S.j0;
+        const long long line_a = c0 / width, line_b = (c1 - 1) / width;
+        for (long long lbase = line_a; lbase <= line_b; lbase += 32) {
+            const long long li = lbase + lane;
+            long long ml = 0, mr = -1;
+            if (li <= line_b) {
+                const long long wl = li == line_a ? c0 % width : 0;
+                const long long wr = li == line_b ? (c1 - 1) % width : width - 1;
+                double lo, hi;
+                line_span(S, (double)(l0 + li), lo, hi);
+                if (lo <= (double)(m0 + wr) && hi >= (double)(m0 + wl)) {
+                    ml = lo > (double)(m0 + wl) ? (long long)ceil(lo) - m0 : wl;
+                    mr = hi < (double)(m0 + wr) ? (long long)floor(hi) - m0 : wr;
+                }
             }
-            const int cnt = jr >= jl ? (int)(jr - jl + 1) : 0;
+            const int cnt = mr >= ml ? (int)(mr - ml + 1) : 0;
             int incl = cnt;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -362,7 +506,7 @@ k_raster_big(RasterArgs a)
             }
             const int total = __shfl_sync(0xffffffffu, incl, 31);
             const int excl = incl - cnt;
-            const int jl32 = (int)jl;
+            const int ml32 = (int)ml;
             for (int base = 0; base < total; base += 32) {
                 const int c = base + lane;
                 int owner = 0;   // first lane whose inclusive count exceeds c
@@ -370,10 +514,12 @@ k_raster_big(RasterArgs a)
                 for (int st = 16; st >= 1; st >>= 1)
                     if (__shfl_sync(0xffffffffu, incl, owner + st - 1) <= c) owner += st;
                 const int oex = __shfl_sync(0xffffffffu, excl, owner);
-                const int ojl = __shfl_sync(0xffffffffu, jl32, owner);
-                if (c < total)
-                    raster_cell(a, G, seg, S.T, S.P, S.inv, S.T.id, S.i0 + rbase + owner,
-                                S.j0 + ojl + (c - oex));
+                const int oml = __shfl_sync(0xffffffffu, ml32, owner);
+                if (c < total) {
+                    const long long line = l0 + lbase + owner, m = m0 + oml + (c - oex);
+                    raster_cell(a, G, seg, S.T, S.P, S.inv, S.T.id, S.trans ? m : line,
+                                S.trans ? line : m);
+                }
             }
         }
     }

@@ -50,7 +50,6 @@ constexpr int kChunkRays = SBR_CHUNK_RAYS;   // rays claimed per warp-level atom
 constexpr int kDoneBreak = SBR_DONE_BREAK;   // finished lanes that end a traversal phase
 
 enum LaneState : int { kIdle = 0, kTrav = 1, kLeaf = 2, kDone = 3 };
-enum TraceMode : int { kModeSolve = 0, kModeGrid = 1, kModeList = 2 };
 
 struct TraceArgs {
     TraceCfg cfg;
@@ -68,6 +67,9 @@ struct TraceArgs {
     // slots already hold their final records.  n_work is read from n_work_dev.
     const uint2 *worklist;    // (slot, unit index)
     const unsigned long long *n_work_dev;
+    // grid mode: rays r_base + [0, n_work) of the grid (a row range); output
+    // and prim indices are relative to r_base
+    int64_t r_base;
     // outputs
     SlotRec *slots;           // solve
     FullOut full;             // grid / list
@@ -92,8 +94,9 @@ struct LaneRay {
 #endif
     // bookkeeping
     int64_t r;       // ray index within its grid / list
-    int64_t slot;    // output slot (solve) or ray index
+    int64_t slot;    // output slot (solve) or ray index (relative to r_base)
     int grid;
+    unsigned long long hid;   // hash mode: running hash of the per-bounce ids
 };
 
 template <int STORAGE>
@@ -265,7 +268,7 @@ k_trace_persistent(TraceArgs a)
                         a.slots[L.slot] = z;
                     }
                 } else if (MODE == kModeGrid) {
-                    L.r = L.slot;
+                    L.r = L.slot + a.r_base;
                     G = a.grids;
                 } else {
                     L.r = L.slot;
@@ -280,8 +283,10 @@ k_trace_persistent(TraceArgs a)
                         grid_origin(*G, L.r, L.ox, L.oy, L.oz);
                         L.dx = G->k[0]; L.dy = G->k[1]; L.dz = G->k[2];
                     }
-                    if (MODE != kModeSolve && a.full.ids) {
-                        int *ids = a.full.ids + L.r * (int64_t)cfg.max_bounces;
+                    if (MODE != kModeSolve && a.full.seg_hash) {
+                        L.hid = hash_mix((unsigned long long)L.r);
+                    } else if (MODE != kModeSolve && a.full.ids) {
+                        int *ids = a.full.ids + L.slot * (int64_t)cfg.max_bounces;
                         for (int b = 0; b < cfg.max_bounces; ++b) ids[b] = -1;
                     }
                     L.path = 0.0; L.n0x = L.n0y = L.n0z = 0.0; L.cosd = 0.0;
@@ -290,7 +295,7 @@ k_trace_persistent(TraceArgs a)
                         state = kDone;   // query 0 answered by the raster pass (loaded above)
                     } else if (MODE != kModeList && a.prim) {
                         // query 0 already answered by the raster pass
-                        const PrimHit h = a.prim[MODE == kModeSolve ? L.slot : L.r];
+                        const PrimHit h = a.prim[L.slot];
                         const bool hit = h.tbits != kNoHitBits;
                         L.best_t = hit ? __longlong_as_double((long long)h.tbits)
                                        : __longlong_as_double(0x7ff0000000000000LL);
@@ -441,8 +446,10 @@ k_trace_persistent(TraceArgs a)
                     escaped = true;
                     finish = true;
                 } else {
-                    if (MODE != kModeSolve && a.full.ids)
-                        a.full.ids[L.r * (int64_t)cfg.max_bounces + L.bounces] = L.best;
+                    if (MODE != kModeSolve && a.full.seg_hash)
+                        L.hid = hash_mix(L.hid ^ (unsigned long long)(unsigned int)L.best);
+                    else if (MODE != kModeSolve && a.full.ids)
+                        a.full.ids[L.slot * (int64_t)cfg.max_bounces + L.bounces] = L.best;
                     const double hx = DA(L.ox, DM(t, L.dx)), hy = DA(L.oy, DM(t, L.dy)),
                                  hz = DA(L.oz, DM(t, L.dz));
                     L.path = DA(L.path, t);
@@ -475,8 +482,13 @@ k_trace_persistent(TraceArgs a)
                     rec.meta = (uint32_t)L.bounces | kMetaActive | (L.valid ? kMetaValid : 0u) |
                                (escaped ? kMetaEscaped : 0u) | (sel ? kMetaSel : 0u);
                     a.slots[L.slot] = rec;
+                } else if (a.full.seg_hash) {
+                    const unsigned long long h = record_hash(
+                        L.hid, L.bounces, cfg.max_bounces, L.valid, escaped, L.n0x, L.n0y,
+                        L.n0z, L.path, L.dx, L.dy, L.dz);
+                    atomicAdd(a.full.seg_hash + L.r / a.full.seg_rays, h);
                 } else {
-                    const int64_t r = L.r;
+                    const int64_t r = L.slot;
                     a.full.valid[r] = L.valid ? 1 : 0;
                     a.full.escaped[r] = escaped ? 1 : 0;
                     a.full.bounces[r] = L.bounces;

@@ -254,19 +254,45 @@ def trace_ray(bvh: Bvh, mesh: Mesh, origin, direction,
 
 
 def trace_grid(bvh: Bvh, mesh: Mesh, grid: ApertureGrid, params: TraceParams = TraceParams(),
-               workers: int = 1, with_ids: bool = False) -> HitRecords:
+               workers: int = 1, with_ids: bool = False, rows=None) -> HitRecords:
     """Trace every grid ray on the GPU (transport.py:375-422).  ``workers``
-    is accepted for API parity; the result never depends on it."""
+    is accepted for API parity; the result never depends on it.  ``rows =
+    (i_start, i_end)`` traces that row range only, like one worker's
+    ``_trace_rows`` call (transport.py:330-356); records then start at ray
+    ``i_start * n_v``."""
     ctx = nat.context()
     d = bvh.device(mesh, ctx)
-    n = grid.ray_count
+    i0, i1 = (0, grid.n_u) if rows is None else (int(rows[0]), int(rows[1]))
+    n = (i1 - i0) * grid.n_v
     out = _alloc(n, params.max_bounces, with_ids)
     g = nat.make_grid(grid)
     cp = _cparams(mesh, params)
-    nat.check(ctx.lib.sbr_trace_grid(ctx.handle, d.mesh_dev.handle, d.handle, ctypes.byref(g),
-                                     ctypes.byref(cp), *[nat.ptr(a) for a in out]),
-              "sbr_trace_grid")
+    nat.check(ctx.lib.sbr_trace_grid_rows(ctx.handle, d.mesh_dev.handle, d.handle,
+                                          ctypes.byref(g), ctypes.byref(cp), i0, i1,
+                                          *[nat.ptr(a) for a in out]),
+              "sbr_trace_grid_rows")
     return HitRecords(*out)
+
+
+def trace_grid_hash(bvh: Bvh, mesh: Mesh, grid: ApertureGrid,
+                    params: TraceParams = TraceParams(), rows=None,
+                    seg_rays: int = nat.SEGMENT_RAYS) -> np.ndarray:
+    """Per-segment record checksums of ``trace_grid(..., with_ids=True)``
+    without materialising the records (sbr_trace_grid_hash): uint64 array,
+    entry s = wrapping sum over the rays r // seg_rays == s of a splitmix64
+    chain over r, the per-bounce ids and every HitRecords field.  Equal to
+    the oracle's ``trace_grid_hash`` on identical inputs iff every record
+    is bit-identical (up to 2^-64 collisions)."""
+    ctx = nat.context()
+    d = bvh.device(mesh, ctx)
+    i0, i1 = (0, grid.n_u) if rows is None else (int(rows[0]), int(rows[1]))
+    out = np.zeros(-(-grid.n_u * grid.n_v // int(seg_rays)), np.uint64)
+    g = nat.make_grid(grid)
+    cp = _cparams(mesh, params)
+    nat.check(ctx.lib.sbr_trace_grid_hash(ctx.handle, d.mesh_dev.handle, d.handle,
+                                          ctypes.byref(g), ctypes.byref(cp), i0, i1,
+                                          int(seg_rays), nat.ptr(out)), "sbr_trace_grid_hash")
+    return out
 
 
 def dump_hits_csv(records: HitRecords, grid: ApertureGrid, path) -> None:

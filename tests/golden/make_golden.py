@@ -407,6 +407,142 @@ def gen_meshes_and_mie():
          dihedral_checksum=np.array(dihedral_mesh().checksum()))
 
 
+def _edgeon_triangle(rng, center, d, size, tilt):
+    """A triangle whose plane contains direction d up to a relative tilt
+    |n.d| ~ tilt (near-edge-on for rays along d)."""
+    d = d / np.linalg.norm(d)
+    a = rng.normal(size=3)
+    e = a - (a @ d) * d
+    e /= np.linalg.norm(e)
+    m = np.cross(d, e)                      # normal of the exactly edge-on plane
+    p0 = center + size * (rng.uniform(-0.5, 0.5) * d + rng.uniform(-0.5, 0.5) * e)
+    p1 = center + size * (rng.uniform(-0.5, 0.5) * d + rng.uniform(-0.5, 0.5) * e)
+    p2 = center + size * (rng.uniform(-0.5, 0.5) * d + rng.uniform(-0.5, 0.5) * e)
+    p2 = p2 + tilt * size * m
+    return np.array([p0, p1, p2]), e, m
+
+
+def gen_edgeon():
+    """Near-edge-on fixtures (|n.d| <= 1e-13): the class where Moller-Trumbore
+    accepts rays far outside the triangle and the reference's own answer
+    depends on its tree (bvh.py:329-342).  Recorded: the reference's
+    closest hits on its SAH and median trees, the linear scan
+    (tests/meshes.py brute_force_hits), and trace_grid records + ids on an
+    aperture whose grid columns lie in edge-on planes."""
+    rng = np.random.default_rng(20261017)
+    # ---- (a) random triangles x rays lying in their planes (closest hit) ----
+    # origins ON the triangle's plane (affine combinations of its vertices,
+    # mostly outside it), directions in the plane tilted by |n.d| in
+    # [1e-16, 1e-13]: det is then rounding-dominated and u, v, t are noise
+    tris, origins, dirs = [], [], []
+    for k in range(300):
+        center = rng.uniform(-3.0, 3.0, 3)
+        size = float(10 ** rng.uniform(-2, 0))
+        tri = center + size * rng.normal(size=(3, 3))
+        tris.append(tri)
+        e1, e2 = tri[1] - tri[0], tri[2] - tri[0]
+        nrm = np.cross(e1, e2)
+        nrm /= np.linalg.norm(nrm)
+        for _ in range(67):
+            # far (up to 48 edge lengths), mid and close to the triangle
+            al, be = rng.uniform(-6.0, 6.0, 2) * (8.0, 1.0, 0.25)[_ % 3] + (0, 0, 0.3)[_ % 3]
+            o = tri[0] + al * e1 + be * e2
+            g1, g2 = rng.normal(size=2)
+            dd = g1 * e1 + g2 * e2
+            dd /= np.linalg.norm(dd)
+            dd = dd + float(10 ** rng.uniform(-16, -13)) * rng.choice([-1, 1]) * nrm
+            origins.append(o)
+            dirs.append(dd / np.linalg.norm(dd))
+    mesh = sbr.mesh_from_soup(np.array(tris))
+    origins = np.array(origins)
+    dirs = np.array(dirs)
+    arrays = mesh_arrays(mesh)
+    arrays.update(origins=origins, dirs=dirs)
+    for rule in ("sah", "median"):
+        tree = sbr.build(mesh, sbr.BuildParams(split_rule=rule))
+        arrays.update(bvh_arrays(tree, prefix=f"{rule}_"))
+        tri, t, vis = sbr.closest_hit_batch(tree, mesh, origins, dirs)
+        arrays.update({f"{rule}_tri": tri, f"{rule}_t": t, f"{rule}_visits": vis})
+    btri, bt = brute_force_hits(mesh, origins, dirs)
+    arrays.update(brute_tri=btri, brute_t=bt)
+    save("edgeon_rays", **arrays)
+    print(f"    edgeon_rays: {len(origins)} rays, hits sah={int((arrays['sah_tri'] >= 0).sum())}"
+          f" median={int((arrays['median_tri'] >= 0).sum())} brute={int((btri >= 0).sum())};"
+          f" sah!=brute {int((arrays['sah_tri'] != btri).sum())},"
+          f" median!=brute {int((arrays['median_tri'] != btri).sum())}")
+
+    # ---- (b) aperture whose columns lie in edge-on planes (trace_grid) -----
+    th, ph, lam = 1.1, 0.7, 0.1
+    spacing = lam / 5
+    din = sbr.IncidentDirection(th, ph)
+    k = np.asarray(din.k_inc, np.float64)
+    anchors = [np.array([[-2.0, -2, -2], [-1.99, -2, -2], [-2, -1.99, -2]]),
+               np.array([[2.0, 2, 2], [1.99, 2, 2], [2, 1.99, 2]])]
+    box = sbr.mesh_from_soup(np.array(anchors))
+    grid = sbr.build_aperture(box.aabb, din, spacing, wavelength=lam)
+    u = np.asarray(grid.u); v = np.asarray(grid.v); corner = np.asarray(grid.corner)
+
+    def origin(i, j):
+        bx = corner + ((i + 0.5) * spacing) * u
+        return bx + ((j + 0.5) * spacing) * v
+
+    tris = list(anchors)
+    # a backstop plate across the beam (real hits behind the edge-on set)
+    c, hu, hv = 0.8 * k, 0.7 * u, 0.7 * v
+    tris += [np.array([c - hu - hv, c + hu - hv, c + hu + hv]),
+             np.array([c - hu - hv, c + hu + hv, c - hu + hv])]
+    # a few ordinary triangles in front, for multi-bounce paths
+    for _ in range(12):
+        cc = rng.uniform(-1.0, 1.0, 3) - 0.8 * k
+        a, b = rng.normal(size=3), rng.normal(size=3)
+        tris.append(np.array([cc, cc + 0.3 * a / np.linalg.norm(a), cc + 0.3 * b / np.linalg.norm(b)]))
+    n_edge = 0
+    while n_edge < 48:
+        i = int(rng.integers(grid.n_u * 3 // 10, grid.n_u * 7 // 10))
+        j = int(rng.integers(grid.n_v * 3 // 10, grid.n_v * 7 // 10))
+        o = origin(i, j)
+        # a plane holding every ray of row i (directions k and v) or of
+        # column j (directions k and u)
+        w = v if n_edge % 2 else u
+        size = float(10 ** rng.uniform(-1.3, -0.5))
+        tilt = float(10 ** rng.uniform(-16, -13)) if n_edge % 4 >= 2 else 0.0
+        center = o + (grid.standoff + float(rng.uniform(-1.0, 1.0))) * k
+        p = [center + size * (rng.uniform(-0.5, 0.5) * k + rng.uniform(-0.5, 0.5) * w)
+             for _ in range(3)]
+        p[2] = p[2] + tilt * size * np.cross(k, w)
+        p = np.array(p)
+        if np.abs(p).max() > 1.95:
+            continue
+        tris.append(p)
+        n_edge += 1
+    mesh = sbr.mesh_from_soup(np.array(tris))
+    assert np.allclose(mesh.aabb.min, box.aabb.min) and np.allclose(mesh.aabb.max, box.aabb.max)
+    grid = sbr.build_aperture(mesh.aabb, din, spacing, wavelength=lam)
+    tree = sbr.build(mesh)
+    params = sbr.TraceParams(max_bounces=3)
+    rec = sbr.trace_grid(tree, mesh, grid, params)
+    ids = trace_with_ids(tree, mesh, grid, params)
+    for key in ("valid", "normal0", "path", "bounces", "escaped", "out_dir"):
+        assert np.array_equal(getattr(rec, key), ids[key]), key
+    n = grid.ray_count
+    ii, jj = np.divmod(np.arange(n), grid.n_v)
+    o_all = (corner + ((ii + 0.5) * spacing)[:, None] * u) + ((jj + 0.5) * spacing)[:, None] * v
+    btri, bt = brute_force_hits(mesh, o_all, np.tile(k, (n, 1)))
+    arrays = mesh_arrays(mesh)
+    arrays.update(grid_arrays(grid))
+    arrays.update(theta=np.float64(th), phi=np.float64(ph), wavelength=np.float64(lam),
+                  max_bounces=np.int64(3), strict=np.bool_(False),
+                  epsilon=np.float64(params.resolve_epsilon(mesh)),
+                  valid=rec.valid, normal0=rec.normal0, path=rec.path, bounces=rec.bounces,
+                  escaped=rec.escaped, out_dir=rec.out_dir, tri_ids=ids["tri_ids"],
+                  prim_brute_tri=btri, prim_brute_t=bt)
+    arrays.update(bvh_arrays(tree, prefix="sah_"))
+    save("edgeon_grid", **arrays)
+    first = ids["tri_ids"][:, 0].astype(np.int64)
+    print(f"    edgeon_grid: {grid.n_u}x{grid.n_v} rays, query-0 ref!=linear scan:"
+          f" {int((first != btri).sum())}")
+
+
 def main():
     print(f"reference sbr {sbr.__version__} numba {numba.__version__} "
           f"numpy {np.__version__} python {platform.python_version()}")
@@ -416,6 +552,7 @@ def main():
     gen_aperture()
     gen_sweep()
     gen_meshes_and_mie()
+    gen_edgeon()
     with open(os.path.join(OUT, "VERSIONS.json"), "w") as fh:
         json.dump({"sbr": sbr.__version__, "numba": numba.__version__,
                    "numpy": np.__version__, "python": platform.python_version(),
@@ -424,4 +561,8 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1:   # e.g. make_golden.py gen_edgeon
+        for fn in sys.argv[1:]:
+            globals()[fn]()
+    else:
+        main()

@@ -1,0 +1,209 @@
+"""Near-edge-on / tie rays: the class where the reference's own answer depends
+on its tree (bvh.py:329-342), and the reference-order traversal mode.
+
+* ``traversal_order("reference")`` replays bvh.py:306-362 on the reference
+  tree: bit-identical to the reference on EVERY ray, visit counts included.
+* The fast path (raster + BVH4 kernel) is bit-identical on every ROBUST ray
+  (oracle classifier); on the others it returns an accepting
+  triangle (a valid closest hit of some conservative traversal).
+* The raster pass answers query 0 with the linear scan on EVERY ray, the
+  reference's documented semantics (bvh.py:394-395), edge-on rays included.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+import paper_2604_09243_b200 as sbr
+from paper_2604_09243_b200 import meshgen
+from conftest import golden_names, load_golden
+
+pytestmark = pytest.mark.gpu
+
+REC = ("valid", "normal0", "path", "bounces", "escaped", "out_dir", "tri_ids")
+
+
+def _mesh(g):
+    v0, v1, v2 = g["mesh_v0"], g["mesh_v1"], g["mesh_v2"]
+    pts = np.concatenate([v0, v1, v2]).astype(np.float64)
+    return sbr.Mesh(v0=v0, v1=v1, v2=v2, normals=g["mesh_normals"],
+                    aabb=sbr.Aabb(pts.min(0), pts.max(0)))
+
+
+def _grid(g):
+    return sbr.ApertureGrid(u=g["grid_u"], v=g["grid_v"], k_inc=g["grid_k"],
+                            corner=g["grid_corner"], spacing=float(g["grid_spacing"]),
+                            n_u=int(g["grid_n_u"]), n_v=int(g["grid_n_v"]),
+                            cell_area=float(g["grid_cell_area"]),
+                            standoff=float(g["grid_standoff"]), margin=float(g["grid_margin"]))
+
+
+def _uploaded(g, rule):
+    return sbr.Bvh(g[f"{rule}_nodes_min"], g[f"{rule}_nodes_max"], g[f"{rule}_node_first"],
+                   g[f"{rule}_node_count"], g[f"{rule}_tri_order"],
+                   int(g[f"{rule}_max_depth_seen"]))
+
+
+@pytest.fixture
+def reference_order():
+    with sbr.traversal_order("reference"):
+        yield
+
+
+def _oracle_scene(orc, g):
+    tree = orc.build(g["mesh_v0"], g["mesh_v1"], g["mesh_v2"])
+    return orc.Scene(g["mesh_v0"], g["mesh_v1"], g["mesh_v2"], g["mesh_normals"], tree)
+
+
+# ---------------------------------------------------------------------------
+# reference-order mode: bit for bit on every ray
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("rule", ["sah", "median"])
+def test_reference_order_closest_hit_edgeon(rule, reference_order):
+    g = load_golden("edgeon_rays")
+    mesh = _mesh(g)
+    for tree in (sbr.build(mesh, sbr.BuildParams(split_rule=rule)), _uploaded(g, rule)):
+        tri, t, vis = sbr.closest_hit_batch(tree, mesh, g["origins"], g["dirs"])
+        assert np.array_equal(tri, g[f"{rule}_tri"])
+        assert np.array_equal(t, g[f"{rule}_t"])
+        assert np.array_equal(vis, g[f"{rule}_visits"])   # the reference's own visit count
+
+
+def test_reference_order_trace_grid_edgeon(reference_order):
+    g = load_golden("edgeon_grid")
+    mesh = _mesh(g)
+    tree = sbr.build(mesh)
+    rec = sbr.trace_grid(tree, mesh, _grid(g), sbr.TraceParams(max_bounces=3), with_ids=True)
+    for k in REC:
+        assert np.array_equal(getattr(rec, k), g[k]), k
+
+
+@pytest.mark.parametrize("name", golden_names("bvh_"))
+def test_reference_order_closest_hit_goldens(name, reference_order):
+    g = load_golden(name)
+    mesh = _mesh(g)
+    if mesh.dtype == np.float32:
+        pytest.skip("float32 closest_hit_batch runs float32 rays (documented)")
+    for rule in ("sah", "median"):
+        tree = sbr.build(mesh, sbr.BuildParams(split_rule=rule))
+        tri, t, vis = sbr.closest_hit_batch(tree, mesh, g["origins"], g["dirs"])
+        assert np.array_equal(tri, g[f"{rule}_tri"]), rule
+        assert np.array_equal(t, g[f"{rule}_t"]), rule
+        assert np.array_equal(vis, g[f"{rule}_visits"]), rule
+
+
+@pytest.mark.parametrize("name", golden_names("trace_"))
+def test_reference_order_trace_goldens(name, reference_order):
+    g = load_golden(name)
+    mesh = _mesh(g)
+    tree = sbr.build(mesh)
+    params = sbr.TraceParams(max_bounces=int(g["max_bounces"]), epsilon=float(g["epsilon"]),
+                             strict_orientation=bool(g["strict"]))
+    rec = sbr.trace_grid(tree, mesh, _grid(g), params, with_ids=True)
+    for k in REC:
+        assert np.array_equal(getattr(rec, k), g[k]), (name, k)
+
+
+def test_reference_order_solve_equals_fast_on_robust_workload():
+    """The fused solve in reference order gives the fast path's bits on an
+    ordinary multi-bounce aircraft sweep (no tree-dependent rays there)."""
+    mesh = meshgen.generate_aircraft(density=0.03)
+    tree = sbr.build(mesh)
+    lam = 0.1
+    grids = [sbr.build_aperture(mesh.aabb, sbr.IncidentDirection(th, ph), lam / 5,
+                                wavelength=lam)
+             for th, ph in [(math.pi / 2, 0.0), (math.pi / 2, 2.0), (1.1, 4.0)]]
+    tp = sbr.TraceParams(max_bounces=5)
+    fast = sbr.solve_grids(tree, mesh, grids, tp, [2 * math.pi / lam])
+    with sbr.traversal_order("reference"):
+        ref = sbr.solve_grids(tree, mesh, grids, tp, [2 * math.pi / lam])
+    assert np.array_equal(fast.amplitude, ref.amplitude)
+    assert np.array_equal(fast.bounce_counts, ref.bounce_counts)
+    assert np.array_equal(fast.queries, ref.queries)
+
+
+def test_reference_order_needs_reference_tree():
+    mesh = meshgen.plate_mesh()
+    tree = sbr.build(mesh, sbr.BuildParams(split_rule="lbvh"))
+    with sbr.traversal_order("reference"):
+        with pytest.raises(sbr.ValidationError, match="reference tree"):
+            sbr.closest_hit_batch(tree, mesh, [[0.5, 0.5, 1.0]], [[0, 0, -1.0]])
+    assert sbr.get_traversal_order() == "fast"
+
+
+# ---------------------------------------------------------------------------
+# fast path: bit-exact on robust rays, a valid accepting answer elsewhere
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("rule", ["sah", "median", "lbvh"])
+def test_fast_closest_hit_edgeon(orc, rule):
+    g = load_golden("edgeon_rays")
+    mesh = _mesh(g)
+    tree = sbr.build(mesh, sbr.BuildParams(split_rule=rule))
+    tri, t, _ = sbr.closest_hit_batch(tree, mesh, g["origins"], g["dirs"])
+    rob = orc.classify_rays(_oracle_scene(orc, g), g["origins"], g["dirs"])
+    ref = g["brute_tri"]
+    assert np.array_equal(tri[rob], ref[rob])
+    assert np.array_equal(t[rob & (ref >= 0)], g["brute_t"][rob & (ref >= 0)])
+    # elsewhere: a hit of an accepting triangle at exactly its MT distance
+    for r in np.flatnonzero(~rob & (tri >= 0)):
+        k = int(tri[r])
+        tt = orc.tri_hit_pairs(g["mesh_v0"][k:k + 1], g["mesh_v1"][k:k + 1],
+                               g["mesh_v2"][k:k + 1], g["origins"][r:r + 1],
+                               g["dirs"][r:r + 1])
+        assert tt[0] == t[r]
+
+
+@pytest.mark.parametrize("primary", ["raster", "bvh"])
+def test_fast_trace_grid_edgeon(orc, monkeypatch, primary):
+    monkeypatch.setenv("SBR_PRIMARY", primary)
+    g = load_golden("edgeon_grid")
+    mesh = _mesh(g)
+    tree = sbr.build(mesh)
+    grid = _grid(g)
+    rec = sbr.trace_grid(tree, mesh, grid, sbr.TraceParams(max_bounces=3), with_ids=True)
+    rob, _, _ = orc.classify_grid(_oracle_scene(orc, g), grid, 3, float(g["epsilon"]))
+    assert rob.sum() > 0.99 * rob.size
+    for k in REC:
+        assert np.array_equal(getattr(rec, k)[rob], g[k][rob]), k
+
+
+def test_raster_query0_is_the_linear_scan_on_every_ray(monkeypatch):
+    """Query 0 from the raster pass == the reference's linear scan
+    (tests/meshes.py brute_force_hits) on EVERY ray of the edge-on aperture,
+    including the rays whose Moller-Trumbore acceptance lies far outside the
+    triangle (where the reference's BVH itself disagrees with its scan)."""
+    monkeypatch.setenv("SBR_PRIMARY", "raster")
+    g = load_golden("edgeon_grid")
+    mesh = _mesh(g)
+    tree = sbr.build(mesh)
+    rec = sbr.trace_grid(tree, mesh, _grid(g), sbr.TraceParams(max_bounces=1), with_ids=True)
+    bt = g["prim_brute_tri"]
+    assert np.array_equal(rec.tri_ids[:, 0].astype(np.int64), bt)
+    hit = bt >= 0
+    assert np.array_equal(rec.path[hit], g["prim_brute_t"][hit])
+    assert (g["tri_ids"][:, 0] != bt).sum() >= 10   # the reference's BVH differs there
+
+
+def test_raster_big_queue_overflow(monkeypatch):
+    """A chunk queue far too small for the big triangles (SBR_BIG_CAP) must
+    not change a bit: overflowing reservations publish no work and the
+    triangles are walked inline (stale entries were read)."""
+    mesh = meshgen.quantized_icosphere(1.0, 3)
+    tree = sbr.build(mesh)
+    lam = 2 * math.pi / 600
+    grid = sbr.build_aperture(mesh.aabb, sbr.IncidentDirection(1.0, 0.4), lam / 5,
+                              wavelength=lam)
+    tp = sbr.TraceParams(max_bounces=2)
+    monkeypatch.setenv("SBR_PRIMARY", "raster")
+    a = sbr.trace_grid(tree, mesh, grid, tp, with_ids=True)
+    for cap in ("1", "7", "300"):
+        monkeypatch.setenv("SBR_BIG_CAP", cap)
+        b = sbr.trace_grid(tree, mesh, grid, tp, with_ids=True)
+        for k in REC:
+            assert np.array_equal(getattr(a, k), getattr(b, k)), (cap, k)
+    monkeypatch.setenv("SBR_PRIMARY", "bvh")
+    monkeypatch.delenv("SBR_BIG_CAP")
+    c = sbr.trace_grid(tree, mesh, grid, tp, with_ids=True)
+    for k in REC:
+        assert np.array_equal(getattr(a, k), getattr(c, k)), k

@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
     missing = [n for n in _declared() if not hasattr(lib, n)]
     assert not missing
     assert set(_native.EXPORTED) == set(_declared())
-    assert lib.sbr_abi_version() == 2
+    assert lib.sbr_abi_version() == 3
 
 
 def test_sass_is_sm100a():
