@@ -45,6 +45,7 @@ typedef enum {
     SBR_ENOTSUP = 5,   /* input outside the native fast path (caller falls back to the
                           reference-equivalent Python reader; host I/O only) */
     SBR_ECUDA = 10,    /* CUDA runtime failure */
+    SBR_ENCCL = 11,    /* NCCL unavailable or a collective failed */
     SBR_ENOMEM = 12    /* device or host allocation failure */
 } sbr_status;
 
@@ -287,6 +288,47 @@ int sbr_finalize(sbr_ctx *ctx, const sbr_grid *grids, int32_t ngrids,
                  const double *k, int32_t nk, int32_t max_bounces,
                  const double *seg_dev, const int64_t *diag_dev, double *amp,
                  sbr_diag *diag);
+
+/* ---- one-collective sharding -------------------------------------------
+ * The same units as sbr_solve_shard, but partials AND diagnostics go into
+ * ONE float64 device buffer of sbr_packed_layout() doubles:
+ *   [segment partials (nseg*nk*2)][diagnostics (ngrids*(3+B+1)), integers
+ *   as doubles, max-bounce column 0][max-bounce slots (ngrids*nranks), this
+ *   rank's value in its own slot]
+ * so a single element-wise SUM over ranks (one ncclReduce) is exact
+ * (disjoint support; integers < 2^53) and sbr_finalize_packed takes the
+ * max over the slots.  Bit-identical to sbr_solve for any nranks. */
+int sbr_packed_layout(const sbr_grid *grids, int32_t ngrids, int32_t nk,
+                      int32_t max_bounces, int32_t nranks, int64_t *count);
+int sbr_solve_shard_packed(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *bvh,
+                           const sbr_grid *grids, int32_t ngrids,
+                           const sbr_trace_params *params, const double *k, int32_t nk,
+                           double gamma, int32_t count_trapped, int32_t rank,
+                           int32_t nranks, int32_t shard_mode, double *buf_dev);
+int sbr_finalize_packed(sbr_ctx *ctx, const sbr_grid *grids, int32_t ngrids,
+                        const double *k, int32_t nk, int32_t max_bounces, int32_t nranks,
+                        const double *buf_dev, double *amp, sbr_diag *diag);
+
+/* NCCL communicator of a context (one process per GPU; replaces the paper's
+ * MPI layer).  libnccl is loaded at run time: the library
+ * itself never needs it, these calls return SBR_ENCCL when it is absent.
+ * Rank 0 calls sbr_comm_unique_id and ships the 128 bytes to the others
+ * (any out-of-band channel: MPI, a file, torch.distributed, a socket). */
+int sbr_comm_version(int32_t *nccl_version);
+int sbr_comm_unique_id(uint8_t id[128]);
+int sbr_comm_init(sbr_ctx *ctx, int32_t nranks, int32_t rank, const uint8_t id[128]);
+int sbr_comm_destroy(sbr_ctx *ctx);
+/* in-place ncclReduce(sum, float64) of a device buffer to `root` */
+int sbr_reduce_sum_f64(sbr_ctx *ctx, double *buf_dev, int64_t count, int32_t root);
+/* sweep.py:296-370 run_sweep's solve across the communicator's ranks: shard
+ * (mode as sbr_solve_shard) -> one ncclReduce of the packed buffer ->
+ * finalize on `root` (amp/diag written there only; other ranks may pass
+ * NULL). */
+int sbr_solve_distributed(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *bvh,
+                          const sbr_grid *grids, int32_t ngrids,
+                          const sbr_trace_params *params, const double *k, int32_t nk,
+                          double gamma, int32_t count_trapped, int32_t shard_mode,
+                          int32_t root, double *amp, sbr_diag *diag);
 
 /* ---- mesh I/O (host only, no GPU needed) ---------------------------------
  * geometry.py:190-241 load_mesh: parse a Wavefront OBJ ("v"/"f" records,

@@ -19,8 +19,8 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 # SBR_LIB points at an alternative build (e.g. an instrumented variant)
 LIB_PATH = os.environ.get("SBR_LIB") or os.path.join(_PKG, "libsbr200.so")
 
-SBR_OK, SBR_EINVAL, SBR_EIO, SBR_ENUMERIC, SBR_ENOTSUP, SBR_ECUDA, SBR_ENOMEM = \
-    0, 2, 3, 4, 5, 10, 12
+SBR_OK, SBR_EINVAL, SBR_EIO, SBR_ENUMERIC, SBR_ENOTSUP, SBR_ECUDA, SBR_ENCCL, SBR_ENOMEM = \
+    0, 2, 3, 4, 5, 10, 11, 12
 STORAGE_AUTO, STORAGE_F32_EXACT, STORAGE_F64, STORAGE_SINGLE = 0, 1, 2, 3
 SEGMENT_RAYS = 1 << 19
 TRAVERSAL_FAST, TRAVERSAL_REFERENCE = 0, 1
@@ -32,6 +32,10 @@ class NativeUnavailable(SbrError, RuntimeError):
 
 class CudaError(SbrError, RuntimeError):
     """A CUDA runtime failure inside the library."""
+
+
+class CommError(SbrError, RuntimeError):
+    """NCCL is unavailable or a collective failed (SBR_ENCCL)."""
 
 
 c_i32, c_i64, c_dbl, c_vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p
@@ -105,6 +109,21 @@ _SIGS = {
                                            ctypes.POINTER(TraceParams), c_i64, c_i64, c_i64,
                                            c_vp]),
     "sbr_ctx_set_traversal": (ctypes.c_int, [c_vp, c_i32]),
+    "sbr_packed_layout": (ctypes.c_int, [c_vp, c_i32, c_i32, c_i32, c_i32,
+                                         ctypes.POINTER(c_i64)]),
+    "sbr_solve_shard_packed": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_i32,
+                                              ctypes.POINTER(TraceParams), c_vp, c_i32, c_dbl,
+                                              c_i32, c_i32, c_i32, c_i32, c_vp]),
+    "sbr_finalize_packed": (ctypes.c_int, [c_vp, c_vp, c_i32, c_vp, c_i32, c_i32, c_i32, c_vp,
+                                           c_vp, ctypes.POINTER(Diag)]),
+    "sbr_comm_version": (ctypes.c_int, [ctypes.POINTER(c_i32)]),
+    "sbr_comm_unique_id": (ctypes.c_int, [c_vp]),
+    "sbr_comm_init": (ctypes.c_int, [c_vp, c_i32, c_i32, c_vp]),
+    "sbr_comm_destroy": (ctypes.c_int, [c_vp]),
+    "sbr_reduce_sum_f64": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32]),
+    "sbr_solve_distributed": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_i32,
+                                             ctypes.POINTER(TraceParams), c_vp, c_i32, c_dbl,
+                                             c_i32, c_i32, c_i32, c_vp, ctypes.POINTER(Diag)]),
     "sbr_ctx_get_traversal": (ctypes.c_int, [c_vp, ctypes.POINTER(c_i32)]),
     "sbr_trace_rays": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64,
                                       ctypes.POINTER(TraceParams), c_vp, c_vp, c_vp, c_vp,
@@ -166,6 +185,8 @@ def check(rc: int, what: str = ""):
         raise OSError(text)
     if rc == SBR_ENOMEM:
         raise MemoryError(text)
+    if rc == SBR_ENCCL:
+        raise CommError(text)
     raise CudaError(f"[{rc}] {text}")
 
 

@@ -1,6 +1,7 @@
 // capi.cu -- the extern "C" boundary (include/sbr200.h): handles, argument
 // validation, host<->device staging and the batched solve orchestration.
 #include <chrono>
+#include <dlfcn.h>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -15,6 +16,7 @@
 #include "lbvh.h"
 #include "pipeline.h"
 #include "sahbuild.h"
+#include <nccl.h>   // types and enums only: libnccl is dlopen-ed (comm section)
 
 using namespace sbr;
 
@@ -77,6 +79,8 @@ struct sbr_ctx {
     int64_t launches = 0;
     std::mutex mu;
     int traversal = SBR_TRAVERSAL_FAST;   // sbr_ctx_set_traversal
+    void *comm = nullptr;                 // ncclComm_t (sbr_comm_init)
+    int comm_rank = 0, comm_size = 0;
     DevBuf<unsigned long long> counter;
     DevBuf<unsigned int> err_flag;
     DevBuf<unsigned long long> bad;
@@ -228,6 +232,7 @@ extern "C" int sbr_ctx_create(int device, sbr_ctx **out)
 extern "C" int sbr_ctx_destroy(sbr_ctx *ctx)
 {
     if (!ctx) return SBR_OK;
+    sbr_comm_destroy(ctx);
     const int dev = ctx->device;
     cudaStream_t s = ctx->stream;
     cudaSetDevice(dev);
@@ -1561,6 +1566,245 @@ static int finalize_locked(sbr_ctx *ctx, const sbr_grid *grids, int32_t ngrids, 
         }
     }
     return SBR_OK;
+}
+
+// ---------------------------------------------------------------------------
+// one-collective sharding: packed reduce buffer + NCCL (replaces the paper's
+// MPI layer; the reference's worker pool over angles,
+// sweep.py:327-349)
+// ---------------------------------------------------------------------------
+static int64_t packed_count(const sbr_grid *grids, int32_t ngrids, int32_t nk, int32_t B,
+                            int32_t nranks)
+{
+    std::vector<int64_t> seg_base(ngrids + 1);
+    sbr_segment_layout(grids, ngrids, seg_base.data());
+    return seg_base[ngrids] * nk * 2 + (int64_t)ngrids * (3 + B + 1 + nranks);
+}
+
+extern "C" int sbr_packed_layout(const sbr_grid *grids, int32_t ngrids, int32_t nk,
+                                 int32_t max_bounces, int32_t nranks, int64_t *count)
+{
+    REQUIRE(grids && count && ngrids >= 1 && nk >= 1 && max_bounces >= 1 && nranks >= 1,
+            "bad arguments");
+    *count = packed_count(grids, ngrids, nk, max_bounces, nranks);
+    return SBR_OK;
+}
+
+extern "C" int sbr_solve_shard_packed(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *bvh,
+                                      const sbr_grid *grids, int32_t ngrids,
+                                      const sbr_trace_params *params, const double *k,
+                                      int32_t nk, double gamma, int32_t count_trapped,
+                                      int32_t rank, int32_t nranks, int32_t shard_mode,
+                                      double *buf_dev)
+{
+    if (int rc = validate_solve(ctx, mesh, bvh, grids, ngrids, params, k, nk, gamma)) return rc;
+    REQUIRE(nranks >= 1 && rank >= 0 && rank < nranks, "bad rank %d / %d", rank, nranks);
+    REQUIRE(shard_mode == 0 || shard_mode == 1, "bad shard_mode");
+    REQUIRE(buf_dev, "NULL device buffer");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (int rc = set_device(ctx)) return rc;
+    const int B = params->max_bounces, stride = 3 + B + 1;
+    std::vector<int64_t> seg_base(ngrids + 1);
+    sbr_segment_layout(grids, ngrids, seg_base.data());
+    CUDA_TRY(ctx->diag.reserve((size_t)ngrids * stride));
+    if (int rc = solve_shard_locked(ctx, mesh, bvh, grids, ngrids, params, k, nk, gamma,
+                                    count_trapped, rank, nranks, shard_mode, (double2 *)buf_dev,
+                                    ctx->diag.p))
+        return rc;
+    CUDA_TRY(launch_pack_diag(ctx->diag.p, ngrids, stride, nranks, rank,
+                              buf_dev + seg_base[ngrids] * nk * 2, ctx->stream, ctx->stats()));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    return SBR_OK;
+}
+
+static int finalize_packed_locked(sbr_ctx *ctx, const sbr_grid *grids, int32_t ngrids,
+                                  const double *k, int32_t nk, int32_t B, int32_t nranks,
+                                  const double *buf_dev, double *amp, sbr_diag *diag)
+{
+    const int stride = 3 + B + 1;
+    std::vector<int64_t> seg_base(ngrids + 1);
+    sbr_segment_layout(grids, ngrids, seg_base.data());
+    DevBuf<int64_t> dg((size_t)ngrids * stride);
+    CUDA_TRY(dg.status());
+    CUDA_TRY(launch_unpack_diag(buf_dev + seg_base[ngrids] * nk * 2, ngrids, stride, nranks,
+                                dg.p, ctx->stream, ctx->stats()));
+    return finalize_locked(ctx, grids, ngrids, k, nk, B, (const double2 *)buf_dev, dg.p, amp,
+                           diag);
+}
+
+extern "C" int sbr_finalize_packed(sbr_ctx *ctx, const sbr_grid *grids, int32_t ngrids,
+                                   const double *k, int32_t nk, int32_t max_bounces,
+                                   int32_t nranks, const double *buf_dev, double *amp,
+                                   sbr_diag *diag)
+{
+    REQUIRE(ctx && amp && buf_dev, "NULL argument");
+    if (int rc = check_grids(grids, ngrids)) return rc;
+    REQUIRE(k && nk >= 1 && nk <= 65535, "need 1..65535 wavenumbers");
+    REQUIRE(max_bounces >= 1 && nranks >= 1, "bad max_bounces / nranks");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (int rc = set_device(ctx)) return rc;
+    return finalize_packed_locked(ctx, grids, ngrids, k, nk, max_bounces, nranks, buf_dev, amp,
+                                  diag);
+}
+
+// ---- NCCL, loaded at run time (no link-time dependency: the library still
+// loads on a host without NCCL; only the comm entry points need it).  The
+// first libnccl.so.2 already in the process (e.g. torch's) wins, else the
+// system's; SBR_NCCL_LIB names another.
+struct NcclApi {
+    bool tried = false;
+    void *h = nullptr;
+    std::string why;
+    decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+    decltype(&ncclCommInitRank) init_rank = nullptr;
+    decltype(&ncclCommDestroy) destroy = nullptr;
+    decltype(&ncclReduce) reduce = nullptr;
+    decltype(&ncclGetErrorString) error_string = nullptr;
+    decltype(&ncclGetVersion) version = nullptr;
+};
+static std::mutex g_nccl_mu;
+static NcclApi g_nccl;
+
+static const NcclApi *nccl_api()
+{
+    std::lock_guard<std::mutex> lk(g_nccl_mu);
+    if (g_nccl.tried) return g_nccl.h ? &g_nccl : nullptr;
+    g_nccl.tried = true;
+    const char *env = getenv("SBR_NCCL_LIB");
+    const char *cands[] = {env, "libnccl.so.2", "libnccl.so",
+                           "/usr/lib/x86_64-linux-gnu/libnccl.so.2"};
+    for (const char *c : cands) {
+        if (!c) continue;
+        g_nccl.h = dlopen(c, RTLD_NOW | RTLD_GLOBAL);
+        if (g_nccl.h) break;
+        g_nccl.why = dlerror();
+    }
+    if (!g_nccl.h) return nullptr;
+#define SBR_NCCL_SYM(f, n) g_nccl.f = (decltype(g_nccl.f))dlsym(g_nccl.h, n)
+    SBR_NCCL_SYM(get_unique_id, "ncclGetUniqueId");
+    SBR_NCCL_SYM(init_rank, "ncclCommInitRank");
+    SBR_NCCL_SYM(destroy, "ncclCommDestroy");
+    SBR_NCCL_SYM(reduce, "ncclReduce");
+    SBR_NCCL_SYM(error_string, "ncclGetErrorString");
+    SBR_NCCL_SYM(version, "ncclGetVersion");
+#undef SBR_NCCL_SYM
+    if (!(g_nccl.get_unique_id && g_nccl.init_rank && g_nccl.destroy && g_nccl.reduce &&
+          g_nccl.error_string && g_nccl.version)) {
+        g_nccl.why = "libnccl lacks a required symbol";
+        dlclose(g_nccl.h);
+        g_nccl.h = nullptr;
+        return nullptr;
+    }
+    return &g_nccl;
+}
+
+#define NCCL_TRY(api, x)                                                               \
+    do {                                                                               \
+        ncclResult_t r_ = (x);                                                         \
+        if (r_ != ncclSuccess)                                                         \
+            return fail(SBR_ENCCL, "%s failed: %s", #x, (api)->error_string(r_));      \
+    } while (0)
+
+extern "C" int sbr_comm_version(int32_t *version)
+{
+    REQUIRE(version, "NULL argument");
+    const NcclApi *api = nccl_api();
+    if (!api) return fail(SBR_ENCCL, "NCCL unavailable: %s", g_nccl.why.c_str());
+    int v = 0;
+    NCCL_TRY(api, api->version(&v));
+    *version = v;
+    return SBR_OK;
+}
+
+extern "C" int sbr_comm_unique_id(uint8_t id[128])
+{
+    REQUIRE(id, "NULL argument");
+    const NcclApi *api = nccl_api();
+    if (!api) return fail(SBR_ENCCL, "NCCL unavailable: %s", g_nccl.why.c_str());
+    ncclUniqueId u;
+    NCCL_TRY(api, api->get_unique_id(&u));
+    static_assert(sizeof(u) == 128, "ncclUniqueId is 128 bytes");
+    memcpy(id, &u, 128);
+    return SBR_OK;
+}
+
+extern "C" int sbr_comm_init(sbr_ctx *ctx, int32_t nranks, int32_t rank, const uint8_t id[128])
+{
+    REQUIRE(ctx && id, "NULL argument");
+    REQUIRE(nranks >= 1 && rank >= 0 && rank < nranks, "bad rank %d / %d", rank, nranks);
+    const NcclApi *api = nccl_api();
+    if (!api) return fail(SBR_ENCCL, "NCCL unavailable: %s", g_nccl.why.c_str());
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    REQUIRE(!ctx->comm, "context already has a communicator");
+    if (int rc = set_device(ctx)) return rc;
+    ncclUniqueId u;
+    memcpy(&u, id, 128);
+    ncclComm_t c = nullptr;
+    NCCL_TRY(api, api->init_rank(&c, nranks, u, rank));
+    ctx->comm = c;
+    ctx->comm_rank = rank;
+    ctx->comm_size = nranks;
+    return SBR_OK;
+}
+
+extern "C" int sbr_comm_destroy(sbr_ctx *ctx)
+{
+    REQUIRE(ctx, "ctx is NULL");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (!ctx->comm) return SBR_OK;
+    const NcclApi *api = nccl_api();
+    if (int rc = set_device(ctx)) return rc;
+    ncclComm_t c = (ncclComm_t)ctx->comm;
+    ctx->comm = nullptr;
+    if (api) NCCL_TRY(api, api->destroy(c));
+    return SBR_OK;
+}
+
+static int reduce_locked(sbr_ctx *ctx, double *buf_dev, int64_t count, int32_t root)
+{
+    REQUIRE(ctx->comm, "no communicator: call sbr_comm_init first");
+    REQUIRE(root >= 0 && root < ctx->comm_size, "bad root %d", root);
+    const NcclApi *api = nccl_api();
+    NCCL_TRY(api, api->reduce(buf_dev, buf_dev, (size_t)count, ncclFloat64, ncclSum, root,
+                              (ncclComm_t)ctx->comm, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    return SBR_OK;
+}
+
+extern "C" int sbr_reduce_sum_f64(sbr_ctx *ctx, double *buf_dev, int64_t count, int32_t root)
+{
+    REQUIRE(ctx && (buf_dev || count == 0) && count >= 0, "bad arguments");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (int rc = set_device(ctx)) return rc;
+    return reduce_locked(ctx, buf_dev, count, root);
+}
+
+extern "C" int sbr_solve_distributed(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *bvh,
+                                     const sbr_grid *grids, int32_t ngrids,
+                                     const sbr_trace_params *params, const double *k,
+                                     int32_t nk, double gamma, int32_t count_trapped,
+                                     int32_t shard_mode, int32_t root, double *amp,
+                                     sbr_diag *diag)
+{
+    REQUIRE(ctx && ctx->comm, "no communicator: call sbr_comm_init first");
+    if (int rc = validate_solve(ctx, mesh, bvh, grids, ngrids, params, k, nk, gamma)) return rc;
+    const int64_t count = packed_count(grids, ngrids, nk, params->max_bounces, ctx->comm_size);
+    DevBuf<double> buf;
+    {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        if (int rc = set_device(ctx)) return rc;
+        CUDA_TRY(buf.alloc((size_t)count));
+    }
+    if (int rc = sbr_solve_shard_packed(ctx, mesh, bvh, grids, ngrids, params, k, nk, gamma,
+                                        count_trapped, ctx->comm_rank, ctx->comm_size,
+                                        shard_mode, buf.p))
+        return rc;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (int rc = reduce_locked(ctx, buf.p, count, root)) return rc;
+    if (ctx->comm_rank != root) return SBR_OK;
+    REQUIRE(amp, "NULL amp on the root");
+    return finalize_packed_locked(ctx, grids, ngrids, k, nk, params->max_bounces,
+                                  ctx->comm_size, buf.p, amp, diag);
 }
 
 extern "C" int sbr_finalize(sbr_ctx *ctx, const sbr_grid *grids, int32_t ngrids,

@@ -509,6 +509,60 @@ __global__ void k_finalize(const double2 *__restrict__ seg_part,
 }
 
 // ---------------------------------------------------------------------------
+// packed reduce buffer (one SUM collective for partials AND diagnostics)
+// ---------------------------------------------------------------------------
+// tail = [diag (ng x stride) as doubles, column 2 zeroed][max bounce slots
+// (ng x nranks), this rank's value in slot `rank`]: every entry is an
+// integer < 2^53, so the SUM over ranks is exact, and the per-grid max bounce
+// is the max over the slots after the sum.
+__global__ void k_pack_diag(const int64_t *diag, int ng, int stride, int nranks, int rank,
+                            double *tail)
+{
+    const int64_t n = (int64_t)ng * stride;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t g = i / stride, c = i - g * stride;
+        tail[i] = c == 2 ? 0.0 : (double)diag[i];
+        if (c == 2) {
+            for (int r = 0; r < nranks; ++r)
+                tail[n + g * nranks + r] = r == rank ? (double)diag[i] : 0.0;
+        }
+    }
+}
+
+__global__ void k_unpack_diag(const double *tail, int ng, int stride, int nranks, int64_t *diag)
+{
+    const int64_t n = (int64_t)ng * stride;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t g = i / stride, c = i - g * stride;
+        if (c == 2) {
+            double m = 0.0;
+            for (int r = 0; r < nranks; ++r) m = fmax(m, tail[n + g * nranks + r]);
+            diag[i] = (int64_t)m;
+        } else {
+            diag[i] = (int64_t)tail[i];
+        }
+    }
+}
+
+cudaError_t launch_pack_diag(const int64_t *d_diag, int ng, int stride, int nranks, int rank,
+                             double *d_tail, cudaStream_t st, const LaunchStats &ls)
+{
+    k_pack_diag<<<64, 256, 0, st>>>(d_diag, ng, stride, nranks, rank, d_tail);
+    ++*ls.launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_unpack_diag(const double *d_tail, int ng, int stride, int nranks,
+                               int64_t *d_diag, cudaStream_t st, const LaunchStats &ls)
+{
+    k_unpack_diag<<<64, 256, 0, st>>>(d_tail, ng, stride, nranks, d_diag);
+    ++*ls.launches;
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // launch wrappers
 // ---------------------------------------------------------------------------
 template <class K>

@@ -261,6 +261,12 @@ cudaError_t launch_finalize(const double2 *d_seg_part, const int64_t *d_seg_base
                             int ngrids, int nk, const double *d_scale, double2 *d_amp,
                             cudaStream_t st, const LaunchStats &ls);
 
+// ---- packed reduce buffer (sbr_solve_shard_packed / sbr_finalize_packed) ---
+cudaError_t launch_pack_diag(const int64_t *d_diag, int ng, int stride, int nranks, int rank,
+                             double *d_tail, cudaStream_t st, const LaunchStats &ls);
+cudaError_t launch_unpack_diag(const double *d_tail, int ng, int stride, int nranks,
+                               int64_t *d_diag, cudaStream_t st, const LaunchStats &ls);
+
 // ---- scalar predicates ------------------------------------------------------
 cudaError_t launch_tri_pairs(const double *v0, const double *v1, const double *v2,
                              const double *o, const double *d, int64_t n, double t_min,

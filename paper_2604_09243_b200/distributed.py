@@ -1,4 +1,4 @@
-"""Multi-GPU sweep driver: one process per GPU, one NCCL reduce.
+"""Multi-GPU sweep driver: one process per GPU, ONE collective.
 
 Replaces the paper's MPI layer and the reference's
 thread pool over angles (pkg/src/sbr/sweep.py:327-349).
@@ -6,18 +6,24 @@ thread pool over angles (pkg/src/sbr/sweep.py:327-349).
 Work is cut into fixed units (grid g, segment s) of SEGMENT_RAYS consecutive
 ray indices.  ``shard_mode="angles"`` gives rank r every unit of the grids
 g = r (mod N) (the C2-C4 sweeps); ``shard_mode="rays"`` deals units of all
-grids round-robin (the single huge aperture of C5).  Each rank writes the
-FP64 partial sums of its own units into a buffer that is zero everywhere
-else, so the single ``reduce(SUM)`` adds exactly one non-zero term per
-element: the result is exact, order-independent and therefore bit-identical
-to the one-GPU run for any N.  Integer diagnostics ride in a second buffer
-(sum) plus a tiny MAX reduce for the per-grid max bounce.
+grids round-robin (the single huge aperture of C5).  Each rank writes into
+ONE float64 buffer (``sbr_solve_shard_packed``): the FP64 partial sums of
+its own units (zero everywhere else), its integer diagnostics as exact
+doubles, and its per-grid max bounce in a slot of its own.  A single
+element-wise ``reduce(SUM)`` therefore adds exactly one non-zero term per
+partial (exact, order-independent: bit-identical to the one-GPU run for
+any N) and the root takes the max over the max-bounce slots
+(``sbr_finalize_packed``).
+
+Two carriers for that one reduce: the caller's ``torch.distributed`` group
+(``comm="torch"``, NCCL on GPUs, gloo on CPU), or the library's own NCCL
+communicator (``comm="library"``: ``sbr_comm_init`` + ``sbr_solve_distributed``,
+the path a non-Python host binds through the C ABI).
 """
 
 from __future__ import annotations
 
 import ctypes
-import math
 from typing import Callable, Optional, Sequence
 
 import numpy as np
@@ -51,38 +57,97 @@ def diag_stride(max_bounces: int) -> int:
     return 3 + max_bounces + 1
 
 
-def reduce_partials(seg, diag, root: int = 0, group=None):
-    """One SUM reduce of the disjoint-support partial buffer, one SUM of the
-    integer diagnostics and one MAX of the max-bounce column (torch tensors
-    on the rank's device; NCCL on GPUs, gloo on CPU)."""
-    import torch
+def packed_count(grids: Sequence, nk: int, max_bounces: int, world: int) -> int:
+    """Doubles in the packed reduce buffer (mirrors sbr_packed_layout)."""
+    return int(segment_layout(grids)[-1]) * nk * 2 + len(grids) * (diag_stride(max_bounces)
+                                                                    + world)
+
+
+def pack_host(seg, diag, rank: int, world: int) -> np.ndarray:
+    """Host mirror of k_pack_diag (for CPU tests of the collective): the
+    packed buffer of one rank from its partials and int64 diagnostics."""
+    seg = np.asarray(seg, np.float64).ravel()
+    diag = np.asarray(diag, np.int64)
+    ng = diag.shape[0]
+    d = diag.astype(np.float64)
+    d[:, 2] = 0.0
+    slots = np.zeros((ng, world))
+    slots[:, rank] = diag[:, 2]
+    return np.concatenate([seg, d.ravel(), slots.ravel()])
+
+
+def unpack_host(buf, nseg_doubles: int, ng: int, stride: int, world: int):
+    """Host mirror of k_unpack_diag: (partials, int64 diagnostics)."""
+    buf = np.asarray(buf, np.float64)
+    seg = buf[:nseg_doubles]
+    d = buf[nseg_doubles:nseg_doubles + ng * stride].reshape(ng, stride)
+    slots = buf[nseg_doubles + ng * stride:].reshape(ng, world)
+    diag = d.astype(np.int64)
+    diag[:, 2] = slots.max(axis=1).astype(np.int64)
+    return seg, diag
+
+
+def _dst(root: int, group) -> int:
+    """``dist.reduce`` takes a GLOBAL rank; ``root`` is group-local."""
     import torch.distributed as dist
-    stride = diag.shape[1]
+    return dist.get_global_rank(group, root) if group is not None else root
+
+
+def reduce_packed(buf, root: int = 0, group=None):
+    """The one collective: element-wise SUM of the packed buffer to ``root``
+    (torch tensor on the rank's device; NCCL on GPUs, gloo on CPU)."""
+    import torch.distributed as dist
     # gloo reduces host tensors only: stage device buffers through the host
     # (a CPU process group driving GPUs, e.g. several ranks sharing one GPU)
-    staged = dist.get_backend(group) == "gloo" and seg.is_cuda
-    s, d = (seg.cpu(), diag.cpu()) if staged else (seg, diag)
-    maxb = d[:, 2].clone()
-    dist.reduce(s, dst=root, op=dist.ReduceOp.SUM, group=group)
-    dist.reduce(d, dst=root, op=dist.ReduceOp.SUM, group=group)
-    dist.reduce(maxb, dst=root, op=dist.ReduceOp.MAX, group=group)
-    if dist.get_rank(group) == root:
-        d[:, 2] = maxb
-        if staged:
-            seg.copy_(s)
-            diag.copy_(d)
-    assert stride == diag.shape[1]
-    return seg, diag
+    staged = dist.get_backend(group) == "gloo" and buf.is_cuda
+    b = buf.cpu() if staged else buf
+    dist.reduce(b, dst=_dst(root, group), op=dist.ReduceOp.SUM, group=group)
+    if staged and dist.get_rank(group) == root:
+        buf.copy_(b)
+    return buf
+
+
+# ---- library communicator (sbr_comm_*) -------------------------------------
+def init_library_comm(group=None, ctx: Optional[nat.Context] = None) -> nat.Context:
+    """Give this rank's library context an NCCL communicator over the ranks
+    of ``group``: rank 0 draws the unique id (sbr_comm_unique_id) and the
+    torch group ships it to the others (any out-of-band channel would do)."""
+    import torch.distributed as dist
+    ctx = ctx or nat.context()
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    uid = np.zeros(128, np.uint8)
+    if rank == 0:
+        nat.check(ctx.lib.sbr_comm_unique_id(nat.ptr(uid)), "sbr_comm_unique_id")
+    box = [uid.tobytes()]
+    dist.broadcast_object_list(box, src=_dst(0, group), group=group)
+    uid = np.frombuffer(box[0], np.uint8).copy()
+    nat.check(ctx.lib.sbr_comm_init(ctx.handle, world, rank, nat.ptr(uid)), "sbr_comm_init")
+    return ctx
+
+
+def destroy_library_comm(ctx: Optional[nat.Context] = None) -> None:
+    ctx = ctx or nat.context()
+    nat.check(ctx.lib.sbr_comm_destroy(ctx.handle), "sbr_comm_destroy")
+
+
+def _cparams(tree, mesh, trace_params, lambda_min, allow_aliasing):
+    return nat.make_trace_params(trace_params.max_bounces, trace_params.resolve_epsilon(mesh),
+                                 trace_params.strict_orientation, allow_aliasing,
+                                 lambda_min or 0.0, trace_params.sampling_factor)
 
 
 def solve_grids_distributed(tree, mesh, grids: Sequence, trace_params, wavenumbers,
                             gamma: float = -1.0, count_trapped: bool = False,
                             shard_mode: str = "angles", root: int = 0, group=None,
                             lambda_min: Optional[float] = None, allow_aliasing: bool = True,
-                            timer: Optional[Callable] = None, stats: Optional[dict] = None):
+                            timer: Optional[Callable] = None, stats: Optional[dict] = None,
+                            comm: str = "torch"):
     """Sharded fused solve; returns the sweep.SolveResult on ``root`` and
     None elsewhere.  Every rank must call it with identical arguments.
-    ``stats`` (optional) receives this rank's own query count."""
+    ``comm="library"`` uses the context's NCCL communicator
+    (init_library_comm) through sbr_solve_distributed; ``"torch"`` reduces
+    over the torch group.  ``stats`` (optional) receives this rank's own
+    query count (torch carrier only)."""
     import torch
     import torch.distributed as dist
     from .sweep import SolveResult, grid_array
@@ -92,45 +157,61 @@ def solve_grids_distributed(tree, mesh, grids: Sequence, trace_params, wavenumbe
     d = tree.device(mesh, ctx)
     ks = nat.f64(np.atleast_1d(wavenumbers))
     ng, B = len(grids), trace_params.max_bounces
-    base = segment_layout(grids)
-    dev = torch.device("cuda", ctx.device)
-    seg = torch.zeros(int(base[-1]) * ks.size * 2, dtype=torch.float64, device=dev)
-    diag = torch.zeros((ng, diag_stride(B)), dtype=torch.int64, device=dev)
     garr = grid_array(grids)
-    cp = nat.make_trace_params(B, trace_params.resolve_epsilon(mesh),
-                               trace_params.strict_orientation, allow_aliasing,
-                               lambda_min or 0.0, trace_params.sampling_factor)
-    torch.cuda.synchronize(dev)
-    if timer:
-        timer("start")
-    nat.check(ctx.lib.sbr_solve_shard(ctx.handle, d.mesh_dev.handle, d.handle, garr, ng,
-                                      ctypes.byref(cp), nat.ptr(ks), ks.size, float(gamma),
-                                      int(bool(count_trapped)), rank, world,
-                                      MODES[shard_mode], nat.c_vp(seg.data_ptr()),
-                                      nat.c_vp(diag.data_ptr())), "sbr_solve_shard")
-    ctx.synchronize()   # library stream -> visible to NCCL on torch's stream
-    if timer:
-        timer("traced")
-    if stats is not None:
-        stats["local_queries"] = int(diag[:, 1].sum().item())
-    reduce_partials(seg, diag, root, group)
-    if rank != root:
-        return None
+    cp = _cparams(tree, mesh, trace_params, lambda_min, allow_aliasing)
     amp = np.zeros((ng, ks.size, 2))
     valid = np.zeros(ng, np.int64)
     maxb = np.zeros(ng, np.int32)
     hist = np.zeros((ng, B + 1), np.int64)
     queries = np.zeros(ng, np.int64)
     dg = nat.Diag(valid.ctypes.data, maxb.ctypes.data, hist.ctypes.data, queries.ctypes.data)
+    dev = torch.device("cuda", ctx.device)
+    if comm == "library":
+        torch.cuda.synchronize(dev)
+        if timer:
+            timer("start")
+        nat.check(ctx.lib.sbr_solve_distributed(ctx.handle, d.mesh_dev.handle, d.handle, garr,
+                                                ng, ctypes.byref(cp), nat.ptr(ks), ks.size,
+                                                float(gamma), int(bool(count_trapped)),
+                                                MODES[shard_mode], root, nat.ptr(amp),
+                                                ctypes.byref(dg)), "sbr_solve_distributed")
+        if timer:
+            timer("traced")
+        if rank != root:
+            return None
+        return SolveResult(amp.view(np.complex128)[..., 0], valid, maxb, hist, queries)
+    if comm != "torch":
+        raise ValueError(f"unknown comm {comm!r}")
+    cnt = nat.c_i64()
+    nat.check(ctx.lib.sbr_packed_layout(garr, ng, ks.size, B, world, ctypes.byref(cnt)))
+    buf = torch.empty(int(cnt.value), dtype=torch.float64, device=dev)
     torch.cuda.synchronize(dev)
-    nat.check(ctx.lib.sbr_finalize(ctx.handle, garr, ng, nat.ptr(ks), ks.size, B,
-                                   nat.c_vp(seg.data_ptr()), nat.c_vp(diag.data_ptr()),
-                                   nat.ptr(amp), ctypes.byref(dg)), "sbr_finalize")
+    if timer:
+        timer("start")
+    nat.check(ctx.lib.sbr_solve_shard_packed(ctx.handle, d.mesh_dev.handle, d.handle, garr, ng,
+                                             ctypes.byref(cp), nat.ptr(ks), ks.size,
+                                             float(gamma), int(bool(count_trapped)), rank,
+                                             world, MODES[shard_mode],
+                                             nat.c_vp(buf.data_ptr())),
+              "sbr_solve_shard_packed")
+    if timer:
+        timer("traced")
+    if stats is not None:
+        nseg = int(segment_layout(grids)[-1]) * ks.size * 2
+        q = buf[nseg:nseg + ng * diag_stride(B)].view(ng, diag_stride(B))[:, 1]
+        stats["local_queries"] = int(q.sum().item())
+    reduce_packed(buf, root, group)     # the one collective
+    if rank != root:
+        return None
+    torch.cuda.synchronize(dev)
+    nat.check(ctx.lib.sbr_finalize_packed(ctx.handle, garr, ng, nat.ptr(ks), ks.size, B, world,
+                                          nat.c_vp(buf.data_ptr()), nat.ptr(amp),
+                                          ctypes.byref(dg)), "sbr_finalize_packed")
     return SolveResult(amp.view(np.complex128)[..., 0], valid, maxb, hist, queries)
 
 
 def run_sweep_distributed(config, mesh=None, shard_mode: str = "angles", root: int = 0,
-                          group=None):
+                          group=None, comm: str = "torch"):
     """``sweep.run_sweep`` across the ranks of the process group: every rank
     builds the (replicated) BVH on its GPU and traces its shard of the
     cells; the SweepResult is returned on ``root`` (None elsewhere)."""
@@ -143,5 +224,6 @@ def run_sweep_distributed(config, mesh=None, shard_mode: str = "angles", root: i
                allow_aliasing=True):
         return solve_grids_distributed(tree, m, grids, tp, ks, gamma, count_trapped,
                                        shard_mode=shard_mode, root=root, group=group,
-                                       lambda_min=lambda_min, allow_aliasing=allow_aliasing)
+                                       lambda_min=lambda_min, allow_aliasing=allow_aliasing,
+                                       comm=comm)
     return S._run_sweep(config, mesh, solver)

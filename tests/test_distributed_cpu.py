@@ -1,9 +1,11 @@
 """Host logic of the multi-GPU driver, run with world_size=2 over gloo.
 
-The device compute is replaced by the CPU oracle (test-only): each rank
-produces the partial sums of the segments it owns, zero elsewhere; the one
-SUM reduce must reproduce the single-rank buffer bit for bit, for both the
-angle and the ray-tile shard modes.
+The device compute is replaced by deterministic fake partials: each rank
+produces the partial sums of the segments it owns, zero elsewhere, packs
+them with its diagnostics into ONE buffer (the layout of
+sbr_solve_shard_packed); the one SUM reduce must reproduce the single-rank
+partials bit for bit and the per-grid max bounce, for both the angle and
+the ray-tile shard modes, also inside a sub-group.
 """
 
 import math
@@ -44,44 +46,62 @@ def _partials(grids, owners, rank, world, nk):
     return seg
 
 
-def _worker(rank, world, port, mode, out):
+GRIDS = [(700, 900), (1300, 1100), (10, 10), (2048, 1024)]
+
+
+def _worker(rank, world, port, mode, sub, out):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    grids = [_G(700, 900), _G(1300, 1100), _G(10, 10), _G(2048, 1024)]
+    group = None
+    if sub:   # ranks [1, world) form the group; group-local root 0 = global rank 1
+        group = dist.new_group(list(range(1, world)))
+        if rank == 0:
+            dist.destroy_process_group()
+            return
+    g_rank, g_world = dist.get_rank(group), dist.get_world_size(group)
+    grids = [_G(*g) for g in GRIDS]
     nk, B = 3, 4
-    owners = D.unit_owners(grids, world, mode)
-    seg = torch.from_numpy(_partials(grids, owners, rank, world, nk).ravel().copy())
-    diag = torch.zeros((len(grids), D.diag_stride(B)), dtype=torch.int64)
+    owners = D.unit_owners(grids, g_world, mode)
+    seg = _partials(grids, owners, g_rank, g_world, nk).ravel()
+    diag = np.zeros((len(grids), D.diag_stride(B)), np.int64)
+    base = D.segment_layout(grids)
     for g in range(len(grids)):
-        rows = np.arange(D.segment_layout(grids)[g], D.segment_layout(grids)[g + 1])
-        mine = (owners[rows] == rank).sum()
+        mine = (owners[np.arange(base[g], base[g + 1])] == g_rank).sum()
         diag[g, 0] = 10 * mine
-        diag[g, 2] = rank + g if mine else 0
-    D.reduce_partials(seg, diag, root=0)
-    if rank == 0:
-        out.put((seg.numpy().copy(), diag.numpy().copy()))
+        diag[g, 2] = g_rank + g if mine else 0
+    buf = torch.from_numpy(D.pack_host(seg, diag, g_rank, g_world))
+    assert buf.numel() == D.packed_count(grids, nk, B, g_world)
+    D.reduce_packed(buf, root=0, group=group)
+    if g_rank == 0:
+        out.put(D.unpack_host(buf.numpy(), seg.size, len(grids), D.diag_stride(B), g_world)
+                + (g_world,))
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["angles", "rays"])
-def test_disjoint_reduce_is_exact(mode):
-    world = 2
+@pytest.mark.parametrize("mode,world,sub", [("angles", 2, False), ("rays", 2, False),
+                                            ("rays", 3, True)])
+def test_one_packed_reduce_is_exact(mode, world, sub):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, sub, q))
+             for r in range(world)]
     for p in procs:
         p.start()
-    seg, diag = q.get(timeout=120)
+    seg, diag, g_world = q.get(timeout=120)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    grids = [_G(700, 900), _G(1300, 1100), _G(10, 10), _G(2048, 1024)]
+    grids = [_G(*g) for g in GRIDS]
     ref = _partials(grids, np.zeros(D.segment_layout(grids)[-1], np.int64), 0, 1, 3)
     assert np.array_equal(seg, ref.ravel())   # bit-identical to the 1-rank buffer
     base = D.segment_layout(grids)
     assert np.array_equal(diag[:, 0], 10 * np.diff(base))
+    owners = D.unit_owners(grids, g_world, mode)
+    for g in range(len(grids)):
+        ranks = set(owners[base[g]:base[g + 1]].tolist())
+        assert diag[g, 2] == max(r + g for r in ranks)   # max over the rank slots
 
 
 def test_unit_owner_rules():
