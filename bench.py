@@ -154,7 +154,18 @@ def cpu_sample(mesh, lam, cfg, n_angles_sample=8, bands=8, band_rows=8):
     return scene, eps, build_s, [(phis[i]) for i in picks]
 
 
-def cpu_run(scene, eps, lam, phis, bands, band_rows):
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def cpu_run(scene, eps, lam, phis, bands, band_rows, threads=0):
     from oracle import oracle as orc
     import paper_2604_09243_b200 as sbr
     mesh_box = sbr.Aabb(scene.aabb_min, scene.aabb_max)
@@ -166,7 +177,7 @@ def cpu_run(scene, eps, lam, phis, bands, band_rows):
         for b in range(bands):
             r0 = (2 * b + 1) * g.n_u // (2 * bands)
             rows = (r0, min(g.n_u, r0 + band_rows))
-            rec = orc.trace_grid(scene, g, MAX_BOUNCES, eps, rows=rows)
+            rec = orc.trace_grid(scene, g, MAX_BOUNCES, eps, rows=rows, threads=threads)
             orc.accumulate(rec, g.k_inc, lam, g.cell_area)
             queries += int((rec.bounces.astype(np.int64) + 1).sum())
             rays += rec.valid.shape[0]
@@ -203,18 +214,9 @@ def run_reference(args):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": config_dict(mesh, args.angles, 1),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": sample},
+                         "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
-
-
-def l2_line(achieved):
-    path = os.path.join(ROOT, "profiles", "l2_peak.json")
-    if not (achieved and os.path.exists(path)):
-        return None
-    peak = json.load(open(path))["l2_gbs"]
-    return {"achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "peak_source": "profiles/l2_peak.json (sbr_probe_l2_bandwidth, measured on B200)"}
 
 
 # ---------------------------------------------------------------------------
@@ -279,6 +281,7 @@ def main():
     total_ms = 0.0
     queries = 0
     local_queries = 0
+    local_valid = 0
     for _ in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
@@ -294,6 +297,7 @@ def main():
         if res is not None:
             queries += int(res.queries.sum())
         local_queries += stats.get("local_queries", int(res.queries.sum()) if res else 0)
+        local_valid += stats.get("local_valid", int(res.valid_rays.sum()) if res else 0)
     launches = ctx.launches - launches0
     clk = clocks.stop()
     kst = ctx.kernel_stats()
@@ -349,20 +353,68 @@ def main():
         return
 
     value = queries / (total_ms / 1e3)
+    # ---- per-kernel rooflines (algorithmic bytes / kernel time) ----------
+    # SURVEY 8d yardstick split by query kind (profiles/algorithmic_bytes_c4.json,
+    # scripts/algorithmic_bytes.py): query 0 of every ray is answered by the
+    # raster pass, which moves no BVH bytes, so only the secondary queries
+    # (bounces + escape probes) are charged to k_trace_persistent
     ab = json.load(open(os.path.join(ROOT, "profiles", "algorithmic_bytes_c4.json")))
-    bpq = ab["bytes_per_query"]
+    b_sec = ab["secondary"]["bytes_per_query"]
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     peak = peaks.get("hbm_gbs", 6650.0)
-    stage_ms = kst["trace_ms"] + kst["raster_ms"]   # query 0 (raster) + bounces (trace)
-    achieved = bpq * local_queries / (stage_ms / 1e3) / 1e9 if stage_ms else None
+    peak_src = ("MEASURED_PEAKS.json hbm_gbs (driver-measured copy bandwidth)" if peaks
+                else "fallback 6650 GB/s (B200_PROFILING.md)")
+    l2pk = json.load(open(os.path.join(ROOT, "profiles", "l2_peak.json")))["l2_gbs"]
+    steps = max(args.steps, 1)
+    rays_step = sum(g.ray_count for i, g in enumerate(grids) if i % world == rank)  # own angles
+    q_step = local_queries / steps
+    sec_step = max(q_step - rays_step, 0.0)          # sum_i N_i: bounces + probes
+    hits_step = local_valid / steps                   # primary hits (every hit is valid)
+    ms = {k: kst[k] / steps for k in ("raster_ms", "compact_ms", "trace_ms", "po_ms")}
+
+    def rl(bytes_, ms_, bound_peak, unit_note):
+        a = bytes_ / (ms_ / 1e3) / 1e9 if ms_ else None
+        return a, (a / bound_peak if a else None)
+
+    tr_a, tr_f = rl(sec_step * b_sec, ms["trace_ms"], peak, "")
     traffic = None
     ncu_path = os.path.join(ROOT, "profiles", "ncu_trace_summary.json")
     if os.path.exists(ncu_path):
-        # DRAM bytes per query of the captured trace stage (raster + trace
-        # kernels) x this step's queries: bytes per step (one launch each)
-        bq = json.load(open(ncu_path)).get("dram_bytes_per_query")
-        traffic = bq * local_queries / args.steps if bq else None
+        nt = json.load(open(ncu_path))
+        # dram read+write bytes of one k_trace_persistent launch (ncu --set
+        # full) per secondary query, scaled to this step's launch
+        bq = nt.get("dram_bytes_per_secondary_query")
+        traffic = bq * sec_step if bq else None
+    ntri = mesh.triangle_count
+    n_ang = len(grids) // max(world, 1)
+    ras_bytes = 48.0 * ntri * n_ang + 16.0 * hits_step
+    ras_a, ras_f = rl(ras_bytes, ms["raster_ms"], peak, "")
+    cmp_bytes = 16.0 * rays_step + 8.0 * hits_step
+    cmp_a, cmp_f = rl(cmp_bytes, ms["compact_ms"], peak, "")
+    po_bytes = (8.0 + 16.0 + 16.0) * hits_step + 8.0 * rays_step / 1024 + 16.0 * rays_step / 1024
+    po_a, po_f = rl(po_bytes, ms["po_ms"], peak, "")
+    rooflines = {
+        "k_trace_persistent": {
+            "bound": "hbm", "achieved": tr_a, "peak": peak, "unit": "GB/s", "frac": tr_f,
+            "l2_frac": tr_a / l2pk if tr_a else None, "l2_peak": l2pk,
+            "ms": ms["trace_ms"], "secondary_queries": sec_step,
+            "bytes_per_query": b_sec,
+            "yardstick": "56 I + 40 T + 64 per secondary query, I/T of the reference SAH tree"},
+        "k_raster": {
+            "bound": "hbm", "achieved": ras_a, "peak": peak, "unit": "GB/s", "frac": ras_f,
+            "ms": ms["raster_ms"],
+            "yardstick": "48 B per triangle per angle + 16 B per hit cell (query 0)"},
+        "k_prim_compact": {
+            "bound": "hbm", "achieved": cmp_a, "peak": peak, "unit": "GB/s", "frac": cmp_f,
+            "ms": ms["compact_ms"],
+            "yardstick": "16 B read per ray slot + 8 B hit-list entry per hit"},
+        "k_po": {
+            "bound": "hbm", "achieved": po_a, "peak": peak, "unit": "GB/s", "frac": po_f,
+            "ms": ms["po_ms"],
+            "yardstick": "per primary hit: 8 B list entry + 16 B record read + 16 B reset; "
+                         "per 1024-ray chunk: 8 B run + 16 B partial (nk=1)"},
+    }
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -371,20 +423,21 @@ def main():
         "angles_per_s": args.angles * args.steps / (total_ms / 1e3),
         "queries_per_step": queries // max(args.steps, 1),
         "gpu_launches": launches,
-        "kernel_ms": {"raster": kst["raster_ms"] / args.steps,
-                      "trace": kst["trace_ms"] / args.steps, "compact_po": kst["po_ms"] / args.steps,
-                      "trace_launches_per_step": kst["trace_launches"] / args.steps},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                     "kernel": "trace stage: k_raster (query 0 of every ray) + k_trace_persistent "
-                               "(launcher + 5-bounce traversal)",
-                     "bytes_per_query": bpq,
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback",
-                     # the node/triangle working set (~100 MB at 1M tris) lives in
-                     # the 126 MB L2: the algorithmic bytes are served by L2/L1
-                     # (DRAM `traffic` is ~4% of them), so the meaningful ceiling
-                     # is the measured L2 read bandwidth
-                     "l2": l2_line(achieved)},
+        "kernel_ms": {"raster": ms["raster_ms"], "compact": ms["compact_ms"],
+                      "trace": ms["trace_ms"], "po": ms["po_ms"],
+                      "trace_launches_per_step": kst["trace_launches"] / steps},
+        "roofline": {"bound": "hbm", "achieved": tr_a, "peak": peak, "unit": "GB/s",
+                     "frac": tr_f, "traffic": traffic,
+                     "kernel": "k_trace_persistent (bounces 1..5 + escape probes; query 0 is "
+                               "the raster pass, see rooflines.k_raster)",
+                     "bytes_per_query": b_sec, "peak_source": peak_src,
+                     # the node/triangle working set (~100 MB at 1M tris) lives in the
+                     # 126 MB L2: the algorithmic bytes are served by L2/L1, so the
+                     # measured L2 read bandwidth is the tighter ceiling
+                     "l2": {"achieved": tr_a, "peak": l2pk, "unit": "GB/s",
+                            "frac": tr_a / l2pk if tr_a else None,
+                            "peak_source": "profiles/l2_peak.json (sbr_probe_l2_bandwidth)"}},
+        "rooflines": rooflines,
         "clocks": clk,
     }
     if e2e:
@@ -392,11 +445,20 @@ def main():
     if world == 1 and not args.no_cpu:
         scene, eps, build_s, phis = cpu_sample(mesh, lam, cfg)
         q, r, t = cpu_run(scene, eps, lam, phis, 16, 64)
+        # the same kernels on one thread (a smaller slice of the same sample)
+        q1, r1, t1 = cpu_run(scene, eps, lam, phis[:2], 4, 16, threads=1)
+        cores = host_cores()
         line["cpu_baseline"] = {
-            "value": q / t, "unit": UNIT, "cores": host_cores(), "kind": "port",
+            "value": q / t, "unit": UNIT, "cores": cores, "kind": "port",
+            "cpu_model": cpu_model(),
+            "value_1_thread": q1 / t1,
+            "parallel_efficiency": (q / t) / (cores * q1 / t1),
             "sample": f"{len(phis)} azimuths x 16 row bands of 64 rows ({r} rays, {q} queries) "
                       f"of the same sweep, reference SAH tree (built in {build_s:.2f} s, not "
-                      "timed), oracle/ C port of the numba kernels, OpenMP all cores"}
+                      f"timed), oracle/ C port of the numba kernels, OpenMP {cores} threads; "
+                      f"1-thread rate on 2 azimuths x 4 bands x 16 rows ({q1} queries). The "
+                      "reference itself (numba) cannot run on the GPU box (no /root/reference "
+                      "there); the port is pinned to it bit for bit (tests/test_oracle_golden.py)"}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

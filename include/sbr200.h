@@ -149,6 +149,10 @@ int sbr_ctx_kernel_stats(sbr_ctx *ctx, double *trace_ms, int64_t *trace_launches
 /* Accumulated time of the primary-visibility raster pass (memset + two
  * sweeps) that precedes each trace launch; trace_ms excludes it. */
 int sbr_ctx_raster_stats(sbr_ctx *ctx, double *raster_ms);
+/* Accumulated per-stage times of the solve pipeline with profiling on:
+ * ms = {raster pass (incl. any slot memset), hit-list compaction, trace
+ * kernel, compaction+PO kernel}. */
+int sbr_ctx_stage_ms(sbr_ctx *ctx, double ms[4]);
 /* Instrumentation: read bandwidth (GB/s) of a `bytes` buffer re-read `reps`
  * times from L2 (16-byte ld.global.cg, 8 CTAs/SM, best of 5). */
 int sbr_probe_l2_bandwidth(sbr_ctx *ctx, int64_t bytes, int32_t reps, double *gbs);

@@ -79,6 +79,7 @@ _SIGS = {
     "sbr_ctx_kernel_stats": (ctypes.c_int, [c_vp, ctypes.POINTER(c_dbl), ctypes.POINTER(c_i64),
                                             ctypes.POINTER(c_dbl), ctypes.POINTER(c_i64)]),
     "sbr_ctx_raster_stats": (ctypes.c_int, [c_vp, ctypes.POINTER(c_dbl)]),
+    "sbr_ctx_stage_ms": (ctypes.c_int, [c_vp, c_vp]),
     "sbr_probe_l2_bandwidth": (ctypes.c_int, [c_vp, c_i64, c_i32, ctypes.POINTER(c_dbl)]),
     "sbr_ctx_debug_counters": (ctypes.c_int, [c_vp, c_vp, c_i32]),
     "sbr_mesh_create": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i32,
@@ -272,8 +273,11 @@ class Context:
                                             ctypes.byref(pm), ctypes.byref(pn)))
         rm = c_dbl()
         check(self.lib.sbr_ctx_raster_stats(self.handle, ctypes.byref(rm)))
+        ms = np.zeros(4)
+        check(self.lib.sbr_ctx_stage_ms(self.handle, ptr(ms)))
         return {"trace_ms": tm.value, "trace_launches": int(tn.value), "po_ms": pm.value,
-                "po_launches": int(pn.value), "raster_ms": rm.value}
+                "po_launches": int(pn.value), "raster_ms": float(ms[0]),
+                "compact_ms": float(ms[1])}
 
     @property
     def traversal(self) -> int:

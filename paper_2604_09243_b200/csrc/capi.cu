@@ -95,6 +95,10 @@ struct sbr_ctx {
     DevBuf<int64_t> seg_slot;    // raster pass: global segment row -> slot offset
     DevBuf<int> bgrids;          // raster pass: grids of the current batch
     DevBuf<uint2> worklist;                 // raster pass: (slot, unit) whose query 0 hit
+    DevBuf<uint2> chunk_hits;               // raster pass: per chunk (list start, count)
+    // slots [0, clean_slots) hold all-ones (the raster pass's "no hit"): list
+    // mode PO restores that after every batch, so only growth needs a memset
+    int64_t clean_slots = 0;
     DevBuf<unsigned long long> nwork;
     DevBuf<int4> big;                       // raster pass: big-triangle chunk queue
     DevBuf<unsigned long long> nbig;
@@ -109,8 +113,8 @@ struct sbr_ctx {
     SahWork sah;                 // SAH build workspace
     // optional per-kernel CUDA-event timing of the solve pipeline
     bool profile = false;
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
-    double trace_ms = 0.0, po_ms = 0.0, raster_ms = 0.0;
+    cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    double trace_ms = 0.0, po_ms = 0.0, raster_ms = 0.0, compact_ms = 0.0;
     int64_t trace_n = 0, po_n = 0;
     LaunchStats stats() { return LaunchStats{&launches, num_sms}; }
     ~sbr_ctx()
@@ -264,6 +268,8 @@ extern "C" int sbr_ctx_trim(sbr_ctx *ctx)
     if (int rc = set_device(ctx)) return rc;
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     ctx->slots.release(); ctx->units.release(); ctx->grids.release();
+    ctx->clean_slots = 0;
+    ctx->chunk_hits.release();
     ctx->chunk_part.release(); ctx->seg_part.release(); ctx->diag.release();
     ctx->seg_base.release(); ctx->seg_slot.release(); ctx->bgrids.release();
     ctx->worklist.release(); ctx->big.release(); ctx->amp.release(); ctx->stage.release();
@@ -1325,14 +1331,19 @@ static int run_units(sbr_ctx *ctx, const sbr_bvh *bvh, const std::vector<UnitDev
             ++u1;
         }
         {   // device memory for the batch; on exhaustion retry with half the slots
+            const void *before = ctx->slots.p;
             cudaError_t e = ctx->slots.reserve(slots);
+            if (ctx->slots.p != before) ctx->clean_slots = 0;   // fresh memory
             if (e == cudaSuccess && raster) e = ctx->worklist.reserve(slots);
+            if (e == cudaSuccess && raster) e = ctx->chunk_hits.reserve(slots / kChunk);
             if (e == cudaSuccess) e = ctx->chunk_part.reserve((size_t)(slots / kChunk) * nk);
             if (e == cudaErrorMemoryAllocation && budget > ((int64_t)1 << 22)) {
                 cudaGetLastError();
                 ctx->slots.release();
                 ctx->worklist.release();
+                ctx->chunk_hits.release();
                 ctx->chunk_part.release();
+                ctx->clean_slots = 0;
                 budget = round_chunk(budget / 2);
                 continue;
             }
@@ -1342,6 +1353,10 @@ static int run_units(sbr_ctx *ctx, const sbr_bvh *bvh, const std::vector<UnitDev
         CUDA_TRY(cudaMemcpyAsync(ctx->units.p, batch.data(), sizeof(UnitDev) * batch.size(),
                                  cudaMemcpyHostToDevice, st));
         if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev[0], st));
+        // the batch's slots are all-ones after a list-mode PO; anything
+        // else (BVH primary, reference order, an error) leaves them dirty
+        const int64_t clean = ctx->clean_slots;
+        ctx->clean_slots = 0;
         if (raster) {
             seg_slot.assign(seg_base[ngrids], kNoSlot);
             bgrids.clear();
@@ -1353,7 +1368,9 @@ static int run_units(sbr_ctx *ctx, const sbr_bvh *bvh, const std::vector<UnitDev
                                      cudaMemcpyHostToDevice, st));
             CUDA_TRY(cudaMemcpyAsync(ctx->bgrids.p, bgrids.data(), 4 * bgrids.size(),
                                      cudaMemcpyHostToDevice, st));
-            CUDA_TRY(cudaMemsetAsync(ctx->slots.p, 0xff, sizeof(SlotRec) * slots, st));
+            if (clean < slots)
+                CUDA_TRY(cudaMemsetAsync(ctx->slots.p + clean, 0xff,
+                                         sizeof(SlotRec) * (slots - clean), st));
             RasterArgs ra = raster_args(bvh, ctx->grids.p, ctx->bgrids.p, (int)bgrids.size(),
                                         ctx->seg_base.p, ctx->seg_slot.p,
                                         reinterpret_cast<PrimHit *>(ctx->slots.p));
@@ -1364,12 +1381,13 @@ static int run_units(sbr_ctx *ctx, const sbr_bvh *bvh, const std::vector<UnitDev
                     ra.sparse = seg_slot[q] == kNoSlot;
             CUDA_TRY(launch_raster(ra, st, ctx->stats()));
         }
+        if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev[4], st));
         if (raster) {
             CUDA_TRY(ctx->worklist.reserve(slots));
             CUDA_TRY(ctx->nwork.reserve(1));
             CUDA_TRY(launch_prim_compact(cfg, ctx->grids.p, ctx->units.p, (int)batch.size(),
-                                         slots, ctx->slots.p, ctx->worklist.p, ctx->nwork.p, st,
-                                         ctx->stats()));
+                                         slots, ctx->slots.p, ctx->worklist.p, ctx->nwork.p,
+                                         ctx->chunk_hits.p, st, ctx->stats()));
         }
         if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev[3], st));
         if (refmode) {
@@ -1384,18 +1402,24 @@ static int run_units(sbr_ctx *ctx, const sbr_bvh *bvh, const std::vector<UnitDev
                                         raster ? ctx->nwork.p : nullptr, st, ctx->stats()));
         }
         if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev[1], st));
-        CUDA_TRY(launch_po(ctx->slots.p, ctx->units.p, (int)batch.size(), slots / kChunk,
-                           ctx->k2.p, nk, ctx->dkturn, ctx->gpow.p, cfg.max_bounces, ctx->chunk_part.p,
+        CUDA_TRY(launch_po(ctx->slots.p, ctx->units.p, (int)batch.size(),
+                           raster ? ctx->worklist.p : nullptr,
+                           raster ? ctx->chunk_hits.p : nullptr, slots / kChunk, ctx->k2.p, nk,
+                           ctx->dkturn, ctx->gpow.p, cfg.max_bounces, ctx->chunk_part.p,
                            diag_dev, ctx->bad.p, st, ctx->stats()));
         if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev[2], st));
         CUDA_TRY(launch_seg_reduce(ctx->chunk_part.p, ctx->units.p, (int)batch.size(), nk,
                                    seg_dev, st, ctx->stats()));
         // the units buffer is rewritten by the next batch: keep batches ordered
         CUDA_TRY(cudaStreamSynchronize(st));
+        if (raster) ctx->clean_slots = std::max(clean, slots);
         if (ctx->profile) {
             float a = 0.f, b = 0.f;
             float c = 0.f;
-            CUDA_TRY(cudaEventElapsedTime(&c, ctx->ev[0], ctx->ev[3]));
+            float cc = 0.f;
+            CUDA_TRY(cudaEventElapsedTime(&c, ctx->ev[0], ctx->ev[4]));
+            CUDA_TRY(cudaEventElapsedTime(&cc, ctx->ev[4], ctx->ev[3]));
+            ctx->compact_ms += cc;
             CUDA_TRY(cudaEventElapsedTime(&a, ctx->ev[3], ctx->ev[1]));
             CUDA_TRY(cudaEventElapsedTime(&b, ctx->ev[1], ctx->ev[2]));
             ctx->raster_ms += c;
@@ -1902,10 +1926,12 @@ extern "C" int sbr_accumulate(sbr_ctx *ctx, const uint8_t *valid, const double *
     CUDA_TRY(cudaMemcpyAsync(ctx->units.p, units.data(), sizeof(UnitDev) * nseg,
                              cudaMemcpyHostToDevice, st));
     if (int rc = upload_freqs(ctx, k, nk, gamma, maxb)) return rc;
+    ctx->clean_slots = 0;   // the records overwrite the raster's all-ones slots
     CUDA_TRY(launch_records_to_slots(dv.p, dn.p, dp.p, db.p, de.p, n, k_inc[0], k_inc[1],
                                      k_inc[2], count_trapped, slots_used, ctx->slots.p, st,
                                      ctx->stats()));
-    CUDA_TRY(launch_po(ctx->slots.p, ctx->units.p, (int)nseg, slots_used / kChunk, ctx->k2.p, nk,
+    CUDA_TRY(launch_po(ctx->slots.p, ctx->units.p, (int)nseg, nullptr, nullptr,
+                       slots_used / kChunk, ctx->k2.p, nk,
                        ctx->dkturn, ctx->gpow.p, maxb, ctx->chunk_part.p, ctx->diag.p, ctx->bad.p, st,
                        ctx->stats()));
     CUDA_TRY(launch_seg_reduce(ctx->chunk_part.p, ctx->units.p, (int)nseg, nk, ctx->seg_part.p, st,
@@ -1993,7 +2019,7 @@ extern "C" int sbr_ctx_profile(sbr_ctx *ctx, int32_t enable)
     if (enable && !ctx->ev[0])
         for (auto &e : ctx->ev) CUDA_TRY(cudaEventCreate(&e));
     ctx->profile = enable != 0;
-    ctx->trace_ms = ctx->po_ms = ctx->raster_ms = 0.0;
+    ctx->trace_ms = ctx->po_ms = ctx->raster_ms = ctx->compact_ms = 0.0;
     ctx->trace_n = ctx->po_n = 0;
     return SBR_OK;
 }
@@ -2025,6 +2051,16 @@ extern "C" int sbr_ctx_raster_stats(sbr_ctx *ctx, double *raster_ms)
 {
     REQUIRE(ctx && raster_ms, "NULL argument");
     *raster_ms = ctx->raster_ms;
+    return SBR_OK;
+}
+
+extern "C" int sbr_ctx_stage_ms(sbr_ctx *ctx, double ms[4])
+{
+    REQUIRE(ctx && ms, "NULL argument");
+    ms[0] = ctx->raster_ms;
+    ms[1] = ctx->compact_ms;
+    ms[2] = ctx->trace_ms;
+    ms[3] = ctx->po_ms;
     return SBR_OK;
 }
 

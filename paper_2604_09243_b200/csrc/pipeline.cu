@@ -105,7 +105,8 @@ constexpr int kMaxHist = 64;                      // bounce histogram bins in sm
 // ROT: equally spaced wavenumbers, phases by rotation recurrence (FPT > 1)
 template <int FPT, bool ROT>
 __global__ void __launch_bounds__(kPoThreads)
-k_po(const SlotRec *__restrict__ slots, const UnitDev *__restrict__ units, int n_units,
+k_po(SlotRec *__restrict__ slots, const UnitDev *__restrict__ units, int n_units,
+     const uint2 *__restrict__ list, const uint2 *__restrict__ chunk_hits,
      const double *__restrict__ kturn, int nk, double dkturn, const double *__restrict__ gpow,
      int max_bounces,
      double2 *__restrict__ chunk_part, int64_t *__restrict__ diag,
@@ -133,6 +134,13 @@ k_po(const SlotRec *__restrict__ slots, const UnitDev *__restrict__ units, int n
     if (tid == 0) { s_valid = 0u; s_queries = 0u; s_maxb = 0u; }
 
     // ---- load + ballot ----
+    // list mode (raster pass): only the chunk's primary hits are read, in
+    // slot order, from its run of the hit list, and each read slot is reset
+    // to all-ones so the buffer is ready for the next raster pass without a
+    // memset; the chunk's other real slots are primary misses (one query,
+    // invalid, nothing to integrate) and are never touched
+    uint2 run = make_uint2(0u, 0u);
+    if (list) run = __ldg(&chunk_hits[chunk]);
     SlotRec rec[kPerThread];
     unsigned selmask = 0;
     unsigned long long my_q = 0;
@@ -140,11 +148,28 @@ k_po(const SlotRec *__restrict__ slots, const UnitDev *__restrict__ units, int n
     int my_valid = 0;
 #pragma unroll
     for (int q = 0; q < kPerThread; ++q) {
-        SlotRec r = slots[slot0 + q * kPoThreads + tid];
-        if (r.meta == kMissMeta) {   // primary miss left by k_prim_compact
-            r.R = 0.0;
-            r.cosv = 0.f;
-            r.meta = kMetaActive | kMetaEscaped;
+        const int e = q * kPoThreads + tid;
+        SlotRec r;
+        if (list) {
+            if (e < (int)run.y) {
+                const int64_t slot = (int64_t)__ldg(&list[run.x + e]).x;
+                r = slots[slot];
+                SlotRec ones;
+                ones.R = __longlong_as_double(-1LL);
+                ones.cosv = __int_as_float(-1);
+                ones.meta = kMissMeta;
+                __stcs(reinterpret_cast<float4 *>(slots + slot),
+                       *reinterpret_cast<const float4 *>(&ones));
+            } else {
+                r.R = 0.0; r.cosv = 0.f; r.meta = 0u;
+            }
+        } else {
+            r = slots[slot0 + e];
+            if (r.meta == kMissMeta) {   // primary miss left by k_prim_compact
+                r.R = 0.0;
+                r.cosv = 0.f;
+                r.meta = kMetaActive | kMetaEscaped;
+            }
         }
         rec[q] = r;
         const bool sel = (r.meta & kMetaSel) != 0;
@@ -189,7 +214,9 @@ k_po(const SlotRec *__restrict__ slots, const UnitDev *__restrict__ units, int n
             const double w = 2.0 * (double)r.cosv * gpow[b];
             srec[pos] = make_double2(r.R, w);
             if (!isfinite(r.R) || !isfinite(w)) {
-                const int64_t ridx = U.ray_begin + (slot0 - U.slot_base) + q * kPoThreads + tid;
+                const int64_t sl = list ? (int64_t)__ldg(&list[run.x + q * kPoThreads + tid]).x
+                                        : slot0 + q * kPoThreads + tid;
+                const int64_t ridx = U.ray_begin + (sl - U.slot_base);
                 atomicMin(bad, (unsigned long long)ridx);
             }
         }
@@ -216,6 +243,12 @@ k_po(const SlotRec *__restrict__ slots, const UnitDev *__restrict__ units, int n
         atomicAdd(&s_queries, (unsigned)my_q);
         atomicAdd(&s_valid, (unsigned)my_valid);
         atomicMax(&s_maxb, my_maxb);
+    }
+    if (list && tid == 0) {   // the chunk's primary misses: one query each
+        const int64_t first_r = U.ray_begin + (slot0 - U.slot_base);
+        int64_t real = U.ray_end - first_r;
+        real = real < 0 ? 0 : (real > kChunk ? kChunk : real);
+        atomicAdd(&s_queries, (unsigned)(real - (int64_t)run.y));
     }
     __syncthreads();
     if (diag) {
@@ -345,8 +378,8 @@ constexpr int kCompactTile = kCompactThreads * kCompactPer;   // == kChunk
 __global__ void __launch_bounds__(kCompactThreads)
 k_prim_compact(TraceCfg cfg, const GridDev *__restrict__ grids,
                const UnitDev *__restrict__ units, int n_units, int64_t n_slots,
-               SlotRec *__restrict__ slots, uint2 *__restrict__ list,
-               unsigned long long *__restrict__ nlist)
+               const SlotRec *__restrict__ slots, uint2 *__restrict__ list,
+               unsigned long long *__restrict__ nlist, uint2 *__restrict__ chunk_hits)
 {
     constexpr int W = kCompactThreads / 32;
     __shared__ int cnt[kCompactPer][W];
@@ -369,18 +402,13 @@ k_prim_compact(TraceCfg cfg, const GridDev *__restrict__ grids,
             if (slot < n_slots) {
                 const int64_t r = U.ray_begin + (slot - U.slot_base);
                 const bool real = r < U.ray_end && alias_ok;
-                const PrimHit h = reinterpret_cast<const PrimHit *>(slots)[slot];
-                hit = real && h.tbits != kNoHitBits;
-                // a real miss keeps the all-ones PrimHit: k_po reads it as the
-                // finished miss record (kMissMeta); only padding / refused
-                // slots are rewritten
-                if (!real) {
-                    SlotRec z;
-                    z.R = 0.0;
-                    z.cosv = 0.f;
-                    z.meta = 0u;
-                    slots[slot] = z;
-                }
+                // streaming read: every slot is read once here and the
+                // misses (most of them) never again
+                const ulonglong2 h =
+                    __ldcs(reinterpret_cast<const ulonglong2 *>(slots) + slot);
+                hit = real && h.x != kNoHitBits;
+                // misses and padding keep their all-ones bits: k_po derives
+                // them from the unit (list mode), nothing is rewritten
             }
             const unsigned bal = __ballot_sync(0xffffffffu, hit);
             if (lane == 0) cnt[q][warp] = __popc(bal);
@@ -395,6 +423,8 @@ k_prim_compact(TraceCfg cfg, const GridDev *__restrict__ grids,
                     run += cnt[q][w];
                 }
             s_at = run ? atomicAdd(nlist, (unsigned long long)run) : 0ULL;
+            // this chunk's hits: list[at, at + run), in slot order
+            chunk_hits[tile / kCompactTile] = make_uint2((unsigned int)s_at, (unsigned int)run);
         }
         __syncthreads();
         const unsigned long long at = s_at;
@@ -413,8 +443,8 @@ k_prim_compact(TraceCfg cfg, const GridDev *__restrict__ grids,
 cudaError_t launch_prim_compact(const TraceCfg &cfg, const GridDev *d_grids,
                                 const UnitDev *d_units, int n_units, int64_t n_slots,
                                 SlotRec *d_slots, uint2 *d_worklist,
-                                unsigned long long *d_nwork, cudaStream_t st,
-                                const LaunchStats &ls)
+                                unsigned long long *d_nwork, uint2 *d_chunk_hits,
+                                cudaStream_t st, const LaunchStats &ls)
 {
     cudaError_t e = cudaMemsetAsync(d_nwork, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
@@ -424,7 +454,7 @@ cudaError_t launch_prim_compact(const TraceCfg &cfg, const GridDev *d_grids,
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     k_prim_compact<<<(unsigned)blocks, kCompactThreads, 0, st>>>(
-        cfg, d_grids, d_units, n_units, n_slots, d_slots, d_worklist, d_nwork);
+        cfg, d_grids, d_units, n_units, n_slots, d_slots, d_worklist, d_nwork, d_chunk_hits);
     ++*ls.launches;
     return cudaGetLastError();
 }
@@ -685,7 +715,8 @@ cudaError_t launch_records_to_slots(const uint8_t *valid, const double *n0,
     return cudaGetLastError();
 }
 
-cudaError_t launch_po(const SlotRec *d_slots, const UnitDev *d_units, int n_units,
+cudaError_t launch_po(SlotRec *d_slots, const UnitDev *d_units, int n_units,
+                      const uint2 *d_list, const uint2 *d_chunk_hits,
                       int64_t n_chunks, const double *d_k2, int nk, double dkturn,
                       const double *d_gpow,
                       int max_bounces, double2 *d_chunk_part, int64_t *d_diag,
@@ -698,8 +729,9 @@ cudaError_t launch_po(const SlotRec *d_slots, const UnitDev *d_units, int n_unit
     static const bool force64 = getenv("SBR_PO_FP64") && atoi(getenv("SBR_PO_FP64")) != 0;
     const bool rot = nk > 1 && dkturn != 0.0 && !force64;
 #define SBR_PO(F, R)                                                                       \
-    k_po<F, R><<<grid, kPoThreads, 0, st>>>(d_slots, d_units, n_units, d_k2, nk, dkturn,    \
-                                            d_gpow, max_bounces, d_chunk_part, d_diag, d_bad)
+    k_po<F, R><<<grid, kPoThreads, 0, st>>>(d_slots, d_units, n_units, d_list, d_chunk_hits, \
+                                            d_k2, nk, dkturn, d_gpow, max_bounces,          \
+                                            d_chunk_part, d_diag, d_bad)
     if (nk >= 8) { if (rot) SBR_PO(8, true); else SBR_PO(8, false); }
     else if (nk >= 4) { if (rot) SBR_PO(4, true); else SBR_PO(4, false); }
     else if (nk >= 2) { if (rot) SBR_PO(2, true); else SBR_PO(2, false); }

@@ -116,11 +116,13 @@ cudaError_t launch_trace_solve(const TraceCfg &cfg, const GridDev *d_grids,
 
 // After the raster pass: final records for padding / aliasing-rejected /
 // missed slots, and the list of slots whose query 0 hit (warp-ordered).
+// d_chunk_hits[c] = (first list entry, count) of chunk c's hits (list mode of
+// launch_po); misses and padding slots are left untouched (all-ones)
 cudaError_t launch_prim_compact(const TraceCfg &cfg, const GridDev *d_grids,
                                 const UnitDev *d_units, int n_units, int64_t n_slots,
                                 SlotRec *d_slots, uint2 *d_worklist,
-                                unsigned long long *d_nwork, cudaStream_t st,
-                                const LaunchStats &ls);
+                                unsigned long long *d_nwork, uint2 *d_chunk_hits,
+                                cudaStream_t st, const LaunchStats &ls);
 
 struct FullOut {
     uint8_t *valid;
@@ -247,7 +249,10 @@ cudaError_t launch_records_to_slots(const uint8_t *valid, const double *n0,
                                     const LaunchStats &ls);
 
 // dkturn != 0: the nk wavenumbers are equally spaced, (k[f+1]-k[f]) / pi
-cudaError_t launch_po(const SlotRec *d_slots, const UnitDev *d_units, int n_units,
+// d_list != null (raster pass): list mode -- each chunk reads only its hits
+// (d_chunk_hits) and resets them to all-ones; otherwise every slot is read
+cudaError_t launch_po(SlotRec *d_slots, const UnitDev *d_units, int n_units,
+                      const uint2 *d_list, const uint2 *d_chunk_hits,
                       int64_t n_chunks, const double *d_k2, int nk, double dkturn,
                       const double *d_gpow,
                       int max_bounces, double2 *d_chunk_part, int64_t *d_diag,

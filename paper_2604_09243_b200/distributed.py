@@ -198,8 +198,9 @@ def solve_grids_distributed(tree, mesh, grids: Sequence, trace_params, wavenumbe
         timer("traced")
     if stats is not None:
         nseg = int(segment_layout(grids)[-1]) * ks.size * 2
-        q = buf[nseg:nseg + ng * diag_stride(B)].view(ng, diag_stride(B))[:, 1]
-        stats["local_queries"] = int(q.sum().item())
+        dg_ = buf[nseg:nseg + ng * diag_stride(B)].view(ng, diag_stride(B))
+        stats["local_queries"] = int(dg_[:, 1].sum().item())
+        stats["local_valid"] = int(dg_[:, 0].sum().item())
     reduce_packed(buf, root, group)     # the one collective
     if rank != root:
         return None

@@ -577,3 +577,42 @@ def test_po_field_precision_at_near_nulls(orc):
         a_ref = orc.accumulate(ref, g.k_inc, lam, g.cell_area)
         worst = max(worst, abs(complex(a) - a_ref) / abs(a_ref))
     assert worst < 1e-5, worst
+
+
+def test_slot_reuse_without_memset_is_exact(monkeypatch):
+    """List-mode PO restores the raster's all-ones slots, so repeated solves
+    skip the memset; interleaving paths that dirty the slots (host-record
+    accumulate, BVH primary, reference order, smaller batches) must not
+    change a bit of the next raster solve."""
+    mesh = meshgen.generate_aircraft(density=0.03)
+    tree = sbr.build(mesh)
+    lam = 0.1
+    grids = [sbr.build_aperture(mesh.aabb, sbr.IncidentDirection(math.pi / 2, ph), lam / 5,
+                                wavelength=lam) for ph in (0.0, 1.0, 2.5)]
+    tp = sbr.TraceParams(max_bounces=5)
+    ks = [2 * math.pi / lam]
+    monkeypatch.setenv("SBR_PRIMARY", "raster")
+    first = sbr.solve_grids(tree, mesh, grids, tp, ks)
+
+    def again(tag):
+        r = sbr.solve_grids(tree, mesh, grids, tp, ks)
+        assert np.array_equal(r.amplitude, first.amplitude), tag
+        assert np.array_equal(r.queries, first.queries), tag
+        assert np.array_equal(r.bounce_counts, first.bounce_counts), tag
+
+    again("repeat")
+    rec = sbr.trace_grid(tree, mesh, grids[1], tp)
+    sbr.accumulate_multi(rec, grids[1].k_inc, np.array(ks), grids[1].cell_area)
+    again("after accumulate")
+    monkeypatch.setenv("SBR_PRIMARY", "bvh")
+    b = sbr.solve_grids(tree, mesh, grids, tp, ks)
+    assert np.array_equal(b.amplitude, first.amplitude)
+    monkeypatch.setenv("SBR_PRIMARY", "raster")
+    again("after bvh primary")
+    with sbr.traversal_order("reference"):
+        sbr.solve_grids(tree, mesh, grids, tp, ks)
+    again("after reference order")
+    monkeypatch.setenv("SBR_SLOT_BUDGET", "4096")
+    again("small batches")
+    monkeypatch.delenv("SBR_SLOT_BUDGET")
+    again("back to one batch")
