@@ -149,6 +149,10 @@ int sbr_ctx_kernel_stats(sbr_ctx *ctx, double *trace_ms, int64_t *trace_launches
 /* Accumulated time of the primary-visibility raster pass (memset + two
  * sweeps) that precedes each trace launch; trace_ms excludes it. */
 int sbr_ctx_raster_stats(sbr_ctx *ctx, double *raster_ms);
+/* Read and clear the raster pass's counters, accumulated since the last
+ * call: {candidate cells tested, ill-conditioned (WIDE) (grid, triangle)
+ * pairs, chunk-queue overflows}. */
+int sbr_ctx_raster_counters(sbr_ctx *ctx, int64_t out[3]);
 /* Accumulated per-stage times of the solve pipeline with profiling on:
  * ms = {raster pass (incl. any slot memset), hit-list compaction, trace
  * kernel, compaction+PO kernel}. */

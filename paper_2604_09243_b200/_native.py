@@ -80,6 +80,7 @@ _SIGS = {
                                             ctypes.POINTER(c_dbl), ctypes.POINTER(c_i64)]),
     "sbr_ctx_raster_stats": (ctypes.c_int, [c_vp, ctypes.POINTER(c_dbl)]),
     "sbr_ctx_stage_ms": (ctypes.c_int, [c_vp, c_vp]),
+    "sbr_ctx_raster_counters": (ctypes.c_int, [c_vp, c_vp]),
     "sbr_probe_l2_bandwidth": (ctypes.c_int, [c_vp, c_i64, c_i32, ctypes.POINTER(c_dbl)]),
     "sbr_ctx_debug_counters": (ctypes.c_int, [c_vp, c_vp, c_i32]),
     "sbr_mesh_create": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i32,
@@ -278,6 +279,14 @@ class Context:
         return {"trace_ms": tm.value, "trace_launches": int(tn.value), "po_ms": pm.value,
                 "po_launches": int(pn.value), "raster_ms": float(ms[0]),
                 "compact_ms": float(ms[1])}
+
+    def raster_counters(self) -> dict:
+        """Read and clear {candidates, wide_pairs, queue_overflows} of the
+        raster pass (accumulated since the last read)."""
+        out = np.zeros(3, np.int64)
+        check(self.lib.sbr_ctx_raster_counters(self.handle, ptr(out)))
+        return {"candidates": int(out[0]), "wide_pairs": int(out[1]),
+                "queue_overflows": int(out[2])}
 
     @property
     def traversal(self) -> int:

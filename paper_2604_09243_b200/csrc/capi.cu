@@ -222,7 +222,10 @@ extern "C" int sbr_ctx_create(int device, sbr_ctx **out)
             if (!g_alloc_stream[device]) g_alloc_stream[device] = ctx->stream;
         }
     }
-    if (e == cudaSuccess) e = ctx->counter.alloc(32);  // [0] trace, [1] raster, [8..] stats builds
+    // [0] trace, [1] raster work, [2..4] raster counters, [8..] stats builds
+    if (e == cudaSuccess) e = ctx->counter.alloc(32);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ctx->counter.p, 0, 32 * sizeof(unsigned long long),
+                                              ctx->stream);
     if (e == cudaSuccess) e = ctx->err_flag.alloc(1);
     if (e == cudaSuccess) e = ctx->bad.alloc(1);
     if (e != cudaSuccess) {
@@ -995,6 +998,7 @@ static RasterArgs raster_args(const sbr_bvh *bvh, const GridDev *grids, const in
     r.big_cap = 0;
     r.row_lo = 0;
     r.row_hi = INT64_MAX;
+    r.stats = nullptr;
     return r;
 }
 
@@ -1156,6 +1160,7 @@ static int trace_full_common(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *
             CUDA_TRY(cudaMemsetAsync(prim.p, 0xff, sizeof(PrimHit) * n, st));
             RasterArgs ra = raster_args(bvh, dg.p, dbg.p, 1, dsb.p, dss.p, prim.p);
             ra.counter = ctx->counter.p + 1;
+            ra.stats = ctx->counter.p + 2;
             ra.row_lo = i_begin;
             ra.row_hi = i_end;
             CUDA_TRY(attach_big_queue(ctx, ra));
@@ -1375,6 +1380,7 @@ static int run_units(sbr_ctx *ctx, const sbr_bvh *bvh, const std::vector<UnitDev
                                         ctx->seg_base.p, ctx->seg_slot.p,
                                         reinterpret_cast<PrimHit *>(ctx->slots.p));
             ra.counter = ctx->counter.p + 1;
+            ra.stats = ctx->counter.p + 2;
             CUDA_TRY(attach_big_queue(ctx, ra));
             for (int g : bgrids)       // a grid of the batch with a segment outside it
                 for (int64_t q = seg_base[g]; q < seg_base[g + 1] && !ra.sparse; ++q)
@@ -2051,6 +2057,18 @@ extern "C" int sbr_ctx_raster_stats(sbr_ctx *ctx, double *raster_ms)
 {
     REQUIRE(ctx && raster_ms, "NULL argument");
     *raster_ms = ctx->raster_ms;
+    return SBR_OK;
+}
+
+extern "C" int sbr_ctx_raster_counters(sbr_ctx *ctx, int64_t out[3])
+{
+    REQUIRE(ctx && out, "NULL argument");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (int rc = set_device(ctx)) return rc;
+    CUDA_TRY(cudaMemcpyAsync(out, ctx->counter.p + 2, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    CUDA_TRY(cudaMemsetAsync(ctx->counter.p + 2, 0, 3 * sizeof(int64_t), ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     return SBR_OK;
 }
 

@@ -236,6 +236,9 @@ struct RasterArgs {
     unsigned long long *nbig;      // its fill counter
     int64_t big_cap;               // its capacity (items beyond it stay in k_raster)
     int64_t row_lo, row_hi;        // rows [row_lo, row_hi) only (a partial trace_grid)
+    // accumulating counters (may be null): [0] candidate cells tested,
+    // [1] WIDE (ill-conditioned) pairs, [2] chunk-queue overflows
+    unsigned long long *stats;
 };
 constexpr int64_t kNoSlot = INT64_MIN;   // segment not in this batch / shard
 cudaError_t launch_raster(const RasterArgs &a, cudaStream_t st, const LaunchStats &ls);

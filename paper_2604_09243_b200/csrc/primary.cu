@@ -152,8 +152,8 @@ __device__ __forceinline__ RasterSetup raster_setup(const TriF64 &T, const GridD
     if (fabs(det2) > 1e-6 * kd) {
         const double cf[3] = {-S.eu, -S.eu, S.h + S.ev};
         const double cg[3] = {-S.ev, S.h + S.eu, -S.ev};
-        alo = bhi = -INFINITY;
-        ahi = blo = INFINITY;
+        alo = blo = INFINITY;      // running minima
+        ahi = bhi = -INFINITY;     // running maxima
         double emax = 0.0;
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
@@ -368,6 +368,7 @@ k_raster(RasterArgs a, int64_t ntri_pad)
             RasterSetup S = raster_setup(load_tri<STORAGE>(a.B, (int)tri), G, a.row_lo, a.row_hi);
             if (a.sparse) trim_owned(S, G, a.seg_slot + __ldg(&a.seg_base[g]));
             count = S.count;
+            if (S.wide && count && a.stats) atomicAdd(a.stats + 1, 1ULL);
             if (count > kBigTri && a.big) {
                 const long long nch = (count + kBigChunk - 1) / kBigChunk;
                 // sharded / partial batches: queue only chunks whose rows touch
@@ -398,6 +399,7 @@ k_raster(RasterArgs a, int64_t ntri_pad)
                     // work in its in-range part (k_raster_big walks every
                     // entry below min(nbig, cap)) and walk the triangle here
                     for (unsigned long long w = at; w < cap; ++w) a.big[w] = make_int4(-1, 0, 0, 0);
+                    if (a.stats) atomicAdd(a.stats + 2, 1ULL);
                 }
             }
             if (count) {
@@ -418,6 +420,7 @@ k_raster(RasterArgs a, int64_t ntri_pad)
         }
         const long long total = __shfl_sync(0xffffffffu, incl, 31);
         if (total == 0) continue;
+        if (lane == 0 && a.stats) atomicAdd(a.stats, (unsigned long long)total);
         if (count) R.excl = incl - count;
         const int64_t *seg = a.seg_slot + __ldg(&a.seg_base[g]);
         // walk the flattened list in windows of 2^30 so the prefix search
@@ -505,6 +508,7 @@ k_raster_big(RasterArgs a)
                 if (lane >= o) incl += y;
             }
             const int total = __shfl_sync(0xffffffffu, incl, 31);
+            if (lane == 0 && a.stats && total) atomicAdd(a.stats, (unsigned long long)total);
             const int excl = incl - cnt;
             const int ml32 = (int)ml;
             for (int base = 0; base < total; base += 32) {
