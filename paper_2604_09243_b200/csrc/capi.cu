@@ -94,7 +94,9 @@ struct sbr_ctx {
     DevBuf<int64_t> seg_base;
     DevBuf<int64_t> seg_slot;    // raster pass: global segment row -> slot offset
     DevBuf<int> bgrids;          // raster pass: grids of the current batch
-    DevBuf<uint2> worklist;                 // raster pass: (slot, unit) whose query 0 hit
+    // raster pass: (slot, unit) of every slot whose query 0 hit; the trace
+    // kernel overwrites entry w with that ray's SlotRec (k_po reads them)
+    DevBuf<uint4> worklist;
     DevBuf<uint2> chunk_hits;               // raster pass: per chunk (list start, count)
     // slots [0, clean_slots) hold all-ones (the raster pass's "no hit"): list
     // mode PO restores that after every batch, so only growth needs a memset
@@ -1418,6 +1420,7 @@ static int run_units(sbr_ctx *ctx, const sbr_bvh *bvh, const std::vector<UnitDev
                                    seg_dev, st, ctx->stats()));
         // the units buffer is rewritten by the next batch: keep batches ordered
         CUDA_TRY(cudaStreamSynchronize(st));
+        // the trace kernel reset every hit slot it consumed: all-ones again
         if (raster) ctx->clean_slots = std::max(clean, slots);
         if (ctx->profile) {
             float a = 0.f, b = 0.f;

@@ -106,7 +106,7 @@ constexpr int kMaxHist = 64;                      // bounce histogram bins in sm
 template <int FPT, bool ROT>
 __global__ void __launch_bounds__(kPoThreads)
 k_po(SlotRec *__restrict__ slots, const UnitDev *__restrict__ units, int n_units,
-     const uint2 *__restrict__ list, const uint2 *__restrict__ chunk_hits,
+     const uint4 *__restrict__ list, const uint2 *__restrict__ chunk_hits,
      const double *__restrict__ kturn, int nk, double dkturn, const double *__restrict__ gpow,
      int max_bounces,
      double2 *__restrict__ chunk_part, int64_t *__restrict__ diag,
@@ -134,11 +134,10 @@ k_po(SlotRec *__restrict__ slots, const UnitDev *__restrict__ units, int n_units
     if (tid == 0) { s_valid = 0u; s_queries = 0u; s_maxb = 0u; }
 
     // ---- load + ballot ----
-    // list mode (raster pass): only the chunk's primary hits are read, in
-    // slot order, from its run of the hit list, and each read slot is reset
-    // to all-ones so the buffer is ready for the next raster pass without a
-    // memset; the chunk's other real slots are primary misses (one query,
-    // invalid, nothing to integrate) and are never touched
+    // list mode (raster pass): only the chunk's primary hits are read -- the
+    // records the trace kernel wrote over the chunk's run of the hit list,
+    // in slot order, contiguous; the chunk's other real slots are primary
+    // misses (one query, invalid, nothing to integrate), never touched
     uint2 run = make_uint2(0u, 0u);
     if (list) run = __ldg(&chunk_hits[chunk]);
     SlotRec rec[kPerThread];
@@ -152,14 +151,7 @@ k_po(SlotRec *__restrict__ slots, const UnitDev *__restrict__ units, int n_units
         SlotRec r;
         if (list) {
             if (e < (int)run.y) {
-                const int64_t slot = (int64_t)__ldg(&list[run.x + e]).x;
-                r = slots[slot];
-                SlotRec ones;
-                ones.R = __longlong_as_double(-1LL);
-                ones.cosv = __int_as_float(-1);
-                ones.meta = kMissMeta;
-                __stcs(reinterpret_cast<float4 *>(slots + slot),
-                       *reinterpret_cast<const float4 *>(&ones));
+                r = reinterpret_cast<const SlotRec *>(list)[run.x + e];
             } else {
                 r.R = 0.0; r.cosv = 0.f; r.meta = 0u;
             }
@@ -214,7 +206,7 @@ k_po(SlotRec *__restrict__ slots, const UnitDev *__restrict__ units, int n_units
             const double w = 2.0 * (double)r.cosv * gpow[b];
             srec[pos] = make_double2(r.R, w);
             if (!isfinite(r.R) || !isfinite(w)) {
-                const int64_t sl = list ? (int64_t)__ldg(&list[run.x + q * kPoThreads + tid]).x
+                const int64_t sl = list ? slot0 + ((r.meta >> kMetaOffShift) & (kChunk - 1))
                                         : slot0 + q * kPoThreads + tid;
                 const int64_t ridx = U.ray_begin + (sl - U.slot_base);
                 atomicMin(bad, (unsigned long long)ridx);
@@ -378,7 +370,7 @@ constexpr int kCompactTile = kCompactThreads * kCompactPer;   // == kChunk
 __global__ void __launch_bounds__(kCompactThreads)
 k_prim_compact(TraceCfg cfg, const GridDev *__restrict__ grids,
                const UnitDev *__restrict__ units, int n_units, int64_t n_slots,
-               const SlotRec *__restrict__ slots, uint2 *__restrict__ list,
+               const SlotRec *__restrict__ slots, uint4 *__restrict__ list,
                unsigned long long *__restrict__ nlist, uint2 *__restrict__ chunk_hits)
 {
     constexpr int W = kCompactThreads / 32;
@@ -434,7 +426,8 @@ k_prim_compact(TraceCfg cfg, const GridDev *__restrict__ grids,
             const unsigned bal = __ballot_sync(0xffffffffu, hit);
             if (hit)
                 list[at + pos[q][warp] + __popc(bal & ((1u << lane) - 1u))] =
-                    make_uint2((unsigned int)(tile + q * kCompactThreads + tid), (unsigned int)ui);
+                    make_uint4((unsigned int)(tile + q * kCompactThreads + tid), (unsigned int)ui,
+                               0u, 0u);
         }
         __syncthreads();
     }
@@ -442,7 +435,7 @@ k_prim_compact(TraceCfg cfg, const GridDev *__restrict__ grids,
 
 cudaError_t launch_prim_compact(const TraceCfg &cfg, const GridDev *d_grids,
                                 const UnitDev *d_units, int n_units, int64_t n_slots,
-                                SlotRec *d_slots, uint2 *d_worklist,
+                                SlotRec *d_slots, uint4 *d_worklist,
                                 unsigned long long *d_nwork, uint2 *d_chunk_hits,
                                 cudaStream_t st, const LaunchStats &ls)
 {
@@ -634,7 +627,7 @@ static void trace_storage_dispatch(const TraceArgs &a, cudaStream_t st, int num_
 cudaError_t launch_trace_solve(const TraceCfg &cfg, const GridDev *d_grids,
                                const UnitDev *d_units, int n_units, int64_t n_slots,
                                SlotRec *d_slots, unsigned long long *d_counter,
-                               bool prim_from_slots, const uint2 *d_worklist,
+                               bool prim_from_slots, uint4 *d_worklist,
                                const unsigned long long *d_nwork, cudaStream_t st,
                                const LaunchStats &ls)
 {
@@ -716,7 +709,7 @@ cudaError_t launch_records_to_slots(const uint8_t *valid, const double *n0,
 }
 
 cudaError_t launch_po(SlotRec *d_slots, const UnitDev *d_units, int n_units,
-                      const uint2 *d_list, const uint2 *d_chunk_hits,
+                      const uint4 *d_list, const uint2 *d_chunk_hits,
                       int64_t n_chunks, const double *d_k2, int nk, double dkturn,
                       const double *d_gpow,
                       int max_bounces, double2 *d_chunk_part, int64_t *d_diag,

@@ -41,6 +41,10 @@ constexpr uint32_t kMetaEscaped = 1u << 17;
 constexpr uint32_t kMetaSel = 1u << 18;
 constexpr uint32_t kMetaActive = 1u << 19;
 constexpr uint32_t kMetaBounceMask = 0xffffu;
+// list-mode records (written over work-list entries) carry the ray's offset
+// within its 1024-slot chunk in bits 20..29 (r mod 1024: units are chunk-
+// and segment-aligned), for the NumericalError record index
+constexpr int kMetaOffShift = 20;
 // meta of an all-ones slot (a PrimHit that no triangle reached): a finished
 // primary miss -- no real record has bits 20..31 set
 constexpr uint32_t kMissMeta = 0xffffffffu;
@@ -110,7 +114,7 @@ struct LaunchStats {
 cudaError_t launch_trace_solve(const TraceCfg &cfg, const GridDev *d_grids,
                                const UnitDev *d_units, int n_units, int64_t n_slots,
                                SlotRec *d_slots, unsigned long long *d_counter,
-                               bool prim_from_slots, const uint2 *d_worklist,
+                               bool prim_from_slots, uint4 *d_worklist,
                                const unsigned long long *d_nwork, cudaStream_t st,
                                const LaunchStats &ls);
 
@@ -120,7 +124,7 @@ cudaError_t launch_trace_solve(const TraceCfg &cfg, const GridDev *d_grids,
 // launch_po); misses and padding slots are left untouched (all-ones)
 cudaError_t launch_prim_compact(const TraceCfg &cfg, const GridDev *d_grids,
                                 const UnitDev *d_units, int n_units, int64_t n_slots,
-                                SlotRec *d_slots, uint2 *d_worklist,
+                                SlotRec *d_slots, uint4 *d_worklist,
                                 unsigned long long *d_nwork, uint2 *d_chunk_hits,
                                 cudaStream_t st, const LaunchStats &ls);
 
@@ -252,10 +256,11 @@ cudaError_t launch_records_to_slots(const uint8_t *valid, const double *n0,
                                     const LaunchStats &ls);
 
 // dkturn != 0: the nk wavenumbers are equally spaced, (k[f+1]-k[f]) / pi
-// d_list != null (raster pass): list mode -- each chunk reads only its hits
-// (d_chunk_hits) and resets them to all-ones; otherwise every slot is read
+// d_list != null (raster pass): list mode -- each chunk reads only its hits'
+// records, which the trace kernel wrote over their work-list entries
+// (d_chunk_hits: the chunk's run of the list); otherwise every slot is read
 cudaError_t launch_po(SlotRec *d_slots, const UnitDev *d_units, int n_units,
-                      const uint2 *d_list, const uint2 *d_chunk_hits,
+                      const uint4 *d_list, const uint2 *d_chunk_hits,
                       int64_t n_chunks, const double *d_k2, int nk, double dkturn,
                       const double *d_gpow,
                       int max_bounces, double2 *d_chunk_part, int64_t *d_diag,

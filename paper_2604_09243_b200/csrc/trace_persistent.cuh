@@ -65,7 +65,8 @@ struct TraceArgs {
     const PrimHit *prim;
     // solve + raster: the slots whose query 0 hit (k_prim_compact); the other
     // slots already hold their final records.  n_work is read from n_work_dev.
-    const uint2 *worklist;    // (slot, unit index)
+    // (slot, unit index) per hit; entry w is overwritten with ray w's SlotRec
+    uint4 *worklist;
     const unsigned long long *n_work_dev;
     // grid mode: rays r_base + [0, n_work) of the grid (a row range); output
     // and prim indices are relative to r_base
@@ -220,19 +221,26 @@ k_trace_persistent(TraceArgs a)
                 fresh = (int64_t)__shfl_sync(0xffffffffu, base, 0);
             }
             int wl_unit = -1;
+            int64_t wl_slot = 0;
             if (want & (1u << lane)) {
                 const int rank = __popc(want & lt_mask);
                 const int64_t w = rank < avail ? chunk_next + rank : fresh + (rank - avail);
                 if (w < n_work) {
                     if (a.worklist) {
-                        const uint2 e = __ldg(&a.worklist[w]);
-                        L.slot = (int64_t)e.x;
+                        const uint4 e = a.worklist[w];
+                        L.slot = w;                 // output: the list entry itself
+                        wl_slot = (int64_t)e.x;
                         wl_unit = (int)e.y;
                         // listed slots are raster hits: their query-0 result is
-                        // loaded now, beside the unit / grid loads below
-                        const PrimHit h = a.prim[L.slot];
+                        // loaded now, beside the unit / grid loads below, and
+                        // the slot is reset to the raster's all-ones "no hit"
+                        // (this is its last reader: no memset before the next
+                        // raster pass)
+                        PrimHit *hp = const_cast<PrimHit *>(a.prim) + wl_slot;
+                        const PrimHit h = *hp;
                         L.best_t = __longlong_as_double((long long)h.tbits);
                         L.best = (int)h.id;
+                        __stcs(reinterpret_cast<int4 *>(hp), make_int4(-1, -1, -1, -1));
                     } else {
                         L.slot = w;
                     }
@@ -253,7 +261,7 @@ k_trace_persistent(TraceArgs a)
                 if (MODE == kModeSolve) {
                     const int ui = wl_unit >= 0 ? wl_unit : find_unit(a.units, a.n_units, L.slot);
                     const UnitDev U = a.units[ui];
-                    L.r = U.ray_begin + (L.slot - U.slot_base);
+                    L.r = U.ray_begin + ((wl_unit >= 0 ? wl_slot : L.slot) - U.slot_base);
                     L.grid = U.grid;
                     G = a.grids + U.grid;
                     real = L.r < U.ray_end;
@@ -481,7 +489,12 @@ k_trace_persistent(TraceArgs a)
                     rec.cosv = (float)c;
                     rec.meta = (uint32_t)L.bounces | kMetaActive | (L.valid ? kMetaValid : 0u) |
                                (escaped ? kMetaEscaped : 0u) | (sel ? kMetaSel : 0u);
-                    a.slots[L.slot] = rec;
+                    if (a.worklist) {
+                        rec.meta |= (uint32_t)(L.r & (kChunk - 1)) << kMetaOffShift;
+                        reinterpret_cast<SlotRec *>(a.worklist)[L.slot] = rec;
+                    } else {
+                        a.slots[L.slot] = rec;
+                    }
                 } else if (a.full.seg_hash) {
                     const unsigned long long h = record_hash(
                         L.hid, L.bounces, cfg.max_bounces, L.valid, escaped, L.n0x, L.n0y,
