@@ -1331,7 +1331,8 @@ static int run_units(sbr_ctx *ctx, const sbr_bvh *bvh, const std::vector<UnitDev
         while (u1 < all_units.size()) {
             UnitDev u = all_units[u1];
             int64_t need = round_chunk(u.ray_end - u.ray_begin);
-            if (!batch.empty() && slots + need > budget) break;
+            if (!batch.empty() && (slots + need > budget || (int64_t)batch.size() >= kMaxBatchUnits))
+                break;   // work-list entries hold the unit index in 20 bits
             u.slot_base = slots;
             slots += need;
             batch.push_back(u);
@@ -1362,7 +1363,8 @@ static int run_units(sbr_ctx *ctx, const sbr_bvh *bvh, const std::vector<UnitDev
         if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev[0], st));
         // the batch's slots are all-ones after a list-mode PO; anything
         // else (BVH primary, reference order, an error) leaves them dirty
-        const int64_t clean = ctx->clean_slots;
+        static const bool force_memset = getenv("SBR_FORCE_MEMSET") != nullptr;  // A/B only
+        const int64_t clean = force_memset ? 0 : ctx->clean_slots;
         ctx->clean_slots = 0;
         if (raster) {
             seg_slot.assign(seg_base[ngrids], kNoSlot);

@@ -370,7 +370,7 @@ constexpr int kCompactTile = kCompactThreads * kCompactPer;   // == kChunk
 __global__ void __launch_bounds__(kCompactThreads)
 k_prim_compact(TraceCfg cfg, const GridDev *__restrict__ grids,
                const UnitDev *__restrict__ units, int n_units, int64_t n_slots,
-               const SlotRec *__restrict__ slots, uint4 *__restrict__ list,
+               SlotRec *__restrict__ slots, uint4 *__restrict__ list,
                unsigned long long *__restrict__ nlist, uint2 *__restrict__ chunk_hits)
 {
     constexpr int W = kCompactThreads / 32;
@@ -387,20 +387,25 @@ k_prim_compact(TraceCfg cfg, const GridDev *__restrict__ grids,
             cfg.allow_aliasing || !(grids[U.grid].spacing > cfg.spacing_limit);
         if (!alias_ok && tid == 0) atomicOr(cfg.error_flag, 1u);
         unsigned hitmask = 0;
+        ulonglong2 hv[kCompactPer];
 #pragma unroll
         for (int q = 0; q < kCompactPer; ++q) {
             const int64_t slot = tile + q * kCompactThreads + tid;
             bool hit = false;
+            hv[q] = make_ulonglong2(kNoHitBits, kNoHitBits);
             if (slot < n_slots) {
                 const int64_t r = U.ray_begin + (slot - U.slot_base);
                 const bool real = r < U.ray_end && alias_ok;
                 // streaming read: every slot is read once here and the
                 // misses (most of them) never again
-                const ulonglong2 h =
-                    __ldcs(reinterpret_cast<const ulonglong2 *>(slots) + slot);
-                hit = real && h.x != kNoHitBits;
-                // misses and padding keep their all-ones bits: k_po derives
-                // them from the unit (list mode), nothing is rewritten
+                hv[q] = __ldcs(reinterpret_cast<const ulonglong2 *>(slots) + slot);
+                hit = real && hv[q].x != kNoHitBits;
+                // the hit moves into the work list; its slot returns to the
+                // raster's all-ones "no hit" (no memset before the next
+                // pass).  Misses and padding keep their all-ones bits.
+                if (hit)
+                    __stcs(reinterpret_cast<ulonglong2 *>(slots) + slot,
+                           make_ulonglong2(kNoHitBits, kNoHitBits));
             }
             const unsigned bal = __ballot_sync(0xffffffffu, hit);
             if (lane == 0) cnt[q][warp] = __popc(bal);
@@ -424,10 +429,17 @@ k_prim_compact(TraceCfg cfg, const GridDev *__restrict__ grids,
         for (int q = 0; q < kCompactPer; ++q) {
             const bool hit = (hitmask >> q) & 1u;
             const unsigned bal = __ballot_sync(0xffffffffu, hit);
-            if (hit)
+            if (hit) {
+                // (t bits, id | offset in unit << 25 | unit << 44): the trace
+                // refill needs nothing else
+                const unsigned long long off = (unsigned long long)(tile - U.slot_base) +
+                                               (unsigned long long)(q * kCompactThreads + tid);
+                const unsigned long long pk = (hv[q].y >> 32) | (off << kWlOffShift) |
+                                              ((unsigned long long)ui << kWlUnitShift);
                 list[at + pos[q][warp] + __popc(bal & ((1u << lane) - 1u))] =
-                    make_uint4((unsigned int)(tile + q * kCompactThreads + tid), (unsigned int)ui,
-                               0u, 0u);
+                    make_uint4((unsigned int)hv[q].x, (unsigned int)(hv[q].x >> 32),
+                               (unsigned int)pk, (unsigned int)(pk >> 32));
+            }
         }
         __syncthreads();
     }

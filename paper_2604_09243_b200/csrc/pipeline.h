@@ -45,6 +45,15 @@ constexpr uint32_t kMetaBounceMask = 0xffffu;
 // within its 1024-slot chunk in bits 20..29 (r mod 1024: units are chunk-
 // and segment-aligned), for the NumericalError record index
 constexpr int kMetaOffShift = 20;
+
+// Work-list entry (16 B) of a primary hit, written by k_prim_compact:
+//   x, y = bits of the query-0 t; z, w = id | (ray offset in its unit) << 25
+//   | (unit index in the batch) << 44 -- ids < 2^25 (kMaxTriangles), unit
+//   offsets < 2^19 (kSegRays), units per batch < 2^20 (run_units).
+// The trace kernel overwrites the entry with the ray's SlotRec.
+constexpr int kWlOffShift = 25;
+constexpr int kWlUnitShift = 44;
+constexpr int kMaxBatchUnits = 1 << 20;
 // meta of an all-ones slot (a PrimHit that no triangle reached): a finished
 // primary miss -- no real record has bits 20..31 set
 constexpr uint32_t kMissMeta = 0xffffffffu;

@@ -65,7 +65,8 @@ struct TraceArgs {
     const PrimHit *prim;
     // solve + raster: the slots whose query 0 hit (k_prim_compact); the other
     // slots already hold their final records.  n_work is read from n_work_dev.
-    // (slot, unit index) per hit; entry w is overwritten with ray w's SlotRec
+    // packed query-0 hit per entry (pipeline.h kWl*); entry w is overwritten
+    // with ray w's SlotRec
     uint4 *worklist;
     const unsigned long long *n_work_dev;
     // grid mode: rays r_base + [0, n_work) of the grid (a row range); output
@@ -227,20 +228,18 @@ k_trace_persistent(TraceArgs a)
                 const int64_t w = rank < avail ? chunk_next + rank : fresh + (rank - avail);
                 if (w < n_work) {
                     if (a.worklist) {
-                        const uint4 e = a.worklist[w];
+                        // one 16-byte load: the raster's query-0 result, the
+                        // ray's unit and its offset in the unit
+                        const uint4 e = __ldg(&a.worklist[w]);
+                        const unsigned long long pk =
+                            (unsigned long long)e.z | ((unsigned long long)e.w << 32);
                         L.slot = w;                 // output: the list entry itself
-                        wl_slot = (int64_t)e.x;
-                        wl_unit = (int)e.y;
-                        // listed slots are raster hits: their query-0 result is
-                        // loaded now, beside the unit / grid loads below, and
-                        // the slot is reset to the raster's all-ones "no hit"
-                        // (this is its last reader: no memset before the next
-                        // raster pass)
-                        PrimHit *hp = const_cast<PrimHit *>(a.prim) + wl_slot;
-                        const PrimHit h = *hp;
-                        L.best_t = __longlong_as_double((long long)h.tbits);
-                        L.best = (int)h.id;
-                        __stcs(reinterpret_cast<int4 *>(hp), make_int4(-1, -1, -1, -1));
+                        L.best_t = __longlong_as_double((long long)e.x |
+                                                        ((long long)e.y << 32));
+                        L.best = (int)(pk & ((1ULL << kWlOffShift) - 1));
+                        wl_slot = (int64_t)((pk >> kWlOffShift) &
+                                            ((1ULL << (kWlUnitShift - kWlOffShift)) - 1));
+                        wl_unit = (int)(pk >> kWlUnitShift);
                     } else {
                         L.slot = w;
                     }
@@ -261,7 +260,9 @@ k_trace_persistent(TraceArgs a)
                 if (MODE == kModeSolve) {
                     const int ui = wl_unit >= 0 ? wl_unit : find_unit(a.units, a.n_units, L.slot);
                     const UnitDev U = a.units[ui];
-                    L.r = U.ray_begin + ((wl_unit >= 0 ? wl_slot : L.slot) - U.slot_base);
+                    // list entries carry the ray's offset within its unit
+                    L.r = wl_unit >= 0 ? U.ray_begin + wl_slot
+                                       : U.ray_begin + (L.slot - U.slot_base);
                     L.grid = U.grid;
                     G = a.grids + U.grid;
                     real = L.r < U.ray_end;
