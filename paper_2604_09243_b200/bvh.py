@@ -1,16 +1,23 @@
 """Bounding volume hierarchy (API of pkg/src/sbr/bvh.py).
 
-``build`` constructs the tree on the GPU (LBVH: Morton codes, radix sort,
-radix-tree emit, FP64 refit, leaf collapse to ``n_leaf``).  The returned
-``Bvh`` exposes the reference preorder layout (exported lazily from the
-device tree) so ``Bvh.validate`` and CPU consumers keep working; closest-hit
-queries run on the device tree.  A ``Bvh`` constructed from reference
-arrays is uploaded on first use.
+``build`` constructs the tree on the GPU.  ``split_rule="sah"`` (the
+reference default) and ``"median"`` build the reference's own tree, node
+for node (level-synchronous binned SAH / median split, csrc/sahbuild.cu);
+``"lbvh"`` builds a Morton-code LBVH (csrc/lbvh.cu).  Every tree is
+collapsed to a 4-wide tree for traversal.  The returned ``Bvh`` exposes the
+reference preorder layout (verbatim for SAH/median, exported lazily from the
+device) so ``Bvh.validate`` and CPU consumers keep working.  A ``Bvh``
+constructed from reference arrays is uploaded on first use.
 
-Closest-hit results do not depend on the tree (ties resolve to the lowest
-triangle index, bvh.py:340), so the GPU tree returns the reference's hits
-bit-for-bit even though its node layout differs.  ``visits`` counts the
-device tree's node fetches.
+Closest-hit results: the fast traversal returns the lexicographic (t, id)
+minimum over the triangles its conservative culling reaches -- the
+reference's answer on every robust ray (the winning
+hit lies inside its triangle's box and no other triangle ties it within
+rounding).  Near-edge-on triangles can make Moller-Trumbore accept rays
+outside their box; there the reference's own answer depends on its tree,
+and ``traversal_order("reference")`` replays bvh.py:306-362 on the
+reference tree, bit for bit on every ray (visit counts included).  In the
+fast mode ``visits`` counts the device tree's node fetches.
 """
 
 from __future__ import annotations

@@ -153,6 +153,10 @@ struct sbr_bvh {
     int ref_depth = -1;
     int ref_round_f32 = 0;     // GPU-built tree of a float32 mesh: replica rounds boxes
     int ref_tree_depth = -1;   // depth of ref_dev (reference-order traversal stack bound)
+    // BVH4 deeper than the fast kernels' stack (kMaxDepth4): every traversal
+    // of this tree replays the reference order on the reference tree instead
+    // (reforder.cu, stack bound 255; the reference itself allows max_depth + 2)
+    bool deep = false;
     double frame[3];
     float scale = 0.f;
     BvhView view() const
@@ -615,10 +619,24 @@ static int upload_ref_tree(sbr_ctx *ctx, const sbr_mesh *mesh, const double *nod
     e = collapse_bvh4(b->out, ctx->ws, ctx->stream, &ctx->launches);
     if (e != cudaSuccess) return fail(SBR_ECUDA, "BVH upload: %s", cudaGetErrorString(e));
     if (b->out.width == 8 && 7 * b->out.depth8 + 1 >= kStack) b->out.width = 4;  // stack bound
-    if (b->out.depth4 > kMaxDepth4)
-        return fail(SBR_EINVAL, "BVH4 depth %d exceeds the traversal stack limit (%d)",
-                    b->out.depth4, kMaxDepth4);
+    b->deep = b->out.depth4 > kMaxDepth4;   // checked against the reference tree by the caller
     return SBR_OK;
+}
+
+// A deep tree (BVH4 depth > kMaxDepth4) is walked in reference order on its
+// reference tree; without one (LBVH) or beyond that kernel's stack: EINVAL.
+static int deep_ok(const sbr_bvh *b)
+{
+    if (!b->deep) return SBR_OK;
+    if (b->ref_dev.nnodes > 0 && b->ref_tree_depth >= 0 && b->ref_tree_depth + 1 < 256)
+        return SBR_OK;
+    return fail(SBR_EINVAL, "BVH4 depth %d exceeds the traversal stack limit (%d) and no "
+                "reference tree of depth < 255 is available", b->out.depth4, kMaxDepth4);
+}
+
+static bool use_ref(const sbr_ctx *ctx, const sbr_bvh *bvh)
+{
+    return ctx->traversal == SBR_TRAVERSAL_REFERENCE || bvh->deep;
 }
 
 extern "C" int sbr_bvh_upload(sbr_ctx *ctx, const sbr_mesh *mesh, const double *nodes_min,
@@ -682,6 +700,10 @@ extern "C" int sbr_bvh_upload(sbr_ctx *ctx, const sbr_mesh *mesh, const double *
         T.max_depth = md;
         b->ref_tree_depth = md;
     }
+    if (int rc = deep_ok(b)) {
+        delete b;
+        return rc;
+    }
     *out = b;
     return SBR_OK;
 }
@@ -729,7 +751,7 @@ static int build_sah(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_build_params 
                                        b->ref_first.data(), b->ref_count.data(),
                                        b->ref_order.data(), (int64_t)b->ref_first.size(), b);
         b->out.max_depth = T.max_depth;
-        return rc;
+        return rc ? rc : deep_ok(b);
     }
     e = pack_tris(mesh->verts.p, T.order.p, mesh->ntri, mesh->storage, b->out, ctx->stream,
                   &ctx->launches);
@@ -745,10 +767,8 @@ static int build_sah(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_build_params 
         fprintf(stderr, "[sah] build+convert %.2f ms, pack+bvh4 %.2f ms, nodes %lld\n",
                 ms(t0, t1), ms(t1, now()), (long long)T.nnodes);
     if (b->out.width == 8 && 7 * b->out.depth8 + 1 >= kStack) b->out.width = 4;  // stack bound
-    if (b->out.depth4 > kMaxDepth4)
-        return fail(SBR_EINVAL, "BVH4 depth %d exceeds the traversal stack limit (%d)",
-                    b->out.depth4, kMaxDepth4);
-    return SBR_OK;
+    b->deep = b->out.depth4 > kMaxDepth4;
+    return deep_ok(b);
 }
 
 static int ref_download(const sbr_bvh *bvh)
@@ -938,7 +958,7 @@ static RefView ref_view(const sbr_bvh *b)
 // reference-order traversal needs the reference-layout tree on the device
 static int check_ref_mode(const sbr_ctx *ctx, const sbr_bvh *bvh)
 {
-    if (ctx->traversal != SBR_TRAVERSAL_REFERENCE) return SBR_OK;
+    if (!use_ref(ctx, bvh)) return SBR_OK;
     REQUIRE(bvh->ref_dev.nnodes > 0,
             "reference-order traversal needs the reference tree (split_rule 'sah' or 'median', "
             "or an uploaded tree)");
@@ -1067,7 +1087,7 @@ extern "C" int sbr_closest_hit(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh
     CUDA_TRY(cudaMemcpyAsync(o.p, origins, 24 * n, cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaMemcpyAsync(d.p, dirs, 24 * n, cudaMemcpyHostToDevice, st));
     if (int rc = check_ref_mode(ctx, bvh)) return rc;
-    if (ctx->traversal == SBR_TRAVERSAL_REFERENCE)
+    if (use_ref(ctx, bvh))
         CUDA_TRY(launch_closest_ref(ref_view(bvh), o.p, d.p, n, t_min, t_max, ti.p, tt.p, vi.p,
                                     st, ctx->stats()));
     else
@@ -1141,7 +1161,7 @@ static int trace_full_common(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *
     TraceCfg cfg = make_cfg(bvh, params, ctx);
     FullOut fo{dv.p, dn.p, dp.p, db.p, de.p, dd.p, (tri_ids && !hash) ? di.p : nullptr,
                hash ? dh.p : nullptr, seg_rays};
-    if (ctx->traversal == SBR_TRAVERSAL_REFERENCE) {
+    if (use_ref(ctx, bvh)) {
         CUDA_TRY(launch_trace_ref(ref_view(bvh), cfg, dg.p, o.p, d.p, n, r_base, fo, nullptr,
                                   nullptr, 0, st, ctx->stats()));
     } else {
@@ -1311,7 +1331,7 @@ static int run_units(sbr_ctx *ctx, const sbr_bvh *bvh, const std::vector<UnitDev
     cudaStream_t st = ctx->stream;
     int64_t budget = slot_budget();
     const int ngrids = (int)seg_base.size() - 1;
-    const bool refmode = ctx->traversal == SBR_TRAVERSAL_REFERENCE;
+    const bool refmode = use_ref(ctx, bvh);
     const bool raster = !refmode && raster_primary(bvh->mesh->ntri, ngrids);
     std::vector<int64_t> seg_slot;
     std::vector<int> bgrids;

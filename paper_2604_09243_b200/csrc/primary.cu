@@ -56,6 +56,9 @@ namespace sbr {
 // every row), always through the chunk queue.
 constexpr double kEps = 1.1102230246251565e-16;   // 2^-53
 constexpr double kTiny = 1e-290;
+#ifndef SBR_RASTER_MINB
+#define SBR_RASTER_MINB 4
+#endif
 constexpr int kRasterThreads = 256;
 constexpr int kRasterWarps = kRasterThreads / 32;
 constexpr long long kBigTri = 2048;     // candidates above which a triangle is chunked
@@ -102,6 +105,60 @@ struct RasterSetup {
     int trans, wide;
     double f0, fi, fj, g0, gi, gj, eu, ev, h, err;
 };
+
+// Candidate box of an ill-conditioned (WIDE) pair: the boxes of the two edge
+// strips -Eu <= F <= H + Ev and -Ev <= G <= H + Eu, clipped to the aperture.
+// Rare (204 of C4's 354M pairs), so kept out of line: its registers do not
+// weigh on the common path.  Returns false when the region is empty.
+__device__ __forceinline__ bool wide_region(const RasterSetup &S, int64_t n_u, int64_t n_v,
+                                         double &alo_o, double &ahi_o, double &blo_o,
+                                         double &bhi_o)
+{
+    double alo, ahi, blo, bhi;
+    alo = 0.0; ahi = (double)(n_u - 1);
+    blo = 0.0; bhi = (double)(n_v - 1);
+    const double xs[3] = {S.f0, S.fi, S.fj}, ys[3] = {S.g0, S.gi, S.gj};
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+        const double *c = s ? ys : xs;
+        const double lo = s ? -S.ev : -S.eu, hi = s ? S.h + S.eu : S.h + S.ev;
+        // column range over the aperture's rows (extremes at the end rows)
+        if (c[2] != 0.0) {
+            double mn = INFINITY, mx = -INFINITY;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const double x = e ? (double)(n_u - 1) : 0.0;
+                const double q0 = (lo - c[0] - c[1] * x) / c[2];
+                const double q1 = (hi - c[0] - c[1] * x) / c[2];
+                const double w = (S.err + 8.0 * kEps * (fabs(lo) + fabs(hi) + fabs(c[0]) +
+                                                        fabs(c[1] * x))) / fabs(c[2]);
+                mn = fmin(mn, fmin(q0, q1) - w);
+                mx = fmax(mx, fmax(q0, q1) + w);
+            }
+            blo = fmax(blo, mn - 1e-9 * (1.0 + fabs(mn)));
+            bhi = fmin(bhi, mx + 1e-9 * (1.0 + fabs(mx)));
+        }
+        // row range over the aperture's columns
+        if (c[1] != 0.0) {
+            double mn = INFINITY, mx = -INFINITY;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const double y = e ? (double)(n_v - 1) : 0.0;
+                const double q0 = (lo - c[0] - c[2] * y) / c[1];
+                const double q1 = (hi - c[0] - c[2] * y) / c[1];
+                const double w = (S.err + 8.0 * kEps * (fabs(lo) + fabs(hi) + fabs(c[0]) +
+                                                        fabs(c[2] * y))) / fabs(c[1]);
+                mn = fmin(mn, fmin(q0, q1) - w);
+                mx = fmax(mx, fmax(q0, q1) + w);
+            }
+            alo = fmax(alo, mn - 1e-9 * (1.0 + fabs(mn)));
+            ahi = fmin(ahi, mx + 1e-9 * (1.0 + fabs(mx)));
+        }
+    }
+    if (!(alo <= ahi && blo <= bhi)) return false;   // NaN-safe: empty
+    alo_o = alo; ahi_o = ahi; blo_o = blo; bhi_o = bhi;
+    return true;
+}
 
 __device__ __forceinline__ RasterSetup raster_setup(const TriF64 &T, const GridDev &G,
                                                     int64_t row_lo, int64_t row_hi)
@@ -155,18 +212,21 @@ __device__ __forceinline__ RasterSetup raster_setup(const TriF64 &T, const GridD
         alo = blo = INFINITY;      // running minima
         ahi = bhi = -INFINITY;     // running maxima
         double emax = 0.0;
+        // one division per pair: x * fl(1/det2) is within 2 ulp of x / det2,
+        // covered by the 4e|a| term added to each bound below
+        const double inv2 = 1.0 / det2, ainv2 = fabs(inv2);
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
             const double nf = cf[k] - S.f0, ng = cg[k] - S.g0;
-            const double a = (nf * S.gj - S.fj * ng) / det2;
-            const double b = (S.fi * ng - S.gi * nf) / det2;
+            const double a = (nf * S.gj - S.fj * ng) * inv2;
+            const double b = (S.fi * ng - S.gi * nf) * inv2;
             // first-order error bound of the 2x2 solve, x4 (relative error of
             // det2 <= 2e kd/|det2|; numerators carry their own few ulp)
             const double mf = fabs(cf[k]) + fabs(S.f0), mg = fabs(cg[k]) + fabs(S.g0);
-            const double ea = 16.0 * kEps * (fabs(a) * kd + mf * fabs(S.gj) + fabs(S.fj) * mg) /
-                              fabs(det2);
-            const double eb = 16.0 * kEps * (fabs(b) * kd + mg * fabs(S.fi) + fabs(S.gi) * mf) /
-                              fabs(det2);
+            const double ea = 16.0 * kEps * (fabs(a) * kd + mf * fabs(S.gj) + fabs(S.fj) * mg) *
+                              ainv2 * (1.0 + 8.0 * kEps) + 4.0 * kEps * fabs(a);
+            const double eb = 16.0 * kEps * (fabs(b) * kd + mg * fabs(S.fi) + fabs(S.gi) * mf) *
+                              ainv2 * (1.0 + 8.0 * kEps) + 4.0 * kEps * fabs(b);
             emax = fmax(emax, fmax(ea, eb));
             alo = fmin(alo, a - ea); ahi = fmax(ahi, a + ea);
             blo = fmin(blo, b - eb); bhi = fmax(bhi, b + eb);
@@ -177,51 +237,7 @@ __device__ __forceinline__ RasterSetup raster_setup(const TriF64 &T, const GridD
             blo -= 1e-9 * (1.0 + fabs(blo)); bhi += 1e-9 * (1.0 + fabs(bhi));
         }
     }
-    if (S.wide) {
-        // ---- ill-conditioned: intersect the boxes of the two edge strips
-        // -Eu <= F <= H + Ev and -Ev <= G <= H + Eu, clipped to the aperture
-        alo = 0.0; ahi = (double)(n_u - 1);
-        blo = 0.0; bhi = (double)(n_v - 1);
-        const double xs[3] = {S.f0, S.fi, S.fj}, ys[3] = {S.g0, S.gi, S.gj};
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-            const double *c = s ? ys : xs;
-            const double lo = s ? -S.ev : -S.eu, hi = s ? S.h + S.eu : S.h + S.ev;
-            // column range over the aperture's rows (extremes at the end rows)
-            if (c[2] != 0.0) {
-                double mn = INFINITY, mx = -INFINITY;
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const double x = e ? (double)(n_u - 1) : 0.0;
-                    const double q0 = (lo - c[0] - c[1] * x) / c[2];
-                    const double q1 = (hi - c[0] - c[1] * x) / c[2];
-                    const double w = (S.err + 8.0 * kEps * (fabs(lo) + fabs(hi) + fabs(c[0]) +
-                                                            fabs(c[1] * x))) / fabs(c[2]);
-                    mn = fmin(mn, fmin(q0, q1) - w);
-                    mx = fmax(mx, fmax(q0, q1) + w);
-                }
-                blo = fmax(blo, mn - 1e-9 * (1.0 + fabs(mn)));
-                bhi = fmin(bhi, mx + 1e-9 * (1.0 + fabs(mx)));
-            }
-            // row range over the aperture's columns
-            if (c[1] != 0.0) {
-                double mn = INFINITY, mx = -INFINITY;
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const double y = e ? (double)(n_v - 1) : 0.0;
-                    const double q0 = (lo - c[0] - c[2] * y) / c[1];
-                    const double q1 = (hi - c[0] - c[2] * y) / c[1];
-                    const double w = (S.err + 8.0 * kEps * (fabs(lo) + fabs(hi) + fabs(c[0]) +
-                                                            fabs(c[2] * y))) / fabs(c[1]);
-                    mn = fmin(mn, fmin(q0, q1) - w);
-                    mx = fmax(mx, fmax(q0, q1) + w);
-                }
-                alo = fmax(alo, mn - 1e-9 * (1.0 + fabs(mn)));
-                ahi = fmin(ahi, mx + 1e-9 * (1.0 + fabs(mx)));
-            }
-        }
-        if (!(alo <= ahi && blo <= bhi)) return S;   // NaN-safe: empty
-    }
+    if (S.wide && !wide_region(S, n_u, n_v, alo, ahi, blo, bhi)) return S;
     if (!(ahi >= 0.0 && bhi >= 0.0 && alo <= (double)(n_u - 1) && blo <= (double)(n_v - 1)))
         return S;                               // outside the aperture (or non-finite)
     int64_t i0 = alo <= 0.0 ? 0 : (int64_t)ceil(alo);
@@ -293,6 +309,9 @@ __device__ __forceinline__ void raster_cell(const RasterArgs &a, const GridDev &
     const int64_t r = i * G.n_v + j;
     // sharded / partial batches: skip cells of segments this launch does not
     // own before doing any arithmetic
+#ifdef SBR_RASTER_NOWALK   // experiment: set-up cost only
+    if (i >= 0) return;
+#endif
     const int64_t off = __ldg(&seg[r / kSegRays]);
     if (a.sparse && off == kNoSlot) return;
     // origin exactly as the launcher builds it (pipeline.cu grid_origin)
@@ -304,6 +323,10 @@ __device__ __forceinline__ void raster_cell(const RasterArgs &a, const GridDev &
     const double oz = DA(DA(G.corner[2], DM(si, G.u[2])), DM(sj, G.v[2]));
     const double t = tri_hit_origin<true>(T, P, inv, ox, oy, oz, G.k[0], G.k[1], G.k[2], 0.0,
                                           inf);
+#ifdef SBR_RASTER_NOCAS   // experiment: cost of the exact tests without the minimum
+    if (t == 1.2345) prim_min(a.prim + (off + r), 0, 0);
+    return;
+#endif
     if (t > 0.0 && t < inf && off != kNoSlot)
         prim_min(a.prim + (off + r), (unsigned long long)__double_as_longlong(t),
                  (unsigned int)id);
@@ -344,7 +367,7 @@ __device__ __forceinline__ void line_span(const RasterSetup &S, double x, double
 // kBigChunk-candidate chunks for k_raster_big, so no warp ever holds a huge
 // triangle at the tail of the launch.
 template <int STORAGE>
-__global__ void __launch_bounds__(kRasterThreads, 4)
+__global__ void __launch_bounds__(kRasterThreads, SBR_RASTER_MINB)
 k_raster(RasterArgs a, int64_t ntri_pad)
 {
     __shared__ RasterTri st[kRasterWarps][32];
@@ -463,7 +486,7 @@ k_raster(RasterArgs a, int64_t ntri_pad)
 // line r's cells inside the half-plane span (not the whole box line), then
 // the warp walks the concatenated spans 32 cells at a time.
 template <int STORAGE>
-__global__ void __launch_bounds__(kRasterThreads, 4)
+__global__ void __launch_bounds__(kRasterThreads, SBR_RASTER_MINB)
 k_raster_big(RasterArgs a)
 {
     const int lane = threadIdx.x & 31;

@@ -26,6 +26,10 @@ out = {"trav_steps": int(buf[0]), "lanes_traversing": buf[1] / it, "lanes_parked
        "leaf_phases": int(buf[5]), "lanes_in_leaf_phase": buf[6] / max(buf[5], 1),
        "trav_steps_per_leaf_phase": buf[0] / max(buf[5], 1),
        "queries": int(res.queries.sum())}
+sq = max(int(buf[16]), 1)   # BVH-traced queries (secondary + any unresolved primary)
+out["per_traced_query"] = {"bvh4_node_visits": buf[12] / sq, "triangle_tests": buf[13] / sq,
+                           "leaf_visits": buf[14] / sq, "stack_pushes": buf[15] / sq,
+                           "traced_queries": sq}
 cyc = buf[8:12].astype(float)
 out["cycle_share"] = dict(zip(("refill", "traversal", "leaf", "completion"),
                               (cyc / max(cyc.sum(), 1)).round(3).tolist()))

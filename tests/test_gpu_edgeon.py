@@ -247,3 +247,62 @@ def test_raster_candidates_are_tight():
         bound += int((np.clip(i1 - i0 + 1, 0, None) * np.clip(j1 - j0 + 1, 0, None)).sum())
     assert 0 < got["candidates"] <= bound, (got, bound)
     assert got["queue_overflows"] == 0
+
+
+def _chain_tree(mesh):
+    """A valid reference-layout tree that is a chain: node 2k is internal
+    (left = leaf 2k+1 holding triangle k, right = node 2k+2), so its depth is
+    ntri - 1 -- far past the fast kernels' BVH4 stack bound."""
+    n = mesh.triangle_count
+    lo = np.minimum(np.minimum(mesh.v0, mesh.v1), mesh.v2).astype(np.float64)
+    hi = np.maximum(np.maximum(mesh.v0, mesh.v1), mesh.v2).astype(np.float64)
+    suf_lo = np.minimum.accumulate(lo[::-1])[::-1]
+    suf_hi = np.maximum.accumulate(hi[::-1])[::-1]
+    m = 2 * n - 1
+    nmin, nmax = np.zeros((m, 3)), np.zeros((m, 3))
+    first, count = np.zeros(m, np.int32), np.zeros(m, np.int32)
+    for k in range(n - 1):
+        nmin[2 * k], nmax[2 * k], first[2 * k] = suf_lo[k], suf_hi[k], 2 * k + 2
+        nmin[2 * k + 1], nmax[2 * k + 1] = lo[k], hi[k]
+        first[2 * k + 1], count[2 * k + 1] = k, 1
+    nmin[m - 1], nmax[m - 1], first[m - 1], count[m - 1] = lo[n - 1], hi[n - 1], n - 1, 1
+    return nmin, nmax, first, count, np.arange(n, dtype=np.int32), n - 1
+
+
+def test_deep_tree_is_traced_in_reference_order(orc):
+    """BVH4 depth > 31 (a 127-deep chain): no EINVAL; every traversal of that
+    tree replays bvh.py:306-362 on it (the reference's stack is max_depth+2,
+    bvh.py:381-382), bit for bit against the oracle on the same tree."""
+    mesh = meshgen.perturbed_grid_mesh(cells=8, extent=1.0, amplitude=0.05, seed=5)
+    arrays = _chain_tree(mesh)
+    tree = sbr.Bvh(*arrays)
+    tree.validate(mesh)
+    origins, dirs = meshgen_probe(mesh)
+    tri, t, vis = sbr.closest_hit_batch(tree, mesh, origins, dirs)
+    scene = orc.Scene(mesh.v0, mesh.v1, mesh.v2, mesh.normals,
+                      orc.OracleBvh(*arrays[:5], arrays[5], 200))
+    btri, bt = orc.brute_force_hits(scene, origins, dirs)
+    assert np.array_equal(tri, btri)
+    assert np.array_equal(t[tri >= 0], bt[tri >= 0])
+    lam = 0.05
+    grid = sbr.build_aperture(mesh.aabb, sbr.IncidentDirection(0.4, 0.9), lam / 5,
+                              wavelength=lam)
+    params = sbr.TraceParams(max_bounces=3)
+    rec = sbr.trace_grid(tree, mesh, grid, params, with_ids=True)
+    ref = orc.trace_grid(scene, grid, 3, params.resolve_epsilon(mesh), with_ids=True)
+    for k in REC:
+        assert np.array_equal(getattr(rec, k), getattr(ref, k)), k
+    sol = sbr.solve_direction(tree, mesh, sbr.IncidentDirection(0.4, 0.9), lam / 5, lam,
+                              trace_params=params)
+    assert sol.valid_rays == int(ref.valid.sum())
+
+
+def meshgen_probe(mesh, n=4000, seed=3):
+    rng = np.random.default_rng(seed)
+    c = 0.5 * (mesh.aabb.min + mesh.aabb.max)
+    r = mesh.aabb.diagonal()
+    g = rng.normal(size=(n, 3))
+    g /= np.linalg.norm(g, axis=1)[:, None]
+    o = c + 1.6 * r * g
+    d = c + 0.4 * r * rng.uniform(-1, 1, size=(n, 3)) - o
+    return o, d / np.linalg.norm(d, axis=1)[:, None]
