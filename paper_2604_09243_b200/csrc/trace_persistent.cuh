@@ -131,32 +131,6 @@ __device__ __forceinline__ bool leaf_test(const BvhView &B, LaneRay &L, int leaf
 #ifdef SBR_TRACE_STATS
     L.st_leaves += 1;
 #endif
-#ifdef SBR_LEAF_PAIR
-    // two triangles per iteration: the second one's loads are in flight
-    // while the first is tested
-    const int end = first + cnt;
-    for (int k = first; k < end; k += 2) {
-        const TriF64 T0 = load_tri<STORAGE>(B, k);
-        const bool two = k + 1 < end;
-        const TriF64 T1 = load_tri<STORAGE>(B, two ? k + 1 : k);
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            if (h == 1 && !two) break;
-            const TriF64 &T = h ? T1 : T0;
-#ifdef SBR_TRACE_STATS
-            L.st_tris += 1;
-#endif
-            const double t = tri_hit_exact(T, L.ox, L.oy, L.oz, L.dx, L.dy, L.dz, 0.0, L.best_t);
-            if (t > 0.0 && (t < L.best_t || (t == L.best_t && T.id < L.best))) {
-                L.best_t = t;
-                L.best = T.id;
-                L.tmax = __double2float_ru(t);
-                if (L.probe) return true;   // escape probe: any hit decides
-            }
-        }
-    }
-    return false;
-#else
     for (int k = first; k < first + cnt; ++k) {
 #ifdef SBR_TRACE_STATS
         L.st_tris += 1;
@@ -171,7 +145,6 @@ __device__ __forceinline__ bool leaf_test(const BvhView &B, LaneRay &L, int leaf
         }
     }
     return false;
-#endif
 }
 
 // pop the next stack entry whose entry distance can still beat best_t
@@ -403,43 +376,10 @@ k_trace_persistent(TraceArgs a)
                 const int n = WideNode<W>::visit(wide_nodes<W>(B) + L.ref, L.rb, L.tmax, rr, tt);
                 bool have = true;
                 if (n > 0) {
-#ifdef SBR_PARK_CHILDREN
-                    // children near -> far: the nearest internal child is the
-                    // next node; leaf children go straight into free park
-                    // slots (no push + pop round trip through the local
-                    // stack); the rest is pushed far-first
-                    int next = 0;   // 0 = none (node 0 is the root, never a child)
-                    bool keep[W];
-#pragma unroll
-                    for (int c = 0; c < W; ++c) {
-                        keep[c] = false;
-                        if (c < n) {
-                            const int ch = rr[c];
-                            if (ch >= 0) {
-                                if (next == 0) next = ch;
-                                else keep[c] = true;
-                            } else if (L.pend == 0) {
-                                L.pend = ch;
-#ifdef SBR_PARK2
-                            } else if (L.pend2 == 0) {
-                                L.pend2 = ch;
-#endif
-                            } else {
-                                keep[c] = true;
-                            }
-                        }
-                    }
-#pragma unroll
-                    for (int c = W - 1; c >= 0; --c)
-                        if (keep[c]) push_entry(stack, L, rr[c], tt[c]);
-                    if (next != 0) L.ref = next;
-                    else have = pop_next(stack, L);
-#else
 #pragma unroll
                     for (int c = W - 1; c >= 1; --c)   // farther hits first: nearest pops first
                         if (c < n) push_entry(stack, L, rr[c], tt[c]);
                     L.ref = rr[0];
-#endif
                 } else {
                     have = pop_next(stack, L);
                 }
