@@ -1028,7 +1028,7 @@ static RasterArgs raster_args(const sbr_bvh *bvh, const GridDev *grids, const in
 // SBR_BIG_CAP (tests) shrinks it to force the overflow path
 static cudaError_t attach_big_queue(sbr_ctx *ctx, RasterArgs &ra)
 {
-    size_t cap = (size_t)1 << 22;
+    size_t cap = (size_t)1 << 24;   // 16M chunks (256 MB): C5 needs ~3.7M
     if (const char *s = getenv("SBR_BIG_CAP")) {
         const long long v = atoll(s);
         if (v >= 1 && v < (long long)cap) cap = (size_t)v;
@@ -1436,7 +1436,7 @@ static int run_units(sbr_ctx *ctx, const sbr_bvh *bvh, const std::vector<UnitDev
                            raster ? ctx->worklist.p : nullptr,
                            raster ? ctx->chunk_hits.p : nullptr, slots / kChunk, ctx->k2.p, nk,
                            ctx->dkturn, ctx->gpow.p, cfg.max_bounces, ctx->chunk_part.p,
-                           diag_dev, ctx->bad.p, st, ctx->stats()));
+                           diag_dev, ctx->bad.p, ctx->counter.p + 5, st, ctx->stats()));
         if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev[2], st));
         CUDA_TRY(launch_seg_reduce(ctx->chunk_part.p, ctx->units.p, (int)batch.size(), nk,
                                    seg_dev, st, ctx->stats()));
@@ -1963,8 +1963,8 @@ extern "C" int sbr_accumulate(sbr_ctx *ctx, const uint8_t *valid, const double *
                                      ctx->stats()));
     CUDA_TRY(launch_po(ctx->slots.p, ctx->units.p, (int)nseg, nullptr, nullptr,
                        slots_used / kChunk, ctx->k2.p, nk,
-                       ctx->dkturn, ctx->gpow.p, maxb, ctx->chunk_part.p, ctx->diag.p, ctx->bad.p, st,
-                       ctx->stats()));
+                       ctx->dkturn, ctx->gpow.p, maxb, ctx->chunk_part.p, ctx->diag.p, ctx->bad.p,
+                       ctx->counter.p + 5, st, ctx->stats()));
     CUDA_TRY(launch_seg_reduce(ctx->chunk_part.p, ctx->units.p, (int)nseg, nk, ctx->seg_part.p, st,
                                ctx->stats()));
     sbr_grid g;

@@ -257,7 +257,9 @@ k_po(SlotRec *__restrict__ slots, const UnitDev *__restrict__ units, int n_units
     // ---- PO terms ----
     const int M = s_total;
     const int G = (nk + FPT - 1) / FPT;        // frequency groups
-    const int wpg = G >= kPoWarps ? 1 : kPoWarps / G;   // warps per group
+    // warps per group; one wavenumber: one warp (lane m mod 32 sums the m-th
+    // selected record -- the sum k_po_list forms in list mode)
+    const int wpg = (G >= kPoWarps || FPT == 1) ? 1 : kPoWarps / G;
     const int passes = (G + kPoWarps - 1) / kPoWarps;
     for (int pass = 0; pass < passes; ++pass) {
         int grp, sub;
@@ -352,6 +354,159 @@ k_po(SlotRec *__restrict__ slots, const UnitDev *__restrict__ units, int n_units
         }
         __syncthreads();
     }
+}
+
+// ---------------------------------------------------------------------------
+// PO over the hit list (raster mode, one wavenumber): one warp per chunk
+// ---------------------------------------------------------------------------
+// After the raster pass a chunk's only records with anything to integrate
+// are its primary hits, which the trace kernel wrote contiguously over the
+// chunk's run of the hit list (chunk_hits).  A warp integrates one chunk
+// with no block barriers and no full-chunk staging: the m-th SELECTED record
+// of the chunk (slot order) goes to lane m mod 32 (a 32-entry shared-memory
+// hand-off per batch of 32 records), each lane sums its terms in order in
+// FP64, and a fixed xor-shuffle tree gives the partial -- exactly the sum
+// k_po forms for the same chunk (one warp per wavenumber group there), so
+// list and slot modes agree bit for bit.  Warps pull runs of kPoSuper
+// consecutive chunks; the per-grid diagnostics (valid rays, queries, max
+// bounce, bounce histogram) accumulate per warp and are flushed when the
+// grid changes.
+constexpr int kPoListThreads = 256;
+constexpr int kPoListWarps = kPoListThreads / 32;
+constexpr int kPoSuper = 16;
+
+__global__ void __launch_bounds__(kPoListThreads)
+k_po_list(const UnitDev *__restrict__ units, int n_units, const uint4 *__restrict__ list,
+          const uint2 *__restrict__ chunk_hits, int64_t n_chunks,
+          const double *__restrict__ kturn, const double *__restrict__ gpow, int max_bounces,
+          double2 *__restrict__ chunk_part, int64_t *__restrict__ diag,
+          unsigned long long *__restrict__ bad, unsigned long long *__restrict__ counter)
+{
+    __shared__ unsigned int s_hist[kPoListWarps][kMaxHist];
+    __shared__ double2 xfer[kPoListWarps][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const int nb = max_bounces + 1;
+    const int64_t dstride = 3 + nb;
+    const double kk = __ldg(&kturn[0]);
+    const SlotRec *recs = reinterpret_cast<const SlotRec *>(list);
+    for (int b = lane; b < kMaxHist; b += 32) s_hist[warp][b] = 0u;
+    __syncwarp();
+    int cur_grid = -1;
+    unsigned long long acc_q = 0;
+    unsigned int acc_valid = 0, acc_maxb = 0;
+    auto flush = [&]() {
+        unsigned long long q = acc_q;
+        unsigned int v = acc_valid, m = acc_maxb;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            q += __shfl_xor_sync(0xffffffffu, q, o);
+            v += __shfl_xor_sync(0xffffffffu, v, o);
+            m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+        }
+        __syncwarp();
+        if (cur_grid >= 0 && diag) {
+            int64_t *dg = diag + (int64_t)cur_grid * dstride;
+            if (lane == 0) {
+                if (v) atomicAdd((unsigned long long *)&dg[0], (unsigned long long)v);
+                if (q) atomicAdd((unsigned long long *)&dg[1], q);
+                atomicMax((unsigned long long *)&dg[2], (unsigned long long)m);
+            }
+            for (int b = lane; b < nb && b < kMaxHist; b += 32)
+                if (s_hist[warp][b])
+                    atomicAdd((unsigned long long *)&dg[3 + b], (unsigned long long)s_hist[warp][b]);
+        }
+        __syncwarp();
+        for (int b = lane; b < kMaxHist; b += 32) s_hist[warp][b] = 0u;
+        __syncwarp();
+        acc_q = 0;
+        acc_valid = 0;
+        acc_maxb = 0;
+    };
+    while (true) {
+        unsigned long long got = 0;
+        if (lane == 0) got = atomicAdd(counter, (unsigned long long)kPoSuper);
+        const int64_t c0 = (int64_t)__shfl_sync(0xffffffffu, got, 0);
+        if (c0 >= n_chunks) break;
+        const int64_t c1 = c0 + kPoSuper < n_chunks ? c0 + kPoSuper : n_chunks;
+        for (int64_t chunk = c0; chunk < c1; ++chunk) {
+            const int64_t slot0 = chunk * kChunk;
+            const int ui = find_unit(units, n_units, slot0);
+            const UnitDev U = units[ui];
+            if (U.grid != cur_grid) {
+                flush();
+                cur_grid = U.grid;
+            }
+            const uint2 run = __ldg(&chunk_hits[chunk]);
+            if (lane == 0) {   // the chunk's primary misses: one query each
+                const int64_t first_r = U.ray_begin + (slot0 - U.slot_base);
+                int64_t real = U.ray_end - first_r;
+                real = real < 0 ? 0 : (real > kChunk ? kChunk : real);
+                acc_q += (unsigned long long)(real - (int64_t)run.y);
+            }
+            const int nrec = (int)run.y;
+            double sred = 0.0, cred = 0.0;
+            int m_base = 0;   // selected records handed out so far
+            for (int base = 0; base < nrec; base += 32) {
+                const int e = base + lane;
+                SlotRec r;
+                if (e < nrec) {
+                    r = recs[run.x + e];
+                } else {
+                    r.R = 0.0; r.cosv = 0.f; r.meta = 0u;
+                }
+                const unsigned b = r.meta & kMetaBounceMask;
+                if (r.meta & kMetaActive) {
+                    acc_q += b + 1;
+                    acc_maxb = max(acc_maxb, b);
+                }
+                const bool v = (r.meta & kMetaValid) != 0;
+                acc_valid += v ? 1u : 0u;
+                {   // bounce histogram: one shared atomic per distinct value
+                    const unsigned key = v ? b : 0xffffffffu;
+                    const unsigned peers = __match_any_sync(0xffffffffu, key);
+                    if (v && lane == __ffs(peers) - 1) {
+                        if (b < (unsigned)kMaxHist)
+                            atomicAdd(&s_hist[warp][b], (unsigned)__popc(peers));
+                        else if (diag)
+                            atomicAdd((unsigned long long *)&diag[(int64_t)U.grid * dstride + 3 + b],
+                                      (unsigned long long)__popc(peers));
+                    }
+                }
+                const bool sel = (r.meta & kMetaSel) != 0;
+                const unsigned bal = __ballot_sync(0xffffffffu, sel);
+                const int cnt = __popc(bal);
+                if (sel) {
+                    const double w = 2.0 * (double)r.cosv * __ldg(&gpow[b]);
+                    if (!isfinite(r.R) || !isfinite(w)) {
+                        const int64_t sl = slot0 + ((r.meta >> kMetaOffShift) & (kChunk - 1));
+                        atomicMin(bad, (unsigned long long)(U.ray_begin + (sl - U.slot_base)));
+                    }
+                    xfer[warp][(m_base + __popc(bal & lt)) & 31] = make_double2(r.R, w);
+                }
+                __syncwarp();
+                if (((lane - m_base) & 31) < cnt) {
+                    const double2 rw = xfer[warp][lane];
+                    // phase 2 k R in turns, reduced exactly in FP64; FP64
+                    // sincospi (2 pi folded in), FP64 lane sums (as k_po)
+                    const double tau = kk * rw.x;
+                    double sn, cs;
+                    sincospi(2.0 * (tau - rint(tau)), &sn, &cs);
+                    sred = fma(rw.y, sn, sred);
+                    cred = fma(rw.y, cs, cred);
+                }
+                __syncwarp();
+                m_base += cnt;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                sred += __shfl_xor_sync(0xffffffffu, sred, o);
+                cred += __shfl_xor_sync(0xffffffffu, cred, o);
+            }
+            if (lane == 0) chunk_part[chunk] = make_double2(0.0 + sred, 0.0 + cred);
+        }
+    }
+    flush();
 }
 
 // ---------------------------------------------------------------------------
@@ -725,7 +880,8 @@ cudaError_t launch_po(SlotRec *d_slots, const UnitDev *d_units, int n_units,
                       int64_t n_chunks, const double *d_k2, int nk, double dkturn,
                       const double *d_gpow,
                       int max_bounces, double2 *d_chunk_part, int64_t *d_diag,
-                      unsigned long long *d_bad, cudaStream_t st, const LaunchStats &ls)
+                      unsigned long long *d_bad, unsigned long long *d_counter,
+                      cudaStream_t st, const LaunchStats &ls)
 {
     if (n_chunks <= 0) return cudaSuccess;
     dim3 grid((unsigned)n_chunks);
@@ -737,10 +893,19 @@ cudaError_t launch_po(SlotRec *d_slots, const UnitDev *d_units, int n_units,
     k_po<F, R><<<grid, kPoThreads, 0, st>>>(d_slots, d_units, n_units, d_list, d_chunk_hits, \
                                             d_k2, nk, dkturn, d_gpow, max_bounces,          \
                                             d_chunk_part, d_diag, d_bad)
-    if (nk >= 8) { if (rot) SBR_PO(8, true); else SBR_PO(8, false); }
-    else if (nk >= 4) { if (rot) SBR_PO(4, true); else SBR_PO(4, false); }
-    else if (nk >= 2) { if (rot) SBR_PO(2, true); else SBR_PO(2, false); }
-    else SBR_PO(1, false);
+    static const bool block_po = getenv("SBR_PO_BLOCK") != nullptr;   // A/B: one block per chunk
+    if (d_list && nk == 1 && !block_po) {
+        cudaError_t e = cudaMemsetAsync(d_counter, 0, sizeof(unsigned long long), st);
+        if (e != cudaSuccess) return e;
+        k_po_list<<<(unsigned)(ls.num_sms * 8), kPoListThreads, 0, st>>>(
+            d_units, n_units, d_list, d_chunk_hits, n_chunks, d_k2, d_gpow, max_bounces,
+            d_chunk_part, d_diag, d_bad, d_counter);
+    } else {
+        if (nk >= 8) { if (rot) SBR_PO(8, true); else SBR_PO(8, false); }
+        else if (nk >= 4) { if (rot) SBR_PO(4, true); else SBR_PO(4, false); }
+        else if (nk >= 2) { if (rot) SBR_PO(2, true); else SBR_PO(2, false); }
+        else SBR_PO(1, false);
+    }
 #undef SBR_PO
     ++*ls.launches;
     return cudaGetLastError();

@@ -273,7 +273,8 @@ cudaError_t launch_po(SlotRec *d_slots, const UnitDev *d_units, int n_units,
                       int64_t n_chunks, const double *d_k2, int nk, double dkturn,
                       const double *d_gpow,
                       int max_bounces, double2 *d_chunk_part, int64_t *d_diag,
-                      unsigned long long *d_bad, cudaStream_t st, const LaunchStats &ls);
+                      unsigned long long *d_bad, unsigned long long *d_counter,
+                      cudaStream_t st, const LaunchStats &ls);
 
 cudaError_t launch_seg_reduce(const double2 *d_chunk_part, const UnitDev *d_units,
                               int n_units, int nk, double2 *d_seg_part, cudaStream_t st,

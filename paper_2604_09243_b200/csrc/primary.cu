@@ -103,6 +103,7 @@ struct RasterSetup {
     long long i0, j0, rows, count;
     int cols;
     int trans, wide;
+    int span;        // chunk by lines (32 per chunk), walking each line's span
     double f0, fi, fj, g0, gi, gj, eu, ev, h, err;
 };
 
@@ -202,6 +203,7 @@ __device__ __forceinline__ RasterSetup raster_setup(const TriF64 &T, const GridD
           isfinite(S.fj) && isfinite(S.gi) && isfinite(S.gj)))
         return S;   // non-finite geometry: the exact test accepts nothing finite
     double alo, ahi, blo, bhi;
+    double area = INFINITY;   // of the candidate region, in cells
     // ---- well-conditioned: the region's vertices by Cramer's rule --------
     const double det2 = S.fi * S.gj - S.fj * S.gi;
     const double kd = fabs(S.fi * S.gj) + fabs(S.fj * S.gi);
@@ -233,6 +235,10 @@ __device__ __forceinline__ RasterSetup raster_setup(const TriF64 &T, const GridD
         }
         if (emax <= 0.25 && isfinite(alo) && isfinite(ahi) && isfinite(blo) && isfinite(bhi)) {
             S.wide = 0;
+            // the region is the (F, G) triangle with legs H + Eu + Ev, mapped
+            // to cells through a Jacobian of det2
+            const double leg = S.h + S.eu + S.ev;
+            area = 0.5 * leg * leg * ainv2;
             alo -= 1e-9 * (1.0 + fabs(alo)); ahi += 1e-9 * (1.0 + fabs(ahi));
             blo -= 1e-9 * (1.0 + fabs(blo)); bhi += 1e-9 * (1.0 + fabs(bhi));
         }
@@ -252,7 +258,13 @@ __device__ __forceinline__ RasterSetup raster_setup(const TriF64 &T, const GridD
     S.j0 = j0;
     S.rows = rows;
     S.cols = (int)cols;
-    S.trans = S.wide && cols < rows;
+    // Span mode: a region much smaller than its bounding box (the long thin
+    // sliver of a nearly edge-on triangle, or a WIDE strip) is chunked by
+    // lines and walked span by span -- bounding-box chunks would enumerate
+    // (and queue) the whole box, up to hundreds of millions of cells
+    S.span = S.wide ||
+             (double)rows * (double)cols > 4.0 * (area + (double)rows + (double)cols + 256.0);
+    S.trans = S.span && cols < rows;
     S.count = rows * cols;
     S.inv = __drcp_rn(S.P.det);                 // == IEEE 1.0 / det
     return S;
@@ -285,6 +297,17 @@ __device__ __forceinline__ void trim_owned(RasterSetup &S, const GridDev &G, con
     S.rows = b - a + 1;
     S.trans = S.trans && S.cols < S.rows;
     S.count = S.rows * S.cols;
+}
+
+// chunks of a queued pair: span mode = 32 lines each, else kBigChunk cells
+// of the bounding box in line-major order
+__device__ __forceinline__ long long span_lines(const RasterSetup &S)
+{
+    return S.trans ? (long long)S.cols : S.rows;
+}
+__device__ __forceinline__ long long big_chunks(const RasterSetup &S)
+{
+    return S.span ? (span_lines(S) + 31) / 32 : (S.count + kBigChunk - 1) / kBigChunk;
 }
 
 __device__ __forceinline__ void split_cell(long long local, int cols, long long &li, long long &lj)
@@ -393,16 +416,25 @@ k_raster(RasterArgs a, int64_t ntri_pad)
             count = S.count;
             if (S.wide && count && a.stats) atomicAdd(a.stats + 1, 1ULL);
             if (count > kBigTri && a.big) {
-                const long long nch = (count + kBigChunk - 1) / kBigChunk;
+                const long long nch = big_chunks(S);
                 // sharded / partial batches: queue only chunks whose rows touch
                 // a segment of this launch (ray-tile shards skip 7/8 of them);
                 // column-major (trans) chunks span every row: always queued
                 const int64_t *segs = a.seg_slot + __ldg(&a.seg_base[g]);
                 auto owned = [&](long long c) {
                     if (!a.sparse || S.trans) return true;
-                    const long long c1 = (c + 1) * kBigChunk < count ? (c + 1) * kBigChunk : count;
-                    const int64_t r0 = (S.i0 + c * kBigChunk / S.cols) * G.n_v + S.j0;
-                    const int64_t r1 = (S.i0 + (c1 - 1) / S.cols) * G.n_v + S.j0 + S.cols - 1;
+                    int64_t r0, r1;
+                    if (S.span) {
+                        const long long la = 32 * c;
+                        const long long lb = la + 31 < S.rows - 1 ? la + 31 : S.rows - 1;
+                        r0 = (S.i0 + la) * G.n_v + S.j0;
+                        r1 = (S.i0 + lb) * G.n_v + S.j0 + S.cols - 1;
+                    } else {
+                        const long long c1 =
+                            (c + 1) * kBigChunk < count ? (c + 1) * kBigChunk : count;
+                        r0 = (S.i0 + c * kBigChunk / S.cols) * G.n_v + S.j0;
+                        r1 = (S.i0 + (c1 - 1) / S.cols) * G.n_v + S.j0 + S.cols - 1;
+                    }
                     for (int64_t q = r0 / kSegRays; q <= r1 / kSegRays; ++q)
                         if (__ldg(&segs[q]) != kNoSlot) return true;
                     return false;
@@ -420,7 +452,9 @@ k_raster(RasterArgs a, int64_t ntri_pad)
                 } else {
                     // the reservation straddles the queue's end: publish no
                     // work in its in-range part (k_raster_big walks every
-                    // entry below min(nbig, cap)) and walk the triangle here
+                    // entry below min(nbig, cap)) and walk the triangle's box
+                    // here -- exact, but slow for span-mode regions (the
+                    // queue holds 16M chunks; C5 needs ~3.7M)
                     for (unsigned long long w = at; w < cap; ++w) a.big[w] = make_int4(-1, 0, 0, 0);
                     if (a.stats) atomicAdd(a.stats + 2, 1ULL);
                 }
@@ -504,12 +538,22 @@ k_raster_big(RasterArgs a)
         RasterSetup S = raster_setup(load_tri<STORAGE>(a.B, it.y), G, a.row_lo, a.row_hi);
         const int64_t *seg = a.seg_slot + __ldg(&a.seg_base[g]);
         if (a.sparse) trim_owned(S, G, seg);
-        const long long c0 = (long long)it.z * kBigChunk;
-        const long long c1 = c0 + kBigChunk < S.count ? c0 + kBigChunk : S.count;
-        if (c0 >= c1) continue;
         const long long width = S.trans ? S.rows : (long long)S.cols;   // cells per line
         const long long l0 = S.trans ? S.j0 : S.i0, m0 = S.trans ? S.i0 : S.j0;
-        const long long line_a = c0 / width, line_b = (c1 - 1) / width;
+        long long c0, c1, line_a, line_b;
+        if (S.span) {   // 32 whole lines
+            line_a = 32LL * it.z;
+            line_b = line_a + 31 < span_lines(S) - 1 ? line_a + 31 : span_lines(S) - 1;
+            if (line_a > line_b) continue;
+            c0 = line_a * width;
+            c1 = (line_b + 1) * width;
+        } else {
+            c0 = (long long)it.z * kBigChunk;
+            c1 = c0 + kBigChunk < S.count ? c0 + kBigChunk : S.count;
+            if (c0 >= c1) continue;
+            line_a = c0 / width;
+            line_b = (c1 - 1) / width;
+        }
         for (long long lbase = line_a; lbase <= line_b; lbase += 32) {
             const long long li = lbase + lane;
             long long ml = 0, mr = -1;
