@@ -163,6 +163,10 @@ int sbr_probe_l2_bandwidth(sbr_ctx *ctx, int64_t bytes, int32_t reps, double *gb
 /* Instrumented builds only (-DSBR_TRACE_STATS): read and clear n <= 24
  * lane-state counters of the trace kernel (zeros otherwise). */
 int sbr_ctx_debug_counters(sbr_ctx *ctx, int64_t *out, int32_t n);
+/* Device allocations the library holds right now (all contexts, meshes,
+ * trees, scratch): for leak checks -- destroying every handle returns both
+ * counts to zero. */
+int sbr_debug_live_allocations(int64_t *count, int64_t *bytes);
 
 /* ---- mesh: geometry.py:130-180 mesh_from_soup output -> device --------- */
 int sbr_mesh_create(sbr_ctx *ctx, const double *v0, const double *v1,

@@ -10,6 +10,7 @@ from __future__ import annotations
 import ctypes
 import os
 import threading
+import weakref
 
 import numpy as np
 
@@ -83,6 +84,7 @@ _SIGS = {
     "sbr_ctx_raster_counters": (ctypes.c_int, [c_vp, c_vp]),
     "sbr_probe_l2_bandwidth": (ctypes.c_int, [c_vp, c_i64, c_i32, ctypes.POINTER(c_dbl)]),
     "sbr_ctx_debug_counters": (ctypes.c_int, [c_vp, c_vp, c_i32]),
+    "sbr_debug_live_allocations": (ctypes.c_int, [ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),
     "sbr_mesh_create": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i32,
                                        ctypes.POINTER(c_vp)]),
     "sbr_mesh_destroy": (ctypes.c_int, [c_vp]),
@@ -307,6 +309,44 @@ class Context:
 
 _contexts: dict[int, Context] = {}
 _ctx_lock = threading.Lock()
+
+
+def live_allocations() -> tuple:
+    """(count, bytes) of device allocations the library holds right now."""
+    lib = load_library()
+    n, b = c_i64(), c_i64()
+    check(lib.sbr_debug_live_allocations(ctypes.byref(n), ctypes.byref(b)))
+    return int(n.value), int(b.value)
+
+
+# owning Python handles of device meshes / trees (geometry._DeviceMesh,
+# bvh._DeviceBvh): shutdown() releases whatever is still alive
+_handles: "weakref.WeakSet" = weakref.WeakSet()
+
+
+def register_handle(obj) -> None:
+    _handles.add(obj)
+
+
+def shutdown() -> None:
+    """Destroy every device object the library still holds -- trees, then
+    meshes (any Python wrapper left alive is released and becomes unusable)
+    -- and every device context with its scratch and streams.  Used by the
+    leak check (scripts/sanitize_workload.py); afterwards
+    live_allocations() is (0, 0)."""
+    import gc
+    gc.collect()
+    live = list(_handles)
+    for order in (0, 1):          # trees before the meshes they reference
+        for h in live:
+            if getattr(h, "is_tree", False) == (order == 0):
+                h.release()
+    with _ctx_lock:
+        for dev, ctx in list(_contexts.items()):
+            ctx.synchronize()
+            check(ctx.lib.sbr_ctx_destroy(ctx.handle), "sbr_ctx_destroy")
+            ctx.handle = None
+            del _contexts[dev]
 
 
 def current_device() -> int:

@@ -68,15 +68,22 @@ class Hit(NamedTuple):
 
 
 class _DeviceBvh:
+    is_tree = True
+
     def __init__(self, ctx, handle, mesh_dev):
         self.ctx = ctx
         self.handle = handle
         self.mesh_dev = mesh_dev   # keeps the device mesh alive
+        nat.register_handle(self)
+
+    def release(self):
+        if self.handle:
+            self.ctx.lib.sbr_bvh_destroy(self.handle)
+            self.handle = None
 
     def __del__(self):
         try:
-            if self.handle:
-                self.ctx.lib.sbr_bvh_destroy(self.handle)
+            self.release()
         except Exception:  # pragma: no cover
             pass
 

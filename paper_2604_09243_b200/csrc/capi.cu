@@ -8,6 +8,7 @@
 #include <cstring>
 #include <mutex>
 #include <algorithm>
+#include <atomic>
 #include <string>
 #include <thread>
 #include <vector>
@@ -1150,6 +1151,7 @@ static int trace_full_common(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *
         g.spacing = grid->spacing;
         g.n_v = grid->n_v;
         g.n_rays = n_grid;
+        grid_derive(g);
         CUDA_TRY(dg.alloc(1));
         CUDA_TRY(cudaMemcpyAsync(dg.p, &g, sizeof(g), cudaMemcpyHostToDevice, st));
     } else {
@@ -1475,6 +1477,7 @@ static int upload_grids(sbr_ctx *ctx, const sbr_grid *grids, int ngrids)
         g[i].spacing = grids[i].spacing;
         g[i].n_v = grids[i].n_v;
         g[i].n_rays = grids[i].n_u * grids[i].n_v;
+        grid_derive(g[i]);
     }
     CUDA_TRY(ctx->grids.reserve(ngrids));
     CUDA_TRY(cudaMemcpyAsync(ctx->grids.p, g.data(), sizeof(GridDev) * ngrids,
@@ -2066,6 +2069,22 @@ extern "C" int sbr_probe_l2_bandwidth(sbr_ctx *ctx, int64_t bytes, int32_t reps,
 
 // Instrumented builds (-DSBR_TRACE_STATS) accumulate lane-state counters in
 // counter[8..31]; this reads and clears them (all zero in normal builds).
+static std::atomic<int64_t> g_live_allocs{0}, g_live_bytes{0};
+
+void sbr::count_alloc(int64_t bytes)
+{
+    g_live_allocs += bytes >= 0 ? 1 : -1;
+    g_live_bytes += bytes;
+}
+
+extern "C" int sbr_debug_live_allocations(int64_t *count, int64_t *bytes)
+{
+    REQUIRE(count && bytes, "NULL argument");
+    *count = g_live_allocs.load();
+    *bytes = g_live_bytes.load();
+    return SBR_OK;
+}
+
 extern "C" int sbr_ctx_debug_counters(sbr_ctx *ctx, int64_t *out, int32_t n)
 {
     REQUIRE(ctx && out && n >= 0 && n <= 24, "bad arguments");

@@ -16,17 +16,21 @@ namespace sbr {
 // scenes).  Without a context on the device, plain cudaMalloc/cudaFree.
 cudaStream_t alloc_stream(int device);   // capi.cu; nullptr if no context
 
+void count_alloc(int64_t bytes);        // capi.cu: live-allocation counters
 inline cudaError_t dev_alloc(void **p, size_t bytes, int &device)
 {
     cudaGetDevice(&device);
     cudaStream_t s = alloc_stream(device);
-    return s ? cudaMallocAsync(p, bytes, s) : cudaMalloc(p, bytes);
+    const cudaError_t e = s ? cudaMallocAsync(p, bytes, s) : cudaMalloc(p, bytes);
+    if (e == cudaSuccess) count_alloc((int64_t)bytes);
+    return e;
 }
-inline void dev_free(void *p, int device)
+inline void dev_free(void *p, int device, size_t bytes)
 {
     cudaStream_t s = alloc_stream(device);
     if (s) cudaFreeAsync(p, s);
     else cudaFree(p);
+    count_alloc(-(int64_t)bytes);
 }
 
 // Owning device buffer (RAII, move-only).
@@ -76,7 +80,7 @@ struct DevBuf {
     cudaError_t status() const { return err; }
     void release()
     {
-        if (p) dev_free(p, device);
+        if (p) dev_free(p, device, n * sizeof(T));
         p = nullptr;
         n = 0;
     }

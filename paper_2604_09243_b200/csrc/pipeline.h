@@ -18,7 +18,23 @@ struct GridDev {
     double spacing;
     int64_t n_v;
     int64_t n_rays;
+    // derived on the host (grid_derive): rows, and per axis the raster's
+    // magnitude bound |corner| + n_u ds |u| + n_v ds |v| (primary.cu)
+    int64_t n_u;
+    double rbound[3];
 };
+
+inline void grid_derive(GridDev &g)
+{
+    g.n_u = g.n_v > 0 ? g.n_rays / g.n_v : 0;
+    const double su = (double)g.n_u * g.spacing, sv = (double)g.n_v * g.spacing;
+    for (int a = 0; a < 3; ++a) {
+        const double c = g.corner[a] < 0 ? -g.corner[a] : g.corner[a];
+        const double u = g.u[a] < 0 ? -g.u[a] : g.u[a];
+        const double v = g.v[a] < 0 ? -g.v[a] : g.v[a];
+        g.rbound[a] = (c + su * u + sv * v) * (1.0 + 1e-12);
+    }
+}
 
 // Unit of work: rays [ray_begin, ray_end) of grid `grid` (segment `seg`),
 // occupying slots [slot_base, slot_base + roundup(len, kChunk)) of a batch.

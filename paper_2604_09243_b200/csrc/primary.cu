@@ -169,7 +169,7 @@ __device__ __forceinline__ RasterSetup raster_setup(const TriF64 &T, const GridD
     S.count = 0;
     S.P = tri_dir(T, G.k[0], G.k[1], G.k[2]);
     if (S.P.det == 0.0) return S;
-    const int64_t n_v = G.n_v, n_u = G.n_rays / n_v;
+    const int64_t n_v = G.n_v, n_u = G.n_u;
     const double dx = G.k[0], dy = G.k[1], dz = G.k[2];
     const double sg = S.P.det > 0.0 ? 1.0 : -1.0;
     const double D = fabs(S.P.det);
@@ -177,10 +177,9 @@ __device__ __forceinline__ RasterSetup raster_setup(const TriF64 &T, const GridD
     const double rx = T.e1y * dz - T.e1z * dy;
     const double ry = T.e1z * dx - T.e1x * dz;
     const double rz = T.e1x * dy - T.e1y * dx;
-    const double su = (double)n_u * G.spacing, sv = (double)n_v * G.spacing;
-    const double Rx = fabs(G.corner[0]) + fabs(T.ax) + su * fabs(G.u[0]) + sv * fabs(G.v[0]);
-    const double Ry = fabs(G.corner[1]) + fabs(T.ay) + su * fabs(G.u[1]) + sv * fabs(G.v[1]);
-    const double Rz = fabs(G.corner[2]) + fabs(T.az) + su * fabs(G.u[2]) + sv * fabs(G.v[2]);
+    const double Rx = G.rbound[0] + fabs(T.ax);
+    const double Ry = G.rbound[1] + fabs(T.ay);
+    const double Rz = G.rbound[2] + fabs(T.az);
     const double Mp = fabs(S.P.px) * Rx + fabs(S.P.py) * Ry + fabs(S.P.pz) * Rz;
     const double Mr = (fabs(T.e1y * dz) + fabs(T.e1z * dy)) * Rx +
                       (fabs(T.e1z * dx) + fabs(T.e1x * dz)) * Ry +
@@ -205,53 +204,52 @@ __device__ __forceinline__ RasterSetup raster_setup(const TriF64 &T, const GridD
     double alo, ahi, blo, bhi;
     double area = INFINITY;   // of the candidate region, in cells
     // ---- well-conditioned: the region's vertices by Cramer's rule --------
+    // vertex 0 solves M x = (-Eu - f0, -Ev - g0) with M = [fi fj; gi gj];
+    // vertices 1 and 2 add M^-1 (0, L) and M^-1 (L, 0), L = H + Eu + Ev (the
+    // region's legs in (F, G)).  One bound per axis covers all three: the
+    // first-order error of the 2x2 solve (relative error of det2 <= 2e kd /
+    // |det2|, numerators a few ulp of their magnitude sums), the rounded
+    // reciprocal and the vertex additions -- each x4 or more
     const double det2 = S.fi * S.gj - S.fj * S.gi;
     const double kd = fabs(S.fi * S.gj) + fabs(S.fj * S.gi);
     S.wide = 1;
     if (fabs(det2) > 1e-6 * kd) {
-        const double cf[3] = {-S.eu, -S.eu, S.h + S.ev};
-        const double cg[3] = {-S.ev, S.h + S.eu, -S.ev};
-        alo = blo = INFINITY;      // running minima
-        ahi = bhi = -INFINITY;     // running maxima
-        double emax = 0.0;
-        // one division per pair: x * fl(1/det2) is within 2 ulp of x / det2,
-        // covered by the 4e|a| term added to each bound below
+        const double L = S.h + S.eu + S.ev;
         const double inv2 = 1.0 / det2, ainv2 = fabs(inv2);
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            const double nf = cf[k] - S.f0, ng = cg[k] - S.g0;
-            const double a = (nf * S.gj - S.fj * ng) * inv2;
-            const double b = (S.fi * ng - S.gi * nf) * inv2;
-            // first-order error bound of the 2x2 solve, x4 (relative error of
-            // det2 <= 2e kd/|det2|; numerators carry their own few ulp)
-            const double mf = fabs(cf[k]) + fabs(S.f0), mg = fabs(cg[k]) + fabs(S.g0);
-            const double ea = 16.0 * kEps * (fabs(a) * kd + mf * fabs(S.gj) + fabs(S.fj) * mg) *
-                              ainv2 * (1.0 + 8.0 * kEps) + 4.0 * kEps * fabs(a);
-            const double eb = 16.0 * kEps * (fabs(b) * kd + mg * fabs(S.fi) + fabs(S.gi) * mf) *
-                              ainv2 * (1.0 + 8.0 * kEps) + 4.0 * kEps * fabs(b);
-            emax = fmax(emax, fmax(ea, eb));
-            alo = fmin(alo, a - ea); ahi = fmax(ahi, a + ea);
-            blo = fmin(blo, b - eb); bhi = fmax(bhi, b + eb);
-        }
-        if (emax <= 0.25 && isfinite(alo) && isfinite(ahi) && isfinite(blo) && isfinite(bhi)) {
+        const double nf = -S.eu - S.f0, ng = -S.ev - S.g0;
+        const double a0 = (nf * S.gj - S.fj * ng) * inv2;
+        const double b0 = (S.fi * ng - S.gi * nf) * inv2;
+        const double La = L * inv2;
+        const double a1 = a0 - S.fj * La, b1 = b0 + S.fi * La;
+        const double a2 = a0 + S.gj * La, b2 = b0 - S.gi * La;
+        const double amax = fmax(fmax(fabs(a0), fabs(a1)), fabs(a2));
+        const double bmax = fmax(fmax(fabs(b0), fabs(b1)), fabs(b2));
+        const double mf = fabs(S.f0) + S.eu + L, mg = fabs(S.g0) + S.ev + L;
+        const double ea = 16.0 * kEps * ((amax * kd + mf * fabs(S.gj) + fabs(S.fj) * mg) *
+                                             ainv2 * (1.0 + 16.0 * kEps) + 2.0 * amax);
+        const double eb = 16.0 * kEps * ((bmax * kd + mg * fabs(S.fi) + fabs(S.gi) * mf) *
+                                             ainv2 * (1.0 + 16.0 * kEps) + 2.0 * bmax);
+        if (fmax(ea, eb) <= 0.25 && amax < 1e300 && bmax < 1e300) {   // NaN fails too
             S.wide = 0;
-            // the region is the (F, G) triangle with legs H + Eu + Ev, mapped
-            // to cells through a Jacobian of det2
-            const double leg = S.h + S.eu + S.ev;
-            area = 0.5 * leg * leg * ainv2;
-            alo -= 1e-9 * (1.0 + fabs(alo)); ahi += 1e-9 * (1.0 + fabs(ahi));
-            blo -= 1e-9 * (1.0 + fabs(blo)); bhi += 1e-9 * (1.0 + fabs(bhi));
+            // the region is the (F, G) triangle with legs L, mapped to cells
+            // through a Jacobian of det2
+            area = 0.5 * L * L * ainv2;
+            const double wa = ea + 1e-9 * (1.0 + amax), wb = eb + 1e-9 * (1.0 + bmax);
+            alo = fmin(fmin(a0, a1), a2) - wa;
+            ahi = fmax(fmax(a0, a1), a2) + wa;
+            blo = fmin(fmin(b0, b1), b2) - wb;
+            bhi = fmax(fmax(b0, b1), b2) + wb;
         }
     }
     if (S.wide && !wide_region(S, n_u, n_v, alo, ahi, blo, bhi)) return S;
     if (!(ahi >= 0.0 && bhi >= 0.0 && alo <= (double)(n_u - 1) && blo <= (double)(n_v - 1)))
         return S;                               // outside the aperture (or non-finite)
-    int64_t i0 = alo <= 0.0 ? 0 : (int64_t)ceil(alo);
-    int64_t i1 = ahi >= (double)(n_u - 1) ? n_u - 1 : (int64_t)floor(ahi);
+    int64_t i0 = alo <= 0.0 ? 0 : __double2ll_ru(alo);
+    int64_t i1 = ahi >= (double)(n_u - 1) ? n_u - 1 : __double2ll_rd(ahi);
     if (i0 < row_lo) i0 = row_lo;               // row window of a partial trace
     if (i1 > row_hi - 1) i1 = row_hi - 1;
-    const int64_t j0 = blo <= 0.0 ? 0 : (int64_t)ceil(blo);
-    const int64_t j1 = bhi >= (double)(n_v - 1) ? n_v - 1 : (int64_t)floor(bhi);
+    const int64_t j0 = blo <= 0.0 ? 0 : __double2ll_ru(blo);
+    const int64_t j1 = bhi >= (double)(n_v - 1) ? n_v - 1 : __double2ll_rd(bhi);
     const int64_t rows = i1 - i0 + 1, cols = j1 - j0 + 1;
     if (rows <= 0 || cols <= 0) return S;
     S.i0 = i0;

@@ -83,14 +83,19 @@ class _DeviceMesh:
                                           nat.ctypes.byref(h)), "sbr_mesh_create")
         self.ctx = ctx
         self.handle = h
+        nat.register_handle(self)
         n = nat.c_i64(); st = nat.c_i32()
         nat.check(ctx.lib.sbr_mesh_info(h, nat.ctypes.byref(n), nat.ctypes.byref(st), None))
         self.storage = int(st.value)
 
+    def release(self):
+        if self.handle:
+            self.ctx.lib.sbr_mesh_destroy(self.handle)
+            self.handle = None
+
     def __del__(self):
         try:
-            if self.handle:
-                self.ctx.lib.sbr_mesh_destroy(self.handle)
+            self.release()
         except Exception:  # pragma: no cover - interpreter shutdown
             pass
 

@@ -626,3 +626,97 @@ def test_slot_reuse_without_memset_is_exact(monkeypatch):
     again("small batches")
     monkeypatch.delenv("SBR_SLOT_BUDGET")
     again("back to one batch")
+
+
+def test_aabb_conservative_over_triangle_hits():
+    """pkg/tests/test_geometry.py:255-272 on the device slab predicate
+    (geometry.py:358-391 restated): every ray that hits a random triangle
+    also hits the triangle's box (2000 triangles, seed 99)."""
+    rng = np.random.default_rng(99)
+    checked = 0
+    for _ in range(2000):
+        verts = rng.uniform(-1, 1, size=(3, 3))
+        normal = np.cross(verts[1] - verts[0], verts[2] - verts[0])
+        if np.linalg.norm(normal) < 1e-9:
+            continue
+        tri = sbr.Triangle(verts[0], verts[1], verts[2], normal / np.linalg.norm(normal))
+        box = sbr.Aabb(verts.min(axis=0), verts.max(axis=0))
+        origin = rng.uniform(-3, 3, size=3)
+        # the reference's random direction, and one aimed at a point of the
+        # triangle (edges and vertices included) so that most rays hit
+        w = rng.dirichlet([0.5, 0.5, 0.5])
+        w[rng.integers(0, 3)] *= rng.integers(0, 2)
+        w /= w.sum()
+        for d in (rng.normal(size=3), w @ verts - origin):
+            d = d / np.linalg.norm(d)
+            hit = sbr.ray_triangle_intersect(origin, d, tri)
+            if hit is not None:
+                inv = np.where(d != 0, 1.0 / np.where(d != 0, d, 1.0), np.inf)
+                box_hit, entry = sbr.ray_aabb_intersect(origin, inv, box)
+                assert box_hit and entry <= hit[0]
+                checked += 1
+    assert checked > 1000
+
+
+@pytest.mark.parametrize("rule", ["sah", "lbvh"])
+def test_fp32_slab_culling_is_conservative(orc, rule):
+    """The hot path culls with FP32 outward-rounded boxes and a padded slab
+    (sbr_device.cuh RayBox / node4_visit).  Stress it where FP32 is weakest:
+    origins 1e2..1e5 scene sizes away, rays aimed at triangle vertices and
+    edge points (grazing the leaf boxes' faces), and rays parallel to box
+    faces.  A single wrongly culled box would lose a hit: the closest hits
+    must equal the brute-force linear scan on every robust ray."""
+    rng = np.random.default_rng(7)
+    n = 2000
+    c = rng.uniform(-1, 1, size=(n, 3))
+    v0 = (c + 0.05 * rng.normal(size=(n, 3))).astype(np.float32).astype(np.float64)
+    v1 = (c + 0.05 * rng.normal(size=(n, 3))).astype(np.float32).astype(np.float64)
+    v2 = (c + 0.05 * rng.normal(size=(n, 3))).astype(np.float32).astype(np.float64)
+    verts = np.stack([v0, v1, v2], axis=1).reshape(-1, 3)      # triangle i = rows 3i..3i+2
+    mesh = sbr.mesh_from_arrays(verts, np.arange(3 * n).reshape(n, 3))
+    m = 6000
+    k = rng.integers(0, n, m)
+    w = rng.dirichlet([0.3, 0.3, 0.3], size=m)
+    w[: m // 3] = np.eye(3)[rng.integers(0, 3, m // 3)]            # vertices
+    w[m // 3: m // 2, 2] = 0.0                                     # edge v0-v1
+    w[m // 3: m // 2] /= w[m // 3: m // 2].sum(1, keepdims=True)
+    target = w[:, :1] * mesh.v0[k] + w[:, 1:2] * mesh.v1[k] + w[:, 2:] * mesh.v2[k]
+    d = rng.normal(size=(m, 3))
+    d[: m // 6, rng.integers(0, 3)] = 0.0                          # parallel to a face pair
+    d /= np.linalg.norm(d, axis=1)[:, None]
+    dist = 10.0 ** rng.uniform(0, 5, size=m)
+    origins = target - dist[:, None] * d
+    tree = sbr.build(mesh, sbr.BuildParams(split_rule=rule))
+    tri, t, _ = sbr.closest_hit_batch(tree, mesh, origins, d)
+    scene = orc.Scene.from_mesh(mesh)
+    btri, bt = orc.brute_force_hits(scene, origins, d)
+    rob = orc.classify_rays(scene, origins, d)
+    assert rob.mean() > 0.8          # vertex / edge aims are near-ties by design
+    assert (btri[rob] >= 0).mean() > 0.5
+    assert np.array_equal(tri[rob], btri[rob])
+    assert np.array_equal(t[rob & (btri >= 0)], bt[rob & (btri >= 0)])
+
+
+def test_device_objects_are_released():
+    """Meshes, trees and the fused solve's results own no device memory
+    after they are dropped (live-allocation counter of the library; the
+    solve scratch is grow-only and stays with the context)."""
+    import gc
+    from paper_2604_09243_b200 import _native as nat
+
+    def cycle():
+        mesh = meshgen.generate_aircraft(density=0.02)
+        for rule in ("sah", "lbvh"):
+            tree = sbr.build(mesh, sbr.BuildParams(split_rule=rule))
+            g = sbr.build_aperture(mesh.aabb, sbr.IncidentDirection(1.2, 0.4), 0.04,
+                                   wavelength=0.2)
+            sbr.solve_grids(tree, mesh, [g], sbr.TraceParams(max_bounces=3), [2 * math.pi / 0.2])
+            sbr.trace_grid(tree, mesh, g, sbr.TraceParams(max_bounces=2), with_ids=True)
+
+    cycle()
+    gc.collect()
+    base = nat.live_allocations()
+    for _ in range(3):
+        cycle()
+        gc.collect()
+        assert nat.live_allocations() == base
