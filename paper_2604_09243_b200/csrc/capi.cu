@@ -105,6 +105,8 @@ struct sbr_ctx {
     DevBuf<unsigned long long> nwork;
     DevBuf<int4> big;                       // raster pass: big-triangle chunk queue
     DevBuf<unsigned long long> nbig;
+    DevBuf<unsigned char> setups;           // raster pass: set-ups of queued triangles
+    DevBuf<unsigned long long> nsetup;
     DevBuf<double> k2, gpow, scale;
     double dkturn = 0.0;         // uniform wavenumber step in turns (0: not uniform)
     DevBuf<double2> amp;
@@ -282,7 +284,8 @@ extern "C" int sbr_ctx_trim(sbr_ctx *ctx)
     ctx->chunk_hits.release();
     ctx->chunk_part.release(); ctx->seg_part.release(); ctx->diag.release();
     ctx->seg_base.release(); ctx->seg_slot.release(); ctx->bgrids.release();
-    ctx->worklist.release(); ctx->big.release(); ctx->amp.release(); ctx->stage.release();
+    ctx->worklist.release(); ctx->big.release(); ctx->setups.release();
+    ctx->amp.release(); ctx->stage.release();
     ctx->ws.buf.release();
     ctx->ws.off = 0;
     ctx->sah = SahWork();
@@ -1019,6 +1022,9 @@ static RasterArgs raster_args(const sbr_bvh *bvh, const GridDev *grids, const in
     r.big = nullptr;
     r.nbig = nullptr;
     r.big_cap = 0;
+    r.setups = nullptr;
+    r.nsetup = nullptr;
+    r.setup_cap = 0;
     r.row_lo = 0;
     r.row_hi = INT64_MAX;
     r.stats = nullptr;
@@ -1040,6 +1046,14 @@ static cudaError_t attach_big_queue(sbr_ctx *ctx, RasterArgs &ra)
     ra.big = ctx->big.p;
     ra.nbig = ctx->nbig.p;
     ra.big_cap = (int64_t)cap;
+    // set-up table: 2M triangles (512 MB; C5 queues ~1M)
+    const size_t scap = (size_t)1 << 21;
+    e = ctx->setups.reserve(scap * kRasterSetupBytes);
+    if (e == cudaSuccess) e = ctx->nsetup.reserve(1);
+    if (e != cudaSuccess) return e;
+    ra.setups = ctx->setups.p;
+    ra.nsetup = ctx->nsetup.p;
+    ra.setup_cap = (int64_t)scap;
     return cudaSuccess;
 }
 

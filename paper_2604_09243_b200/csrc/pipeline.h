@@ -261,14 +261,21 @@ struct RasterArgs {
     PrimHit *prim;
     unsigned long long *counter;   // work counter (zeroed by launch_raster)
     int sparse;                    // some segments of the batch's grids are not in it
-    int4 *big;                     // queue of big-triangle chunks (grid, tri, chunk, -)
+    int4 *big;                     // queue of big-triangle chunks (grid, tri, chunk, setup)
     unsigned long long *nbig;      // its fill counter
     int64_t big_cap;               // its capacity (items beyond it stay in k_raster)
+    // set-ups of queued triangles (kRasterSetupBytes each), computed once in
+    // k_raster and read by every chunk of the triangle (-1 in the queue
+    // entry: table full, the chunk recomputes it)
+    unsigned char *setups;
+    unsigned long long *nsetup;
+    int64_t setup_cap;
     int64_t row_lo, row_hi;        // rows [row_lo, row_hi) only (a partial trace_grid)
     // accumulating counters (may be null): [0] candidate cells tested,
     // [1] WIDE (ill-conditioned) pairs, [2] chunk-queue overflows
     unsigned long long *stats;
 };
+constexpr int kRasterSetupBytes = 256;
 constexpr int64_t kNoSlot = INT64_MIN;   // segment not in this batch / shard
 cudaError_t launch_raster(const RasterArgs &a, cudaStream_t st, const LaunchStats &ls);
 

@@ -106,6 +106,7 @@ struct RasterSetup {
     int span;        // chunk by lines (32 per chunk), walking each line's span
     double f0, fi, fj, g0, gi, gj, eu, ev, h, err;
 };
+static_assert(sizeof(RasterSetup) <= kRasterSetupBytes, "set-up table slot");
 
 // Candidate box of an ill-conditioned (WIDE) pair: the boxes of the two edge
 // strips -Eu <= F <= H + Ev and -Ev <= G <= H + Eu, clipped to the aperture.
@@ -443,9 +444,19 @@ k_raster(RasterArgs a, int64_t ntri_pad)
                     nown ? atomicAdd(a.nbig, (unsigned long long)nown) : 0ULL;
                 const unsigned long long cap = (unsigned long long)a.big_cap;
                 if (at + nown <= cap) {
+                    // publish the set-up once for all of the triangle's chunks
+                    int si = -1;
+                    if (nown > 1 && a.setups) {
+                        const unsigned long long k = atomicAdd(a.nsetup, 1ULL);
+                        if (k < (unsigned long long)a.setup_cap) {
+                            si = (int)k;
+                            *reinterpret_cast<RasterSetup *>(a.setups +
+                                                             (size_t)k * kRasterSetupBytes) = S;
+                        }
+                    }
                     long long w = 0;
                     for (long long c = 0; c < nch; ++c)
-                        if (owned(c)) a.big[at + w++] = make_int4(gl, (int)tri, (int)c, 0);
+                        if (owned(c)) a.big[at + w++] = make_int4(gl, (int)tri, (int)c, si);
                     count = 0;                          // walked by k_raster_big
                 } else {
                     // the reservation straddles the queue's end: publish no
@@ -533,9 +544,15 @@ k_raster_big(RasterArgs a)
         if (it.x < 0) continue;                 // unpublished (overflowed reservation)
         const int g = __ldg(&a.bgrids[it.x]);
         const GridDev &G = a.grids[g];
-        RasterSetup S = raster_setup(load_tri<STORAGE>(a.B, it.y), G, a.row_lo, a.row_hi);
         const int64_t *seg = a.seg_slot + __ldg(&a.seg_base[g]);
-        if (a.sparse) trim_owned(S, G, seg);
+        RasterSetup S;
+        if (it.w >= 0) {   // published by k_raster (already trimmed to owned rows)
+            S = *reinterpret_cast<const RasterSetup *>(a.setups +
+                                                       (size_t)it.w * kRasterSetupBytes);
+        } else {
+            S = raster_setup(load_tri<STORAGE>(a.B, it.y), G, a.row_lo, a.row_hi);
+            if (a.sparse) trim_owned(S, G, seg);
+        }
         const long long width = S.trans ? S.rows : (long long)S.cols;   // cells per line
         const long long l0 = S.trans ? S.j0 : S.i0, m0 = S.trans ? S.i0 : S.j0;
         long long c0, c1, line_a, line_b;
@@ -563,6 +580,21 @@ k_raster_big(RasterArgs a)
                 if (lo <= (double)(m0 + wr) && hi >= (double)(m0 + wl)) {
                     ml = lo > (double)(m0 + wl) ? (long long)ceil(lo) - m0 : wl;
                     mr = hi < (double)(m0 + wr) ? (long long)floor(hi) - m0 : wr;
+                }
+                if (a.sparse && !S.trans && mr >= ml) {
+                    // ray-tile shards: a row meets at most two segments (n_v <
+                    // kSegRays); keep only the cells of the owned one(s)
+                    const int64_t rb = (l0 + li) * G.n_v + m0;
+                    const int64_t qa = (rb + ml) / kSegRays, qb = (rb + mr) / kSegRays;
+                    const bool oa = __ldg(&seg[qa]) != kNoSlot;
+                    const bool ob = qb == qa ? oa : __ldg(&seg[qb]) != kNoSlot;
+                    if (!oa && !ob) {
+                        mr = ml - 1;
+                    } else if (!oa) {
+                        ml = qb * kSegRays - rb;
+                    } else if (!ob) {
+                        mr = qb * kSegRays - 1 - rb;
+                    }
                 }
             }
             const int cnt = mr >= ml ? (int)(mr - ml + 1) : 0;
@@ -628,6 +660,8 @@ cudaError_t launch_raster(const RasterArgs &a, cudaStream_t st, const LaunchStat
     cudaError_t e = cudaMemsetAsync(a.counter, 0, sizeof(unsigned long long), st);
     if (e == cudaSuccess && a.big)
         e = cudaMemsetAsync(a.nbig, 0, sizeof(unsigned long long), st);
+    if (e == cudaSuccess && a.setups)
+        e = cudaMemsetAsync(a.nsetup, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
     if (a.storage == kF64) raster_dispatch<kF64>(a, st, ls.num_sms);
     else if (a.storage == kSingle) raster_dispatch<kSingle>(a, st, ls.num_sms);
