@@ -41,7 +41,10 @@ def raw(rep):
     for k in WANT:
         if k in hdr:
             i = hdr.index(k)
-            v = float(vals[i].replace(",", ""))
+            try:
+                v = float(vals[i].replace(",", ""))
+            except ValueError:   # "no data" / "n/a"
+                continue
             d[k] = v * UNITS.get(units[i], 1.0) if units[i] in UNITS else v
     return d
 
@@ -49,6 +52,11 @@ def raw(rep):
 def queries(log):
     m = re.findall(r'"queries_per_step": (\d+)', open(log).read())
     return int(m[-1]) if m else None
+
+
+def secondary_queries(log):
+    m = re.findall(r'"secondary_queries": ([0-9.]+)', open(log).read())
+    return float(m[-1]) if m else None
 
 
 def main():
@@ -79,6 +87,12 @@ def main():
             d["queries_in_capture"] = q
             d["dram_bytes_per_query"] = dram / q
             total += dram / q
+        if tag == "k_trace_persistent" and log:
+            sq = secondary_queries(os.path.join(OUT, log))
+            if sq:
+                # bench.py scales this to its step for the roofline `traffic`
+                res["dram_bytes_per_secondary_query"] = dram / sq
+                d["secondary_queries_in_capture"] = sq
         res["kernels"][tag] = d
     res["dram_bytes_per_query"] = total
     json.dump(res, open(os.path.join(ROOT, "profiles", "ncu_trace_summary.json"), "w"), indent=1)
