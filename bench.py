@@ -390,7 +390,7 @@ def main():
     n_ang = len(grids) // max(world, 1)
     ras_bytes = 48.0 * ntri * n_ang + 16.0 * hits_step
     ras_a, ras_f = rl(ras_bytes, ms["raster_ms"], peak, "")
-    cmp_bytes = 16.0 * rays_step + 8.0 * hits_step
+    cmp_bytes = rays_step / 8.0 + 48.0 * hits_step
     cmp_a, cmp_f = rl(cmp_bytes, ms["compact_ms"], peak, "")
     po_bytes = (8.0 + 16.0 + 16.0) * hits_step + 8.0 * rays_step / 1024 + 16.0 * rays_step / 1024
     po_a, po_f = rl(po_bytes, ms["po_ms"], peak, "")
@@ -408,7 +408,7 @@ def main():
         "k_prim_compact": {
             "bound": "hbm", "achieved": cmp_a, "peak": peak, "unit": "GB/s", "frac": cmp_f,
             "ms": ms["compact_ms"],
-            "yardstick": "16 B read per ray slot + 8 B hit-list entry per hit"},
+            "yardstick": "1 bit of the raster's hit bitmap per ray slot; per hit: 16 B slot read + 16 B slot reset + 16 B work-list entry"},
         "k_po": {
             "bound": "hbm", "achieved": po_a, "peak": peak, "unit": "GB/s", "frac": po_f,
             "ms": ms["po_ms"],

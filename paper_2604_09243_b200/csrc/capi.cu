@@ -103,6 +103,8 @@ struct sbr_ctx {
     // mode PO restores that after every batch, so only growth needs a memset
     int64_t clean_slots = 0;
     DevBuf<unsigned long long> nwork;
+    DevBuf<unsigned int> hitmap;            // raster pass: 1 bit per slot, first hit
+    DevBuf<int> chunk_unit;                 // batch chunk -> unit index
     DevBuf<int4> big;                       // raster pass: big-triangle chunk queue
     DevBuf<unsigned long long> nbig;
     DevBuf<unsigned char> setups;           // raster pass: set-ups of queued triangles
@@ -284,7 +286,8 @@ extern "C" int sbr_ctx_trim(sbr_ctx *ctx)
     ctx->chunk_hits.release();
     ctx->chunk_part.release(); ctx->seg_part.release(); ctx->diag.release();
     ctx->seg_base.release(); ctx->seg_slot.release(); ctx->bgrids.release();
-    ctx->worklist.release(); ctx->big.release(); ctx->setups.release();
+    ctx->worklist.release(); ctx->big.release(); ctx->setups.release(); ctx->hitmap.release();
+    ctx->chunk_unit.release();
     ctx->amp.release(); ctx->stage.release();
     ctx->ws.buf.release();
     ctx->ws.off = 0;
@@ -1025,6 +1028,7 @@ static RasterArgs raster_args(const sbr_bvh *bvh, const GridDev *grids, const in
     r.setups = nullptr;
     r.nsetup = nullptr;
     r.setup_cap = 0;
+    r.hitmap = nullptr;
     r.row_lo = 0;
     r.row_hi = INT64_MAX;
     r.stats = nullptr;
@@ -1379,12 +1383,14 @@ static int run_units(sbr_ctx *ctx, const sbr_bvh *bvh, const std::vector<UnitDev
             cudaError_t e = ctx->slots.reserve(slots);
             if (ctx->slots.p != before) ctx->clean_slots = 0;   // fresh memory
             if (e == cudaSuccess && raster) e = ctx->worklist.reserve(slots);
+            if (e == cudaSuccess && raster) e = ctx->hitmap.reserve((slots + 31) / 32);
             if (e == cudaSuccess && raster) e = ctx->chunk_hits.reserve(slots / kChunk);
             if (e == cudaSuccess) e = ctx->chunk_part.reserve((size_t)(slots / kChunk) * nk);
             if (e == cudaErrorMemoryAllocation && budget > ((int64_t)1 << 22)) {
                 cudaGetLastError();
                 ctx->slots.release();
                 ctx->worklist.release();
+                ctx->hitmap.release();
                 ctx->chunk_hits.release();
                 ctx->chunk_part.release();
                 ctx->clean_slots = 0;
@@ -1396,6 +1402,9 @@ static int run_units(sbr_ctx *ctx, const sbr_bvh *bvh, const std::vector<UnitDev
         CUDA_TRY(ctx->units.reserve(batch.size()));
         CUDA_TRY(cudaMemcpyAsync(ctx->units.p, batch.data(), sizeof(UnitDev) * batch.size(),
                                  cudaMemcpyHostToDevice, st));
+        CUDA_TRY(ctx->chunk_unit.reserve(slots / kChunk));
+        CUDA_TRY(launch_chunk_units(ctx->units.p, (int)batch.size(), ctx->chunk_unit.p, st,
+                                    ctx->stats()));
         if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev[0], st));
         // the batch's slots are all-ones after a list-mode PO; anything
         // else (BVH primary, reference order, an error) leaves them dirty
@@ -1416,9 +1425,11 @@ static int run_units(sbr_ctx *ctx, const sbr_bvh *bvh, const std::vector<UnitDev
             if (clean < slots)
                 CUDA_TRY(cudaMemsetAsync(ctx->slots.p + clean, 0xff,
                                          sizeof(SlotRec) * (slots - clean), st));
+            CUDA_TRY(cudaMemsetAsync(ctx->hitmap.p, 0, sizeof(unsigned) * ((slots + 31) / 32), st));
             RasterArgs ra = raster_args(bvh, ctx->grids.p, ctx->bgrids.p, (int)bgrids.size(),
                                         ctx->seg_base.p, ctx->seg_slot.p,
                                         reinterpret_cast<PrimHit *>(ctx->slots.p));
+            ra.hitmap = ctx->hitmap.p;
             ra.counter = ctx->counter.p + 1;
             ra.stats = ctx->counter.p + 2;
             CUDA_TRY(attach_big_queue(ctx, ra));
@@ -1432,8 +1443,9 @@ static int run_units(sbr_ctx *ctx, const sbr_bvh *bvh, const std::vector<UnitDev
             CUDA_TRY(ctx->worklist.reserve(slots));
             CUDA_TRY(ctx->nwork.reserve(1));
             CUDA_TRY(launch_prim_compact(cfg, ctx->grids.p, ctx->units.p, (int)batch.size(),
-                                         slots, ctx->slots.p, ctx->worklist.p, ctx->nwork.p,
-                                         ctx->chunk_hits.p, st, ctx->stats()));
+                                         slots, ctx->slots.p, ctx->hitmap.p, ctx->chunk_unit.p,
+                                         ctx->worklist.p, ctx->nwork.p, ctx->chunk_hits.p, st,
+                                         ctx->stats()));
         }
         if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev[3], st));
         if (refmode) {
@@ -1452,7 +1464,8 @@ static int run_units(sbr_ctx *ctx, const sbr_bvh *bvh, const std::vector<UnitDev
                            raster ? ctx->worklist.p : nullptr,
                            raster ? ctx->chunk_hits.p : nullptr, slots / kChunk, ctx->k2.p, nk,
                            ctx->dkturn, ctx->gpow.p, cfg.max_bounces, ctx->chunk_part.p,
-                           diag_dev, ctx->bad.p, ctx->counter.p + 5, st, ctx->stats()));
+                           diag_dev, ctx->bad.p, ctx->counter.p + 5, ctx->chunk_unit.p, st,
+                           ctx->stats()));
         if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev[2], st));
         CUDA_TRY(launch_seg_reduce(ctx->chunk_part.p, ctx->units.p, (int)batch.size(), nk,
                                    seg_dev, st, ctx->stats()));
@@ -1981,7 +1994,7 @@ extern "C" int sbr_accumulate(sbr_ctx *ctx, const uint8_t *valid, const double *
     CUDA_TRY(launch_po(ctx->slots.p, ctx->units.p, (int)nseg, nullptr, nullptr,
                        slots_used / kChunk, ctx->k2.p, nk,
                        ctx->dkturn, ctx->gpow.p, maxb, ctx->chunk_part.p, ctx->diag.p, ctx->bad.p,
-                       ctx->counter.p + 5, st, ctx->stats()));
+                       ctx->counter.p + 5, nullptr, st, ctx->stats()));
     CUDA_TRY(launch_seg_reduce(ctx->chunk_part.p, ctx->units.p, (int)nseg, nk, ctx->seg_part.p, st,
                                ctx->stats()));
     sbr_grid g;

@@ -380,7 +380,8 @@ k_po_list(const UnitDev *__restrict__ units, int n_units, const uint4 *__restric
           const uint2 *__restrict__ chunk_hits, int64_t n_chunks,
           const double *__restrict__ kturn, const double *__restrict__ gpow, int max_bounces,
           double2 *__restrict__ chunk_part, int64_t *__restrict__ diag,
-          unsigned long long *__restrict__ bad, unsigned long long *__restrict__ counter)
+          unsigned long long *__restrict__ bad, unsigned long long *__restrict__ counter,
+          const int *__restrict__ chunk_unit)
 {
     __shared__ unsigned int s_hist[kPoListWarps][kMaxHist];
     __shared__ double2 xfer[kPoListWarps][32];
@@ -431,7 +432,7 @@ k_po_list(const UnitDev *__restrict__ units, int n_units, const uint4 *__restric
         const int64_t c1 = c0 + kPoSuper < n_chunks ? c0 + kPoSuper : n_chunks;
         for (int64_t chunk = c0; chunk < c1; ++chunk) {
             const int64_t slot0 = chunk * kChunk;
-            const int ui = find_unit(units, n_units, slot0);
+            const int ui = chunk_unit ? __ldg(&chunk_unit[chunk]) : find_unit(units, n_units, slot0);
             const UnitDev U = units[ui];
             if (U.grid != cur_grid) {
                 flush();
@@ -509,6 +510,28 @@ k_po_list(const UnitDev *__restrict__ units, int n_units, const uint4 *__restric
     flush();
 }
 
+// chunk -> unit table of a batch (units are chunk-aligned): one load instead
+// of a binary search over the units in the compaction and PO kernels
+__global__ void k_chunk_units(const UnitDev *__restrict__ units, int n_units,
+                              int *__restrict__ chunk_unit)
+{
+    const int u = blockIdx.x;
+    if (u >= n_units) return;
+    const UnitDev U = units[u];
+    const int64_t c0 = U.slot_base / kChunk;
+    const int64_t nc = (U.ray_end - U.ray_begin + kChunk - 1) / kChunk;
+    for (int64_t c = threadIdx.x; c < nc; c += blockDim.x) chunk_unit[c0 + c] = u;
+}
+
+cudaError_t launch_chunk_units(const UnitDev *d_units, int n_units, int *d_chunk_unit,
+                               cudaStream_t st, const LaunchStats &ls)
+{
+    if (n_units <= 0) return cudaSuccess;
+    k_chunk_units<<<n_units, 256, 0, st>>>(d_units, n_units, d_chunk_unit);
+    ++*ls.launches;
+    return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------------
 // hit-list compaction after the raster pass
 // ---------------------------------------------------------------------------
@@ -525,7 +548,8 @@ constexpr int kCompactTile = kCompactThreads * kCompactPer;   // == kChunk
 __global__ void __launch_bounds__(kCompactThreads)
 k_prim_compact(TraceCfg cfg, const GridDev *__restrict__ grids,
                const UnitDev *__restrict__ units, int n_units, int64_t n_slots,
-               SlotRec *__restrict__ slots, uint4 *__restrict__ list,
+               SlotRec *__restrict__ slots, const unsigned int *__restrict__ hitmap,
+               const int *__restrict__ chunk_unit, uint4 *__restrict__ list,
                unsigned long long *__restrict__ nlist, uint2 *__restrict__ chunk_hits)
 {
     constexpr int W = kCompactThreads / 32;
@@ -533,10 +557,14 @@ k_prim_compact(TraceCfg cfg, const GridDev *__restrict__ grids,
     __shared__ int pos[kCompactPer][W];
     __shared__ unsigned long long s_at;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int64_t tile = (int64_t)blockIdx.x * kCompactTile; tile < n_slots;
-         tile += (int64_t)gridDim.x * kCompactTile) {
+    // tiles strided over the blocks: at any moment the blocks work on one
+    // window of neighbouring tiles, so the list comes out close to aperture
+    // order (coherent first bounces for the trace kernel)
+    const int64_t ntiles = (n_slots + kCompactTile - 1) / kCompactTile;
+    for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+        const int64_t tile = ti * kCompactTile;
         // slots are chunk-aligned per unit and kCompactTile == kChunk: one unit
-        const int ui = find_unit(units, n_units, tile);
+        const int ui = chunk_unit ? __ldg(&chunk_unit[ti]) : find_unit(units, n_units, tile);
         const UnitDev U = units[ui];
         const bool alias_ok =
             cfg.allow_aliasing || !(grids[U.grid].spacing > cfg.spacing_limit);
@@ -548,11 +576,15 @@ k_prim_compact(TraceCfg cfg, const GridDev *__restrict__ grids,
             const int64_t slot = tile + q * kCompactThreads + tid;
             bool hit = false;
             hv[q] = make_ulonglong2(kNoHitBits, kNoHitBits);
-            if (slot < n_slots) {
+            // the raster's hit bitmap (one word per warp and q): only the
+            // slots that were hit are read at all
+            const bool marked =
+                slot < n_slots &&
+                (!hitmap || ((__ldg(hitmap + (slot >> 5)) >> (unsigned)(slot & 31)) & 1u));
+            if (marked) {
                 const int64_t r = U.ray_begin + (slot - U.slot_base);
                 const bool real = r < U.ray_end && alias_ok;
-                // streaming read: every slot is read once here and the
-                // misses (most of them) never again
+                // streaming read: every hit slot is read once here
                 hv[q] = __ldcs(reinterpret_cast<const ulonglong2 *>(slots) + slot);
                 hit = real && hv[q].x != kNoHitBits;
                 // the hit moves into the work list; its slot returns to the
@@ -567,16 +599,22 @@ k_prim_compact(TraceCfg cfg, const GridDev *__restrict__ grids,
             hitmask |= (hit ? 1u : 0u) << q;
         }
         __syncthreads();
-        if (tid == 0) {   // exclusive scan in slot order + one atomic per tile
-            int run = 0;
-            for (int q = 0; q < kCompactPer; ++q)
-                for (int w = 0; w < W; ++w) {
-                    pos[q][w] = run;
-                    run += cnt[q][w];
-                }
-            s_at = run ? atomicAdd(nlist, (unsigned long long)run) : 0ULL;
-            // this chunk's hits: list[at, at + run), in slot order
-            chunk_hits[tile / kCompactTile] = make_uint2((unsigned int)s_at, (unsigned int)run);
+        static_assert(kCompactPer * W == 32, "one warp scans the (q, warp) counts");
+        if (warp == 0) {   // exclusive scan in slot order + one atomic per tile
+            const int v = (&cnt[0][0])[lane];
+            int incl = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            (&pos[0][0])[lane] = incl - v;
+            if (lane == 31) {
+                const int run = incl;
+                s_at = run ? atomicAdd(nlist, (unsigned long long)run) : 0ULL;
+                // this chunk's hits: list[at, at + run), in slot order
+                chunk_hits[ti] = make_uint2((unsigned int)s_at, (unsigned int)run);
+            }
         }
         __syncthreads();
         const unsigned long long at = s_at;
@@ -602,7 +640,8 @@ k_prim_compact(TraceCfg cfg, const GridDev *__restrict__ grids,
 
 cudaError_t launch_prim_compact(const TraceCfg &cfg, const GridDev *d_grids,
                                 const UnitDev *d_units, int n_units, int64_t n_slots,
-                                SlotRec *d_slots, uint4 *d_worklist,
+                                SlotRec *d_slots, const unsigned int *d_hitmap,
+                                const int *d_chunk_unit, uint4 *d_worklist,
                                 unsigned long long *d_nwork, uint2 *d_chunk_hits,
                                 cudaStream_t st, const LaunchStats &ls)
 {
@@ -614,7 +653,8 @@ cudaError_t launch_prim_compact(const TraceCfg &cfg, const GridDev *d_grids,
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     k_prim_compact<<<(unsigned)blocks, kCompactThreads, 0, st>>>(
-        cfg, d_grids, d_units, n_units, n_slots, d_slots, d_worklist, d_nwork, d_chunk_hits);
+        cfg, d_grids, d_units, n_units, n_slots, d_slots, d_hitmap, d_chunk_unit, d_worklist,
+        d_nwork, d_chunk_hits);
     ++*ls.launches;
     return cudaGetLastError();
 }
@@ -881,7 +921,7 @@ cudaError_t launch_po(SlotRec *d_slots, const UnitDev *d_units, int n_units,
                       const double *d_gpow,
                       int max_bounces, double2 *d_chunk_part, int64_t *d_diag,
                       unsigned long long *d_bad, unsigned long long *d_counter,
-                      cudaStream_t st, const LaunchStats &ls)
+                      const int *d_chunk_unit, cudaStream_t st, const LaunchStats &ls)
 {
     if (n_chunks <= 0) return cudaSuccess;
     dim3 grid((unsigned)n_chunks);
@@ -899,7 +939,7 @@ cudaError_t launch_po(SlotRec *d_slots, const UnitDev *d_units, int n_units,
         if (e != cudaSuccess) return e;
         k_po_list<<<(unsigned)(ls.num_sms * 8), kPoListThreads, 0, st>>>(
             d_units, n_units, d_list, d_chunk_hits, n_chunks, d_k2, d_gpow, max_bounces,
-            d_chunk_part, d_diag, d_bad, d_counter);
+            d_chunk_part, d_diag, d_bad, d_counter, d_chunk_unit);
     } else {
         if (nk >= 8) { if (rot) SBR_PO(8, true); else SBR_PO(8, false); }
         else if (nk >= 4) { if (rot) SBR_PO(4, true); else SBR_PO(4, false); }

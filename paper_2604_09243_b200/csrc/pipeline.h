@@ -149,9 +149,12 @@ cudaError_t launch_trace_solve(const TraceCfg &cfg, const GridDev *d_grids,
 // launch_po); misses and padding slots are left untouched (all-ones)
 cudaError_t launch_prim_compact(const TraceCfg &cfg, const GridDev *d_grids,
                                 const UnitDev *d_units, int n_units, int64_t n_slots,
-                                SlotRec *d_slots, uint4 *d_worklist,
+                                SlotRec *d_slots, const unsigned int *d_hitmap,
+                                const int *d_chunk_unit, uint4 *d_worklist,
                                 unsigned long long *d_nwork, uint2 *d_chunk_hits,
                                 cudaStream_t st, const LaunchStats &ls);
+cudaError_t launch_chunk_units(const UnitDev *d_units, int n_units, int *d_chunk_unit,
+                               cudaStream_t st, const LaunchStats &ls);
 
 struct FullOut {
     uint8_t *valid;
@@ -259,6 +262,7 @@ struct RasterArgs {
     const int64_t *seg_base;   // (ngrids+1) first global segment row of each grid
     const int64_t *seg_slot;   // per global segment row: slot - ray index, or kNoSlot
     PrimHit *prim;
+    unsigned int *hitmap;          // 1 bit per slot, set on a slot's first hit (or null)
     unsigned long long *counter;   // work counter (zeroed by launch_raster)
     int sparse;                    // some segments of the batch's grids are not in it
     int4 *big;                     // queue of big-triangle chunks (grid, tri, chunk, setup)
@@ -297,7 +301,7 @@ cudaError_t launch_po(SlotRec *d_slots, const UnitDev *d_units, int n_units,
                       const double *d_gpow,
                       int max_bounces, double2 *d_chunk_part, int64_t *d_diag,
                       unsigned long long *d_bad, unsigned long long *d_counter,
-                      cudaStream_t st, const LaunchStats &ls);
+                      const int *d_chunk_unit, cudaStream_t st, const LaunchStats &ls);
 
 cudaError_t launch_seg_reduce(const double2 *d_chunk_part, const UnitDev *d_units,
                               int n_units, int nk, double2 *d_seg_part, cudaStream_t st,

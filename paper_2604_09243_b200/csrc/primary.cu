@@ -75,8 +75,12 @@ struct __align__(16) U128 {
     unsigned long long lo, hi;
 };
 
-// (t bits, id) lexicographic minimum into a PrimHit (layout: tbits | pad, id)
-__device__ __forceinline__ void prim_min(PrimHit *h, unsigned long long bits, unsigned int id)
+// (t bits, id) lexicographic minimum into a PrimHit (layout: tbits | pad, id).
+// The thread whose CAS replaces the all-ones "no hit" marks the slot in the
+// hit bitmap (one fire-and-forget OR per hit ray), so the compaction reads
+// only the slots that were hit.
+__device__ __forceinline__ void prim_min(PrimHit *h, unsigned long long bits, unsigned int id,
+                                         unsigned int *hitmap, int64_t slot)
 {
     U128 *p = reinterpret_cast<U128 *>(h);
     // pre-check with one plain 16-byte load; a stale (cached) value is safe:
@@ -87,7 +91,11 @@ __device__ __forceinline__ void prim_min(PrimHit *h, unsigned long long bits, un
     nv.hi = 0xffffffffULL | ((unsigned long long)id << 32);
     while (bits < cur.lo || (bits == cur.lo && id < (unsigned int)(cur.hi >> 32))) {
         const U128 prev = atomicCAS(p, cur, nv);
-        if (prev.lo == cur.lo && prev.hi == cur.hi) break;
+        if (prev.lo == cur.lo && prev.hi == cur.hi) {
+            if (hitmap && cur.lo == kNoHitBits)
+                atomicOr(hitmap + (slot >> 5), 1u << (unsigned)(slot & 31));
+            break;
+        }
         cur = prev;
     }
 }
@@ -331,9 +339,6 @@ __device__ __forceinline__ void raster_cell(const RasterArgs &a, const GridDev &
     const int64_t r = i * G.n_v + j;
     // sharded / partial batches: skip cells of segments this launch does not
     // own before doing any arithmetic
-#ifdef SBR_RASTER_NOWALK   // experiment: set-up cost only
-    if (i >= 0) return;
-#endif
     const int64_t off = __ldg(&seg[r / kSegRays]);
     if (a.sparse && off == kNoSlot) return;
     // origin exactly as the launcher builds it (pipeline.cu grid_origin)
@@ -345,13 +350,9 @@ __device__ __forceinline__ void raster_cell(const RasterArgs &a, const GridDev &
     const double oz = DA(DA(G.corner[2], DM(si, G.u[2])), DM(sj, G.v[2]));
     const double t = tri_hit_origin<true>(T, P, inv, ox, oy, oz, G.k[0], G.k[1], G.k[2], 0.0,
                                           inf);
-#ifdef SBR_RASTER_NOCAS   // experiment: cost of the exact tests without the minimum
-    if (t == 1.2345) prim_min(a.prim + (off + r), 0, 0);
-    return;
-#endif
     if (t > 0.0 && t < inf && off != kNoSlot)
         prim_min(a.prim + (off + r), (unsigned long long)__double_as_longlong(t),
-                 (unsigned int)id);
+                 (unsigned int)id, a.hitmap, off + r);
 }
 
 // Span of line x (a row i, or a column j when S.trans) inside the candidate
