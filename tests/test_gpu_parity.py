@@ -720,3 +720,63 @@ def test_device_objects_are_released():
         cycle()
         gc.collect()
         assert nat.live_allocations() == base
+
+
+@pytest.mark.parametrize("strict", [False, True])
+def test_fused_solve_count_trapped_and_strict(orc, primary, strict):
+    """The fused solve (raster -> compaction -> trace -> list PO) with
+    count_trapped=True (po.py:95-98 keeps valid rays that never escaped) and
+    strict orientation (transport.py:306-307) against the oracle's records +
+    accumulate, on a multi-bounce rough plate where many rays end trapped."""
+    mesh = meshgen.perturbed_grid_mesh(cells=120, extent=4.0, amplitude=0.25, seed=11)
+    tree = sbr.build(mesh)
+    scene = orc.Scene.from_mesh(mesh)
+    lam = 0.1
+    params = sbr.TraceParams(max_bounces=3, strict_orientation=strict)
+    grids = [sbr.build_aperture(mesh.aabb, sbr.IncidentDirection(th, ph), lam / 5,
+                                wavelength=lam)
+             for th, ph in ((0.3, 0.7), (2.6, 4.0), (1.2, 1.9))]
+    res = sbr.solve_grids(tree, mesh, grids, params, [2 * math.pi / lam], count_trapped=True)
+    trapped = 0
+    for i, g in enumerate(grids):
+        ref = orc.trace_grid(scene, g, 3, params.resolve_epsilon(mesh), strict=strict)
+        trapped += int((ref.valid.astype(bool) & ~ref.escaped.astype(bool)).sum())
+        a = orc.accumulate(ref, g.k_inc, lam, g.cell_area, count_trapped=True)
+        _amp_close(res.amplitude[i, 0], a)
+        assert int(res.valid_rays[i]) == int(ref.valid.sum())
+        assert int(res.queries[i]) == int((ref.bounces.astype(np.int64) + 1).sum())
+    assert trapped > 1000
+
+
+def test_empty_and_degenerate_inputs(orc, monkeypatch):
+    """Empty ray lists, empty row ranges, no grids, a single-triangle mesh
+    forced through the raster pass, and an aperture the mesh does not cover
+    (every ray misses): shapes and values as the reference produces them."""
+    mesh = meshgen.plate_mesh(1.0)
+    tree = sbr.build(mesh)
+    tri, t, vis = sbr.closest_hit_batch(tree, mesh, np.zeros((0, 3)), np.zeros((0, 3)))
+    assert tri.shape == (0,) and t.shape == (0,) and vis.shape == (0,)
+    grid = sbr.build_aperture(mesh.aabb, sbr.IncidentDirection(0.2, 0.3), 0.02, wavelength=0.1)
+    rec = sbr.trace_grid(tree, mesh, grid, sbr.TraceParams(max_bounces=2), rows=(5, 5))
+    assert rec.valid.shape == (0,)
+    res = sbr.solve_grids(tree, mesh, [], sbr.TraceParams(max_bounces=2), [2 * math.pi / 0.1])
+    assert res.amplitude.shape == (0, 1)
+    one = sbr.mesh_from_arrays([[0, 0, 0], [1, 0, 0], [0, 1, 0]], [[0, 1, 2]])
+    t1 = sbr.build(one)
+    g1 = sbr.build_aperture(one.aabb, sbr.IncidentDirection(0.0, 0.0), 0.01, wavelength=0.05)
+    scene = orc.Scene.from_mesh(one)
+    for prim in ("raster", "bvh"):
+        monkeypatch.setenv("SBR_PRIMARY", prim)
+        r = sbr.trace_grid(t1, one, g1, sbr.TraceParams(max_bounces=2), with_ids=True)
+        ref = orc.trace_grid(scene, g1, 2, sbr.TraceParams().resolve_epsilon(one), with_ids=True)
+        for k in ("valid", "normal0", "path", "bounces", "escaped", "out_dir", "tri_ids"):
+            assert np.array_equal(getattr(r, k), getattr(ref, k)), (prim, k)
+        assert 0 < r.valid.sum() < r.valid.size
+        s = sbr.solve_grids(t1, one, [g1], sbr.TraceParams(max_bounces=2), [2 * math.pi / 0.05])
+        assert int(s.valid_rays[0]) == int(ref.valid.sum())
+    # an aperture built for another object: every ray misses the plate
+    far = sbr.mesh_from_arrays([[10, 10, 10], [11, 10, 10], [10, 11, 10]], [[0, 1, 2]])
+    gm = sbr.build_aperture(far.aabb, sbr.IncidentDirection(0.0, 0.0), 0.05, wavelength=0.25)
+    sm = sbr.solve_grids(tree, mesh, [gm], sbr.TraceParams(max_bounces=2), [2 * math.pi / 0.25])
+    assert sm.valid_rays[0] == 0 and sm.amplitude[0, 0] == 0
+    assert sm.queries[0] == gm.n_u * gm.n_v
