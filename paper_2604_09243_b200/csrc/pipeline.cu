@@ -113,6 +113,7 @@ k_po(SlotRec *__restrict__ slots, const UnitDev *__restrict__ units, int n_units
      unsigned long long *__restrict__ bad)
 {
     __shared__ double2 srec[kChunk];                 // compacted (R, w)
+    __shared__ float2 srot[ROT ? kChunk : 1];        // per record: sincos of the k step
     __shared__ int wcount[kPerThread][kPoWarps];
     __shared__ int wbase[kPerThread][kPoWarps];
     __shared__ int s_total;
@@ -256,6 +257,18 @@ k_po(SlotRec *__restrict__ slots, const UnitDev *__restrict__ units, int n_units
 
     // ---- PO terms ----
     const int M = s_total;
+    if (ROT) {
+        // the phase step between neighbouring wavenumbers is the same for
+        // every frequency group: its SFU sincos once per record, shared by the
+        // group warps (was once per record and group)
+        for (int m = tid; m < M; m += kPoThreads) {
+            const double dt = dkturn * srec[m].x;
+            float ds, dc;
+            __sincosf((float)(dt - rint(dt)) * 6.28318530717958648f, &ds, &dc);
+            srot[m] = make_float2(ds, dc);
+        }
+        __syncthreads();
+    }
     const int G = (nk + FPT - 1) / FPT;        // frequency groups
     // warps per group; one wavenumber: one warp (lane m mod 32 sums the m-th
     // selected record -- the sum k_po_list forms in list mode)
@@ -289,10 +302,11 @@ k_po(SlotRec *__restrict__ slots, const UnitDev *__restrict__ units, int n_units
             for (int m = sub * 32 + lane; m < M; m += wpg * 32) {
                 const double2 rw = srec[m];
                 const float wf = (float)rw.y;
-                const double t0 = kk[0] * rw.x, dt = dkturn * rw.x;
-                float sn, cs, ds, dc;
+                const double t0 = kk[0] * rw.x;
+                const float2 rot = srot[m];
+                const float ds = rot.x, dc = rot.y;
+                float sn, cs;
                 __sincosf((float)(t0 - rint(t0)) * 6.28318530717958648f, &sn, &cs);
-                __sincosf((float)(dt - rint(dt)) * 6.28318530717958648f, &ds, &dc);
 #pragma unroll
                 for (int f = 0; f < FPT; ++f) {
                     sacc[f] = fmaf(wf, sn, sacc[f]);
