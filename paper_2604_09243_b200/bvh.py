@@ -389,7 +389,12 @@ def closest_hit_counted(bvh: Bvh, mesh: Mesh, origin, direction, t_min: float = 
 
 def closest_hit_batch(bvh: Bvh, mesh: Mesh, origins, dirs, t_min: float = 0.0,
                       t_max: float = np.inf):
-    """(tri, t, visits) arrays; tri = -1 where the ray misses (bvh.py:407-423)."""
+    """(tri, t, visits) arrays; tri = -1 where the ray misses (bvh.py:407-423).
+
+    As in the reference, a float32 mesh casts the rays to float32 too
+    (bvh.py:414-415), so the Moller-Trumbore arithmetic runs in float32 up
+    to the float64 ``1.0 / det`` (sbr_device.cuh tri_hit_f32rays); the
+    multi-bounce walk keeps float64 rays (transport.py:362-363)."""
     ctx = nat.context()
     d = bvh.device(mesh, ctx)
     o = nat.f64(origins, (-1, 3))

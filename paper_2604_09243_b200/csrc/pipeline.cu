@@ -56,9 +56,18 @@ k_closest(BvhView B, const double *__restrict__ orig, const double *__restrict__
          r += (int64_t)gridDim.x * blockDim.x) {
         double t = t_max;
         int visits = 0;
-        int id = closest_hit<STORAGE, false>(B, orig[3 * r], orig[3 * r + 1], orig[3 * r + 2],
+        int id;
+        if (STORAGE == kSingle) {   // float32 mesh: the reference casts the rays too
+            auto f = [](double x) { return (double)__double2float_rn(x); };
+            id = closest_hit<STORAGE, false, true>(B, f(orig[3 * r]), f(orig[3 * r + 1]),
+                                                   f(orig[3 * r + 2]), f(dirs[3 * r]),
+                                                   f(dirs[3 * r + 1]), f(dirs[3 * r + 2]), t_min,
+                                                   t, visits);
+        } else {
+            id = closest_hit<STORAGE, false>(B, orig[3 * r], orig[3 * r + 1], orig[3 * r + 2],
                                              dirs[3 * r], dirs[3 * r + 1], dirs[3 * r + 2],
                                              t_min, t, visits);
+        }
         tri[r] = id;
         t_out[r] = t;
         visits_out[r] = visits;

@@ -93,7 +93,8 @@ __device__ __forceinline__ TriF64 ref_tri(const RefView &V, int ti)
 
 // bvh.py:306-362 _traverse: (triangle or -1, t, visits)
 __device__ int ref_traverse(const RefView &V, const double o[3], const double d[3], double t_min,
-                            double t_max, int *stack, double &t_out, int64_t &visits)
+                            double t_max, int *stack, double &t_out, int64_t &visits,
+                            bool f32rays = false)
 {
     double best_t = t_max;
     int best = -1;
@@ -117,8 +118,10 @@ __device__ int ref_traverse(const RefView &V, const double o[3], const double d[
             const int first = __ldg(V.first + node);
             for (int k = first; k < first + cnt; ++k) {
                 const int ti = __ldg(V.order + k);
-                const double t = tri_hit_exact(ref_tri(V, ti), o[0], o[1], o[2], d[0], d[1],
-                                               d[2], t_min, best_t);
+                const TriF64 T = ref_tri(V, ti);
+                const double t =
+                    f32rays ? tri_hit_f32rays(T, o[0], o[1], o[2], d[0], d[1], d[2], t_min, best_t)
+                            : tri_hit_exact(T, o[0], o[1], o[2], d[0], d[1], d[2], t_min, best_t);
                 if (t > 0.0 && (t < best_t || (t == best_t && ti < best))) {
                     best_t = t;
                     best = ti;
@@ -156,11 +159,13 @@ __global__ void k_closest_ref(RefView V, const double *orig, const double *dirs,
     int stack[kRefStack];
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
          r += (int64_t)gridDim.x * blockDim.x) {
-        const double o[3] = {orig[3 * r], orig[3 * r + 1], orig[3 * r + 2]};
-        const double d[3] = {dirs[3 * r], dirs[3 * r + 1], dirs[3 * r + 2]};
+        // float32 mesh: closest_hit_batch casts the rays to float32 too
+        auto f = [&](double x) { return V.single ? (double)__double2float_rn(x) : x; };
+        const double o[3] = {f(orig[3 * r]), f(orig[3 * r + 1]), f(orig[3 * r + 2])};
+        const double d[3] = {f(dirs[3 * r]), f(dirs[3 * r + 1]), f(dirs[3 * r + 2])};
         double t;
         int64_t vis;
-        const int b = ref_traverse(V, o, d, t_min, t_max, stack, t, vis);
+        const int b = ref_traverse(V, o, d, t_min, t_max, stack, t, vis, V.single != 0);
         tri[r] = b;
         t_out[r] = t;
         if (visits) visits[r] = vis;

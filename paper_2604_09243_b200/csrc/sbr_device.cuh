@@ -224,6 +224,48 @@ __device__ __forceinline__ double tri_hit_exact(const TriF64 &T, double ox,
     return tri_hit_origin<false>(T, P, 0.0, ox, oy, oz, dx, dy, dz, t_min, t_max);
 }
 
+// Closest-hit queries on a float32 mesh (reference closest_hit /
+// closest_hit_batch, bvh.py:395-423, cast the RAYS to the mesh dtype too):
+// numba then evaluates _tri_hit_t (geometry.py:326-355) with float32
+// vertices and rays -- edges, p, det, the t-vector, q and the three dot
+// products in float32 (no contraction) -- and only inv_det = 1.0 / det (a
+// float64 literal) and the products with it in float64.  T comes from
+// load_tri<kSingle> (float32 values held exactly in doubles); o and d must
+// be float32-representable.
+__device__ __forceinline__ double tri_hit_f32rays(const TriF64 &T, double oxd, double oyd,
+                                                  double ozd, double dxd, double dyd,
+                                                  double dzd, double t_min, double t_max)
+{
+#define FM(a, b) __fmul_rn((a), (b))
+#define FA(a, b) __fadd_rn((a), (b))
+#define FS(a, b) __fsub_rn((a), (b))
+    const float ox = (float)oxd, oy = (float)oyd, oz = (float)ozd;
+    const float dx = (float)dxd, dy = (float)dyd, dz = (float)dzd;
+    const float ax = (float)T.ax, ay = (float)T.ay, az = (float)T.az;
+    const float e1x = (float)T.e1x, e1y = (float)T.e1y, e1z = (float)T.e1z;
+    const float e2x = (float)T.e2x, e2y = (float)T.e2y, e2z = (float)T.e2z;
+    const float px = FS(FM(dy, e2z), FM(dz, e2y));
+    const float py = FS(FM(dz, e2x), FM(dx, e2z));
+    const float pz = FS(FM(dx, e2y), FM(dy, e2x));
+    const float det = FA(FA(FM(e1x, px), FM(e1y, py)), FM(e1z, pz));
+    if (det == 0.0f) return -1.0;
+    const double inv = __drcp_rn((double)det);   // == IEEE 1.0 / det in float64
+    const float tx = FS(ox, ax), ty = FS(oy, ay), tz = FS(oz, az);
+    const double u = DM((double)FA(FA(FM(tx, px), FM(ty, py)), FM(tz, pz)), inv);
+    if (u < 0.0 || u > 1.0) return -1.0;
+    const float qx = FS(FM(ty, e1z), FM(tz, e1y));
+    const float qy = FS(FM(tz, e1x), FM(tx, e1z));
+    const float qz = FS(FM(tx, e1y), FM(ty, e1x));
+    const double v = DM((double)FA(FA(FM(dx, qx), FM(dy, qy)), FM(dz, qz)), inv);
+    if (v < 0.0 || DA(u, v) > 1.0) return -1.0;
+    const double t = DM((double)FA(FA(FM(e2x, qx), FM(e2y, qy)), FM(e2z, qz)), inv);
+    if (t <= t_min || t > t_max) return -1.0;
+    return t;
+#undef FM
+#undef FA
+#undef FS
+}
+
 // ---------------------------------------------------------------------------
 // Conservative FP32 slab test
 // ---------------------------------------------------------------------------

@@ -19,7 +19,7 @@ struct StackEntry {
 // Closest hit in (t_min, best_t]; best_t is in/out.  Returns the original
 // triangle id or -1.  ANY: stop at the first accepted triangle (escape
 // probe, transport.py:319-326, only needs hit / no hit).
-template <int STORAGE, bool ANY>
+template <int STORAGE, bool ANY, bool F32RAYS = false>
 __device__ __forceinline__ int closest_hit(const BvhView &B, double ox, double oy,
                                            double oz, double dx, double dy,
                                            double dz, double t_min,
@@ -53,7 +53,8 @@ __device__ __forceinline__ int closest_hit(const BvhView &B, double ox, double o
             const int first = leaf_first(ref), cnt = leaf_count(ref);
             for (int k = first; k < first + cnt; ++k) {
                 TriF64 T = load_tri<STORAGE>(B, k);
-                double t = tri_hit_exact(T, ox, oy, oz, dx, dy, dz, t_min, best_t);
+                double t = F32RAYS ? tri_hit_f32rays(T, ox, oy, oz, dx, dy, dz, t_min, best_t)
+                                   : tri_hit_exact(T, ox, oy, oz, dx, dy, dz, t_min, best_t);
                 if (t > 0.0 && (t < best_t || (t == best_t && T.id < best))) {
                     best_t = t;
                     best = T.id;

@@ -83,8 +83,6 @@ def test_reference_order_trace_grid_edgeon(reference_order):
 def test_reference_order_closest_hit_goldens(name, reference_order):
     g = load_golden(name)
     mesh = _mesh(g)
-    if mesh.dtype == np.float32:
-        pytest.skip("float32 closest_hit_batch runs float32 rays (documented)")
     for rule in ("sah", "median"):
         tree = sbr.build(mesh, sbr.BuildParams(split_rule=rule))
         tri, t, vis = sbr.closest_hit_batch(tree, mesh, g["origins"], g["dirs"])
