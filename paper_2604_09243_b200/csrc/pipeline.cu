@@ -579,12 +579,43 @@ k_prim_compact(TraceCfg cfg, const GridDev *__restrict__ grids,
     __shared__ int cnt[kCompactPer][W];
     __shared__ int pos[kCompactPer][W];
     __shared__ unsigned long long s_at;
+    __shared__ int s_gcnt[W], s_gat[W];
+    __shared__ unsigned long long s_gbase;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     // tiles strided over the blocks: at any moment the blocks work on one
     // window of neighbouring tiles, so the list comes out close to aperture
     // order (coherent first bounces for the trace kernel)
     const int64_t ntiles = (n_slots + kCompactTile - 1) / kCompactTile;
-    for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+    // groups of W consecutive tiles: their hit counts come from the raster's
+    // hit bitmap (warp w pop-counts tile w's 32 words), so one atomic per
+    // group reserves the list space (a single counter for every tile
+    // serialised at L2)
+    const int64_t ngroups = (ntiles + W - 1) / W;
+    for (int64_t gi = blockIdx.x; gi < ngroups; gi += gridDim.x) {
+      if (hitmap) {
+          const int64_t tw = gi * W + warp;
+          int c = 0;
+          if (tw < ntiles) {
+              const int64_t word = tw * (kCompactTile / 32) + lane;
+              if (word * 32 < n_slots) c = __popc(__ldg(hitmap + word));
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+          if (lane == 0) s_gcnt[warp] = c;
+          __syncthreads();
+          if (tid == 0) {
+              int run = 0;
+              for (int w = 0; w < W; ++w) {
+                  s_gat[w] = run;
+                  run += s_gcnt[w];
+              }
+              s_gbase = run ? atomicAdd(nlist, (unsigned long long)run) : 0ULL;
+          }
+          __syncthreads();
+      }
+      for (int t8 = 0; t8 < W; ++t8) {
+        const int64_t ti = gi * W + t8;
+        if (ti >= ntiles) break;
         const int64_t tile = ti * kCompactTile;
         // slots are chunk-aligned per unit and kCompactTile == kChunk: one unit
         const int ui = chunk_unit ? __ldg(&chunk_unit[ti]) : find_unit(units, n_units, tile);
@@ -609,7 +640,10 @@ k_prim_compact(TraceCfg cfg, const GridDev *__restrict__ grids,
                 const bool real = r < U.ray_end && alias_ok;
                 // streaming read: every hit slot is read once here
                 hv[q] = __ldcs(reinterpret_cast<const ulonglong2 *>(slots) + slot);
-                hit = real && hv[q].x != kNoHitBits;
+                // with the bitmap a marked slot IS a hit (the group's list
+                // space was reserved from the bitmap counts); an aliasing
+                // violation is reported through the error flag instead
+                hit = hitmap ? true : (real && hv[q].x != kNoHitBits);
                 // the hit moves into the work list; its slot returns to the
                 // raster's all-ones "no hit" (no memset before the next
                 // pass).  Misses and padding keep their all-ones bits.
@@ -634,7 +668,8 @@ k_prim_compact(TraceCfg cfg, const GridDev *__restrict__ grids,
             (&pos[0][0])[lane] = incl - v;
             if (lane == 31) {
                 const int run = incl;
-                s_at = run ? atomicAdd(nlist, (unsigned long long)run) : 0ULL;
+                s_at = hitmap ? s_gbase + (unsigned long long)s_gat[t8]
+                              : (run ? atomicAdd(nlist, (unsigned long long)run) : 0ULL);
                 // this chunk's hits: list[at, at + run), in slot order
                 chunk_hits[ti] = make_uint2((unsigned int)s_at, (unsigned int)run);
             }
@@ -658,6 +693,7 @@ k_prim_compact(TraceCfg cfg, const GridDev *__restrict__ grids,
             }
         }
         __syncthreads();
+      }
     }
 }
 
