@@ -104,7 +104,15 @@ __device__ inline int find_unit(const UnitDev *u, int n, int64_t slot)
 __device__ inline void grid_origin(const GridDev &g, int64_t r, double &ox,
                                             double &oy, double &oz)
 {
-    int64_t i = r / g.n_v, j = r - i * g.n_v;
+    int64_t i, j;
+    if ((uint64_t)r < 0xffffffffULL) {   // 32-bit division (apertures < 2^32 rays)
+        const uint32_t q = (uint32_t)r / (uint32_t)g.n_v;
+        i = q;
+        j = r - (int64_t)q * g.n_v;
+    } else {
+        i = r / g.n_v;
+        j = r - i * g.n_v;
+    }
     double si = DM(DA((double)i, 0.5), g.spacing);
     double sj = DM(DA((double)j, 0.5), g.spacing);
     double bx = DA(g.corner[0], DM(si, g.u[0]));
