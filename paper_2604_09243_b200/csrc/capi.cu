@@ -1037,9 +1037,14 @@ static RasterArgs raster_args(const sbr_bvh *bvh, const GridDev *grids, const in
 
 // big-triangle chunk queue of the raster pass (grow-only, 4M items = 64 MB);
 // SBR_BIG_CAP (tests) shrinks it to force the overflow path
-static cudaError_t attach_big_queue(sbr_ctx *ctx, RasterArgs &ra)
+// rays: ray slots of the launch.  Queued chunks run at about rays / 256
+// (C5: 3.7M for 1.0e9 rays), so the queue holds rays / 64 (64k .. 16M) and
+// the set-up table rays / 512 triangles (16k .. 2M) -- sized to the launch,
+// not to the largest workload.  Overflow stays exact (walked in k_raster).
+static cudaError_t attach_big_queue(sbr_ctx *ctx, RasterArgs &ra, int64_t rays)
 {
-    size_t cap = (size_t)1 << 24;   // 16M chunks (256 MB): C5 needs ~3.7M
+    size_t cap = (size_t)std::min<int64_t>((int64_t)1 << 24,
+                                           std::max<int64_t>((int64_t)1 << 16, rays / 64));
     if (const char *s = getenv("SBR_BIG_CAP")) {
         const long long v = atoll(s);
         if (v >= 1 && v < (long long)cap) cap = (size_t)v;
@@ -1050,8 +1055,8 @@ static cudaError_t attach_big_queue(sbr_ctx *ctx, RasterArgs &ra)
     ra.big = ctx->big.p;
     ra.nbig = ctx->nbig.p;
     ra.big_cap = (int64_t)cap;
-    // set-up table: 2M triangles (512 MB; C5 queues ~1M)
-    const size_t scap = (size_t)1 << 21;
+    const size_t scap = (size_t)std::min<int64_t>((int64_t)1 << 21,
+                                                  std::max<int64_t>((int64_t)1 << 14, rays / 512));
     e = ctx->setups.reserve(scap * kRasterSetupBytes);
     if (e == cudaSuccess) e = ctx->nsetup.reserve(1);
     if (e != cudaSuccess) return e;
@@ -1205,7 +1210,7 @@ static int trace_full_common(sbr_ctx *ctx, const sbr_mesh *mesh, const sbr_bvh *
             ra.stats = ctx->counter.p + 2;
             ra.row_lo = i_begin;
             ra.row_hi = i_end;
-            CUDA_TRY(attach_big_queue(ctx, ra));
+            CUDA_TRY(attach_big_queue(ctx, ra, n));
             CUDA_TRY(launch_raster(ra, st, ctx->stats()));
         }
         CUDA_TRY(launch_trace_full(cfg, dg.p, o.p, d.p, n, r_base, fo, prim.p, ctx->counter.p,
@@ -1432,7 +1437,7 @@ static int run_units(sbr_ctx *ctx, const sbr_bvh *bvh, const std::vector<UnitDev
             ra.hitmap = ctx->hitmap.p;
             ra.counter = ctx->counter.p + 1;
             ra.stats = ctx->counter.p + 2;
-            CUDA_TRY(attach_big_queue(ctx, ra));
+            CUDA_TRY(attach_big_queue(ctx, ra, slots));
             for (int g : bgrids)       // a grid of the batch with a segment outside it
                 for (int64_t q = seg_base[g]; q < seg_base[g + 1] && !ra.sparse; ++q)
                     ra.sparse = seg_slot[q] == kNoSlot;
