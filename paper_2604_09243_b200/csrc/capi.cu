@@ -1,6 +1,7 @@
 // capi.cu -- the extern "C" boundary (include/sbr200.h): handles, argument
 // validation, host<->device staging and the batched solve orchestration.
 #include <chrono>
+#include <condition_variable>
 #include <dlfcn.h>
 #include <cmath>
 #include <cstdarg>
@@ -73,6 +74,70 @@ extern "C" int sbr_abi_version(void) { return SBR200_ABI_VERSION; }
 // ---------------------------------------------------------------------------
 // handles
 // ---------------------------------------------------------------------------
+// Persistent host copy workers for upload_host: spawning threads per chunk
+// cost ~0.3 ms a chunk, more than the 16 MB copy itself.
+struct CopyPool {
+    std::vector<std::thread> th;
+    std::mutex m;
+    std::condition_variable go, done;
+    uint64_t gen = 0;
+    int pending = 0;
+    bool stop = false;
+    unsigned char *dst = nullptr;
+    const unsigned char *src = nullptr;
+    size_t n = 0, part = 0;
+
+    int workers() const { return (int)th.size() + 1; }
+    void start(int nth)
+    {
+        for (int t = 1; t < nth; ++t)
+            th.emplace_back([this, t] {
+                uint64_t seen = 0;
+                for (;;) {
+                    size_t a, z;
+                    unsigned char *d;
+                    const unsigned char *s;
+                    {
+                        std::unique_lock<std::mutex> lk(m);
+                        go.wait(lk, [&] { return stop || gen != seen; });
+                        if (stop) return;
+                        seen = gen;
+                        a = std::min(n, t * part), z = std::min(n, a + part);
+                        d = dst, s = src;
+                    }
+                    if (z > a) memcpy(d + a, s + a, z - a);
+                    std::lock_guard<std::mutex> lk(m);
+                    if (--pending == 0) done.notify_one();
+                }
+            });
+    }
+    // memcpy(d, s, bytes) split over the workers and the calling thread
+    void copy(unsigned char *d, const unsigned char *s, size_t bytes)
+    {
+        const int w = workers();
+        const size_t p = (bytes + w - 1) / w;
+        if (w > 1) {
+            std::lock_guard<std::mutex> lk(m);
+            dst = d, src = s, n = bytes, part = p, pending = w - 1, ++gen;
+            go.notify_all();
+        }
+        memcpy(d, s, std::min(bytes, p));
+        if (w > 1) {
+            std::unique_lock<std::mutex> lk(m);
+            done.wait(lk, [&] { return pending == 0; });
+        }
+    }
+    ~CopyPool()
+    {
+        {
+            std::lock_guard<std::mutex> lk(m);
+            stop = true;
+        }
+        go.notify_all();
+        for (auto &t : th) t.join();
+    }
+};
+
 struct sbr_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -116,6 +181,7 @@ struct sbr_ctx {
     // pinned double buffer for large host->device uploads (upload_host)
     unsigned char *pin[2] = {nullptr, nullptr};
     cudaEvent_t pin_ev[2] = {nullptr, nullptr};
+    CopyPool copiers;            // host threads filling the pinned buffers
     Arena ws;                    // LBVH build workspace
     SahWork sah;                 // SAH build workspace
     // optional per-kernel CUDA-event timing of the solve pipeline
@@ -323,11 +389,12 @@ extern "C" int sbr_ctx_launch_count(sbr_ctx *ctx, int64_t *count_out)
 // ---------------------------------------------------------------------------
 // mesh
 // ---------------------------------------------------------------------------
-// Host (pageable) -> device upload through two pinned 16 MB chunks: host
-// threads copy chunk k+1 into one pinned buffer while the DMA engine moves
+// Host (pageable) -> device upload through two pinned 16 MB chunks: the
+// persistent copy workers (CopyPool) copy chunk k+1 into one pinned buffer while the DMA engine moves
 // chunk k from the other (pageable cudaMemcpy runs at ~10 GB/s and
 // serialises the staging copy with the transfer).
 static constexpr size_t kPinChunk = (size_t)16 << 20;
+static constexpr unsigned kCopyThreads = 4;   // B200 box: 4 beat 1, 2, 8, 12, 16
 
 static cudaError_t upload_host(sbr_ctx *ctx, void *dst, const void *src, size_t bytes)
 {
@@ -346,8 +413,10 @@ static cudaError_t upload_host(sbr_ctx *ctx, void *dst, const void *src, size_t 
             cudaEventRecord(ctx->pin_ev[b], ctx->stream);
         }
     }
-    const unsigned hw = std::thread::hardware_concurrency();
-    const int nth = (int)std::max(1u, std::min(8u, hw ? hw : 1u));
+    if (ctx->copiers.th.empty()) {
+        const unsigned hw = std::thread::hardware_concurrency();
+        ctx->copiers.start((int)std::max(1u, std::min(kCopyThreads, hw ? hw : 1u)));
+    }
     const unsigned char *s = static_cast<const unsigned char *>(src);
     unsigned char *d = static_cast<unsigned char *>(dst);
     int b = 0;
@@ -355,14 +424,7 @@ static cudaError_t upload_host(sbr_ctx *ctx, void *dst, const void *src, size_t 
         const size_t n = std::min(kPinChunk, bytes - off);
         cudaError_t e = cudaEventSynchronize(ctx->pin_ev[b]);   // buffer b free again
         if (e != cudaSuccess) return e;
-        std::vector<std::thread> pool;
-        const size_t part = (n + nth - 1) / nth;
-        for (int t = 1; t < nth; ++t) {
-            const size_t a = std::min(n, t * part), z = std::min(n, a + part);
-            if (z > a) pool.emplace_back([=] { memcpy(ctx->pin[b] + a, s + off + a, z - a); });
-        }
-        memcpy(ctx->pin[b], s + off, std::min(n, part));
-        for (auto &th : pool) th.join();
+        ctx->copiers.copy(ctx->pin[b], s + off, n);
         e = cudaMemcpyAsync(d + off, ctx->pin[b], n, cudaMemcpyHostToDevice, ctx->stream);
         if (e == cudaSuccess) e = cudaEventRecord(ctx->pin_ev[b], ctx->stream);
         if (e != cudaSuccess) return e;
