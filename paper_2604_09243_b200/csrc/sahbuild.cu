@@ -278,35 +278,85 @@ k_bin(const double *__restrict__ tb, const int *__restrict__ idx,
         __syncthreads();
     }
     // near the root few segments share every bin: R replicas (chosen by
-    // block) spread the global atomics; k_select merges them (exact)
+    // block) spread the global atomics; k_select merges them (exact).
+    // Consecutive elements mostly fall into the same bin (the order is
+    // spatially coherent), so each axis first reduces runs of lanes with
+    // equal (segment, bin) in registers and only run heads touch memory:
+    // shared 64-bit min/max are CAS loops that serialise on a shared bin.
     const int rep = blockIdx.x % R;
-    for (int64_t i = t0 + tid; i < t1; i += blockDim.x) {
-        const int s = eseg[i];
-        if (s < 0 || sc[s] <= kSmallSeg) continue;
-        const double *b = tb + 9 * (int64_t)idx[i];
-        const SegAcc &A = acc[s];
-#pragma unroll
-        for (int axis = 0; axis < 3; ++axis) {
-            const double c_lo = unordd(A.cb[axis]), c_hi = unordd(A.cb[3 + axis]);
-            if (!(c_hi > c_lo)) continue;                   // bvh.py:177-178
-            const double scale = __ddiv_rn((double)nbins, __dsub_rn(c_hi, c_lo));
-            const int bi = bin_of(b[6 + axis], c_lo, scale, nbins);
-            unsigned int *cp;
-            unsigned long long *bb;
-            if (local) {
-                const int k = ((s - s_lo) * 3 + axis) * nbins + bi;
-                cp = scnt + k;
-                bb = sbb + 6 * k;
-            } else {
-                const int64_t slot = (((int64_t)s * R + rep) * 3 + axis) * nbins + bi;
-                cp = cnt + slot;
-                bb = bbox + 6 * slot;
-            }
-            atomicAdd(cp, 1u);
+    const int lane = tid & 31;
+    for (int64_t i = t0 + tid; i - lane < t1; i += blockDim.x) {
+        int s = i < t1 ? eseg[i] : -1;
+        if (s >= 0 && sc[s] <= kSmallSeg) s = -1;
+        unsigned long long bx[6];
+        double cen[3];
+        if (s >= 0) {
+            const double *b = tb + 9 * (int64_t)idx[i];
 #pragma unroll
             for (int q = 0; q < 3; ++q) {
-                atomicMin(&bb[q], ordd(b[q]));
-                atomicMax(&bb[3 + q], ordd(b[3 + q]));
+                bx[q] = ordd(b[q]);
+                bx[3 + q] = ordd(b[3 + q]);
+                cen[q] = b[6 + q];
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                bx[q] = kOrdPosInf;
+                bx[3 + q] = kOrdNegInf;
+                cen[q] = 0.0;
+            }
+        }
+        const SegAcc *A = acc + (s >= 0 ? s : 0);
+#pragma unroll 1
+        for (int axis = 0; axis < 3; ++axis) {
+            int bi = -1;
+            if (s >= 0) {
+                const double c_lo = unordd(A->cb[axis]), c_hi = unordd(A->cb[3 + axis]);
+                if (c_hi > c_lo)                                // bvh.py:177-178
+                    bi = bin_of(cen[axis], c_lo, __ddiv_rn((double)nbins, __dsub_rn(c_hi, c_lo)),
+                                nbins);
+            }
+            unsigned int c = bi >= 0 ? 1u : 0u;
+            unsigned long long v[6];
+#pragma unroll
+            for (int q = 0; q < 6; ++q) v[q] = bx[q];
+            // runs of equal (segment, bin): bins are not monotone along the
+            // elements, so lanes compare run starts, not keys
+            const int sp = __shfl_up_sync(0xffffffffu, s, 1);
+            const int bp = __shfl_up_sync(0xffffffffu, bi, 1);
+            const bool head = lane == 0 || sp != s || bp != bi;
+            const unsigned heads = __ballot_sync(0xffffffffu, head);
+            const int rs = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int ro = __shfl_down_sync(0xffffffffu, rs, o);
+                const unsigned int co = __shfl_down_sync(0xffffffffu, c, o);
+                const bool same = lane + o < 32 && ro == rs;
+                if (same) c += co;
+#pragma unroll
+                for (int q = 0; q < 6; ++q) {
+                    const unsigned long long w = __shfl_down_sync(0xffffffffu, v[q], o);
+                    if (same) v[q] = q < 3 ? (w < v[q] ? w : v[q]) : (w > v[q] ? w : v[q]);
+                }
+            }
+            if (bi >= 0 && head) {                                  // head of its run
+                unsigned int *cp;
+                unsigned long long *bb;
+                if (local) {
+                    const int k = ((s - s_lo) * 3 + axis) * nbins + bi;
+                    cp = scnt + k;
+                    bb = sbb + 6 * k;
+                } else {
+                    const int64_t slot = (((int64_t)s * R + rep) * 3 + axis) * nbins + bi;
+                    cp = cnt + slot;
+                    bb = bbox + 6 * slot;
+                }
+                atomicAdd(cp, c);
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    atomicMin(&bb[q], v[q]);
+                    atomicMax(&bb[3 + q], v[3 + q]);
+                }
             }
         }
     }
