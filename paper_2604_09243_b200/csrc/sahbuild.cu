@@ -403,9 +403,6 @@ k_select(const SegAcc *__restrict__ acc, const unsigned int *__restrict__ cnt,
 {
     __shared__ int64_t sbc[kSelWarps][3][kSahMaxBins];
     __shared__ double smn[kSelWarps][3][3][kSahMaxBins], smx[kSelWarps][3][3][kSahMaxBins];
-    __shared__ double abest[kSelWarps][3];
-    __shared__ int ab[kSelWarps][3], ahave[kSelWarps][3];
-    __shared__ int64_t anl[kSelWarps][3];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int s = blockIdx.x * kSelWarps + w;
     if (s >= S || sc[s] <= kSmallSeg) return;         // warp-uniform; small: k_small
@@ -432,6 +429,7 @@ k_select(const SegAcc *__restrict__ acc, const unsigned int *__restrict__ cnt,
             unsigned long long mn[3] = {kOrdPosInf, kOrdPosInf, kOrdPosInf};
             unsigned long long mx[3] = {kOrdNegInf, kOrdNegInf, kOrdNegInf};
             int64_t c = 0;
+#pragma unroll 4
             for (int rep = 0; rep < R; ++rep) {
                 const int64_t slot = (((int64_t)s * R + rep) * 3 + axis) * B + b;
                 const unsigned long long *bb = bbox + 6 * slot;
@@ -452,74 +450,71 @@ k_select(const SegAcc *__restrict__ acc, const unsigned int *__restrict__ cnt,
         __syncwarp();
         double sa_p = sa_of(lo, hi);
         if (!(sa_p >= 1e-300)) sa_p = 1e-300;          // max(sa, 1e-300)
-        if (lane < 3) {
-            const int axis = lane;
-            bool have = false;
-            double best = 0.0;
-            int bb_best = -1;
-            int64_t nl_best = 0;
-            const double c_lo = unordd(A.cb[axis]), c_hi = unordd(A.cb[3 + axis]);
-            if (c_hi > c_lo) {
-                // suffix sweep (right side of boundary b is bins b+1..B-1)
-                double rlo[3][kSahMaxBins], rhi[3][kSahMaxBins];
-                int64_t rn[kSahMaxBins];
-                double l3[3] = {INFINITY, INFINITY, INFINITY}, h3[3] = {-INFINITY, -INFINITY, -INFINITY};
-                int64_t acc_n = 0;
-                for (int b = B - 1; b >= 0; --b) {
-                    acc_n += sbc[w][axis][b];
+        // every (axis, boundary) candidate in a lane of its own: the child
+        // boxes are unions over bins (exact in any order), so the counts,
+        // boxes and costs are those of the reference's running sweep; the
+        // warp then takes the first minimum in (axis, boundary) order, the
+        // reference's strict-< scan (bvh.py:175-207)
+        bool ok[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) ok[q] = unordd(A.cb[3 + q]) > unordd(A.cb[q]);   // bvh.py:177-178
+        bool have = false;
+        double best = 0.0;
+        int best_c = 0x7fffffff;
+        long long best_nl = 0;
+        const int ncand = 3 * (B - 1);
+        for (int cand = lane; cand < ncand; cand += 32) {
+            const int axis = cand / (B - 1), b = cand - axis * (B - 1);
+            if (!ok[axis]) continue;
+            double l3[3] = {INFINITY, INFINITY, INFINITY}, h3[3] = {-INFINITY, -INFINITY, -INFINITY};
+            double r3[3] = {INFINITY, INFINITY, INFINITY}, g3[3] = {-INFINITY, -INFINITY, -INFINITY};
+            long long ln = 0, nr = 0;
+            for (int k = 0; k < B; ++k) {
+                const long long c = sbc[w][axis][k];
+                if (k <= b) {
+                    ln += c;
+#pragma unroll
                     for (int q = 0; q < 3; ++q) {
-                        l3[q] = fmin(l3[q], smn[w][q][axis][b]);
-                        h3[q] = fmax(h3[q], smx[w][q][axis][b]);
-                        rlo[q][b] = l3[q];
-                        rhi[q][b] = h3[q];
+                        l3[q] = fmin(l3[q], smn[w][q][axis][k]);
+                        h3[q] = fmax(h3[q], smx[w][q][axis][k]);
                     }
-                    rn[b] = acc_n;
-                }
-                for (int q = 0; q < 3; ++q) { l3[q] = INFINITY; h3[q] = -INFINITY; }
-                int64_t ln = 0;
-                for (int b = 0; b < B - 1; ++b) {
-                    ln += sbc[w][axis][b];
+                } else {
+                    nr += c;
+#pragma unroll
                     for (int q = 0; q < 3; ++q) {
-                        l3[q] = fmin(l3[q], smn[w][q][axis][b]);
-                        h3[q] = fmax(h3[q], smx[w][q][axis][b]);
-                    }
-                    const int64_t nr = rn[b + 1];
-                    if (ln == 0 || nr == 0) continue;
-                    double rl[3] = {rlo[0][b + 1], rlo[1][b + 1], rlo[2][b + 1]};
-                    double rh[3] = {rhi[0][b + 1], rhi[1][b + 1], rhi[2][b + 1]};
-                    const double sal = sa_of(l3, h3), sar = sa_of(rl, rh);
-                    // sah_cost (bvh.py:124-127): c_t + (sal/sa_p) n_l c_i + (sar/sa_p) n_r c_i
-                    const double cost = __dadd_rn(
-                        __dadd_rn(P.c_t, __dmul_rn(__dmul_rn(__ddiv_rn(sal, sa_p), (double)ln), P.c_i)),
-                        __dmul_rn(__dmul_rn(__ddiv_rn(sar, sa_p), (double)nr), P.c_i));
-                    if (!have || cost < best) {
-                        have = true;
-                        best = cost;
-                        bb_best = b;
-                        nl_best = ln;
+                        r3[q] = fmin(r3[q], smn[w][q][axis][k]);
+                        g3[q] = fmax(g3[q], smx[w][q][axis][k]);
                     }
                 }
             }
-            ahave[w][axis] = have;
-            abest[w][axis] = best;
-            ab[w][axis] = bb_best;
-            anl[w][axis] = nl_best;
+            if (ln == 0 || nr == 0) continue;
+            const double sal = sa_of(l3, h3), sar = sa_of(r3, g3);
+            // sah_cost (bvh.py:124-127): c_t + (sal/sa_p) n_l c_i + (sar/sa_p) n_r c_i
+            const double cost = __dadd_rn(
+                __dadd_rn(P.c_t, __dmul_rn(__dmul_rn(__ddiv_rn(sal, sa_p), (double)ln), P.c_i)),
+                __dmul_rn(__dmul_rn(__ddiv_rn(sar, sa_p), (double)nr), P.c_i));
+            if (!have || cost < best) {   // candidates ascend per lane: keeps the first
+                have = true;
+                best = cost;
+                best_c = cand;
+                best_nl = ln;
+            }
         }
-        __syncwarp();
-        if (lane == 0) {
-            bool have = false;
-            double best = 0.0;
-            for (int axis = 0; axis < 3; ++axis) {
-                if (!ahave[w][axis]) continue;
-                if (!have || abest[w][axis] < best) {
-                    have = true;
-                    best = abest[w][axis];
-                    r.axis = axis;
-                    r.boundary = ab[w][axis];
-                    r.nl = anl[w][axis];
-                }
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+            const int oh = __shfl_xor_sync(0xffffffffu, (int)have, o);
+            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int oc = __shfl_xor_sync(0xffffffffu, best_c, o);
+            const long long on = __shfl_xor_sync(0xffffffffu, best_nl, o);
+            if (oh && (!have || ob < best || (ob == best && oc < best_c))) {
+                have = true; best = ob; best_c = oc; best_nl = on;
             }
+        }
+        if (lane == 0) {
             if (have) {
+                r.axis = best_c / (B - 1);
+                r.boundary = best_c - r.axis * (B - 1);
+                r.nl = best_nl;
                 const double c_lo = unordd(A.cb[r.axis]), c_hi = unordd(A.cb[3 + r.axis]);
                 r.c_lo = c_lo;
                 r.scale = __ddiv_rn((double)B, __dsub_rn(c_hi, c_lo));
@@ -581,14 +576,24 @@ k_small(const double *__restrict__ tb, const int *__restrict__ idx,
             v[6 + q] = kOrdPosInf; v[9 + q] = kOrdNegInf;
         }
     }
+    // butterfly over the 2^ceil(log2 n) lanes that hold triangles: lane 0
+    // (and its group) ends with the full reduction; the other lanes get it
+    // by broadcast when they take part in the candidate sweep
+    const bool leaf = !(n > P.n_leaf && depth < P.max_depth);
+    const int span = n <= 1 ? 1 : 1 << (32 - __clz(n - 1));
 #pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
+    for (int o = 1; o < 32; o <<= 1) {
+        if (o >= span) break;                          // warp-uniform
 #pragma unroll
         for (int q = 0; q < 12; ++q) {
             const unsigned long long x = __shfl_xor_sync(0xffffffffu, v[q], o);
             const bool is_min = (q < 3) || (q >= 6 && q < 9);
             v[q] = is_min ? (x < v[q] ? x : v[q]) : (x > v[q] ? x : v[q]);
         }
+    }
+    if (!leaf && span < 32) {
+#pragma unroll
+        for (int q = 0; q < 12; ++q) v[q] = __shfl_sync(0xffffffffu, v[q], 0);
     }
     double lo[3], hi[3], clo[3], chi[3];
 #pragma unroll
@@ -604,23 +609,45 @@ k_small(const double *__restrict__ tb, const int *__restrict__ idx,
     SegSplit r;
     r.split = 0; r.axis = -1; r.boundary = -1; r.c_lo = 0.0; r.scale = 0.0; r.nl = 0;
     const int B = P.bins;
-    if (n > P.n_leaf && depth < P.max_depth) {
+    if (!leaf) {
         double scale[3];
+        unsigned occ[3];   // bins holding a triangle (B <= 32)
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
             scale[q] = chi[q] > clo[q] ? __ddiv_rn((double)B, __dsub_rn(chi[q], clo[q])) : 0.0;
-            if (lane < n) sbin[w][q][lane] = (unsigned char)bin_of(c[q], clo[q], scale[q], B);
+            const int bq = lane < n ? bin_of(c[q], clo[q], scale[q], B) : 0;
+            if (lane < n) sbin[w][q][lane] = (unsigned char)bq;
+            occ[q] = __reduce_or_sync(0xffffffffu, lane < n && bq < 32 ? 1u << bq : 0u);
         }
         __syncwarp();
         double sa_p = sa_of(lo, hi);
         if (!(sa_p >= 1e-300)) sa_p = 1e-300;          // max(sa, 1e-300)
+        // Boundary b moves exactly the triangles of bin b to the left, so a
+        // boundary after an empty bin repeats the previous partition (same
+        // cost, later in the scan: never chosen) or has an empty side.  With
+        // B <= 32 only the boundaries after occupied bins are evaluated,
+        // packed onto the lanes (one round instead of two for n <= 10).
+        const bool packed = B <= 32;
+        const unsigned bmask = B >= 33 ? 0xffffffffu : (1u << (B - 1)) - 1u;
+        int nc[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) nc[q] = chi[q] > clo[q] ? __popc(occ[q] & bmask) : 0;
         // best candidate of this lane over the rounds: (have, cost, index)
         bool have = false;
         double best = 0.0;
         int best_c = 0x7fffffff, best_nl = 0;
-        const int ncand = 3 * (B - 1);
-        for (int cand = lane; cand < ncand; cand += 32) {
-            const int axis = cand / (B - 1), b = cand - axis * (B - 1);
+        const int ncand = packed ? nc[0] + nc[1] + nc[2] : 3 * (B - 1);
+        for (int k = lane; k < ncand; k += 32) {
+            int axis, b;
+            if (packed) {   // k-th occupied boundary in (axis, boundary) order
+                axis = k < nc[0] ? 0 : (k < nc[0] + nc[1] ? 1 : 2);
+                const int kk = k - (axis > 0 ? nc[0] : 0) - (axis > 1 ? nc[1] : 0);
+                b = (int)__fns(occ[axis] & bmask, 0, kk + 1);
+            } else {
+                axis = k / (B - 1);
+                b = k - axis * (B - 1);
+            }
+            const int cand = axis * (B - 1) + b;
             if (!(chi[axis] > clo[axis])) continue;     // bvh.py:177-178
             double l3[3] = {INFINITY, INFINITY, INFINITY}, h3[3] = {-INFINITY, -INFINITY, -INFINITY};
             double r3[3] = {INFINITY, INFINITY, INFINITY}, g3[3] = {-INFINITY, -INFINITY, -INFINITY};
