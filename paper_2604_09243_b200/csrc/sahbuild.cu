@@ -258,36 +258,22 @@ k_bin(const double *__restrict__ tb, const int *__restrict__ idx,
       int R, unsigned int *__restrict__ cnt, unsigned long long *__restrict__ bbox,
       const int64_t *__restrict__ sc)
 {
-    __shared__ unsigned int scnt[kLocalSegs * 3 * kSahMaxBins];
-    __shared__ unsigned long long sbb[kLocalSegs * 3 * kSahMaxBins * 6];
-    __shared__ int srange[2];
     const int tid = threadIdx.x;
     const int64_t t0 = (int64_t)blockIdx.x * kTile;
     const int64_t t1 = t0 + kTile < n ? t0 + kTile : n;
-    int s_lo, s_hi;
-    tile_range(eseg, sc, t0, t1, 1, srange, s_lo, s_hi);
-    if (s_hi < 0) return;                               // block-uniform
-    const bool local = s_hi - s_lo < kLocalSegs;
-    const int nloc = (s_hi - s_lo + 1) * 3 * nbins;
-    if (local) {
-        for (int k = tid; k < nloc; k += blockDim.x) {
-            scnt[k] = 0u;
-#pragma unroll
-            for (int q = 0; q < 3; ++q) { sbb[6 * k + q] = kOrdPosInf; sbb[6 * k + 3 + q] = kOrdNegInf; }
-        }
-        __syncthreads();
-    }
     // near the root few segments share every bin: R replicas (chosen by
     // block) spread the global atomics; k_select merges them (exact).
     // Consecutive elements mostly fall into the same bin (the order is
     // spatially coherent), so each axis first reduces runs of lanes with
-    // equal (segment, bin) in registers and only run heads touch memory:
-    // shared 64-bit min/max are CAS loops that serialise on a shared bin.
+    // equal (segment, bin) in registers and only run heads touch memory,
+    // with fire-and-forget global min / max (shared-memory 64-bit min / max
+    // are CAS loops: a block-local pre-reduction was slower).
     const int rep = blockIdx.x % R;
     const int lane = tid & 31;
     for (int64_t i = t0 + tid; i - lane < t1; i += blockDim.x) {
         int s = i < t1 ? eseg[i] : -1;
         if (s >= 0 && sc[s] <= kSmallSeg) s = -1;
+        if (!__any_sync(0xffffffffu, s >= 0)) continue;   // all k_small's (deep levels)
         unsigned long long bx[6];
         double cen[3];
         if (s >= 0) {
@@ -340,38 +326,15 @@ k_bin(const double *__restrict__ tb, const int *__restrict__ idx,
                 }
             }
             if (bi >= 0 && head) {                                  // head of its run
-                unsigned int *cp;
-                unsigned long long *bb;
-                if (local) {
-                    const int k = ((s - s_lo) * 3 + axis) * nbins + bi;
-                    cp = scnt + k;
-                    bb = sbb + 6 * k;
-                } else {
-                    const int64_t slot = (((int64_t)s * R + rep) * 3 + axis) * nbins + bi;
-                    cp = cnt + slot;
-                    bb = bbox + 6 * slot;
-                }
+                const int64_t slot = (((int64_t)s * R + rep) * 3 + axis) * nbins + bi;
+                unsigned int *cp = cnt + slot;
+                unsigned long long *bb = bbox + 6 * slot;
                 atomicAdd(cp, c);
 #pragma unroll
                 for (int q = 0; q < 3; ++q) {
                     atomicMin(&bb[q], v[q]);
                     atomicMax(&bb[3 + q], v[3 + q]);
                 }
-            }
-        }
-    }
-    if (local) {
-        __syncthreads();
-        for (int k = tid; k < nloc; k += blockDim.x) {
-            const unsigned int c = scnt[k];
-            if (c == 0u) continue;
-            const int ls = k / (3 * nbins), rest = k - ls * 3 * nbins;
-            const int64_t slot = ((int64_t)(s_lo + ls) * R + rep) * 3 * nbins + rest;
-            atomicAdd(&cnt[slot], c);
-#pragma unroll
-            for (int q = 0; q < 3; ++q) {
-                atomicMin(&bbox[6 * slot + q], sbb[6 * k + q]);
-                atomicMax(&bbox[6 * slot + 3 + q], sbb[6 * k + 3 + q]);
             }
         }
     }
