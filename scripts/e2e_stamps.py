@@ -8,7 +8,7 @@ import torch
 import bench
 import paper_2604_09243_b200 as sbr
 mesh, lam, cfg = bench.workload(1.0, 360)
-for rep in range(4):
+for rep in range(int(os.environ.get('REPS', '4'))):
     fresh = dataclasses.replace(mesh, _dev={})
     torch.cuda.synchronize()
     t0 = time.perf_counter()
