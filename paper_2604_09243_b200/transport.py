@@ -51,11 +51,15 @@ def _cross3(a, b) -> np.ndarray:
     return np.array([a1 * b2 - a2 * b1, a2 * b0 - a0 * b2, a0 * b1 - a1 * b0])
 
 
+_AXES = np.eye(3)
+_AXES.setflags(write=False)
+
+
 def orthonormal_basis(k_inc) -> tuple[np.ndarray, np.ndarray]:
     """Right-handed (u, v, k): u = normalize(seed x k), v = k x u; the seed is
     the world axis least aligned with k (ties x -> y -> z)."""
     k = np.asarray(k_inc, dtype=np.float64)
-    seed = np.eye(3)[int(np.argmin(np.abs(k)))]
+    seed = _AXES[int(np.argmin(np.abs(k)))]
     u = _cross3(seed, k)
     u /= np.linalg.norm(u)
     return u, _cross3(k, u)
@@ -139,22 +143,30 @@ def build_aperture(aabb: Aabb, direction: IncidentDirection, spacing: float,
                 f"ray spacing {spacing:g} exceeds wavelength/{sampling_factor:g}"
                 f" = {wavelength / sampling_factor:g} (ratio {chk.ratio:.3f});"
                 " pass allow_aliasing to override")
+    return _aperture(aabb.corners(), aabb.diagonal(), direction, spacing, margin)
+
+
+def _aperture(pts: np.ndarray, standoff: float, direction: IncidentDirection, spacing: float,
+              margin: float) -> ApertureGrid:
+    """build_aperture after validation, from the box's corners and diagonal
+    (computed once per sweep by sweep_grids: the same values every cell)."""
     k = direction.k_inc
     u, v = orthonormal_basis(k)
-    pts = aabb.corners()
-    pu, pv, pk = pts @ u, pts @ v, pts @ k
-    ext_u = float(pu.max() - pu.min())
-    ext_v = float(pv.max() - pv.min())
+    # min / max of the eight projections as Python floats: the same values
+    # (and the same IEEE subtraction / addition) as the numpy reductions
+    pu, pv, pk = (pts @ u).tolist(), (pts @ v).tolist(), (pts @ k).tolist()
+    pu_lo, pu_hi, pv_lo, pv_hi = min(pu), max(pu), min(pv), max(pv)
+    ext_u = pu_hi - pu_lo
+    ext_v = pv_hi - pv_lo
     n_u = max(1, math.ceil((1.0 + margin) * ext_u / spacing))
     n_v = max(1, math.ceil((1.0 + margin) * ext_v / spacing))
     jit_u = ((_registration_fraction(direction.theta, direction.phi, 1.0) - 0.5)
              * min(spacing, max(0.0, n_u * spacing - ext_u)))
     jit_v = ((_registration_fraction(direction.theta, direction.phi, 2.0) - 0.5)
              * min(spacing, max(0.0, n_v * spacing - ext_v)))
-    standoff = aabb.diagonal()
-    plane = float(pk.min()) - standoff
-    mid_u = 0.5 * float(pu.max() + pu.min())
-    mid_v = 0.5 * float(pv.max() + pv.min())
+    plane = min(pk) - standoff
+    mid_u = 0.5 * (pu_hi + pu_lo)
+    mid_v = 0.5 * (pv_hi + pv_lo)
     corner = (plane * k + (mid_u - 0.5 * n_u * spacing + jit_u) * u
               + (mid_v - 0.5 * n_v * spacing + jit_v) * v)
     return ApertureGrid(u=u, v=v, k_inc=k, corner=corner, spacing=spacing, n_u=n_u,
