@@ -447,7 +447,19 @@ def test_gpu_build_is_the_reference_tree(name, rule):
     tree.validate(mesh)
 
 
-@pytest.mark.parametrize("case", ["aircraft", "sphere_s6", "rough", "bins8_leaf2", "median"])
+# bins 2 / 32 / 64 exercise the candidate packing of k_small (B <= 32) and
+# its unpacked path (B > 32), and k_select's per-lane candidates over one to
+# several rounds; depth8 forces leaves above 32 triangles at max_depth
+_SAH_CASES = {
+    "bins8_leaf2": dict(bins_per_axis=8, n_leaf=2, c_t=0.5, c_i=2.0),
+    "bins2": dict(bins_per_axis=2, n_leaf=2),
+    "bins32_leaf1": dict(bins_per_axis=32, n_leaf=1),
+    "bins64_ct3": dict(bins_per_axis=64, n_leaf=3, c_t=3.0),
+    "depth8": dict(max_depth=8, n_leaf=2),
+}
+
+
+@pytest.mark.parametrize("case", ["aircraft", "sphere_s6", "rough", "median", *_SAH_CASES])
 def test_gpu_sah_build_matches_oracle_large(orc, case):
     params = sbr.BuildParams(split_rule="median" if case == "median" else "sah")
     if case == "aircraft":
@@ -458,10 +470,11 @@ def test_gpu_sah_build_matches_oracle_large(orc, case):
         mesh = meshgen.perturbed_grid_mesh(cells=150, extent=4.0, amplitude=0.08, seed=3)
     else:
         mesh = meshgen.generate_aircraft(density=0.03)
-        params = sbr.BuildParams(split_rule="sah", bins_per_axis=8, n_leaf=2, c_t=0.5, c_i=2.0)
+        params = sbr.BuildParams(split_rule="sah", **_SAH_CASES[case])
     tree = sbr.build(mesh, params)
     ref = orc.build(mesh.v0, mesh.v1, mesh.v2, split_rule=params.split_rule, n_leaf=params.n_leaf,
-                    bins_per_axis=params.bins_per_axis, c_t=params.c_t, c_i=params.c_i)
+                    bins_per_axis=params.bins_per_axis, c_t=params.c_t, c_i=params.c_i,
+                    max_depth=params.max_depth)
     for k in _TREE_KEYS:
         assert np.array_equal(getattr(tree, k), getattr(ref, k)), (case, k)
     assert tree.max_depth_seen == ref.max_depth_seen
