@@ -7,13 +7,15 @@
 // any order) or a short FP64 formula evaluated once per node, so the tree can
 // be built breadth-first with all nodes of a level in parallel:
 //   level loop (host):
-//     k_seg_of       element -> active segment (binary search on begins)
+//     element -> active segment: written by the previous level's
+//                    k_partition (median splits: k_seg_of, a binary search)
 //     k_bounds       node box + centroid bounds per segment (ordered-int
 //                    atomicMin/Max on doubles: exact)
 //     k_bin          per (segment, axis, bin) counts + child-box bounds
-//     k_select       one warp per segment: the reference's SAH sweep,
-//                    cost formula with the reference's association, tie to
-//                    the lowest (axis, boundary), leaf rule (bvh.py:154-215)
+//     k_select       one warp per segment, a lane per (axis, boundary)
+//                    candidate: the reference's SAH sweep, cost formula with
+//                    the reference's association, tie to the lowest (axis,
+//                    boundary), leaf rule (bvh.py:154-215)
 //     k_small        segments of <= kSmallSeg triangles skip the three
 //                    kernels above: one warp loads the triangles, reduces
 //                    the bounds and evaluates every (axis, boundary) in a
@@ -59,7 +61,8 @@ constexpr unsigned long long kOrdNegInf = 0x000fffffffffffffULL;   // ordd(-inf)
 // per-triangle bounds: tri_min, tri_max, centroid = (min + max) * 0.5
 // (bvh.py:227-231), AoS of 9 doubles
 __global__ void k_tri_bounds(const double *__restrict__ verts, int64_t n,
-                             double *__restrict__ tb, int *__restrict__ idx)
+                             double *__restrict__ tb, int *__restrict__ idx,
+                             int *__restrict__ eseg)
 {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (t >= n) return;
@@ -73,6 +76,7 @@ __global__ void k_tri_bounds(const double *__restrict__ verts, int64_t n,
         tb[9 * t + 6 + a] = __dmul_rn(__dadd_rn(lo, hi), 0.5);
     }
     idx[t] = (int)t;
+    eseg[t] = 0;   // level 0: one segment (later levels: k_partition)
 }
 
 
@@ -752,21 +756,28 @@ __global__ void k_flags(const double *__restrict__ tb, const int *__restrict__ i
     flag[i] = f;
 }
 
+// also the next level's element -> segment map: the children of split
+// segment s are segments 2 crank[s] (left) and 2 crank[s] + 1 (k_children),
+// elements of unsplit segments belong to none
 __global__ void k_partition(const int *__restrict__ idx, const int *__restrict__ eseg,
                             int64_t n, const SegSplit *__restrict__ sp,
                             const int64_t *__restrict__ sb, const int *__restrict__ flag,
-                            const int *__restrict__ rank, int *__restrict__ out)
+                            const int *__restrict__ rank, const int *__restrict__ crank,
+                            int *__restrict__ out, int *__restrict__ eseg_next)
 {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int s = eseg[i];
     int64_t dst = i;
+    int ns = -1;
     if (s >= 0 && sp[s].split) {
         const int64_t b = sb[s];
         const int64_t left = (int64_t)rank[i] - rank[b];       // flags before i in segment
         dst = flag[i] ? b + left : b + sp[s].nl + ((i - b) - left);
+        ns = 2 * crank[s] + (flag[i] ? 0 : 1);
     }
     out[dst] = idx[i];
+    eseg_next[dst] = ns;
 }
 
 // children of split segments -> next level; leaves recorded
@@ -927,7 +938,7 @@ cudaError_t sah_build(const double *d_verts, int64_t n, const SahParams &P, SahT
     const int B = P.bins;
     const int64_t max_nodes = 2 * n;   // binary tree with >= 1 triangle per leaf
     CK(w.tb.reserve(9 * (size_t)n));
-    CK(w.idx.reserve(n)); CK(w.idx2.reserve(n)); CK(w.eseg.reserve(n));
+    CK(w.idx.reserve(n)); CK(w.idx2.reserve(n)); CK(w.eseg.reserve(n)); CK(w.eseg2.reserve(n));
     CK(w.flag.reserve(n + 1)); CK(w.rank.reserve(n + 1));
     CK(w.node_box.reserve(6 * (size_t)max_nodes));
     CK(w.left.reserve(max_nodes)); CK(w.right.reserve(max_nodes));
@@ -946,7 +957,8 @@ cudaError_t sah_build(const double *d_verts, int64_t n, const SahParams &P, SahT
     int64_t *sb = w.sb.p, *sc = w.sc.p, *nsb = w.nsb.p, *nsc = w.nsc.p;
     int *snode = w.snode.p, *nsnode = w.nsnode.p;
 
-    k_tri_bounds<<<nblk(n, T), T, 0, st>>>(d_verts, n, w.tb.p, idx);
+    int *eseg = w.eseg.p, *eseg2 = w.eseg2.p;
+    k_tri_bounds<<<nblk(n, T), T, 0, st>>>(d_verts, n, w.tb.p, idx, eseg);
     ++*launches;
     const int64_t zero64 = 0;
     const int zero = 0;
@@ -972,12 +984,15 @@ cudaError_t sah_build(const double *d_verts, int64_t n, const SahParams &P, SahT
         }
         k_seg_init<<<nblk(std::max<int64_t>(nslots, S), T), T, 0, st>>>(
             w.acc.p, w.cnt.p, w.bbox.p, S, nslots, sc, (int64_t)R * 3 * B);
-        k_seg_of<<<nblk(n, T), T, 0, st>>>(sb, sc, S, n, w.eseg.p);
-        k_bounds<<<nblk(n, kTile), kTileThreads, 0, st>>>(w.tb.p, idx, w.eseg.p, n, w.acc.p, sc,
+        if (P.median && depth > 0) {   // SAH levels get the map from k_partition
+            k_seg_of<<<nblk(n, T), T, 0, st>>>(sb, sc, S, n, eseg);
+            ++*launches;
+        }
+        k_bounds<<<nblk(n, kTile), kTileThreads, 0, st>>>(w.tb.p, idx, eseg, n, w.acc.p, sc,
                                                           !P.median);
         CK(cudaMemsetAsync(w.sflag.p + S, 0, sizeof(int), st));
         if (!P.median) {
-            k_bin<<<nblk(n, kTile), kTileThreads, 0, st>>>(w.tb.p, idx, w.eseg.p, n, w.acc.p, B,
+            k_bin<<<nblk(n, kTile), kTileThreads, 0, st>>>(w.tb.p, idx, eseg, n, w.acc.p, B,
                                                            R, w.cnt.p, w.bbox.p, sc);
             k_select<<<nblk(S, kSelWarps), kSelWarps * 32, 0, st>>>(
                 w.acc.p, w.cnt.p, w.bbox.p, sc, snode, S, R, depth, P, w.node_box.p, w.sp.p,
@@ -994,11 +1009,12 @@ cudaError_t sah_build(const double *d_verts, int64_t n, const SahParams &P, SahT
         CK(cub::DeviceScan::ExclusiveSum(w.scan_tmp.p, scan_bytes, w.sflag.p, w.crank.p, S + 1,
                                          st));
         if (!P.median) {
-            k_flags<<<nblk(n, T), T, 0, st>>>(w.tb.p, idx, w.eseg.p, n, w.sp.p, B, w.flag.p);
+            k_flags<<<nblk(n, T), T, 0, st>>>(w.tb.p, idx, eseg, n, w.sp.p, B, w.flag.p);
             CK(cub::DeviceScan::ExclusiveSum(w.scan_tmp.p, scan_bytes, w.flag.p, w.rank.p,
                                              (int)n, st));
-            k_partition<<<nblk(n, T), T, 0, st>>>(idx, w.eseg.p, n, w.sp.p, sb, w.flag.p,
-                                                  w.rank.p, idx2);
+            k_partition<<<nblk(n, T), T, 0, st>>>(idx, eseg, n, w.sp.p, sb, w.flag.p,
+                                                  w.rank.p, w.crank.p, idx2, eseg2);
+            std::swap(eseg, eseg2);
         } else {
             // stable sort of each split segment by its centroid key; the
             // other positions keep their order
@@ -1009,7 +1025,7 @@ cudaError_t sah_build(const double *d_verts, int64_t n, const SahParams &P, SahT
             if (nsp > 0) {
                 CK(w.key.reserve(n)); CK(w.key2.reserve(n));
                 CK(w.sbeg.reserve(nsp)); CK(w.send.reserve(nsp));
-                k_median_keys<<<nblk(n, T), T, 0, st>>>(w.tb.p, idx, w.eseg.p, n, w.sp.p,
+                k_median_keys<<<nblk(n, T), T, 0, st>>>(w.tb.p, idx, eseg, n, w.sp.p,
                                                         w.key.p);
                 k_split_offsets<<<nblk(S, 128), 128, 0, st>>>(S, w.sflag.p, w.crank.p, sb, sc,
                                                               w.sbeg.p, w.send.p);
@@ -1027,7 +1043,7 @@ cudaError_t sah_build(const double *d_verts, int64_t n, const SahParams &P, SahT
         k_children<<<nblk(S, 128), 128, 0, st>>>(S, w.sp.p, w.crank.p, sb, sc, snode, node_count,
                                                  w.left.p, w.right.p, w.lf.p, w.lc.p, nsb, nsc,
                                                  nsnode);
-        *launches += 9;
+        *launches += 8;
         CK(cudaGetLastError());
         int nsplit = 0;
         CK(cudaMemcpyAsync(&nsplit, w.crank.p + S, sizeof(int), cudaMemcpyDeviceToHost, st));

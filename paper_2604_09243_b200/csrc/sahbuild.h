@@ -40,7 +40,7 @@ struct SegSplit {
 // grow-only scratch of the builder (kept by the context across builds)
 struct SahWork {
     DevBuf<double> tb, node_box;
-    DevBuf<int> idx, idx2, eseg, flag, rank, left, right, snode, nsnode, crank, sflag, big;
+    DevBuf<int> idx, idx2, eseg, eseg2, flag, rank, left, right, snode, nsnode, crank, sflag, big;
     DevBuf<int64_t> lf, lc, size, pre, sb, sc, nsb, nsc;
     DevBuf<unsigned int> cnt;
     DevBuf<unsigned long long> bbox;
