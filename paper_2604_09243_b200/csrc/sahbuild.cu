@@ -974,7 +974,10 @@ cudaError_t sah_build(const double *d_verts, int64_t n, const SahParams &P, SahT
             cudaEventCreate(&lv0); cudaEventCreate(&lv1);
             cudaEventRecord(lv0, st);
         }
-        const int R = S >= 4096 ? 1 : std::min(32, 4096 / S);
+        // bin replicas near the root (k_bin spreads its run heads over them,
+        // k_select merges them): 8 measured best of 1..32 (build 7.15 ->
+        // 6.96 ms against 32; fewer replicas to merge in k_select's warp)
+        const int R = S >= 4096 ? 1 : std::min(8, 4096 / S);
         const int64_t nslots = (int64_t)S * R * 3 * B;
         // grow geometrically so a build allocates O(log) times
         if ((size_t)nslots > w.cnt.n) {
