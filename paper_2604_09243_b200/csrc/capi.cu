@@ -390,9 +390,9 @@ extern "C" int sbr_ctx_launch_count(sbr_ctx *ctx, int64_t *count_out)
 // mesh
 // ---------------------------------------------------------------------------
 // Host (pageable) -> device upload through two pinned 16 MB chunks: the
-// persistent copy workers (CopyPool) copy chunk k+1 into one pinned buffer while the DMA engine moves
-// chunk k from the other (pageable cudaMemcpy runs at ~10 GB/s and
-// serialises the staging copy with the transfer).
+// persistent copy workers (CopyPool) copy chunk k+1 into one pinned buffer
+// while the DMA engine moves chunk k from the other (pageable cudaMemcpy runs
+// at ~10 GB/s and serialises the staging copy with the transfer).
 static constexpr size_t kPinChunk = (size_t)16 << 20;
 static constexpr unsigned kCopyThreads = 4;   // B200 box: 4 beat 1, 2, 8, 12, 16
 
